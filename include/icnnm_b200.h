@@ -1,0 +1,262 @@
+/*
+ * icnnm_b200.h — C ABI of the B200-native ICNNM hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ solver/operator API
+ * (/root/reference/proj/core/include/icnnm/*.hpp).  Every entry point takes
+ * plain host pointers and sizes (no C++ or torch types), f64 data in the
+ * reference's layouts:
+ *   - tensors: row-major, last index fastest            (tensor.hpp:64-68)
+ *   - m x k operator matrices: column-major (Eigen)    (conv_op.hpp:76)
+ *   - basis K: k x k column-major, column j = row-major
+ *     flattened eigen-kernel j                          (spectral.hpp:30-44,
+ *                                                        tensor_io.cpp:111-112)
+ * Device memory is owned by the library; host buffers are owned by the caller.
+ * Supported tensor order: 1..3 (the reference tests use order <= 3).
+ *
+ * Status codes mirror the reference's exception classes:
+ *   ICNNM_OK                 0
+ *   ICNNM_INVALID_ARGUMENT   1   std::invalid_argument (solver.cpp:26-40,66-72;
+ *                                tensor.hpp:100-107; spectral.cpp:25-41)
+ *   ICNNM_RUNTIME_ERROR      2   std::runtime_error
+ *   ICNNM_CUDA_ERROR         3   CUDA / NCCL failure (no reference analogue)
+ * The message of the last failure on the calling thread is returned by
+ * icnnm_last_error().
+ */
+#ifndef ICNNM_B200_H_
+#define ICNNM_B200_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ICNNM_OK 0
+#define ICNNM_INVALID_ARGUMENT 1
+#define ICNNM_RUNTIME_ERROR 2
+#define ICNNM_CUDA_ERROR 3
+
+#define ICNNM_INIT_ZERO 0
+#define ICNNM_INIT_MEAN 1
+
+#define ICNNM_TERM_MAX_ITERS 0
+#define ICNNM_TERM_CONVERGED 1
+
+/* GEMM engine of the two per-iteration contractions. */
+#define ICNNM_ENGINE_FFMA 0     /* exact fp32 FFMA implicit GEMM            */
+#define ICNNM_ENGINE_TF32X3 1   /* tcgen05 kind::tf32, 3-term split (sm_100a) */
+
+/* Field-for-field mirror of icnnm::SolverConfig (solver.hpp:29-43). */
+typedef struct icnnm_solver_config {
+  double lambda;        /* 1000                                       */
+  int has_theta0;       /* std::optional<double> theta0               */
+  double theta0;
+  double theta_growth;  /* 1.05                                       */
+  double theta_max;     /* 1e10                                       */
+  int max_iters;        /* 1000                                       */
+  double tol_primal;    /* 1e-7                                       */
+  double tol_change;    /* 1e-8                                       */
+  double rank_tol;      /* 1e-8 (unused by the solver, as upstream)   */
+  int init_fill;        /* ICNNM_INIT_ZERO | ICNNM_INIT_MEAN          */
+  int engine;           /* ICNNM_ENGINE_* (extension; default FFMA)   */
+} icnnm_solver_config;
+
+/* Mirror of icnnm::SolveReport (solver.hpp:46-52).  objective and
+ * primal_residual are caller-allocated arrays of >= max_iters doubles (or
+ * NULL); the library writes `iterations` entries. */
+typedef struct icnnm_solve_report {
+  int iterations;
+  double* objective;
+  double* primal_residual;
+  double* l_change;          /* extension: per-iteration ||dL||/||L|| */
+  int termination;           /* ICNNM_TERM_*                          */
+  double wall_time_seconds;
+  double loop_seconds;       /* extension: device time of the ADMM loop */
+  double device_seconds;     /* extension: device time of the whole run
+                                (setup kernels + loop), CUDA events      */
+} icnnm_solve_report;
+
+/* Defaults of SolverConfig (solver.hpp:29-43). */
+void icnnm_default_config(icnnm_solver_config* cfg);
+
+/* Replaces SolverConfig::validate (solver.cpp:26-40). */
+int icnnm_validate_config(const icnnm_solver_config* cfg);
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* icnnm_last_error(void);
+
+/* Library / device information. */
+const char* icnnm_version(void);
+int icnnm_device_count(void);
+
+/* ------------------------------------------------------------------------
+ * Solver.  Replaces
+ *   std::pair<DenseTensor,SolveReport> icnnm_solve(const DenseTensor& M_obs,
+ *     const SamplingMask& mask, const EigenBasis& basis, const SolverConfig&)
+ * (solver.hpp:64-67, solver.cpp:150-159 -> admm_solve solver.cpp:62-146).
+ * `eigenvalues` may be NULL (then only K's orthogonality is validated, as
+ * EigenBasis::validate does at spectral.cpp:31-34).
+ * ---------------------------------------------------------------------- */
+int icnnm_cuda_solve(int order, const int64_t* dims, const double* M_obs,
+                     const double* mask, const int64_t* kdims,
+                     const double* K_colmajor, const double* eigenvalues,
+                     const icnnm_solver_config* cfg, int device, double* L_out,
+                     icnnm_solve_report* report);
+
+/* Handle API mirroring BasisConvolver's precompute-once pattern
+ * (conv_op.hpp:61-81): create binds dims, kernel box and K to a device;
+ * upload stages one problem in HBM; run solves it from HBM; download
+ * returns L.  run() is the device-resident hot path timed by bench.py. */
+typedef struct icnnm_solver_s* icnnm_solver_t;
+
+int icnnm_solver_create(int order, const int64_t* dims, const int64_t* kdims,
+                        const double* K_colmajor, const double* eigenvalues,
+                        int device, icnnm_solver_t* out);
+int icnnm_solver_upload(icnnm_solver_t h, const double* M_obs,
+                        const double* mask);
+int icnnm_solver_run(icnnm_solver_t h, const icnnm_solver_config* cfg,
+                     icnnm_solve_report* report);
+int icnnm_solver_download(icnnm_solver_t h, double* L_out);
+/* Kernel launches issued by the last run() (for bench accounting). */
+int64_t icnnm_solver_last_launches(icnnm_solver_t h);
+/* Bytes of device memory held by the handle. */
+int64_t icnnm_solver_device_bytes(icnnm_solver_t h);
+/* Average device time (ms) of each kernel family over the last run() when
+ * profiling was enabled with icnnm_solver_set_profile(h, 1):
+ * out[0]=forward, out[1]=adjoint, out[2]=update, out[3]=coef. */
+int icnnm_solver_set_profile(icnnm_solver_t h, int enable);
+int icnnm_solver_kernel_times(icnnm_solver_t h, double* out_ms4);
+void icnnm_solver_destroy(icnnm_solver_t h);
+
+/* ------------------------------------------------------------------------
+ * Operator-level entry points (parity surface).
+ * ---------------------------------------------------------------------- */
+
+/* BasisConvolver(dims, ks, K).apply(L) (conv_op.cpp:100-114):
+ * out (m x k, column-major) = A_k(L) K. */
+int icnnm_cuda_conv_forward(int order, const int64_t* dims, const double* L,
+                            const int64_t* kdims, const double* K_colmajor,
+                            int device, double* out_colmajor);
+
+/* conv_adjoint(W, ks, dims) (conv_op.cpp:57-77):
+ * out[i] = sum_s W[(i+s) mod dims, s], W m x k column-major. */
+int icnnm_cuda_conv_adjoint(int order, const int64_t* dims,
+                            const int64_t* kdims, const double* W_colmajor,
+                            int device, double* out);
+
+/* prox_l21(W, tau) (solver.cpp:42-50), W rows x cols column-major. */
+int icnnm_cuda_prox_l21(int64_t rows, int64_t cols, const double* W_colmajor,
+                        double tau, int device, double* Z_colmajor);
+
+/* conv_gram(L, ks) (spectral.cpp:54-81): k x k Gram A_k(L)^T A_k(L). */
+int icnnm_cuda_conv_gram(int order, const int64_t* dims, const double* L,
+                         const int64_t* kdims, int device, double* G_colmajor);
+
+/* learn_ensemble_basis(refs, ks) (spectral.cpp:133-161): GPU Gram
+ * accumulation over the references, host eigensolve (descending order,
+ * eigenvalues clamped >= 0, column signs fixed, sigma = sqrt(lambda)).
+ * refs: n_refs pointers to m doubles each.  degenerate: 1 when the Gram is
+ * identically zero (K = I, eigenvalues 0). */
+int icnnm_cuda_learn_basis(int n_refs, int order, const int64_t* dims,
+                           const double* const* refs, const int64_t* kdims,
+                           int device, double* K_colmajor_out,
+                           double* eigenvalues_out, int* degenerate);
+
+/* Host eigensolver used by learn_basis (exported for tests):
+ * symmetric G (n x n, column-major) -> eigenvalues descending and
+ * eigenvectors (column-major), Householder tridiagonalisation + implicit QL. */
+int icnnm_host_symeig(int n, const double* G_colmajor, double* evals_desc,
+                      double* evecs_colmajor);
+
+/* objective_icnnm(L, M, mask, basis, lambda) (solver.cpp:172-187). */
+int icnnm_cuda_objective(int order, const int64_t* dims, const double* L,
+                         const double* M_obs, const double* mask,
+                         const int64_t* kdims, const double* K_colmajor,
+                         double lambda, int device, double* out);
+
+/* ------------------------------------------------------------------------
+ * Sharded solve of one large tensor, split over H into G slabs (one slab per
+ * rank of a NCCL communicator, optionally several virtual slabs per process;
+ * BASELINE config 5).  Periodic halos of kh-1 rows travel from rank g-1 to g
+ * before the forward pass, adjoint partial sums travel back, and the
+ * k-length column-norm vector (+ scalars) is all-reduced once per
+ * iteration.  The result equals the unsharded solve up to fp32 rounding.
+ * ---------------------------------------------------------------------- */
+#define ICNNM_NCCL_UNIQUE_ID_BYTES 128
+
+int icnnm_dist_unique_id(char* out128);
+
+/* Solve with `local_slabs` slabs per process and `world` processes
+ * (G = local_slabs * world slabs).  Each process passes the FULL tensor
+ * (M_obs, mask: m doubles) and receives its own slabs' rows of L in
+ * L_out (rows [row0, row0 + nrows) of the H axis, written to
+ * L_out[0 .. nrows*W*T)).  world == 1 needs no NCCL id (pass NULL).
+ * row0/nrows may be NULL. */
+int icnnm_sharded_solve(int order, const int64_t* dims, const double* M_obs,
+                        const double* mask, const int64_t* kdims,
+                        const double* K_colmajor,
+                        const icnnm_solver_config* cfg, int local_slabs,
+                        int world, int rank, const char* nccl_id128,
+                        int device, double* L_out, int64_t* row0,
+                        int64_t* nrows, icnnm_solve_report* report);
+
+/* Slab plan (host logic, exported for CPU tests): slab g of G over H rows
+ * gets rows [start, start+count); returns 1 (invalid) when a slab would be
+ * thinner than kh-1 rows. */
+int icnnm_shard_plan(int64_t H, int G, int64_t kh, int g, int64_t* start,
+                     int64_t* count);
+
+/* ------------------------------------------------------------------------
+ * BASELINE synthetic generator (host, std::mt19937_64).
+ * ---------------------------------------------------------------------- */
+
+/* Sum of n_sin 3-D sinusoids (amplitude U[0.5,1.5], integer frequencies
+ * 0..4 per axis, phase U[0,2pi)) plus n_blob Gaussian blobs (sigma px,
+ * amplitude U[0.5,1.5], moving 1 px/frame along a random direction,
+ * periodic), min-max scaled to [0,1], then + N(0, noise_sigma^2).
+ * dims = H, W, T; out has H*W*T doubles (row-major). */
+int icnnm_synth_video(int64_t H, int64_t W, int64_t T, int n_sin, int n_blob,
+                      double blob_sigma, double noise_sigma, uint64_t seed,
+                      double* out);
+
+/* Mask kinds. */
+#define ICNNM_MASK_IID 0          /* voxel kept iff U[0,1) < rate            */
+#define ICNNM_MASK_EXACT 1        /* exactly llround(rate*m) kept, shuffle   */
+                                  /* (reference bernoulli_mask, mask.cpp:49-59) */
+#define ICNNM_MASK_T_FRAMES 2     /* keep T-frames t with (t % 2 == 0)       */
+#define ICNNM_MASK_T_PREFIX 3     /* keep T-frames t < (int)rate             */
+#define ICNNM_MASK_IID_BOXES 4    /* iid(rate) minus n_boxes boxes            */
+
+int icnnm_synth_mask(int64_t H, int64_t W, int64_t T, int kind, double rate,
+                     int n_boxes, uint64_t seed, double* out);
+
+/* Reference-test data generators (proj/tests/test_util.hpp:27-49 and
+ * mask.cpp:49-59), reproducing libstdc++'s std::mt19937_64 streams so that
+ * the reference's own known-answer cases can be rebuilt bit-for-bit. */
+typedef struct icnnm_rng_s* icnnm_rng_t;
+icnnm_rng_t icnnm_rng_create(uint64_t seed);
+void icnnm_rng_destroy(icnnm_rng_t r);
+/* uniform_real_distribution<double>(lo, hi) draws */
+void icnnm_rng_uniform(icnnm_rng_t r, double lo, double hi, int64_t n,
+                       double* out);
+/* uniform_int_distribution<int64_t>(lo, hi) draws */
+void icnnm_rng_uniform_int(icnnm_rng_t r, int64_t lo, int64_t hi, int64_t n,
+                           int64_t* out);
+/* normal_distribution<double>(mean, stddev) draws */
+void icnnm_rng_normal(icnnm_rng_t r, double mean, double stddev, int64_t n,
+                      double* out);
+/* bernoulli_mask(dims, rate, seed) of mask.cpp:49-59 (flat, m entries). */
+int icnnm_reference_bernoulli_mask(int64_t m, double rate, uint64_t seed,
+                                   double* out);
+
+/* ------------------------------------------------------------------------
+ * Probes used by bench.py for roofline denominators (device microbenches).
+ * ---------------------------------------------------------------------- */
+/* FP32 FFMA throughput in TFLOP/s measured with a register-resident kernel. */
+int icnnm_probe_ffma_tflops(int device, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ICNNM_B200_H_ */

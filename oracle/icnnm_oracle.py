@@ -1,0 +1,394 @@
+"""CPU ORACLE — test infrastructure only (never the product path).
+
+A literal fp64 numpy/scipy restatement of the reference ICNNM solver path,
+/root/reference/proj/core (Eigen3 + FFTW3, neither present in this image, so
+the reference itself cannot be compiled here: see DESIGN.md §4).  Only
+tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference leg may import this module, and only as the checker / CPU baseline.
+
+Each function cites the reference file:line it restates.  Parity pinning:
+the reference ships no golden data files (proj/test_output.txt is pass/fail
+only), so this oracle is pinned against every known-answer test of the
+reference's own suites for this path (tests/test_oracle_pins.py), with the
+reference tests' inputs rebuilt bit-for-bit from libstdc++'s mt19937_64
+streams (proj/tests/test_util.hpp:27-49, proj/core/src/mask.cpp:49-59).
+
+Conventions (tensor.hpp:64-68, fft.cpp:78-90, conv_op.cpp:42-44,94):
+row-major tensors, kernel taps corner-anchored and flattened row-major,
+periodic boundaries, K column j = eigen-kernel j.  Internally the m x k
+operator matrices are stored transposed, as (k, *dims) arrays (column j of
+the reference's matrix is row j here), so per-column FFTs are contiguous.
+"""
+from __future__ import annotations
+
+import dataclasses
+import itertools
+import os
+import time
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import scipy.fft as sfft
+
+WORKERS = int(os.environ.get("ICNNM_ORACLE_THREADS", "1"))
+
+
+def kernel_offsets(ks: Sequence[int]) -> List[Tuple[int, ...]]:
+    """Row-major multi-indices of the kernel box (for_each_index,
+    tensor.hpp:140-152)."""
+    return list(itertools.product(*[range(int(k)) for k in ks]))
+
+
+def validate_kernel(ks, dims) -> None:
+    """KernelShape::validate_for (tensor.hpp:100-107)."""
+    if len(ks) != len(dims):
+        raise ValueError("KernelShape: order mismatch with tensor")
+    for k, d in zip(ks, dims):
+        if k < 1 or k > d:
+            raise ValueError("KernelShape: kernel dim out of range")
+
+
+def circular_shift(L: np.ndarray, s) -> np.ndarray:
+    """circular_shift (conv_op.cpp:19-33): out[i] = L[(i - s) mod dims]."""
+    return np.roll(L, shift=tuple(int(x) for x in s), axis=tuple(range(L.ndim)))
+
+
+def conv_matrix(L: np.ndarray, ks) -> np.ndarray:
+    """conv_matrix (conv_op.cpp:35-46): m x k, column s = vec(shift(L, s))."""
+    validate_kernel(ks, L.shape)
+    return np.stack([circular_shift(L, s).ravel() for s in kernel_offsets(ks)], axis=1)
+
+
+def pad_to(X: np.ndarray, dims) -> np.ndarray:
+    """pad_to (fft.cpp:78-90): corner-anchored zero padding."""
+    out = np.zeros(tuple(dims))
+    out[tuple(slice(0, k) for k in X.shape)] = X
+    return out
+
+
+def circular_convolve(L: np.ndarray, X: np.ndarray) -> np.ndarray:
+    """circular_convolve (fft.cpp:92-107): (L*X)[i] = sum_s L[i-s] X[s]."""
+    if X.ndim != L.ndim:
+        raise ValueError("pad_to: order mismatch")
+    if any(k > d for k, d in zip(X.shape, L.shape)):
+        raise ValueError("pad_to: kernel dim exceeds tensor dim")
+    fl = sfft.fftn(L, workers=WORKERS)
+    fx = sfft.fftn(pad_to(X, L.shape), workers=WORKERS)
+    return sfft.ifftn(fl * fx, workers=WORKERS).real
+
+
+def circular_autocorrelation(L: np.ndarray) -> np.ndarray:
+    """circular_autocorrelation (fft.cpp:109-118)."""
+    fl = sfft.fftn(L, workers=WORKERS)
+    return sfft.ifftn((fl * fl.conj()).real, workers=WORKERS).real
+
+
+class BasisConvolver:
+    """BasisConvolver (conv_op.cpp:85-114): k kernel spectra precomputed;
+    apply(L) = A_k(L) K via 1 forward + k inverse c2c FFTs.  Returned
+    transposed: (k, *dims)."""
+
+    def __init__(self, dims, ks, K: np.ndarray, chunk: int = 64):
+        validate_kernel(ks, dims)
+        self.dims = tuple(int(d) for d in dims)
+        self.ks = tuple(int(k) for k in ks)
+        k = int(np.prod(self.ks))
+        if K.shape != (k, k):
+            raise ValueError("BasisConvolver: K must be k x k")
+        self.K = np.asarray(K, dtype=np.float64)
+        self.k = k
+        self.chunk = chunk
+        # kernel spectra (conv_op.cpp:92-97); computed lazily per chunk to
+        # avoid the m x k complex cache of the reference when large.
+        self._spec = None
+        if int(np.prod(self.dims)) * k * 16 <= (8 << 30):
+            self._spec = self._spectra(0, k)
+
+    def _spectra(self, j0: int, j1: int) -> np.ndarray:
+        kern = self.K[:, j0:j1].T.reshape((j1 - j0,) + self.ks)
+        padded = np.zeros((j1 - j0,) + self.dims)
+        padded[(slice(None),) + tuple(slice(0, q) for q in self.ks)] = kern
+        return sfft.fftn(padded, axes=tuple(range(1, len(self.dims) + 1)), workers=WORKERS)
+
+    def apply_t(self, L: np.ndarray) -> np.ndarray:
+        if L.shape != self.dims:
+            raise ValueError("BasisConvolver: tensor dims mismatch")
+        fl = sfft.fftn(L, workers=WORKERS)
+        out = np.empty((self.k,) + self.dims)
+        axes = tuple(range(1, len(self.dims) + 1))
+        for j0 in range(0, self.k, self.chunk):
+            j1 = min(self.k, j0 + self.chunk)
+            spec = self._spec[j0:j1] if self._spec is not None else self._spectra(j0, j1)
+            out[j0:j1] = sfft.ifftn(fl[None] * spec, axes=axes, workers=WORKERS).real
+        return out
+
+    def apply(self, L: np.ndarray) -> np.ndarray:
+        """m x k, as the reference returns it."""
+        return self.apply_t(L).reshape(self.k, -1).T
+
+
+def conv_adjoint_t(Wt: np.ndarray, ks, dims) -> np.ndarray:
+    """conv_adjoint (conv_op.cpp:57-77) on a (k, *dims) array:
+    out[i] = sum_s W[(i + s) mod dims, s], s-major then i row-major."""
+    dims = tuple(int(d) for d in dims)
+    validate_kernel(ks, dims)
+    k = int(np.prod(ks))
+    if Wt.shape[0] != k or Wt[0].size != int(np.prod(dims)):
+        raise ValueError("conv_adjoint: W shape mismatch with dims/kernel")
+    out = np.zeros(dims)
+    axes = tuple(range(len(dims)))
+    for col, s in enumerate(kernel_offsets(ks)):
+        out += np.roll(Wt[col].reshape(dims), shift=tuple(-int(x) for x in s), axis=axes)
+    return out
+
+
+def conv_adjoint(W: np.ndarray, ks, dims) -> np.ndarray:
+    """conv_adjoint on an m x k matrix."""
+    m = int(np.prod(dims))
+    k = int(np.prod(ks))
+    if W.shape != (m, k):
+        raise ValueError("conv_adjoint: W shape mismatch with dims/kernel")
+    return conv_adjoint_t(np.ascontiguousarray(W.T), ks, dims)
+
+
+def prox_l21(W: np.ndarray, tau: float) -> np.ndarray:
+    """prox_l21 (solver.cpp:42-50): columns scaled by (n > tau) ? 1 - tau/n : 0."""
+    if tau < 0:
+        raise ValueError("prox_l21: tau must be >= 0")
+    n = np.linalg.norm(W, axis=0)
+    scale = np.where(n > tau, 1.0 - tau / np.where(n > 0, n, 1.0), 0.0)
+    return W * scale[None, :]
+
+
+def _prox_l21_t(Wt: np.ndarray, tau: float) -> Tuple[np.ndarray, np.ndarray]:
+    k = Wt.shape[0]
+    n = np.sqrt(np.einsum("ij,ij->i", Wt.reshape(k, -1), Wt.reshape(k, -1)))
+    scale = np.where(n > tau, 1.0 - tau / np.where(n > 0, n, 1.0), 0.0)
+    return Wt * scale.reshape((k,) + (1,) * (Wt.ndim - 1)), n
+
+
+def conv_gram(L: np.ndarray, ks) -> np.ndarray:
+    """conv_gram (spectral.cpp:54-81): G[s,t] = R[(s - t) mod dims]."""
+    validate_kernel(ks, L.shape)
+    R = circular_autocorrelation(L)
+    offs = np.array(kernel_offsets(ks), dtype=np.int64)
+    dims = np.array(L.shape, dtype=np.int64)
+    diff = np.mod(offs[:, None, :] - offs[None, :, :], dims)
+    return R[tuple(diff[..., j] for j in range(L.ndim))]
+
+
+def fix_column_signs(M: np.ndarray) -> np.ndarray:
+    """fix_column_signs (spectral.cpp:43-52)."""
+    M = M.copy()
+    for c in range(M.shape[1]):
+        nz = np.nonzero(np.abs(M[:, c]) > 1e-12)[0]
+        if nz.size and M[nz[0], c] < 0:
+            M[:, c] = -M[:, c]
+    return M
+
+
+def psd_eig_sorted(G: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """psd_eig_sorted (spectral.cpp:87-98): descending, clamped, signs fixed."""
+    w, V = np.linalg.eigh(G)
+    w = np.maximum(0.0, w[::-1])
+    V = fix_column_signs(V[:, ::-1])
+    return w, V
+
+
+@dataclasses.dataclass
+class EigenBasis:
+    kernel_shape: Tuple[int, ...]
+    K: np.ndarray
+    eigenvalues: np.ndarray
+    degenerate: bool = False
+
+    def validate(self) -> None:
+        """EigenBasis::validate (spectral.cpp:25-41)."""
+        k = int(np.prod(self.kernel_shape))
+        if self.K.shape != (k, k):
+            raise ValueError("EigenBasis: K must be k x k")
+        if len(self.eigenvalues) != k:
+            raise ValueError("EigenBasis: eigenvalue count mismatch")
+        if np.max(np.abs(self.K.T @ self.K - np.eye(k))) > 1e-10:
+            raise ValueError("EigenBasis: K is not orthogonal")
+        ev = np.asarray(self.eigenvalues)
+        if np.any(ev < 0):
+            raise ValueError("EigenBasis: negative eigenvalue")
+        if np.any(ev[1:] > ev[:-1] + 1e-12):
+            raise ValueError("EigenBasis: eigenvalues not nonincreasing")
+
+
+def learn_ensemble_basis(refs: Sequence[np.ndarray], ks) -> EigenBasis:
+    """learn_ensemble_basis (spectral.cpp:133-161)."""
+    if len(refs) == 0:
+        raise ValueError("learn_ensemble_basis: empty reference list")
+    dims = refs[0].shape
+    validate_kernel(ks, dims)
+    k = int(np.prod(ks))
+    G = np.zeros((k, k))
+    for r in refs:
+        if r.shape != dims:
+            raise ValueError("learn_ensemble_basis: dim mismatch among refs")
+        G += conv_gram(r, ks)
+    if np.max(np.abs(G)) == 0.0:
+        return EigenBasis(tuple(ks), np.eye(k), np.zeros(k), True)
+    w, V = psd_eig_sorted(G)
+    return EigenBasis(tuple(ks), V, np.sqrt(w), False)
+
+
+@dataclasses.dataclass
+class SolverConfig:
+    """SolverConfig (solver.hpp:29-43)."""
+    lambda_: float = 1000.0
+    theta0: Optional[float] = None
+    theta_growth: float = 1.05
+    theta_max: float = 1e10
+    max_iters: int = 1000
+    tol_primal: float = 1e-7
+    tol_change: float = 1e-8
+    rank_tol: float = 1e-8
+    init_fill: str = "zero"
+
+    def validate(self) -> None:
+        """SolverConfig::validate (solver.cpp:26-40)."""
+        if not self.lambda_ > 0:
+            raise ValueError("SolverConfig: lambda must be > 0")
+        if self.theta0 is not None and not self.theta0 > 0:
+            raise ValueError("SolverConfig: theta0 must be > 0")
+        if not self.theta_growth >= 1:
+            raise ValueError("SolverConfig: theta_growth must be >= 1")
+        if not self.theta_max > 0:
+            raise ValueError("SolverConfig: theta_max must be > 0")
+        if self.theta0 is not None and self.theta0 > self.theta_max:
+            raise ValueError("SolverConfig: theta0 must be <= theta_max")
+        if self.max_iters < 1:
+            raise ValueError("SolverConfig: max_iters must be >= 1")
+        if not (self.tol_primal > 0 and self.tol_change > 0 and self.rank_tol > 0):
+            raise ValueError("SolverConfig: tolerances must be > 0")
+        if self.init_fill not in ("zero", "mean"):
+            raise ValueError("SolverConfig: init_fill must be 'zero' or 'mean'")
+
+
+@dataclasses.dataclass
+class SolveReport:
+    iterations: int = 0
+    objective: List[float] = dataclasses.field(default_factory=list)
+    primal_residual: List[float] = dataclasses.field(default_factory=list)
+    termination: str = "max_iters"
+    wall_time_seconds: float = 0.0
+    l_change: List[float] = dataclasses.field(default_factory=list)
+
+
+class AdmmSolver:
+    """admm_solve (solver.cpp:62-146) with the prox_l21 Z-update, literally;
+    setup in __init__ (:66-102), one loop body per step() (:108-139)."""
+
+    def __init__(self, M_obs: np.ndarray, mask: np.ndarray, basis: EigenBasis,
+                 cfg: Optional[SolverConfig] = None, validate_basis: bool = True):
+        cfg = cfg or SolverConfig()
+        if validate_basis:
+            basis.validate()                                     # solver.cpp:156
+        cfg.validate()                                           # :66
+        ks = tuple(basis.kernel_shape)
+        validate_kernel(ks, M_obs.shape)                         # :67
+        if mask.shape != M_obs.shape:                            # :68-69
+            raise ValueError("solve: mask dims != observation dims")
+        if np.any((mask != 0.0) & (mask != 1.0)):                # tensor.hpp:115-121
+            raise ValueError("SamplingMask: entries must be 0 or 1")
+        if int(mask.sum() + 0.5) == 0:                           # :70-71
+            raise ValueError("solve: empty sampling set")
+        if not np.all(np.isfinite(M_obs)):                       # :72
+            raise ValueError("solve: observations: non-finite tensor entries")
+        self.t_start = time.perf_counter()
+        self.cfg, self.ks, self.basis = cfg, ks, basis
+        self.M_obs, self.mask = M_obs, mask
+        self.dims = M_obs.shape
+        self.k = k = int(np.prod(ks))
+        self.pm = pm = M_obs * mask                              # :80
+        L = pm.copy()                                            # :82
+        if cfg.init_fill == "mean":                              # :83-86
+            L = L + (1.0 - mask) * (pm.sum() / float(int(mask.sum() + 0.5)))
+        self.L = L
+        theta = cfg.theta0 if cfg.theta0 is not None else 1e-2 * np.max(np.abs(pm)) * k  # :88-89
+        if theta <= 0:
+            theta = 1e-2                                         # :90
+        self.theta = min(theta, cfg.theta_max)                   # :91
+        self.conv = BasisConvolver(self.dims, ks, basis.K)       # :93
+        rs = np.sqrt(k) * np.linalg.norm(pm)                     # :97
+        self.res_scale = rs if rs != 0 else 1.0                  # :98
+        self.AKL = self.conv.apply_t(L)                          # :100  (k, *dims)
+        self.Z = self.AKL.copy()                                 # :101
+        self.Y = np.zeros_like(self.AKL)                         # :102
+        self.report = SolveReport()
+        self.report.termination = "max_iters"
+        self.it = 0
+
+    def step(self) -> bool:
+        """One iteration; returns True when the stopping test fires."""
+        cfg, k, theta = self.cfg, self.k, self.theta
+        flat = (k, -1)
+        self.Z, _ = _prox_l21_t(self.AKL - self.Y / theta, 1.0 / theta)  # :108
+        # WK = (Y + theta Z) K^T  -> transposed: K (Y + theta Z)^T      (:110)
+        WKt = (self.basis.K @ (self.Y + theta * self.Z).reshape(flat)).reshape(self.AKL.shape)
+        adj = conv_adjoint_t(WKt, self.ks, self.dims)            # :111
+        numer = adj / k + cfg.lambda_ * self.pm                  # :112-113
+        denom = cfg.lambda_ * self.mask + theta                  # :114-115
+        L_new = numer / denom                                    # :116
+        l_change = np.linalg.norm(L_new - self.L) / max(np.linalg.norm(self.L), 1e-300)  # :118-119
+        self.L = L_new                                           # :120
+        self.AKL = self.conv.apply_t(self.L)                     # :121
+        gap = self.Z - self.AKL                                  # :123
+        residual = np.linalg.norm(gap) / self.res_scale          # :124
+        self.Y += theta * gap                                    # :125
+        self.theta = min(theta * cfg.theta_growth, cfg.theta_max)  # :126
+        col_sum = float(np.sum(np.linalg.norm(self.Z.reshape(flat), axis=1)))  # :128-129
+        fit = float(np.sum(((self.L - self.M_obs) * self.mask) ** 2))  # :130
+        rep = self.report
+        rep.objective.append(col_sum + 0.5 * cfg.lambda_ * k * fit)    # :131-132
+        rep.primal_residual.append(residual)
+        rep.l_change.append(l_change)
+        self.it += 1
+        rep.iterations = self.it
+        if residual < cfg.tol_primal or l_change < cfg.tol_change:      # :136-139
+            rep.termination = "converged"
+            return True
+        return False
+
+
+def icnnm_solve(M_obs: np.ndarray, mask: np.ndarray, basis: EigenBasis,
+                cfg: Optional[SolverConfig] = None, validate_basis: bool = True
+                ) -> Tuple[np.ndarray, SolveReport]:
+    """icnnm_solve (solver.cpp:150-159)."""
+    s = AdmmSolver(M_obs, mask, basis, cfg, validate_basis)
+    for _ in range(s.cfg.max_iters):                             # :107
+        if s.step():
+            break
+    s.report.wall_time_seconds = time.perf_counter() - s.t_start
+    return s.L, s.report
+
+
+def objective_icnnm(L, M_obs, mask, basis: EigenBasis, lam: float) -> float:
+    """objective_icnnm (solver.cpp:172-187)."""
+    basis.validate()
+    conv = BasisConvolver(L.shape, basis.kernel_shape, basis.K)
+    AKL = conv.apply_t(L).reshape(basis.K.shape[0], -1)
+    col_sum = float(np.sum(np.linalg.norm(AKL, axis=1)))
+    fit = float(np.sum(((L - M_obs) * mask) ** 2))
+    return col_sum + 0.5 * lam * basis.K.shape[0] * fit
+
+
+def mse(ref, est) -> float:
+    """mse (metrics.cpp:28-32)."""
+    return float(np.mean((np.asarray(ref) - np.asarray(est)) ** 2))
+
+
+def psnr(ref, est, peak: float = 1.0) -> float:
+    """psnr (metrics.cpp:34-38): +inf when MSE is 0."""
+    e = mse(ref, est)
+    if e == 0:
+        return float("inf")
+    return 10.0 * np.log10(peak * peak / e)
+
+
+def rel_l2(a, b) -> float:
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))

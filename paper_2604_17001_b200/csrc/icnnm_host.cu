@@ -1,0 +1,1216 @@
+// Host driver of the B200 ICNNM hot path: the C ABI of include/icnnm_b200.h.
+//
+// Mirrors the reference's C++ solver/operator API
+// (/root/reference/proj/core/include/icnnm/{solver,conv_op,spectral}.hpp):
+// validation rules and error classes follow solver.cpp:26-40,66-72,
+// tensor.hpp:100-107,115-121 and spectral.cpp:25-41; the ADMM loop is the
+// restated form of solver.cpp:62-146 documented in DESIGN.md §2.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/icnnm_b200.h"
+#include "icnnm_comm.h"
+#include "icnnm_kernels.cuh"
+
+using icnnm_dev::BK;
+using icnnm_dev::BM;
+using icnnm_dev::BN;
+using icnnm_dev::Geo;
+using icnnm_dev::IterState;
+using icnnm_dev::IterStats;
+
+namespace icnnm_host {
+
+// ---------------------------------------------------------------------------
+// Errors
+// ---------------------------------------------------------------------------
+struct Error {
+  int code;
+  std::string msg;
+};
+thread_local std::string g_last_error;
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+[[noreturn]] void invalid(const std::string& msg) { fail(ICNNM_INVALID_ARGUMENT, msg); }
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      ::icnnm_host::fail(ICNNM_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define CKL() CK(cudaGetLastError())
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return ICNNM_OK;
+  } catch (const Error& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return ICNNM_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ICNNM_RUNTIME_ERROR;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Device buffers
+// ---------------------------------------------------------------------------
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) {
+      cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+      if (e != cudaSuccess) {
+        p = nullptr;
+        fail(ICNNM_CUDA_ERROR, "cudaMalloc(" + std::to_string(count * sizeof(T)) +
+                                   " bytes): " + cudaGetErrorString(e));
+      }
+    }
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+};
+
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    CK(cudaGetDevice(&prev));
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (dev < 0 || dev >= n)
+      invalid("device index " + std::to_string(dev) + " out of range (" + std::to_string(n) +
+              " devices)");
+    CK(cudaSetDevice(dev));
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Problem geometry
+// ---------------------------------------------------------------------------
+struct Problem {
+  int order = 0;
+  int64_t dims[3] = {1, 1, 1};   // H, W, T
+  int64_t kd[3] = {1, 1, 1};     // kh, kw, kt
+  int64_t m = 0;
+  int k = 0;
+  int kp = 0;
+};
+
+inline int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+inline int pow2ceil(int64_t x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// DenseTensor / KernelShape::validate_for (tensor.hpp:81-107).
+Problem make_problem(int order, const int64_t* dims, const int64_t* kdims) {
+  if (order < 1) invalid("DenseTensor: order must be >= 1");
+  if (order > 3) invalid("icnnm_b200: tensor order > 3 is not supported");
+  if (!dims || !kdims) invalid("null dims");
+  Problem p;
+  p.order = order;
+  for (int j = 0; j < order; ++j) {
+    if (dims[j] < 1) invalid("DenseTensor: dims must be positive");
+    if (kdims[j] < 1 || kdims[j] > dims[j]) invalid("KernelShape: kernel dim out of range");
+    p.dims[3 - order + j] = dims[j];
+    p.kd[3 - order + j] = kdims[j];
+  }
+  p.m = p.dims[0] * p.dims[1] * p.dims[2];
+  int64_t k = p.kd[0] * p.kd[1] * p.kd[2];
+  if (p.dims[0] > (1 << 30) || p.m > (int64_t(1) << 40)) invalid("tensor too large");
+  if (k > 4096) invalid("icnnm_b200: kernel with more than 4096 taps is not supported");
+  p.k = static_cast<int>(k);
+  p.kp = static_cast<int>(roundup(k, BN));
+  return p;
+}
+
+// Launch geometry for `rows` H-rows of the tensor.  wrap=1: periodic over the
+// whole tensor; wrap=0: slab buffer with kh-1 halo rows before the own rows.
+Geo make_geo(const Problem& p, int64_t rows, bool wrap) {
+  Geo g{};
+  g.H = static_cast<int>(rows);
+  g.W = static_cast<int>(p.dims[1]);
+  g.T = static_cast<int>(p.dims[2]);
+  g.kh = static_cast<int>(p.kd[0]);
+  g.kw = static_cast<int>(p.kd[1]);
+  g.kt = static_cast<int>(p.kd[2]);
+  g.bt = g.T > 8 ? 16 : 8;
+  const int rem = BM / g.bt;
+  if (g.H == 1) {
+    g.bh = 1;
+    g.bw = rem;
+  } else {
+    g.bw = std::min(pow2ceil(g.W), 4);
+    g.bh = rem / g.bw;
+  }
+  g.nbh = (g.H + g.bh - 1) / g.bh;
+  g.nbw = (g.W + g.bw - 1) / g.bw;
+  g.nbt = (g.T + g.bt - 1) / g.bt;
+  g.HH = g.bh + g.kh - 1;
+  g.HW = g.bw + g.kw - 1;
+  g.HT = g.bt + g.kt - 1;
+  g.k = p.k;
+  g.kp = p.kp;
+  g.ktp = p.kp;
+  if (wrap) {
+    g.Hsrc = g.H;
+    g.hoff = 0;
+    g.wrapH = 1;
+  } else {
+    g.Hsrc = g.H + g.kh - 1;
+    g.hoff = g.kh - 1;
+    g.wrapH = 0;
+  }
+  return g;
+}
+
+inline int64_t n_bricks(const Geo& g) {
+  return static_cast<int64_t>(g.nbh) * g.nbw * g.nbt;
+}
+inline size_t fwd_smem(const Geo& g) {
+  return (2 * BK * BN + g.ktp + static_cast<size_t>(g.HH) * g.HW * g.HT) * 4;
+}
+inline size_t adj_smem(const Geo& g) {
+  return (BK * (BM + 4) + 2 * BK * BN + g.kp + g.ktp +
+          static_cast<size_t>(g.HH) * g.HW * g.HT) * 4;
+}
+
+void check_smem(size_t need) {
+  if (need > 220 * 1024)
+    invalid("icnnm_b200: halo brick too large for shared memory (" + std::to_string(need) +
+            " bytes); kernel box too large");
+}
+
+template <class K>
+void set_max_dyn_smem(K kernel, int optin) {
+  cudaFuncAttributes a;
+  CK(cudaFuncGetAttributes(&a, kernel));
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          optin - static_cast<int>(a.sharedSizeBytes)));
+}
+
+void set_smem_attrs() {
+  static thread_local int done_dev = -1;
+  int dev;
+  CK(cudaGetDevice(&dev));
+  if (done_dev == dev) return;
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  set_max_dyn_smem(icnnm_dev::icnnm_fwd_ffma, optin);
+  set_max_dyn_smem(icnnm_dev::icnnm_adj_ffma, optin);
+  set_max_dyn_smem(icnnm_dev::icnnm_gram_lags, optin);
+  done_dev = dev;
+}
+
+// Brick-ordered row of voxel (h, w, t) in a launch geometry.
+inline int64_t brick_row(const Geo& g, int64_t h, int64_t w, int64_t t) {
+  int64_t b = (h / g.bh * g.nbw + w / g.bw) * g.nbt + t / g.bt;
+  int64_t v = ((h % g.bh) * g.bw + (w % g.bw)) * g.bt + (t % g.bt);
+  return b * BM + v;
+}
+
+// K (k x k column-major, f64) -> Krm [ktp][kp] (K[s][j]) and KT [kp][ktp].
+void pack_basis(const Problem& p, const double* Kcm, std::vector<float>& Krm,
+                std::vector<float>& KT) {
+  const int k = p.k, kp = p.kp;
+  Krm.assign(static_cast<size_t>(kp) * kp, 0.f);
+  KT.assign(static_cast<size_t>(kp) * kp, 0.f);
+  for (int j = 0; j < k; ++j)
+    for (int s = 0; s < k; ++s) {
+      float v = static_cast<float>(Kcm[static_cast<size_t>(j) * k + s]);
+      Krm[static_cast<size_t>(s) * kp + j] = v;
+      KT[static_cast<size_t>(j) * kp + s] = v;
+    }
+}
+
+// EigenBasis::validate (spectral.cpp:25-41).
+void validate_basis(int k, const double* K, const double* evals) {
+  if (!K) invalid("EigenBasis: K must be k x k");
+  double worst = 0.0;
+  std::vector<double> col(k);
+  for (int i = 0; i < k; ++i) {
+    const double* ci = K + static_cast<size_t>(i) * k;
+    for (int j = 0; j <= i; ++j) {
+      const double* cj = K + static_cast<size_t>(j) * k;
+      double d = 0.0;
+      for (int r = 0; r < k; ++r) d += ci[r] * cj[r];
+      if (i == j) d -= 1.0;
+      worst = std::max(worst, std::fabs(d));
+    }
+  }
+  if (!(worst <= 1e-10)) invalid("EigenBasis: K is not orthogonal");
+  if (evals) {
+    for (int i = 0; i < k; ++i) {
+      if (evals[i] < 0) invalid("EigenBasis: negative eigenvalue");
+      if (i > 0 && evals[i] > evals[i - 1] + 1e-12)
+        invalid("EigenBasis: eigenvalues not nonincreasing");
+    }
+  }
+}
+
+void validate_cfg(const icnnm_solver_config* c) {
+  if (!c) invalid("SolverConfig: null");
+  if (!(c->lambda > 0)) invalid("SolverConfig: lambda must be > 0");
+  if (c->has_theta0 && !(c->theta0 > 0)) invalid("SolverConfig: theta0 must be > 0");
+  if (!(c->theta_growth >= 1)) invalid("SolverConfig: theta_growth must be >= 1");
+  if (!(c->theta_max > 0)) invalid("SolverConfig: theta_max must be > 0");
+  if (c->has_theta0 && c->theta0 > c->theta_max)
+    invalid("SolverConfig: theta0 must be <= theta_max");
+  if (c->max_iters < 1) invalid("SolverConfig: max_iters must be >= 1");
+  if (!(c->tol_primal > 0) || !(c->tol_change > 0) || !(c->rank_tol > 0))
+    invalid("SolverConfig: tolerances must be > 0");
+  if (c->init_fill != ICNNM_INIT_ZERO && c->init_fill != ICNNM_INIT_MEAN)
+    invalid("SolverConfig: init_fill must be 'zero' or 'mean'");
+  if (c->engine != ICNNM_ENGINE_FFMA && c->engine != ICNNM_ENGINE_TF32X3)
+    invalid("SolverConfig: unknown engine");
+}
+
+inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 16) {
+  int64_t b = (n + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, max_blocks)));
+}
+
+// ---------------------------------------------------------------------------
+// Solver: one or more H-slabs of one tensor on this process' device.
+// ---------------------------------------------------------------------------
+struct Slab {
+  int64_t row0 = 0, rows = 0;   // own rows [row0, row0 + rows)
+  Geo g{};
+  int64_t m_own = 0;            // rows * W * T
+  int64_t halo_elems = 0;       // (kh-1) * W * T (slab mode)
+  DBuf<float> Lt, adj, pm, mask, W;
+  DBuf<double> L, V;
+};
+
+struct Solver {
+  Problem p;
+  int device = 0;
+  bool sharded = false;          // slab mode with explicit halos
+  int G = 1, world = 1, rank = 0, local = 1;
+  std::vector<Slab> slabs;
+  std::unique_ptr<Comm> comm;    // cross-process exchange (world > 1)
+  DBuf<float> Krm, KT, cvec;
+  DBuf<double> red;              // norm2 (kp) | update slot (8)
+  DBuf<double> theta;
+  DBuf<IterState> st;
+  DBuf<IterStats> stats;
+  DBuf<double> Mstage, maskstage;  // f64 staging of the current problem
+  DBuf<float> xfer_send, xfer_recv;  // cross-process halo buffers
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
+  // host copies of the basis (validation happens once at create)
+  std::vector<double> K;
+  // per-problem scalars (from upload)
+  bool uploaded = false;
+  double pm_absmax = 0, pm_norm2 = 0, pm_sum = 0;
+  int64_t observed = 0;
+  int64_t launches = 0;
+  bool profile = false;
+  double prof_ms[4] = {0, 0, 0, 0};
+
+  ~Solver() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (evs) cudaEventDestroy(evs);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+void solver_alloc(Solver& S) {
+  const Problem& p = S.p;
+  CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&S.ev0));
+  CK(cudaEventCreate(&S.ev1));
+  CK(cudaEventCreate(&S.evs));
+  set_smem_attrs();
+  const int64_t WT = p.dims[1] * p.dims[2];
+  for (auto& s : S.slabs) {
+    s.g = make_geo(p, s.rows, !S.sharded);
+    check_smem(fwd_smem(s.g));
+    check_smem(adj_smem(s.g));
+    s.m_own = s.rows * WT;
+    s.halo_elems = S.sharded ? (p.kd[0] - 1) * WT : 0;
+    s.Lt.alloc(s.m_own + s.halo_elems);
+    s.adj.alloc(s.m_own + s.halo_elems);
+    s.pm.alloc(s.m_own);
+    s.mask.alloc(s.m_own);
+    s.L.alloc(s.m_own);
+    s.V.alloc(s.m_own);
+    s.W.alloc(static_cast<size_t>(n_bricks(s.g)) * BM * p.kp);
+    CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
+  }
+  std::vector<float> Krm, KT;
+  pack_basis(p, S.K.data(), Krm, KT);
+  S.Krm.alloc(Krm.size());
+  S.KT.alloc(KT.size());
+  CK(cudaMemcpyAsync(S.Krm.p, Krm.data(), S.Krm.bytes(), cudaMemcpyHostToDevice, S.stream));
+  CK(cudaMemcpyAsync(S.KT.p, KT.data(), S.KT.bytes(), cudaMemcpyHostToDevice, S.stream));
+  S.cvec.alloc(p.kp);
+  S.red.alloc(p.kp + 8);
+  S.st.alloc(1);
+  int64_t mtot = p.m;
+  S.Mstage.alloc(mtot);
+  S.maskstage.alloc(mtot);
+  if (S.world > 1) {
+    S.xfer_send.alloc((p.kd[0] - 1) * WT + 1);
+    S.xfer_recv.alloc((p.kd[0] - 1) * WT + 1);
+  }
+  CK(cudaStreamSynchronize(S.stream));
+}
+
+// Upload: validation of solver.cpp:66-72 / tensor.hpp:115-121, host scalars.
+void solver_upload(Solver& S, const double* M, const double* mask) {
+  if (!M || !mask) invalid("solve: null input");
+  const int64_t m = S.p.m;
+  double amax = 0, n2 = 0, sum = 0;
+  int64_t obs = 0;
+  for (int64_t i = 0; i < m; ++i) {
+    const double mk = mask[i];
+    if (mk != 0.0 && mk != 1.0) invalid("SamplingMask: entries must be 0 or 1");
+    if (!std::isfinite(M[i])) invalid("solve: observations: non-finite tensor entries");
+    if (mk == 1.0) {
+      const double v = M[i];
+      amax = std::max(amax, std::fabs(v));
+      n2 += v * v;
+      sum += v;
+      ++obs;
+    }
+  }
+  if (obs == 0) invalid("solve: empty sampling set");
+  S.pm_absmax = amax;
+  S.pm_norm2 = n2;
+  S.pm_sum = sum;
+  S.observed = obs;
+  CK(cudaMemcpyAsync(S.Mstage.p, M, m * sizeof(double), cudaMemcpyHostToDevice, S.stream));
+  CK(cudaMemcpyAsync(S.maskstage.p, mask, m * sizeof(double), cudaMemcpyHostToDevice,
+                     S.stream));
+  CK(cudaStreamSynchronize(S.stream));
+  S.uploaded = true;
+}
+
+// L~ halo exchange: slab g's last kh-1 own rows -> slab g+1's halo rows.
+void exchange_lt(Solver& S) {
+  if (!S.sharded) return;
+  const size_t he = S.slabs[0].halo_elems;
+  if (he == 0) return;
+  const int nl = static_cast<int>(S.slabs.size());
+  if (S.world == 1) {
+    for (int i = 0; i < nl; ++i) {
+      const Slab& src = S.slabs[i];
+      Slab& dst = S.slabs[(i + 1) % nl];
+      CK(cudaMemcpyAsync(dst.Lt.p, src.Lt.p + src.m_own, he * sizeof(float),
+                         cudaMemcpyDeviceToDevice, S.stream));
+    }
+    return;
+  }
+  // local neighbours first, then the process boundary through the comm.
+  for (int i = 0; i + 1 < nl; ++i)
+    CK(cudaMemcpyAsync(S.slabs[i + 1].Lt.p, S.slabs[i].Lt.p + S.slabs[i].m_own,
+                       he * sizeof(float), cudaMemcpyDeviceToDevice, S.stream));
+  const Slab& last = S.slabs[nl - 1];
+  S.comm->shift_forward(last.Lt.p + last.m_own, S.slabs[0].Lt.p, he, S.stream);
+}
+
+// Adjoint reverse halo: slab g's halo partials -> added to slab g-1's last rows.
+void exchange_adj(Solver& S) {
+  if (!S.sharded) return;
+  const int64_t he = S.slabs[0].halo_elems;
+  if (he == 0) return;
+  const int nl = static_cast<int>(S.slabs.size());
+  auto add = [&](float* dst, float* src) {
+    icnnm_dev::icnnm_add_rows<<<grid_for(he, 256), 256, 0, S.stream>>>(he, dst, src);
+    CKL();
+    ++S.launches;
+  };
+  if (S.world == 1) {
+    for (int i = 0; i < nl; ++i) {
+      Slab& src = S.slabs[i];
+      Slab& dst = S.slabs[(i + nl - 1) % nl];
+      add(dst.adj.p + dst.m_own, src.adj.p);
+    }
+    return;
+  }
+  for (int i = nl - 1; i >= 1; --i) {
+    Slab& src = S.slabs[i];
+    Slab& dst = S.slabs[i - 1];
+    add(dst.adj.p + dst.m_own, src.adj.p);
+  }
+  // slab 0's partials go to the previous process; ours come from the next.
+  Slab& first = S.slabs[0];
+  Slab& last = S.slabs[nl - 1];
+  S.comm->shift_backward(first.adj.p, S.xfer_recv.p, he, S.stream);
+  CK(cudaMemsetAsync(first.adj.p, 0, he * sizeof(float), S.stream));
+  add(last.adj.p + last.m_own, S.xfer_recv.p);
+}
+
+void launch_fwd(Solver& S, Slab& s, int mode) {
+  icnnm_dev::icnnm_fwd_ffma<<<static_cast<unsigned>(n_bricks(s.g)), 128, fwd_smem(s.g),
+                              S.stream>>>(s.g, s.Lt.p, S.Krm.p, s.W.p, S.cvec.p, S.st.p,
+                                          S.red.p, mode);
+  CKL();
+  ++S.launches;
+}
+void launch_adj(Solver& S, Slab& s) {
+  icnnm_dev::icnnm_adj_ffma<<<static_cast<unsigned>(n_bricks(s.g)), 128, adj_smem(s.g),
+                              S.stream>>>(s.g, s.W.p, S.KT.p, S.cvec.p, s.adj.p, S.st.p, 1);
+  CKL();
+  ++S.launches;
+}
+
+void allreduce_red(Solver& S) {
+  if (S.world > 1) S.comm->allreduce_sum(S.red.p, S.p.kp + 8, S.stream);
+}
+
+struct RunResult {
+  std::vector<IterStats> stats;
+  IterState st{};
+  double loop_ms = 0;
+  double run_ms = 0;
+};
+
+// One full solve of the staged problem (device-resident hot path).
+RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
+  if (!S.uploaded) invalid("solve: no problem uploaded");
+  const Problem& p = S.p;
+  const int iters = cfg.max_iters;
+  const double kd = static_cast<double>(p.k);
+  // theta schedule exactly as solver.cpp:88-91,126 (fp64, sequential).
+  std::vector<double> th(iters + 1);
+  double t0 = cfg.has_theta0 ? cfg.theta0 : 1e-2 * S.pm_absmax * kd;
+  if (t0 <= 0) t0 = 1e-2;
+  t0 = std::min(t0, cfg.theta_max);
+  th[0] = t0;
+  for (int i = 1; i <= iters; ++i) th[i] = std::min(th[i - 1] * cfg.theta_growth, cfg.theta_max);
+  double res_scale = std::sqrt(kd) * std::sqrt(S.pm_norm2);
+  if (res_scale == 0) res_scale = 1.0;
+  const double mean = S.pm_sum / static_cast<double>(S.observed);
+
+  S.theta.alloc(iters + 1);
+  S.stats.alloc(iters);
+  CK(cudaEventRecord(S.evs, S.stream));
+  CK(cudaMemcpyAsync(S.theta.p, th.data(), th.size() * sizeof(double), cudaMemcpyHostToDevice,
+                     S.stream));
+  CK(cudaMemsetAsync(S.stats.p, 0, S.stats.bytes(), S.stream));
+  CK(cudaMemsetAsync(S.red.p, 0, S.red.bytes(), S.stream));
+  IterState st0{};
+  st0.active = 1;
+  st0.max_iters = iters;
+  CK(cudaMemcpyAsync(S.st.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, S.stream));
+  S.launches = 0;
+
+  const int64_t WT = p.dims[1] * p.dims[2];
+  for (auto& s : S.slabs) {
+    const int64_t off = s.row0 * WT;
+    icnnm_dev::icnnm_setup<<<grid_for(s.m_own, 256), 256, 0, S.stream>>>(
+        s.m_own, S.Mstage.p + off, S.maskstage.p + off, cfg.init_fill == ICNNM_INIT_MEAN,
+        mean, s.pm.p, s.mask.p, s.L.p, s.V.p, s.Lt.p + s.halo_elems);
+    CKL();
+    ++S.launches;
+    CK(cudaMemsetAsync(s.W.p, 0, s.W.bytes(), S.stream));
+    CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
+  }
+  exchange_lt(S);
+  for (auto& s : S.slabs) launch_fwd(S, s, 0);
+  allreduce_red(S);
+
+  // One ADMM iteration as a graph: coef -> adjoint -> update -> forward.
+  const double floor_rel = 1e-5;
+  auto iteration = [&]() {
+    icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
+                                                    S.stats.p, p.k, p.kp, kd, res_scale,
+                                                    cfg.tol_primal, cfg.tol_change, floor_rel);
+    CKL();
+    for (auto& s : S.slabs) launch_adj(S, s);
+    exchange_adj(S);
+    for (auto& s : S.slabs) {
+      icnnm_dev::icnnm_update<<<grid_for(s.m_own, 256, 148 * 8), 256, 0, S.stream>>>(
+          s.m_own, S.st.p, cfg.lambda, kd, s.adj.p + s.halo_elems, s.L.p, s.V.p, s.pm.p,
+          s.mask.p, s.Lt.p + s.halo_elems, S.red.p + p.kp);
+      CKL();
+    }
+    exchange_lt(S);
+    for (auto& s : S.slabs) launch_fwd(S, s, 1);
+    allreduce_red(S);
+  };
+
+  const int64_t setup_launches = S.launches;
+  CK(cudaEventRecord(S.ev0, S.stream));
+  if (S.profile) {
+    // Per-family timing (serialised, events between launches; diagnostics).
+    cudaEvent_t e[5];
+    for (auto& x : e) CK(cudaEventCreate(&x));
+    double acc[4] = {0, 0, 0, 0};
+    for (int it = 0; it < iters; ++it) {
+      CK(cudaEventRecord(e[0], S.stream));
+      icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
+                                                      S.stats.p, p.k, p.kp, kd, res_scale,
+                                                      cfg.tol_primal, cfg.tol_change,
+                                                      floor_rel);
+      CK(cudaEventRecord(e[1], S.stream));
+      for (auto& s : S.slabs) launch_adj(S, s);
+      exchange_adj(S);
+      CK(cudaEventRecord(e[2], S.stream));
+      for (auto& s : S.slabs) {
+        icnnm_dev::icnnm_update<<<grid_for(s.m_own, 256, 148 * 8), 256, 0, S.stream>>>(
+            s.m_own, S.st.p, cfg.lambda, kd, s.adj.p + s.halo_elems, s.L.p, s.V.p, s.pm.p,
+            s.mask.p, s.Lt.p + s.halo_elems, S.red.p + p.kp);
+      }
+      exchange_lt(S);
+      CK(cudaEventRecord(e[3], S.stream));
+      for (auto& s : S.slabs) launch_fwd(S, s, 1);
+      allreduce_red(S);
+      CK(cudaEventRecord(e[4], S.stream));
+      CK(cudaEventSynchronize(e[4]));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e[0], e[1])); acc[3] += ms;
+      CK(cudaEventElapsedTime(&ms, e[1], e[2])); acc[1] += ms;
+      CK(cudaEventElapsedTime(&ms, e[2], e[3])); acc[2] += ms;
+      if (it < iters - 1) { CK(cudaEventElapsedTime(&ms, e[3], e[4])); acc[0] += ms; }
+    }
+    S.prof_ms[0] = iters > 1 ? acc[0] / (iters - 1) : 0;
+    S.prof_ms[1] = acc[1] / iters;
+    S.prof_ms[2] = acc[2] / iters;
+    S.prof_ms[3] = acc[3] / iters;
+    for (auto& x : e) cudaEventDestroy(x);
+  } else {
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    const int64_t before = S.launches;
+    CK(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeThreadLocal));
+    iteration();
+    CK(cudaStreamEndCapture(S.stream, &graph));
+    const int64_t per_iter = S.launches - before + 1 /*coef*/ +
+                             static_cast<int64_t>(S.slabs.size()) /*update*/;
+    S.launches = before;
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    const bool may_stop = !(cfg.tol_primal <= 1e-200 && cfg.tol_change <= 1e-200);
+    IterState* hst = nullptr;
+    CK(cudaMallocHost(&hst, sizeof(IterState)));
+    for (int it = 0; it < iters; ++it) {
+      CK(cudaGraphLaunch(exec, S.stream));
+      S.launches += per_iter;
+      if (may_stop && (it % 32) == 31) {
+        CK(cudaMemcpyAsync(hst, S.st.p, sizeof(IterState), cudaMemcpyDeviceToHost, S.stream));
+        CK(cudaStreamSynchronize(S.stream));
+        if (!hst->active) break;
+      }
+    }
+    cudaFreeHost(hst);
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+  }
+  // final coef: moves the last update slot into stats, evaluates the stop test.
+  icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
+                                                  S.stats.p, p.k, p.kp, kd, res_scale,
+                                                  cfg.tol_primal, cfg.tol_change, floor_rel);
+  CKL();
+  ++S.launches;
+  CK(cudaEventRecord(S.ev1, S.stream));
+  RunResult R;
+  R.stats.resize(iters);
+  CK(cudaMemcpyAsync(R.stats.data(), S.stats.p, S.stats.bytes(), cudaMemcpyDeviceToHost,
+                     S.stream));
+  CK(cudaMemcpyAsync(&R.st, S.st.p, sizeof(IterState), cudaMemcpyDeviceToHost, S.stream));
+  CK(cudaStreamSynchronize(S.stream));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, S.ev0, S.ev1));
+  R.loop_ms = ms;
+  CK(cudaEventElapsedTime(&ms, S.evs, S.ev1));
+  R.run_ms = ms;
+  (void)setup_launches;
+  return R;
+}
+
+// Report of solver.cpp:128-139 from the device statistics.
+void fill_report(const Solver& S, const icnnm_solver_config& cfg, const RunResult& R,
+                 icnnm_solve_report* rep, double wall_s) {
+  if (!rep) return;
+  const double kd = static_cast<double>(S.p.k);
+  double res_scale = std::sqrt(kd) * std::sqrt(S.pm_norm2);
+  if (res_scale == 0) res_scale = 1.0;
+  const int executed = R.st.next_it;
+  int n = 0;
+  int term = ICNNM_TERM_MAX_ITERS;
+  for (int it = 0; it < executed; ++it) {
+    const IterStats& q = R.stats[it];
+    const double gap2 = q.z2 - 2.0 * q.ip + kd * q.ln2;
+    const double res = std::sqrt(std::max(gap2, 0.0)) / res_scale;
+    const bool res_ok = gap2 > 1e-5 * (q.z2 + kd * q.ln2);
+    const double lc = std::sqrt(q.dl2) / std::max(std::sqrt(q.l2o), 1e-300);
+    if (rep->objective) rep->objective[it] = q.l21 + 0.5 * cfg.lambda * kd * q.fit;
+    if (rep->primal_residual) rep->primal_residual[it] = res;
+    if (rep->l_change) rep->l_change[it] = lc;
+    n = it + 1;
+    if ((res_ok && res < cfg.tol_primal) || lc < cfg.tol_change) {
+      term = ICNNM_TERM_CONVERGED;
+      break;
+    }
+  }
+  rep->iterations = n;
+  rep->termination = term;
+  rep->wall_time_seconds = wall_s;
+  rep->loop_seconds = R.loop_ms * 1e-3;
+  rep->device_seconds = R.run_ms * 1e-3;
+}
+
+void solver_download(Solver& S, double* L_out) {
+  if (!L_out) invalid("null output");
+  int64_t off = 0;
+  for (auto& s : S.slabs) {
+    CK(cudaMemcpyAsync(L_out + off, s.L.p, s.m_own * sizeof(double), cudaMemcpyDeviceToHost,
+                       S.stream));
+    off += s.m_own;
+  }
+  CK(cudaStreamSynchronize(S.stream));
+}
+
+}  // namespace icnnm_host
+
+using namespace icnnm_host;
+
+struct icnnm_solver_s {
+  Solver S;
+};
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+void icnnm_default_config(icnnm_solver_config* c) {
+  if (!c) return;
+  c->lambda = 1000.0;
+  c->has_theta0 = 0;
+  c->theta0 = 0.0;
+  c->theta_growth = 1.05;
+  c->theta_max = 1e10;
+  c->max_iters = 1000;
+  c->tol_primal = 1e-7;
+  c->tol_change = 1e-8;
+  c->rank_tol = 1e-8;
+  c->init_fill = ICNNM_INIT_ZERO;
+  c->engine = ICNNM_ENGINE_FFMA;
+}
+
+int icnnm_validate_config(const icnnm_solver_config* cfg) {
+  return guard([&] { validate_cfg(cfg); });
+}
+
+const char* icnnm_last_error(void) { return g_last_error.c_str(); }
+
+const char* icnnm_version(void) { return "icnnm_b200 0.1 (sm_100a)"; }
+
+int icnnm_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int icnnm_solver_create(int order, const int64_t* dims, const int64_t* kdims,
+                        const double* K_colmajor, const double* eigenvalues, int device,
+                        icnnm_solver_t* out) {
+  return guard([&] {
+    if (!out) invalid("null handle pointer");
+    *out = nullptr;
+    Problem p = make_problem(order, dims, kdims);
+    validate_basis(p.k, K_colmajor, eigenvalues);
+    DeviceScope ds(device);
+    auto h = std::make_unique<icnnm_solver_s>();
+    Solver& S = h->S;
+    S.p = p;
+    S.device = device;
+    S.K.assign(K_colmajor, K_colmajor + static_cast<size_t>(p.k) * p.k);
+    S.slabs.resize(1);
+    S.slabs[0].row0 = 0;
+    S.slabs[0].rows = p.dims[0];
+    solver_alloc(S);
+    *out = h.release();
+  });
+}
+
+int icnnm_solver_upload(icnnm_solver_t h, const double* M, const double* mask) {
+  return guard([&] {
+    if (!h) invalid("null handle");
+    DeviceScope ds(h->S.device);
+    solver_upload(h->S, M, mask);
+  });
+}
+
+int icnnm_solver_run(icnnm_solver_t h, const icnnm_solver_config* cfg,
+                     icnnm_solve_report* report) {
+  return guard([&] {
+    if (!h) invalid("null handle");
+    validate_cfg(cfg);
+    if (cfg->engine != ICNNM_ENGINE_FFMA)
+      invalid("icnnm_b200: engine TF32X3 is not available in this build");
+    DeviceScope ds(h->S.device);
+    auto t0 = std::chrono::steady_clock::now();
+    RunResult R = solver_run(h->S, *cfg);
+    double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    fill_report(h->S, *cfg, R, report, wall);
+  });
+}
+
+int icnnm_solver_download(icnnm_solver_t h, double* L_out) {
+  return guard([&] {
+    if (!h) invalid("null handle");
+    DeviceScope ds(h->S.device);
+    solver_download(h->S, L_out);
+  });
+}
+
+int64_t icnnm_solver_last_launches(icnnm_solver_t h) { return h ? h->S.launches : -1; }
+
+int64_t icnnm_solver_device_bytes(icnnm_solver_t h) {
+  if (!h) return -1;
+  const Solver& S = h->S;
+  int64_t b = S.Krm.bytes() + S.KT.bytes() + S.cvec.bytes() + S.red.bytes() + S.theta.bytes() +
+              S.stats.bytes() + S.Mstage.bytes() + S.maskstage.bytes();
+  for (auto& s : S.slabs)
+    b += s.Lt.bytes() + s.adj.bytes() + s.pm.bytes() + s.mask.bytes() + s.W.bytes() +
+         s.L.bytes() + s.V.bytes();
+  return b;
+}
+
+int icnnm_solver_set_profile(icnnm_solver_t h, int enable) {
+  return guard([&] {
+    if (!h) invalid("null handle");
+    h->S.profile = enable != 0;
+  });
+}
+
+int icnnm_solver_kernel_times(icnnm_solver_t h, double* out) {
+  return guard([&] {
+    if (!h || !out) invalid("null argument");
+    for (int i = 0; i < 4; ++i) out[i] = h->S.prof_ms[i];
+  });
+}
+
+void icnnm_solver_destroy(icnnm_solver_t h) {
+  if (!h) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->S.device);
+  delete h;
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+int icnnm_cuda_solve(int order, const int64_t* dims, const double* M_obs, const double* mask,
+                     const int64_t* kdims, const double* K_colmajor, const double* eigenvalues,
+                     const icnnm_solver_config* cfg, int device, double* L_out,
+                     icnnm_solve_report* report) {
+  return guard([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    validate_cfg(cfg);
+    if (cfg->engine != ICNNM_ENGINE_FFMA)
+      invalid("icnnm_b200: engine TF32X3 is not available in this build");
+    Problem p = make_problem(order, dims, kdims);
+    if (!L_out) invalid("null output");
+    validate_basis(p.k, K_colmajor, eigenvalues);
+    DeviceScope ds(device);
+    Solver S;
+    S.p = p;
+    S.device = device;
+    S.K.assign(K_colmajor, K_colmajor + static_cast<size_t>(p.k) * p.k);
+    S.slabs.resize(1);
+    S.slabs[0].rows = p.dims[0];
+    solver_alloc(S);
+    solver_upload(S, M_obs, mask);
+    RunResult R = solver_run(S, *cfg);
+    solver_download(S, L_out);
+    double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    fill_report(S, *cfg, R, report, wall);
+  });
+}
+
+// --------------------------------------------------------------------------
+// Operator level
+// --------------------------------------------------------------------------
+int icnnm_cuda_conv_forward(int order, const int64_t* dims, const double* L,
+                            const int64_t* kdims, const double* K_colmajor, int device,
+                            double* out) {
+  return guard([&] {
+    Problem p = make_problem(order, dims, kdims);
+    if (!L || !K_colmajor || !out) invalid("null argument");
+    DeviceScope ds(device);
+    set_smem_attrs();
+    Geo g = make_geo(p, p.dims[0], true);
+    check_smem(fwd_smem(g));
+    std::vector<float> Krm, KT;
+    pack_basis(p, K_colmajor, Krm, KT);
+    std::vector<float> Lf(L, L + p.m);
+    DBuf<float> dL(p.m), dK(Krm.size()), dW(static_cast<size_t>(n_bricks(g)) * BM * p.kp);
+    DBuf<double> dn(p.kp);
+    CK(cudaMemcpy(dL.p, Lf.data(), dL.bytes(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dK.p, Krm.data(), dK.bytes(), cudaMemcpyHostToDevice));
+    CK(cudaMemset(dn.p, 0, dn.bytes()));
+    icnnm_dev::icnnm_fwd_ffma<<<static_cast<unsigned>(n_bricks(g)), 128, fwd_smem(g)>>>(
+        g, dL.p, dK.p, dW.p, nullptr, nullptr, dn.p, 0);
+    CKL();
+    std::vector<float> Wh(dW.n);
+    CK(cudaMemcpy(Wh.data(), dW.p, dW.bytes(), cudaMemcpyDeviceToHost));
+    const int64_t H = p.dims[0], W = p.dims[1], T = p.dims[2];
+    for (int64_t h = 0; h < H; ++h)
+      for (int64_t w = 0; w < W; ++w)
+        for (int64_t t = 0; t < T; ++t) {
+          const int64_t flat = (h * W + w) * T + t;
+          const float* row = Wh.data() + brick_row(g, h, w, t) * p.kp;
+          for (int j = 0; j < p.k; ++j) out[static_cast<size_t>(j) * p.m + flat] = row[j];
+        }
+  });
+}
+
+int icnnm_cuda_conv_adjoint(int order, const int64_t* dims, const int64_t* kdims,
+                            const double* Wcm, int device, double* out) {
+  return guard([&] {
+    Problem p = make_problem(order, dims, kdims);
+    if (!Wcm || !out) invalid("null argument");
+    DeviceScope ds(device);
+    set_smem_attrs();
+    Geo g = make_geo(p, p.dims[0], true);
+    check_smem(adj_smem(g));
+    // W (m x k column-major) -> brick-ordered rows; K = I.
+    std::vector<float> Wb(static_cast<size_t>(n_bricks(g)) * BM * p.kp, 0.f);
+    const int64_t H = p.dims[0], Wd = p.dims[1], T = p.dims[2];
+    for (int64_t h = 0; h < H; ++h)
+      for (int64_t w = 0; w < Wd; ++w)
+        for (int64_t t = 0; t < T; ++t) {
+          const int64_t flat = (h * Wd + w) * T + t;
+          float* row = Wb.data() + brick_row(g, h, w, t) * p.kp;
+          for (int j = 0; j < p.k; ++j) row[j] = static_cast<float>(Wcm[static_cast<size_t>(j) * p.m + flat]);
+        }
+    std::vector<float> I(static_cast<size_t>(p.kp) * p.kp, 0.f);
+    for (int j = 0; j < p.k; ++j) I[static_cast<size_t>(j) * p.kp + j] = 1.f;
+    DBuf<float> dW(Wb.size()), dI(I.size()), dadj(p.m);
+    CK(cudaMemcpy(dW.p, Wb.data(), dW.bytes(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dI.p, I.data(), dI.bytes(), cudaMemcpyHostToDevice));
+    CK(cudaMemset(dadj.p, 0, dadj.bytes()));
+    icnnm_dev::icnnm_adj_ffma<<<static_cast<unsigned>(n_bricks(g)), 128, adj_smem(g)>>>(
+        g, dW.p, dI.p, nullptr, dadj.p, nullptr, 0);
+    CKL();
+    std::vector<float> a(p.m);
+    CK(cudaMemcpy(a.data(), dadj.p, dadj.bytes(), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < p.m; ++i) out[i] = a[i];
+  });
+}
+
+int icnnm_cuda_prox_l21(int64_t rows, int64_t cols, const double* W, double tau, int device,
+                        double* Z) {
+  return guard([&] {
+    if (tau < 0) invalid("prox_l21: tau must be >= 0");
+    if (rows < 0 || cols < 0) invalid("prox_l21: negative shape");
+    if (rows == 0 || cols == 0) return;
+    if (!W || !Z) invalid("null argument");
+    DeviceScope ds(device);
+    DBuf<double> dW(rows * cols), dZ(rows * cols), dn(cols);
+    CK(cudaMemcpy(dW.p, W, dW.bytes(), cudaMemcpyHostToDevice));
+    CK(cudaMemset(dn.p, 0, dn.bytes()));
+    icnnm_dev::icnnm_colnorm2<<<static_cast<unsigned>(cols), 256>>>(rows, cols, dW.p, dn.p);
+    CKL();
+    icnnm_dev::icnnm_colscale<<<grid_for(rows * cols, 256), 256>>>(rows, cols, dW.p, dn.p, tau,
+                                                                  dZ.p);
+    CKL();
+    CK(cudaMemcpy(Z, dZ.p, dZ.bytes(), cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"
+
+namespace icnnm_host {
+
+// R lags (fp64) of one tensor, accumulated into dR.
+void gram_lags_accumulate(const Problem& p, const double* dX, double* dR, cudaStream_t s) {
+  const int H = static_cast<int>(p.dims[0]), W = static_cast<int>(p.dims[1]),
+            T = static_cast<int>(p.dims[2]);
+  const int kh = static_cast<int>(p.kd[0]), kw = static_cast<int>(p.kd[1]),
+            kt = static_cast<int>(p.kd[2]);
+  const int nl = (2 * kw - 1) * (2 * kt - 1);
+  if (nl > 256 * icnnm_dev::GRAM_LPT_HOST)
+    invalid("icnnm_b200: kernel (kw, kt) too large for the Gram kernel");
+  int bt = T >= 16 ? 16 : (T >= 8 ? 8 : T);
+  int bw = W >= 8 ? 8 : W;
+  int bh = H >= 2 ? 2 : 1;
+  size_t smem = (static_cast<size_t>(bh) * bw * bt +
+                 static_cast<size_t>(bh) * (bw + 2 * (kw - 1)) * (bt + 2 * (kt - 1))) *
+                sizeof(double);
+  check_smem(smem);
+  const int nb = ((H + bh - 1) / bh) * ((W + bw - 1) / bw) * ((T + bt - 1) / bt);
+  dim3 grid(2 * kh - 1, std::max(1, std::min(nb, 1184 / (2 * kh - 1) + 1)));
+  icnnm_dev::icnnm_gram_lags<<<grid, 256, smem, s>>>(H, W, T, kh, kw, kt, bh, bw, bt, dX, dR);
+  CKL();
+}
+
+// G[s,t] = R[(s - t)] over the kernel box (spectral.cpp:62-79).
+void gram_from_lags(const Problem& p, const std::vector<double>& R, double* G) {
+  const int kh = static_cast<int>(p.kd[0]), kw = static_cast<int>(p.kd[1]),
+            kt = static_cast<int>(p.kd[2]);
+  const int k = p.k;
+  const int nlw = 2 * kw - 1, nlt = 2 * kt - 1;
+  for (int s = 0; s < k; ++s) {
+    const int sh = s / (kw * kt), sw = (s / kt) % kw, st = s % kt;
+    for (int t = 0; t < k; ++t) {
+      const int th = t / (kw * kt), tw = (t / kt) % kw, tt = t % kt;
+      const int dh = sh - th + kh - 1, dw = sw - tw + kw - 1, dt = st - tt + kt - 1;
+      G[static_cast<size_t>(t) * k + s] = R[(static_cast<size_t>(dh) * nlw + dw) * nlt + dt];
+    }
+  }
+}
+
+}  // namespace icnnm_host
+
+extern "C" int icnnm_host_symeig_impl(int n, const double* G, double* evals, double* evecs);
+
+extern "C" {
+
+int icnnm_cuda_conv_gram(int order, const int64_t* dims, const double* L, const int64_t* kdims,
+                         int device, double* G) {
+  return guard([&] {
+    Problem p = make_problem(order, dims, kdims);
+    if (!L || !G) invalid("null argument");
+    DeviceScope ds(device);
+    set_smem_attrs();
+    const size_t nl = static_cast<size_t>(2 * p.kd[0] - 1) * (2 * p.kd[1] - 1) * (2 * p.kd[2] - 1);
+    DBuf<double> dX(p.m), dR(nl);
+    CK(cudaMemcpy(dX.p, L, dX.bytes(), cudaMemcpyHostToDevice));
+    CK(cudaMemset(dR.p, 0, dR.bytes()));
+    gram_lags_accumulate(p, dX.p, dR.p, 0);
+    std::vector<double> R(nl);
+    CK(cudaMemcpy(R.data(), dR.p, dR.bytes(), cudaMemcpyDeviceToHost));
+    gram_from_lags(p, R, G);
+  });
+}
+
+int icnnm_cuda_learn_basis(int n_refs, int order, const int64_t* dims, const double* const* refs,
+                           const int64_t* kdims, int device, double* K_out, double* evals_out,
+                           int* degenerate) {
+  return guard([&] {
+    if (n_refs <= 0 || !refs) invalid("learn_ensemble_basis: empty reference list");
+    Problem p = make_problem(order, dims, kdims);
+    if (!K_out || !evals_out) invalid("null argument");
+    DeviceScope ds(device);
+    set_smem_attrs();
+    const size_t nl = static_cast<size_t>(2 * p.kd[0] - 1) * (2 * p.kd[1] - 1) * (2 * p.kd[2] - 1);
+    DBuf<double> dX(p.m), dR(nl);
+    CK(cudaMemset(dR.p, 0, dR.bytes()));
+    for (int b = 0; b < n_refs; ++b) {
+      if (!refs[b]) invalid("learn_ensemble_basis: null reference");
+      CK(cudaMemcpy(dX.p, refs[b], dX.bytes(), cudaMemcpyHostToDevice));
+      gram_lags_accumulate(p, dX.p, dR.p, 0);
+    }
+    std::vector<double> R(nl);
+    CK(cudaMemcpy(R.data(), dR.p, dR.bytes(), cudaMemcpyDeviceToHost));
+    const int k = p.k;
+    std::vector<double> G(static_cast<size_t>(k) * k);
+    gram_from_lags(p, R, G.data());
+    double gmax = 0;
+    for (double v : G) gmax = std::max(gmax, std::fabs(v));
+    if (gmax == 0.0) {
+      std::fill(K_out, K_out + static_cast<size_t>(k) * k, 0.0);
+      for (int i = 0; i < k; ++i) K_out[static_cast<size_t>(i) * k + i] = 1.0;
+      std::fill(evals_out, evals_out + k, 0.0);
+      if (degenerate) *degenerate = 1;
+      return;
+    }
+    int rc = icnnm_host_symeig_impl(k, G.data(), evals_out, K_out);
+    if (rc != 0) fail(ICNNM_RUNTIME_ERROR, "eigensolver did not converge");
+    // psd_eig_sorted (spectral.cpp:87-98): clamp >= 0, sign fix, sigma = sqrt.
+    for (int i = 0; i < k; ++i) {
+      evals_out[i] = std::sqrt(std::max(0.0, evals_out[i]));
+      double* col = K_out + static_cast<size_t>(i) * k;
+      for (int r = 0; r < k; ++r) {
+        if (std::fabs(col[r]) > 1e-12) {
+          if (col[r] < 0)
+            for (int q = 0; q < k; ++q) col[q] = -col[q];
+          break;
+        }
+      }
+    }
+    if (degenerate) *degenerate = 0;
+  });
+}
+
+int icnnm_host_symeig(int n, const double* G, double* evals, double* evecs) {
+  return guard([&] {
+    if (n < 1 || !G || !evals || !evecs) invalid("symeig: bad arguments");
+    if (icnnm_host_symeig_impl(n, G, evals, evecs) != 0)
+      fail(ICNNM_RUNTIME_ERROR, "eigensolver did not converge");
+  });
+}
+
+int icnnm_cuda_objective(int order, const int64_t* dims, const double* L, const double* M,
+                         const double* mask, const int64_t* kdims, const double* K, double lambda,
+                         int device, double* out) {
+  return guard([&] {
+    Problem p = make_problem(order, dims, kdims);
+    if (!L || !M || !mask || !K || !out) invalid("null argument");
+    validate_basis(p.k, K, nullptr);
+    for (int64_t i = 0; i < p.m; ++i)
+      if (mask[i] != 0.0 && mask[i] != 1.0) invalid("SamplingMask: entries must be 0 or 1");
+    DeviceScope ds(device);
+    set_smem_attrs();
+    Geo g = make_geo(p, p.dims[0], true);
+    std::vector<float> Krm, KT;
+    pack_basis(p, K, Krm, KT);
+    std::vector<float> Lf(L, L + p.m);
+    DBuf<float> dL(p.m), dK(Krm.size()), dW(static_cast<size_t>(n_bricks(g)) * BM * p.kp);
+    DBuf<double> dn(p.kp);
+    CK(cudaMemcpy(dL.p, Lf.data(), dL.bytes(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dK.p, Krm.data(), dK.bytes(), cudaMemcpyHostToDevice));
+    CK(cudaMemset(dn.p, 0, dn.bytes()));
+    icnnm_dev::icnnm_fwd_ffma<<<static_cast<unsigned>(n_bricks(g)), 128, fwd_smem(g)>>>(
+        g, dL.p, dK.p, dW.p, nullptr, nullptr, dn.p, 0);
+    CKL();
+    std::vector<double> n2(p.kp);
+    CK(cudaMemcpy(n2.data(), dn.p, dn.bytes(), cudaMemcpyDeviceToHost));
+    double col_sum = 0;
+    for (int j = 0; j < p.k; ++j) col_sum += std::sqrt(n2[j]);
+    double fit = 0;
+    for (int64_t i = 0; i < p.m; ++i) {
+      const double d = (L[i] - M[i]) * mask[i];
+      fit += d * d;
+    }
+    *out = col_sum + 0.5 * lambda * static_cast<double>(p.k) * fit;
+  });
+}
+
+// --------------------------------------------------------------------------
+// Sharded solve
+// --------------------------------------------------------------------------
+int icnnm_shard_plan(int64_t H, int G, int64_t kh, int g, int64_t* start, int64_t* count) {
+  return guard([&] {
+    if (G < 1 || g < 0 || g >= G || H < 1 || kh < 1) invalid("shard plan: bad arguments");
+    const int64_t base = H / G, extra = H % G;
+    const int64_t s = g * base + std::min<int64_t>(g, extra);
+    const int64_t c = base + (g < extra ? 1 : 0);
+    if (c < 1 || c < kh - 1) invalid("shard plan: slab thinner than the kernel halo (kh-1 rows)");
+    if (start) *start = s;
+    if (count) *count = c;
+  });
+}
+
+int icnnm_dist_unique_id(char* out128) {
+  return guard([&] {
+    if (!out128) invalid("null argument");
+    comm_unique_id(out128);
+  });
+}
+
+int icnnm_sharded_solve(int order, const int64_t* dims, const double* M_obs, const double* mask,
+                        const int64_t* kdims, const double* K_colmajor,
+                        const icnnm_solver_config* cfg, int local_slabs, int world, int rank,
+                        const char* nccl_id128, int device, double* L_out, int64_t* row0_out,
+                        int64_t* nrows_out, icnnm_solve_report* report) {
+  return guard([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    validate_cfg(cfg);
+    if (cfg->engine != ICNNM_ENGINE_FFMA)
+      invalid("icnnm_b200: engine TF32X3 is not available in this build");
+    Problem p = make_problem(order, dims, kdims);
+    if (local_slabs < 1 || world < 1 || rank < 0 || rank >= world)
+      invalid("sharded solve: bad slab / rank arguments");
+    if (!L_out) invalid("null output");
+    validate_basis(p.k, K_colmajor, nullptr);
+    const int G = local_slabs * world;
+    DeviceScope ds(device);
+    Solver S;
+    S.p = p;
+    S.device = device;
+    S.sharded = true;
+    S.G = G;
+    S.world = world;
+    S.rank = rank;
+    S.local = local_slabs;
+    S.K.assign(K_colmajor, K_colmajor + static_cast<size_t>(p.k) * p.k);
+    S.slabs.resize(local_slabs);
+    for (int i = 0; i < local_slabs; ++i) {
+      int64_t s = 0, c = 0;
+      const int gi = rank * local_slabs + i;
+      if (icnnm_shard_plan(p.dims[0], G, p.kd[0], gi, &s, &c) != ICNNM_OK)
+        invalid(g_last_error);
+      S.slabs[i].row0 = s;
+      S.slabs[i].rows = c;
+    }
+    if (world > 1) {
+      if (!nccl_id128) invalid("sharded solve: NCCL unique id required for world > 1");
+      S.comm = comm_create(nccl_id128, world, rank);
+    }
+    solver_alloc(S);
+    solver_upload(S, M_obs, mask);
+    RunResult R = solver_run(S, *cfg);
+    solver_download(S, L_out);
+    if (row0_out) *row0_out = S.slabs[0].row0;
+    if (nrows_out) {
+      int64_t n = 0;
+      for (auto& s : S.slabs) n += s.rows;
+      *nrows_out = n;
+    }
+    double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    fill_report(S, *cfg, R, report, wall);
+  });
+}
+
+// --------------------------------------------------------------------------
+// Probe
+// --------------------------------------------------------------------------
+int icnnm_probe_ffma_tflops(int device, double* out) {
+  return guard([&] {
+    if (!out) invalid("null argument");
+    DeviceScope ds(device);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    DBuf<float> o(1);
+    const int iters = 1 << 16;
+    const int blocks = sms * 8, threads = 256;
+    icnnm_dev::icnnm_ffma_probe<<<blocks, threads>>>(o.p, 1024, 1.f);
+    CKL();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a));
+    icnnm_dev::icnnm_ffma_probe<<<blocks, threads>>>(o.p, iters, 1.f);
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 16.0 * iters * static_cast<double>(blocks) * threads;
+    *out = flops / (ms * 1e-3) / 1e12;
+  });
+}
+
+}  // extern "C"

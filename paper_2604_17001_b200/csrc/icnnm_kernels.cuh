@@ -1,0 +1,89 @@
+// Shared device-side declarations of the ICNNM hot-path kernels.
+//
+// Tensor geometry follows the reference's conventions
+// (/root/reference/proj/core/include/icnnm/tensor.hpp:64-68, fft.cpp:78-90):
+// row-major [H, W, T] (lower orders are padded with leading 1s), kernel taps
+// corner-anchored and flattened row-major over the (kh, kw, kt) box
+// (conv_op.cpp:42-44,94).  Forward:  T[i, j] = sum_s L[(i - s) mod dims] K[s, j].
+// Adjoint: out[i] = sum_s U[(i + s) mod dims, s].
+#pragma once
+#include <cstdint>
+
+namespace icnnm_dev {
+
+constexpr int BM = 128;   // voxels per tile (one brick)
+constexpr int BN = 64;    // output columns per N-tile
+constexpr int BK = 32;    // reduction chunk
+
+// Geometry of one launch.  The voxel tile is a brick (bh, bw, bt) with
+// bh*bw*bt == 128 and bt a multiple of 8; bricks tile the (H, W, T) box
+// (voxels outside the tensor are masked).  W rows are brick-ordered:
+// row = brick*128 + local voxel, so a CTA's 128 rows are contiguous.
+struct Geo {
+  int H, W, T;          // voxels owned by this launch (H = slab rows)
+  int kh, kw, kt;       // kernel box
+  int bh, bw, bt;       // brick
+  int nbh, nbw, nbt;    // bricks per axis
+  int HH, HW, HT;       // halo box = brick + kernel - 1
+  int k;                // taps
+  int kp;               // W / K columns padded to a multiple of BN
+  int ktp;              // taps padded to a multiple of BN
+  int Hsrc;             // rows of the source (L~) / target (adj) buffer
+  int hoff;             // buffer row = h + hoff   (h may be negative)
+  int wrapH;            // 1: periodic in H over Hsrc rows; 0: slab buffer
+};
+
+// Per-iteration scalars, written by the coefficient kernel and read by the
+// other kernels of the same iteration (stream order, no host round trip).
+struct IterState {
+  int it;          // current iteration
+  int next_it;     // iteration the next coef launch will start
+  int active;      // 0 once converged or max_iters reached
+  int converged;
+  int max_iters;
+  int pad0;
+  double theta;    // theta_it
+  double r;        // theta_it / theta_{it+1}
+};
+
+// Per-iteration reductions (fp64).
+struct IterStats {
+  double l21;   // sum_j max(0, n_j - 1/theta)      = ||Z||_{2,1}
+  double z2;    // sum_j (1-c_j)^2 n_j^2            = ||Z||_F^2
+  double dl2;   // ||L_{t+1} - L_t||^2
+  double l2o;   // ||L_t||^2
+  double fit;   // ||mask (L_{t+1} - M)||^2
+  double ip;    // <k L_t - V_t - adj_t, L_{t+1}>   (= <Z_t, A(L_{t+1})K>)
+  double ln2;   // ||L_{t+1}||^2
+  double pad;
+};
+
+}  // namespace icnnm_dev
+
+// Kernel declarations (defined in icnnm_kernels.cu; launched from the host
+// driver, which is a separate translation unit).
+namespace icnnm_dev {
+__global__ void icnnm_fwd_ffma(Geo g, const float* Lt, const float* Krm, float* Wm,
+                               const float* cvec, const IterState* st, double* norm2,
+                               int mode);
+__global__ void icnnm_adj_ffma(Geo g, const float* Wm, const float* KT, const float* cvec,
+                               float* adj, const IterState* st, int mode);
+__global__ void icnnm_coef(IterState* st, const double* theta, double* red, float* cvec,
+                           IterStats* stats, int k, int kp, double kd, double res_scale,
+                           double tol_p, double tol_c, double floor_rel);
+__global__ void icnnm_update(int64_t m, const IterState* st, double lambda, double kd,
+                             float* adj, double* L, double* V, const float* pm,
+                             const float* mask, float* Lt, double* slot);
+__global__ void icnnm_add_rows(int64_t n, float* dst, float* src);
+__global__ void icnnm_setup(int64_t m, const double* M, const double* msk, int mean_fill,
+                            double mean, float* pm, float* maskf, double* L, double* V,
+                            float* Lt);
+__global__ void icnnm_gram_lags(int H, int W, int T, int kh, int kw, int kt, int bh, int bw,
+                                int bt, const double* X, double* R);
+__global__ void icnnm_colnorm2(int64_t rows, int64_t cols, const double* W, double* out);
+__global__ void icnnm_colscale(int64_t rows, int64_t cols, const double* W, const double* n2,
+                               double tau, double* Z);
+__global__ void icnnm_f64_to_f32(int64_t n, const double* a, float* b);
+__global__ void icnnm_ffma_probe(float* out, int iters, float seed);
+constexpr int GRAM_LPT_HOST = 8;
+}  // namespace icnnm_dev
