@@ -145,6 +145,14 @@ int icnnm_cuda_conv_adjoint(int order, const int64_t* dims,
                             const int64_t* kdims, const double* W_colmajor,
                             int device, double* out);
 
+/* Same operators with an explicit GEMM engine (ICNNM_ENGINE_*). */
+int icnnm_cuda_conv_forward_ex(int order, const int64_t* dims, const double* L,
+                               const int64_t* kdims, const double* K_colmajor,
+                               int engine, int device, double* out_colmajor);
+int icnnm_cuda_conv_adjoint_ex(int order, const int64_t* dims,
+                               const int64_t* kdims, const double* W_colmajor,
+                               int engine, int device, double* out);
+
 /* prox_l21(W, tau) (solver.cpp:42-50), W rows x cols column-major. */
 int icnnm_cuda_prox_l21(int64_t rows, int64_t cols, const double* W_colmajor,
                         double tau, int device, double* Z_colmajor);

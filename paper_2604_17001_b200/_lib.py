@@ -87,6 +87,8 @@ SIGNATURES = {
     "icnnm_solver_destroy": (None, [C.c_void_p]),
     "icnnm_cuda_conv_forward": (C.c_int, [C.c_int, _lp, _dp, _lp, _dp, C.c_int, _dp]),
     "icnnm_cuda_conv_adjoint": (C.c_int, [C.c_int, _lp, _lp, _dp, C.c_int, _dp]),
+    "icnnm_cuda_conv_forward_ex": (C.c_int, [C.c_int, _lp, _dp, _lp, _dp, C.c_int, C.c_int, _dp]),
+    "icnnm_cuda_conv_adjoint_ex": (C.c_int, [C.c_int, _lp, _lp, _dp, C.c_int, C.c_int, _dp]),
     "icnnm_cuda_prox_l21": (C.c_int, [C.c_int64, C.c_int64, _dp, C.c_double, C.c_int, _dp]),
     "icnnm_cuda_conv_gram": (C.c_int, [C.c_int, _lp, _dp, _lp, C.c_int, _dp]),
     "icnnm_cuda_learn_basis": (C.c_int, [C.c_int, C.c_int, _lp, C.POINTER(_dp), _lp,

@@ -248,7 +248,10 @@ class Solver:
 class BasisConvolver:
     """BasisConvolver (conv_op.hpp:65-81): apply(L) = A_k(L) K (m x k)."""
 
-    def __init__(self, tensor_dims, kernel_shape, K, device: int = 0):
+    def __init__(self, tensor_dims, kernel_shape, K, device: int = 0, engine: str = "ffma"):
+        if engine not in ENGINES:
+            raise InvalidArgument("unknown engine")
+        self.engine = ENGINES[engine]
         self.dims = tuple(int(d) for d in tensor_dims)
         self.kernel_shape = tuple(int(d) for d in kernel_shape)
         k = int(np.prod(self.kernel_shape))
@@ -269,13 +272,13 @@ class BasisConvolver:
             raise InvalidArgument("BasisConvolver: tensor dims mismatch")
         m, k = L.size, self.k()
         out = np.empty((k, m))
-        check(lib().icnnm_cuda_conv_forward(L.ndim, lptr(_dims(self.dims)), dptr(L),
-                                            lptr(_dims(self.kernel_shape)), dptr(self._Kc),
-                                            self.device, dptr(out)))
+        check(lib().icnnm_cuda_conv_forward_ex(L.ndim, lptr(_dims(self.dims)), dptr(L),
+                                               lptr(_dims(self.kernel_shape)), dptr(self._Kc),
+                                               self.engine, self.device, dptr(out)))
         return out.T
 
 
-def conv_adjoint(W, kernel_shape, dims, device: int = 0) -> np.ndarray:
+def conv_adjoint(W, kernel_shape, dims, device: int = 0, engine: str = "ffma") -> np.ndarray:
     """conv_adjoint (conv_op.cpp:57-77): out[i] = sum_s W[(i+s) mod dims, s]."""
     dims = tuple(int(d) for d in dims)
     kernel_shape = tuple(int(d) for d in kernel_shape)
@@ -287,8 +290,10 @@ def conv_adjoint(W, kernel_shape, dims, device: int = 0) -> np.ndarray:
         raise InvalidArgument("conv_adjoint: W shape mismatch with dims/kernel")
     Wc = np.ascontiguousarray(W.T)
     out = np.empty(dims)
-    check(lib().icnnm_cuda_conv_adjoint(len(dims), lptr(_dims(dims)), lptr(_dims(kernel_shape)),
-                                        dptr(Wc), device, dptr(out)))
+    if engine not in ENGINES:
+        raise InvalidArgument("unknown engine")
+    check(lib().icnnm_cuda_conv_adjoint_ex(len(dims), lptr(_dims(dims)), lptr(_dims(kernel_shape)),
+                                           dptr(Wc), ENGINES[engine], device, dptr(out)))
     return out
 
 

@@ -20,6 +20,7 @@
 #include "../../include/icnnm_b200.h"
 #include "icnnm_comm.h"
 #include "icnnm_kernels.cuh"
+#include "icnnm_tc.cuh"
 
 using icnnm_dev::BK;
 using icnnm_dev::BM;
@@ -126,7 +127,8 @@ struct Problem {
   int64_t kd[3] = {1, 1, 1};     // kh, kw, kt
   int64_t m = 0;
   int k = 0;
-  int kp = 0;
+  int kp = 0;     // FFMA engine column padding (multiple of 64)
+  int kp_tc = 0;  // tcgen05 engine padding (multiple of 32)
 };
 
 inline int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -155,6 +157,7 @@ Problem make_problem(int order, const int64_t* dims, const int64_t* kdims) {
   if (k > 4096) invalid("icnnm_b200: kernel with more than 4096 taps is not supported");
   p.k = static_cast<int>(k);
   p.kp = static_cast<int>(roundup(k, BN));
+  p.kp_tc = static_cast<int>(roundup(k, icnnm_dev::tc::KC));
   return p;
 }
 
@@ -233,6 +236,10 @@ void set_smem_attrs() {
   set_max_dyn_smem(icnnm_dev::icnnm_fwd_ffma, optin);
   set_max_dyn_smem(icnnm_dev::icnnm_adj_ffma, optin);
   set_max_dyn_smem(icnnm_dev::icnnm_gram_lags, optin);
+  CK(cudaFuncSetAttribute(icnnm_dev::tc::fwd_kernel_ptr(),
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  CK(cudaFuncSetAttribute(icnnm_dev::tc::adj_kernel_ptr(),
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   done_dev = dev;
 }
 
@@ -255,6 +262,103 @@ void pack_basis(const Problem& p, const double* Kcm, std::vector<float>& Krm,
       Krm[static_cast<size_t>(s) * kp + j] = v;
       KT[static_cast<size_t>(j) * kp + s] = v;
     }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 engine plan and B packing
+// ---------------------------------------------------------------------------
+struct TcPlan {
+  int kp = 0, ntn = 0, nkc = 0, nlast = 0;
+};
+
+TcPlan tc_plan(const Problem& p) {
+  TcPlan t;
+  t.kp = p.kp_tc;
+  t.ntn = (t.kp + icnnm_dev::tc::NTMAX - 1) / icnnm_dev::tc::NTMAX;
+  t.nlast = t.kp - (t.ntn - 1) * icnnm_dev::tc::NTMAX;
+  t.nkc = t.kp / icnnm_dev::tc::KC;
+  return t;
+}
+
+Geo tc_geo(const Geo& g, const TcPlan& t) {
+  Geo q = g;
+  q.kp = t.kp;
+  q.ktp = t.kp;
+  return q;
+}
+
+inline float tf32_rna(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+// Pre-packed B tiles in the UMMA canonical SWIZZLE_NONE K-major layout, hi and
+// lo TF32 parts: [nt][kc] blocks of 32 KB = [hl][q][n/8][k/4][n%8][k%4].
+// forward: B(n=j, k=s) = K[s][j];  adjoint: B(n=s, k=j) = K[s][j].
+std::vector<float> pack_b_tiles(const Problem& p, const TcPlan& t, const double* Kcm, bool fwd) {
+  const int k = p.k;
+  const int blk = icnnm_dev::tc::B_STAGE_BYTES / 4;
+  std::vector<float> out(static_cast<size_t>(t.ntn) * t.nkc * blk, 0.f);
+  for (int nt = 0; nt < t.ntn; ++nt) {
+    const int wn = (nt == t.ntn - 1) ? t.nlast : icnnm_dev::tc::NTMAX;
+    for (int kc = 0; kc < t.nkc; ++kc) {
+      float* base = out.data() + (static_cast<size_t>(nt) * t.nkc + kc) * blk;
+      for (int q = 0; q < 4; ++q)
+        for (int n = 0; n < wn; ++n)
+          for (int k8 = 0; k8 < 8; ++k8) {
+            const int nn = nt * icnnm_dev::tc::NTMAX + n;
+            const int kk = kc * icnnm_dev::tc::KC + q * 8 + k8;
+            double x = 0.0;
+            if (nn < k && kk < k)
+              x = fwd ? Kcm[static_cast<size_t>(nn) * k + kk] : Kcm[static_cast<size_t>(kk) * k + nn];
+            const float xf = static_cast<float>(x);
+            const float hi = tf32_rna(xf);
+            const float lo = xf - hi;
+            const size_t off = static_cast<size_t>(q) * (8 * wn) + (n / 8) * 64 + (k8 / 4) * 32 +
+                               (n % 8) * 4 + (k8 % 4);
+            base[off] = hi;
+            base[32 * wn + off] = lo;
+          }
+    }
+  }
+  return out;
+}
+
+inline int64_t tc_w_elems(const Geo& g, const TcPlan& t) {
+  return n_bricks(g) * static_cast<int64_t>(t.ntn) * 128 * 128;
+}
+
+void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const float* src,
+                      float* W, const float* Bpk, const float* cvec, float* adj, double* norm2,
+                      const IterState* st, cudaStream_t stream) {
+  icnnm_dev::tc::TcArgs a{};
+  a.g = gtc;
+  a.src = src;
+  a.Win = W;
+  a.Wout = W;
+  a.Bpk = Bpk;
+  a.cvec = cvec;
+  a.adj = adj;
+  a.norm2 = norm2;
+  a.st = st;
+  a.mode = mode;
+  a.ntn = t.ntn;
+  a.nkc = t.nkc;
+  a.nlast = t.nlast;
+  a.ntj = t.ntn;
+  a.nbricks = n_bricks(gtc);
+  int dev = 0, nsm = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.nbricks, nsm));
+  void* args[] = {&a};
+  const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd);
+  CK(cudaLaunchKernel(fwd ? icnnm_dev::tc::fwd_kernel_ptr() : icnnm_dev::tc::adj_kernel_ptr(),
+                      dim3(grid), dim3(320), args, smem, stream));
 }
 
 // EigenBasis::validate (spectral.cpp:25-41).
@@ -310,6 +414,7 @@ inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 16) {
 struct Slab {
   int64_t row0 = 0, rows = 0;   // own rows [row0, row0 + rows)
   Geo g{};
+  Geo gtc{};                    // tcgen05 engine geometry (kp = ktp = kp_tc)
   int64_t m_own = 0;            // rows * W * T
   int64_t halo_elems = 0;       // (kh-1) * W * T (slab mode)
   DBuf<float> Lt, adj, pm, mask, W;
@@ -324,6 +429,9 @@ struct Solver {
   std::vector<Slab> slabs;
   std::unique_ptr<Comm> comm;    // cross-process exchange (world > 1)
   DBuf<float> Krm, KT, cvec;
+  TcPlan tp;
+  DBuf<float> BpkF, BpkA;        // tcgen05 engine: packed B tiles (fwd / adj)
+  int engine = ICNNM_ENGINE_FFMA;  // engine of the current run
   DBuf<double> red;              // norm2 (kp) | update slot (8)
   DBuf<double> theta;
   DBuf<IterState> st;
@@ -357,6 +465,7 @@ void solver_alloc(Solver& S) {
   CK(cudaEventCreate(&S.ev1));
   CK(cudaEventCreate(&S.evs));
   set_smem_attrs();
+  S.tp = tc_plan(p);
   const int64_t WT = p.dims[1] * p.dims[2];
   for (auto& s : S.slabs) {
     s.g = make_geo(p, s.rows, !S.sharded);
@@ -370,7 +479,10 @@ void solver_alloc(Solver& S) {
     s.mask.alloc(s.m_own);
     s.L.alloc(s.m_own);
     s.V.alloc(s.m_own);
-    s.W.alloc(static_cast<size_t>(n_bricks(s.g)) * BM * p.kp);
+    s.gtc = tc_geo(s.g, S.tp);
+    check_smem(icnnm_dev::tc::smem_bytes(s.gtc, true));
+    check_smem(icnnm_dev::tc::smem_bytes(s.gtc, false));
+    s.W.alloc(std::max<int64_t>(n_bricks(s.g) * BM * p.kp, tc_w_elems(s.gtc, S.tp)));
     CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
   }
   std::vector<float> Krm, KT;
@@ -379,8 +491,18 @@ void solver_alloc(Solver& S) {
   S.KT.alloc(KT.size());
   CK(cudaMemcpyAsync(S.Krm.p, Krm.data(), S.Krm.bytes(), cudaMemcpyHostToDevice, S.stream));
   CK(cudaMemcpyAsync(S.KT.p, KT.data(), S.KT.bytes(), cudaMemcpyHostToDevice, S.stream));
-  S.cvec.alloc(p.kp);
-  S.red.alloc(p.kp + 8);
+  {
+    auto bf = pack_b_tiles(p, S.tp, S.K.data(), true);
+    auto ba = pack_b_tiles(p, S.tp, S.K.data(), false);
+    S.BpkF.alloc(bf.size());
+    S.BpkA.alloc(ba.size());
+    CK(cudaMemcpyAsync(S.BpkF.p, bf.data(), S.BpkF.bytes(), cudaMemcpyHostToDevice, S.stream));
+    CK(cudaMemcpyAsync(S.BpkA.p, ba.data(), S.BpkA.bytes(), cudaMemcpyHostToDevice, S.stream));
+    CK(cudaStreamSynchronize(S.stream));
+  }
+  const int kpmax = std::max(p.kp, S.tp.kp);
+  S.cvec.alloc(kpmax);
+  S.red.alloc(kpmax + 8);
   S.st.alloc(1);
   int64_t mtot = p.m;
   S.Mstage.alloc(mtot);
@@ -478,6 +600,12 @@ void exchange_adj(Solver& S) {
 }
 
 void launch_fwd(Solver& S, Slab& s, int mode) {
+  if (S.engine == ICNNM_ENGINE_TF32X3) {
+    launch_tc_kernel(s.gtc, S.tp, true, mode, s.Lt.p, s.W.p, S.BpkF.p, S.cvec.p, s.adj.p, S.red.p,
+                     S.st.p, S.stream);
+    ++S.launches;
+    return;
+  }
   icnnm_dev::icnnm_fwd_ffma<<<static_cast<unsigned>(n_bricks(s.g)), 128, fwd_smem(s.g),
                               S.stream>>>(s.g, s.Lt.p, S.Krm.p, s.W.p, S.cvec.p, S.st.p,
                                           S.red.p, mode);
@@ -485,14 +613,24 @@ void launch_fwd(Solver& S, Slab& s, int mode) {
   ++S.launches;
 }
 void launch_adj(Solver& S, Slab& s) {
+  if (S.engine == ICNNM_ENGINE_TF32X3) {
+    launch_tc_kernel(s.gtc, S.tp, false, 1, s.Lt.p, s.W.p, S.BpkA.p, S.cvec.p, s.adj.p, S.red.p,
+                     S.st.p, S.stream);
+    ++S.launches;
+    return;
+  }
   icnnm_dev::icnnm_adj_ffma<<<static_cast<unsigned>(n_bricks(s.g)), 128, adj_smem(s.g),
                               S.stream>>>(s.g, s.W.p, S.KT.p, S.cvec.p, s.adj.p, S.st.p, 1);
   CKL();
   ++S.launches;
 }
 
+inline int engine_kp(const Solver& S) {
+  return S.engine == ICNNM_ENGINE_TF32X3 ? S.tp.kp : S.p.kp;
+}
+
 void allreduce_red(Solver& S) {
-  if (S.world > 1) S.comm->allreduce_sum(S.red.p, S.p.kp + 8, S.stream);
+  if (S.world > 1) S.comm->allreduce_sum(S.red.p, engine_kp(S) + 8, S.stream);
 }
 
 struct RunResult {
@@ -506,6 +644,8 @@ struct RunResult {
 RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   if (!S.uploaded) invalid("solve: no problem uploaded");
   const Problem& p = S.p;
+  S.engine = cfg.engine;
+  const int kpe = engine_kp(S);
   const int iters = cfg.max_iters;
   const double kd = static_cast<double>(p.k);
   // theta schedule exactly as solver.cpp:88-91,126 (fp64, sequential).
@@ -551,7 +691,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   const double floor_rel = 1e-5;
   auto iteration = [&]() {
     icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
-                                                    S.stats.p, p.k, p.kp, kd, res_scale,
+                                                    S.stats.p, p.k, kpe, kd, res_scale,
                                                     cfg.tol_primal, cfg.tol_change, floor_rel);
     CKL();
     for (auto& s : S.slabs) launch_adj(S, s);
@@ -559,7 +699,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     for (auto& s : S.slabs) {
       icnnm_dev::icnnm_update<<<grid_for(s.m_own, 256, 148 * 8), 256, 0, S.stream>>>(
           s.m_own, S.st.p, cfg.lambda, kd, s.adj.p + s.halo_elems, s.L.p, s.V.p, s.pm.p,
-          s.mask.p, s.Lt.p + s.halo_elems, S.red.p + p.kp);
+          s.mask.p, s.Lt.p + s.halo_elems, S.red.p + kpe);
       CKL();
     }
     exchange_lt(S);
@@ -577,7 +717,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     for (int it = 0; it < iters; ++it) {
       CK(cudaEventRecord(e[0], S.stream));
       icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
-                                                      S.stats.p, p.k, p.kp, kd, res_scale,
+                                                      S.stats.p, p.k, kpe, kd, res_scale,
                                                       cfg.tol_primal, cfg.tol_change,
                                                       floor_rel);
       CK(cudaEventRecord(e[1], S.stream));
@@ -587,7 +727,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
       for (auto& s : S.slabs) {
         icnnm_dev::icnnm_update<<<grid_for(s.m_own, 256, 148 * 8), 256, 0, S.stream>>>(
             s.m_own, S.st.p, cfg.lambda, kd, s.adj.p + s.halo_elems, s.L.p, s.V.p, s.pm.p,
-            s.mask.p, s.Lt.p + s.halo_elems, S.red.p + p.kp);
+            s.mask.p, s.Lt.p + s.halo_elems, S.red.p + kpe);
       }
       exchange_lt(S);
       CK(cudaEventRecord(e[3], S.stream));
@@ -635,7 +775,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   }
   // final coef: moves the last update slot into stats, evaluates the stop test.
   icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
-                                                  S.stats.p, p.k, p.kp, kd, res_scale,
+                                                  S.stats.p, p.k, kpe, kd, res_scale,
                                                   cfg.tol_primal, cfg.tol_change, floor_rel);
   CKL();
   ++S.launches;
@@ -672,7 +812,9 @@ void fill_report(const Solver& S, const icnnm_solver_config& cfg, const RunResul
     const bool res_ok = gap2 > 1e-5 * (q.z2 + kd * q.ln2);
     const double lc = std::sqrt(q.dl2) / std::max(std::sqrt(q.l2o), 1e-300);
     if (rep->objective) rep->objective[it] = q.l21 + 0.5 * cfg.lambda * kd * q.fit;
-    if (rep->primal_residual) rep->primal_residual[it] = res;
+    // Below the fp32 floor the identity cannot resolve the gap: report NaN
+    // (never "converged" on it) instead of a rounding artefact.
+    if (rep->primal_residual) rep->primal_residual[it] = res_ok ? res : std::nan("");
     if (rep->l_change) rep->l_change[it] = lc;
     n = it + 1;
     if ((res_ok && res < cfg.tol_primal) || lc < cfg.tol_change) {
@@ -775,8 +917,6 @@ int icnnm_solver_run(icnnm_solver_t h, const icnnm_solver_config* cfg,
   return guard([&] {
     if (!h) invalid("null handle");
     validate_cfg(cfg);
-    if (cfg->engine != ICNNM_ENGINE_FFMA)
-      invalid("icnnm_b200: engine TF32X3 is not available in this build");
     DeviceScope ds(h->S.device);
     auto t0 = std::chrono::steady_clock::now();
     RunResult R = solver_run(h->S, *cfg);
@@ -836,8 +976,6 @@ int icnnm_cuda_solve(int order, const int64_t* dims, const double* M_obs, const 
   return guard([&] {
     auto t0 = std::chrono::steady_clock::now();
     validate_cfg(cfg);
-    if (cfg->engine != ICNNM_ENGINE_FFMA)
-      invalid("icnnm_b200: engine TF32X3 is not available in this build");
     Problem p = make_problem(order, dims, kdims);
     if (!L_out) invalid("null output");
     validate_basis(p.k, K_colmajor, eigenvalues);
@@ -860,22 +998,49 @@ int icnnm_cuda_solve(int order, const int64_t* dims, const double* M_obs, const 
 // --------------------------------------------------------------------------
 // Operator level
 // --------------------------------------------------------------------------
-int icnnm_cuda_conv_forward(int order, const int64_t* dims, const double* L,
-                            const int64_t* kdims, const double* K_colmajor, int device,
-                            double* out) {
+int icnnm_cuda_conv_forward_ex(int order, const int64_t* dims, const double* L,
+                               const int64_t* kdims, const double* K_colmajor, int engine,
+                               int device, double* out) {
   return guard([&] {
     Problem p = make_problem(order, dims, kdims);
     if (!L || !K_colmajor || !out) invalid("null argument");
+    if (engine != ICNNM_ENGINE_FFMA && engine != ICNNM_ENGINE_TF32X3) invalid("unknown engine");
     DeviceScope ds(device);
     set_smem_attrs();
     Geo g = make_geo(p, p.dims[0], true);
+    const int64_t H = p.dims[0], W = p.dims[1], T = p.dims[2];
+    std::vector<float> Lf(L, L + p.m);
+    DBuf<float> dL(p.m);
+    CK(cudaMemcpy(dL.p, Lf.data(), dL.bytes(), cudaMemcpyHostToDevice));
+    if (engine == ICNNM_ENGINE_TF32X3) {
+      TcPlan t = tc_plan(p);
+      Geo gt = tc_geo(g, t);
+      check_smem(icnnm_dev::tc::smem_bytes(gt, true));
+      auto bf = pack_b_tiles(p, t, K_colmajor, true);
+      DBuf<float> dB(bf.size()), dW(tc_w_elems(gt, t));
+      DBuf<double> dn(t.kp);
+      CK(cudaMemcpy(dB.p, bf.data(), dB.bytes(), cudaMemcpyHostToDevice));
+      CK(cudaMemset(dn.p, 0, dn.bytes()));
+      launch_tc_kernel(gt, t, true, 0, dL.p, dW.p, dB.p, nullptr, nullptr, dn.p, nullptr, 0);
+      std::vector<float> Wh(dW.n);
+      CK(cudaMemcpy(Wh.data(), dW.p, dW.bytes(), cudaMemcpyDeviceToHost));
+      for (int64_t h = 0; h < H; ++h)
+        for (int64_t w = 0; w < W; ++w)
+          for (int64_t tt = 0; tt < T; ++tt) {
+            const int64_t flat = (h * W + w) * T + tt;
+            const int64_t r = brick_row(gt, h, w, tt);
+            const int64_t b = r / BM, v = r % BM;
+            for (int j = 0; j < p.k; ++j)
+              out[static_cast<size_t>(j) * p.m + flat] =
+                  Wh[((static_cast<size_t>(b) * t.ntn + j / 128) * 128 + (j % 128)) * 128 + v];
+          }
+      return;
+    }
     check_smem(fwd_smem(g));
     std::vector<float> Krm, KT;
     pack_basis(p, K_colmajor, Krm, KT);
-    std::vector<float> Lf(L, L + p.m);
-    DBuf<float> dL(p.m), dK(Krm.size()), dW(static_cast<size_t>(n_bricks(g)) * BM * p.kp);
+    DBuf<float> dK(Krm.size()), dW(static_cast<size_t>(n_bricks(g)) * BM * p.kp);
     DBuf<double> dn(p.kp);
-    CK(cudaMemcpy(dL.p, Lf.data(), dL.bytes(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dK.p, Krm.data(), dK.bytes(), cudaMemcpyHostToDevice));
     CK(cudaMemset(dn.p, 0, dn.bytes()));
     icnnm_dev::icnnm_fwd_ffma<<<static_cast<unsigned>(n_bricks(g)), 128, fwd_smem(g)>>>(
@@ -883,7 +1048,6 @@ int icnnm_cuda_conv_forward(int order, const int64_t* dims, const double* L,
     CKL();
     std::vector<float> Wh(dW.n);
     CK(cudaMemcpy(Wh.data(), dW.p, dW.bytes(), cudaMemcpyDeviceToHost));
-    const int64_t H = p.dims[0], W = p.dims[1], T = p.dims[2];
     for (int64_t h = 0; h < H; ++h)
       for (int64_t w = 0; w < W; ++w)
         for (int64_t t = 0; t < T; ++t) {
@@ -894,38 +1058,77 @@ int icnnm_cuda_conv_forward(int order, const int64_t* dims, const double* L,
   });
 }
 
-int icnnm_cuda_conv_adjoint(int order, const int64_t* dims, const int64_t* kdims,
-                            const double* Wcm, int device, double* out) {
+int icnnm_cuda_conv_forward(int order, const int64_t* dims, const double* L,
+                            const int64_t* kdims, const double* K_colmajor, int device,
+                            double* out) {
+  return icnnm_cuda_conv_forward_ex(order, dims, L, kdims, K_colmajor, ICNNM_ENGINE_FFMA, device,
+                                    out);
+}
+
+int icnnm_cuda_conv_adjoint_ex(int order, const int64_t* dims, const int64_t* kdims,
+                               const double* Wcm, int engine, int device, double* out) {
   return guard([&] {
     Problem p = make_problem(order, dims, kdims);
     if (!Wcm || !out) invalid("null argument");
+    if (engine != ICNNM_ENGINE_FFMA && engine != ICNNM_ENGINE_TF32X3) invalid("unknown engine");
     DeviceScope ds(device);
     set_smem_attrs();
     Geo g = make_geo(p, p.dims[0], true);
-    check_smem(adj_smem(g));
-    // W (m x k column-major) -> brick-ordered rows; K = I.
-    std::vector<float> Wb(static_cast<size_t>(n_bricks(g)) * BM * p.kp, 0.f);
     const int64_t H = p.dims[0], Wd = p.dims[1], T = p.dims[2];
-    for (int64_t h = 0; h < H; ++h)
-      for (int64_t w = 0; w < Wd; ++w)
-        for (int64_t t = 0; t < T; ++t) {
-          const int64_t flat = (h * Wd + w) * T + t;
-          float* row = Wb.data() + brick_row(g, h, w, t) * p.kp;
-          for (int j = 0; j < p.k; ++j) row[j] = static_cast<float>(Wcm[static_cast<size_t>(j) * p.m + flat]);
-        }
-    std::vector<float> I(static_cast<size_t>(p.kp) * p.kp, 0.f);
-    for (int j = 0; j < p.k; ++j) I[static_cast<size_t>(j) * p.kp + j] = 1.f;
-    DBuf<float> dW(Wb.size()), dI(I.size()), dadj(p.m);
-    CK(cudaMemcpy(dW.p, Wb.data(), dW.bytes(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(dI.p, I.data(), dI.bytes(), cudaMemcpyHostToDevice));
+    DBuf<float> dadj(p.m);
     CK(cudaMemset(dadj.p, 0, dadj.bytes()));
-    icnnm_dev::icnnm_adj_ffma<<<static_cast<unsigned>(n_bricks(g)), 128, adj_smem(g)>>>(
-        g, dW.p, dI.p, nullptr, dadj.p, nullptr, 0);
-    CKL();
+    if (engine == ICNNM_ENGINE_TF32X3) {
+      TcPlan t = tc_plan(p);
+      Geo gt = tc_geo(g, t);
+      check_smem(icnnm_dev::tc::smem_bytes(gt, false));
+      std::vector<double> I(static_cast<size_t>(p.k) * p.k, 0.0);
+      for (int j = 0; j < p.k; ++j) I[static_cast<size_t>(j) * p.k + j] = 1.0;
+      auto ba = pack_b_tiles(p, t, I.data(), false);
+      std::vector<float> Wt(tc_w_elems(gt, t), 0.f);
+      for (int64_t h = 0; h < H; ++h)
+        for (int64_t w = 0; w < Wd; ++w)
+          for (int64_t tt = 0; tt < T; ++tt) {
+            const int64_t flat = (h * Wd + w) * T + tt;
+            const int64_t r = brick_row(gt, h, w, tt);
+            const int64_t b = r / BM, v = r % BM;
+            for (int j = 0; j < p.k; ++j)
+              Wt[((static_cast<size_t>(b) * t.ntn + j / 128) * 128 + (j % 128)) * 128 + v] =
+                  static_cast<float>(Wcm[static_cast<size_t>(j) * p.m + flat]);
+          }
+      DBuf<float> dB(ba.size()), dW(Wt.size());
+      CK(cudaMemcpy(dB.p, ba.data(), dB.bytes(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(dW.p, Wt.data(), dW.bytes(), cudaMemcpyHostToDevice));
+      launch_tc_kernel(gt, t, false, 0, nullptr, dW.p, dB.p, nullptr, dadj.p, nullptr, nullptr, 0);
+    } else {
+      check_smem(adj_smem(g));
+      // W (m x k column-major) -> brick-ordered rows; K = I.
+      std::vector<float> Wb(static_cast<size_t>(n_bricks(g)) * BM * p.kp, 0.f);
+      for (int64_t h = 0; h < H; ++h)
+        for (int64_t w = 0; w < Wd; ++w)
+          for (int64_t t = 0; t < T; ++t) {
+            const int64_t flat = (h * Wd + w) * T + t;
+            float* row = Wb.data() + brick_row(g, h, w, t) * p.kp;
+            for (int j = 0; j < p.k; ++j)
+              row[j] = static_cast<float>(Wcm[static_cast<size_t>(j) * p.m + flat]);
+          }
+      std::vector<float> I(static_cast<size_t>(p.kp) * p.kp, 0.f);
+      for (int j = 0; j < p.k; ++j) I[static_cast<size_t>(j) * p.kp + j] = 1.f;
+      DBuf<float> dW(Wb.size()), dI(I.size());
+      CK(cudaMemcpy(dW.p, Wb.data(), dW.bytes(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(dI.p, I.data(), dI.bytes(), cudaMemcpyHostToDevice));
+      icnnm_dev::icnnm_adj_ffma<<<static_cast<unsigned>(n_bricks(g)), 128, adj_smem(g)>>>(
+          g, dW.p, dI.p, nullptr, dadj.p, nullptr, 0);
+      CKL();
+    }
     std::vector<float> a(p.m);
     CK(cudaMemcpy(a.data(), dadj.p, dadj.bytes(), cudaMemcpyDeviceToHost));
     for (int64_t i = 0; i < p.m; ++i) out[i] = a[i];
   });
+}
+
+int icnnm_cuda_conv_adjoint(int order, const int64_t* dims, const int64_t* kdims,
+                            const double* Wcm, int device, double* out) {
+  return icnnm_cuda_conv_adjoint_ex(order, dims, kdims, Wcm, ICNNM_ENGINE_FFMA, device, out);
 }
 
 int icnnm_cuda_prox_l21(int64_t rows, int64_t cols, const double* W, double tau, int device,
@@ -1137,8 +1340,6 @@ int icnnm_sharded_solve(int order, const int64_t* dims, const double* M_obs, con
   return guard([&] {
     auto t0 = std::chrono::steady_clock::now();
     validate_cfg(cfg);
-    if (cfg->engine != ICNNM_ENGINE_FFMA)
-      invalid("icnnm_b200: engine TF32X3 is not available in this build");
     Problem p = make_problem(order, dims, kdims);
     if (local_slabs < 1 || world < 1 || rank < 0 || rank >= world)
       invalid("sharded solve: bad slab / rank arguments");

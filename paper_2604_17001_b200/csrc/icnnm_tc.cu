@@ -1,0 +1,456 @@
+// ICNNM forward / adjoint contractions on the 5th-gen tensor cores (sm_100a).
+//
+// Engine ICNNM_ENGINE_TF32X3: each fp32 GEMM is computed as three tcgen05
+// kind::tf32 MMAs per K-step with fp32 accumulation in TMEM,
+//     D += A_hi B_hi + A_lo B_hi + A_hi B_lo,     x_hi = rna_tf32(x), x_lo = x - x_hi,
+// which keeps ~22 mantissa bits of every product (the parity study in
+// DESIGN.md §5 shows 1-term TF32 misses the 1e-4 tolerance).
+//
+// Kernel shape (persistent, one CTA per SM, 320 threads):
+//   warps 0-3  builders : im2col / scaled-W rows -> hi/lo split -> tcgen05.st
+//                         into a TMEM A-stage (row = TMEM lane = voxel)
+//   warps 4-7  epilogue : tcgen05.ld the accumulator; forward: W update +
+//                         column norms; adjoint: col2im into per-warp SMEM
+//                         output bricks, flushed with one atomic per entry
+//   warp 8     MMA      : one elected thread issues tcgen05.mma (A from TMEM,
+//                         B from SMEM via a SWIZZLE_NONE K-major descriptor)
+//   warp 9     loader   : cp.async.bulk of host-pre-packed B tiles (UMMA
+//                         canonical layout) into a 3-stage SMEM ring
+// TMEM: two 128-column accumulators (epilogue of tile i overlaps MMAs of
+// tile i+1) + four 64-column A stages = 512 columns.
+//
+// Forward  (a)+(b): D[v, j] = sum_s L~[v - s] K[s, j]          (N = columns j)
+// Adjoint  (c)    : D[v, s] = sum_j W[v, j] c_j K[s, j]        (N = taps s)
+// W layout (this engine): [brick][jt][jj][row], jt = j / 128, jj = j % 128,
+// so epilogue/builder threads (one per row) access it coalesced.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "icnnm_kernels.cuh"
+#include "icnnm_tc.cuh"
+
+namespace icnnm_dev {
+namespace tc {
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t f2tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return r;
+}
+
+#define R8(i) "r"(v[i]), "r"(v[i + 1]), "r"(v[i + 2]), "r"(v[i + 3]), "r"(v[i + 4]), "r"(v[i + 5]), "r"(v[i + 6]), "r"(v[i + 7])
+#define W8(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31, %32};\n" ::"r"(taddr),
+      R8(0), R8(8), R8(16), R8(24)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31}, [%32];\n"
+      : W8(0), W8(8), W8(16), W8(24)
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// SWIZZLE_NONE K-major shared-memory matrix descriptor: core matrices of
+// 8 rows x 16 B; LBO = 128 B (next 16 B along K), SBO = 256 B (next 8 rows).
+__device__ __forceinline__ uint64_t bdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(128 >> 4) << 16;
+  d |= static_cast<uint64_t>(256 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version (sm_100)
+  return d;                            // base_offset 0, lbo_mode 0, SWIZZLE_NONE
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M=128.
+__device__ __forceinline__ uint32_t idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ int wrapi(int x, int n) {
+  int r = x % n;
+  return r < 0 ? r + n : r;
+}
+
+// ---------------------------------------------------------------------------
+// The kernel (FWD = forward implicit GEMM, !FWD = adjoint)
+// ---------------------------------------------------------------------------
+template <bool FWD>
+__global__ void __launch_bounds__(320, 1)
+icnnm_tc_kernel(TcArgs a) {
+  const Geo& g = a.g;
+  float rr = 0.f;
+  if (a.mode == 1) {
+    if (!a.st->active) return;
+    if (FWD && a.st->it >= a.st->max_iters - 1) return;
+    rr = static_cast<float>(a.st->r);
+  }
+  extern __shared__ __align__(1024) uint8_t smem[];
+  // ---- carve shared memory ----
+  uint8_t* p = smem;
+  float* Bst = reinterpret_cast<float*>(p);             // SB x B_STAGE_BYTES
+  p += SB * B_STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p);      // 2*SA + 2*SB + 4
+  uint64_t* A_full = bars;
+  uint64_t* A_empty = bars + SA;
+  uint64_t* B_full = bars + 2 * SA;
+  uint64_t* B_empty = bars + 2 * SA + SB;
+  uint64_t* ACC_full = bars + 2 * SA + 2 * SB;
+  uint64_t* ACC_empty = ACC_full + 2;
+  p += 128;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p);
+  p += 16;
+  int* tapoff = reinterpret_cast<int*>(p);              // ktp
+  p += ((g.ktp * 4 + 15) / 16) * 16;
+  float* cs = reinterpret_cast<float*>(p);              // kp
+  p += ((g.kp * 4 + 15) / 16) * 16;
+  const int nob = g.HH * g.HW * g.HT;
+  // FWD: halo (nob) | red scratch 4 x 32 x 33 | nrm (kp doubles)
+  // ADJ: 4 output bricks (4 x nob)
+  float* halo = reinterpret_cast<float*>(p);
+  float* red = halo + ((nob + 3) / 4) * 4;
+  double* nrm = reinterpret_cast<double*>(red + 4 * 32 * 33);
+  float* ob = reinterpret_cast<float*>(p);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  // ---- one-time setup ----
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < SA; ++i) {
+      mbar_init(A_full + i, 128);
+      mbar_init(A_empty + i, 1);
+    }
+    for (int i = 0; i < SB; ++i) {
+      mbar_init(B_full + i, 1);
+      mbar_init(B_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(ACC_full + i, 1);
+      mbar_init(ACC_empty + i, 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int s = tid; s < g.ktp; s += blockDim.x) {
+    int off = 0;
+    if (s < g.k) {
+      int st = s % g.kt, q = s / g.kt, sw = q % g.kw, sh = q / g.kw;
+      off = (sh * g.HW + sw) * g.HT + st;
+    }
+    tapoff[s] = off;
+  }
+  for (int j = tid; j < g.kp; j += blockDim.x) {
+    float c = 1.f;
+    if (a.mode == 1) c = a.cvec[j];
+    cs[j] = (j < g.k) ? c : 0.f;
+  }
+  if (FWD) {
+    for (int j = tid; j < g.kp; j += blockDim.x) nrm[j] = 0.0;
+  } else {
+    for (int e = tid; e < 4 * nob; e += blockDim.x) ob[e] = 0.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  const int nbr = static_cast<int>(a.nbricks);
+  const int ntn = a.ntn;                 // N-tiles per brick
+  const int nkc = a.nkc;                 // K-chunks per tile
+  const int nlast = a.nlast;             // width of the last N-tile
+
+  if (warp < 4) {
+    // ===================== builders =====================
+    const int row = tid;                 // TMEM lane / voxel of the brick
+    const int v = row;
+    const int vt = v % g.bt, vw = (v / g.bt) % g.bw, vh = v / (g.bt * g.bw);
+    const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
+    const uint32_t lane_base = static_cast<uint32_t>(32 * warp) << 16;
+    uint32_t cnt = 0;
+    for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+      if (FWD) {
+        int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
+        const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
+        named_sync(1, 128);  // previous brick fully built
+        for (int e = tid; e < nob; e += 128) {
+          int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
+          int hs = h0 - (g.kh - 1) + aa + g.hoff;
+          hs = g.wrapH ? wrapi(hs, g.Hsrc) : (hs < 0 ? 0 : (hs >= g.Hsrc ? g.Hsrc - 1 : hs));
+          int ws = wrapi(w0 - (g.kw - 1) + bb, g.W);
+          int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
+          halo[e] = __ldg(a.src + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts);
+        }
+        named_sync(1, 128);
+      }
+      const float* Wrow = FWD ? nullptr : a.Win + static_cast<size_t>(b) * a.ntj * 128 * 128 + row;
+      for (int nt = 0; nt < ntn; ++nt) {
+        for (int kc = 0; kc < nkc; ++kc, ++cnt) {
+          const int sa = cnt % SA;
+          const uint32_t ph = (cnt / SA) & 1;
+          mbar_wait(A_empty + sa, ph ^ 1);
+          tc_fence_after();
+          uint32_t hi[32], lo[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float x;
+            const int q = kc * KC + i;
+            if (FWD) {
+              x = halo[hidx - tapoff[q]];
+            } else {
+              const int jt = q >> 7, jj = q & 127;
+              x = __ldg(Wrow + (static_cast<size_t>(jt) * 128 + jj) * 128) * cs[q];
+            }
+            const uint32_t h = f2tf32(x);
+            hi[i] = h;
+            lo[i] = __float_as_uint(x - __uint_as_float(h));
+          }
+          const uint32_t col = A_COL0 + sa * 64;
+          tmem_st32(tbase + lane_base + col, hi);
+          tmem_st32(tbase + lane_base + col + 32, lo);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(A_full + sa);
+        }
+      }
+    }
+  } else if (warp < 8) {
+    // ===================== epilogue =====================
+    const int ew = warp - 4;
+    const int row = 32 * ew + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(32 * ew) << 16;
+    const int v = row;
+    const int vt = v % g.bt, vw = (v / g.bt) % g.bw, vh = v / (g.bt * g.bw);
+    const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
+    float* myob = ob + ew * nob;
+    float* myred = red + ew * 32 * 33;
+    uint32_t tcount = 0;
+    for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+      int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
+      const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
+      const bool valid = (h0 + vh < g.H) && (w0 + vw < g.W) && (t0 + vt < g.T);
+      for (int nt = 0; nt < ntn; ++nt, ++tcount) {
+        const int acc = tcount & 1;
+        const uint32_t ph = (tcount >> 1) & 1;
+        const int wn = (nt == ntn - 1) ? nlast : 128;
+        mbar_wait(ACC_full + acc, ph);
+        tc_fence_after();
+        for (int c0 = 0; c0 < wn; c0 += 32) {
+          uint32_t u[32];
+          tmem_ld32(tbase + lane_base + acc * 128 + c0, u);
+          tmem_wait_ld();
+          if (FWD) {
+            float* wp = a.Wout + ((static_cast<size_t>(b) * a.ntj + nt) * 128 + c0) * 128 + row;
+            const int j0 = nt * 128 + c0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              float w = __uint_as_float(u[i]);
+              if (a.mode == 1) w = fmaf(rr * cs[j0 + i], wp[static_cast<size_t>(i) * 128], w);
+              w = valid ? w : 0.f;
+              if (c0 + i < wn) wp[static_cast<size_t>(i) * 128] = w;
+              myred[i * 33 + lane] = w * w;
+            }
+            __syncwarp();
+            float s = 0.f;
+#pragma unroll 8
+            for (int i = 0; i < 32; ++i) s += myred[lane * 33 + i];
+            __syncwarp();
+            if (c0 + lane < wn) atomicAdd(nrm + j0 + lane, static_cast<double>(s));
+          } else {
+            const int s0 = nt * 128 + c0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int s = s0 + i;
+              if (s < g.k) {
+                float* o = myob + (hidx - tapoff[s]);
+                *o += __uint_as_float(u[i]);
+              }
+              __syncwarp();
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(ACC_empty + acc);
+      }
+      if (!FWD) {
+        // flush this brick's output bricks (one fp32 atomic per entry)
+        named_sync(2, 128);
+        for (int e = row; e < nob; e += 128) {
+          float s = ob[e] + ob[nob + e] + ob[2 * nob + e] + ob[3 * nob + e];
+          ob[e] = 0.f;
+          ob[nob + e] = 0.f;
+          ob[2 * nob + e] = 0.f;
+          ob[3 * nob + e] = 0.f;
+          if (s == 0.f) continue;
+          int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
+          int hs = h0 - (g.kh - 1) + aa + g.hoff;
+          if (g.wrapH) hs = wrapi(hs, g.Hsrc);
+          if (hs < 0 || hs >= g.Hsrc) continue;
+          int ws = wrapi(w0 - (g.kw - 1) + bb, g.W);
+          int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
+          atomicAdd(a.adj + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts, s);
+        }
+        named_sync(2, 128);
+      }
+    }
+    if (FWD && a.norm2 != nullptr) {
+      named_sync(2, 128);
+      for (int j = row; j < g.kp; j += 128)
+        if (nrm[j] != 0.0) atomicAdd(a.norm2 + j, nrm[j]);
+    }
+  } else if (warp == 8) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      uint32_t cnt = 0, bcnt = 0, tcount = 0;
+      const uint32_t bs0 = smem_u32(Bst);
+      for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+        for (int nt = 0; nt < ntn; ++nt, ++tcount) {
+          const int acc = tcount & 1;
+          const uint32_t aph = (tcount >> 1) & 1;
+          const int wn = (nt == ntn - 1) ? nlast : 128;
+          const uint32_t idesc = idesc_tf32(wn);
+          const uint32_t dcol = tbase + acc * 128;
+          mbar_wait(ACC_empty + acc, aph ^ 1);
+          tc_fence_after();
+          for (int kc = 0; kc < nkc; ++kc, ++cnt, ++bcnt) {
+            const int sa = cnt % SA;
+            const int sb = bcnt % SB;
+            mbar_wait(A_full + sa, (cnt / SA) & 1);
+            mbar_wait(B_full + sb, (bcnt / SB) & 1);
+            tc_fence_after();
+            const uint32_t acol = tbase + A_COL0 + sa * 64;
+            const uint32_t bhi = bs0 + sb * B_STAGE_BYTES;
+            const uint32_t blo = bhi + wn * 128;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint64_t dh = bdesc(bhi + q * wn * 32);
+              const uint64_t dl = bdesc(blo + q * wn * 32);
+              const uint32_t first = (kc == 0 && q == 0) ? 0u : 1u;
+              tc_mma_ts(dcol, acol + q * 8, dh, idesc, first);
+              tc_mma_ts(dcol, acol + 32 + q * 8, dh, idesc, 1u);
+              tc_mma_ts(dcol, acol + q * 8, dl, idesc, 1u);
+            }
+            tc_commit(A_empty + sa);
+            tc_commit(B_empty + sb);
+          }
+          tc_commit(ACC_full + acc);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== B loader =====================
+    if (lane == 0) {
+      uint32_t bcnt = 0;
+      for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+        for (int nt = 0; nt < ntn; ++nt) {
+          const int wn = (nt == ntn - 1) ? nlast : 128;
+          const uint32_t bytes = static_cast<uint32_t>(wn) * 256;
+          for (int kc = 0; kc < nkc; ++kc, ++bcnt) {
+            const int sb = bcnt % SB;
+            mbar_wait(B_empty + sb, ((bcnt / SB) & 1) ^ 1);
+            mbar_arrive_expect_tx(B_full + sb, bytes);
+            const float* src = a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4);
+            bulk_g2s(reinterpret_cast<uint8_t*>(Bst) + sb * B_STAGE_BYTES, src, bytes, B_full + sb);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 8) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+  }
+}
+
+template __global__ void icnnm_tc_kernel<true>(TcArgs);
+template __global__ void icnnm_tc_kernel<false>(TcArgs);
+
+void* fwd_kernel_ptr() { return reinterpret_cast<void*>(&icnnm_tc_kernel<true>); }
+void* adj_kernel_ptr() { return reinterpret_cast<void*>(&icnnm_tc_kernel<false>); }
+
+}  // namespace tc
+}  // namespace icnnm_dev

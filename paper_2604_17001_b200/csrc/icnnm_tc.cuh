@@ -1,0 +1,56 @@
+// tcgen05 (TF32x3) engine of the two ICNNM contractions: shared host/device
+// declarations.  See icnnm_tc.cu for the kernel design.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "icnnm_kernels.cuh"
+
+namespace icnnm_dev {
+namespace tc {
+
+constexpr int KC = 32;                         // K per chunk (4 MMA K-steps of 8)
+constexpr int SA = 4;                          // TMEM A stages (64 columns each)
+constexpr int SB = 3;                          // SMEM B stages
+constexpr int NTMAX = 128;                     // accumulator width (N per tile)
+constexpr int B_STAGE_BYTES = NTMAX * KC * 4 * 2;  // hi + lo = 32 KB
+constexpr int A_COL0 = 256;                    // TMEM columns 0..255: 2 accumulators
+
+struct TcArgs {
+  Geo g;                 // kp = ktp = roundup(k, 32)
+  const float* src;      // forward: L~ (natural [H,W,T] layout, slab halo rows first)
+  const float* Win;      // adjoint: W in this engine's layout
+  float* Wout;           // forward: W (read-modify-write in mode 1)
+  const float* Bpk;      // pre-packed B tiles [nt][kc][hi|lo][q][n/8][2][8][4]
+  const float* cvec;     // shrink factors (mode 1)
+  float* adj;            // adjoint output (natural layout, slab halo rows first)
+  double* norm2;         // forward: column norms^2 accumulator
+  const IterState* st;
+  int mode;              // 0: plain operator, 1: ADMM iteration
+  int ntn;               // N-tiles per brick
+  int nkc;               // K-chunks per N-tile
+  int nlast;             // width of the last N-tile (multiple of 32)
+  int ntj;               // j-tiles of the W layout
+  int64_t nbricks;
+};
+
+template <bool FWD>
+__global__ void icnnm_tc_kernel(TcArgs a);
+
+void* fwd_kernel_ptr();
+void* adj_kernel_ptr();
+
+inline size_t smem_bytes(const Geo& g, bool fwd) {
+  const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
+  size_t b = static_cast<size_t>(SB) * B_STAGE_BYTES + 128 + 16;
+  b += ((g.ktp * 4 + 15) / 16) * 16;
+  b += ((g.kp * 4 + 15) / 16) * 16;
+  if (fwd)
+    b += ((nob + 3) / 4) * 16 + 4 * 32 * 33 * 4 + static_cast<size_t>(g.kp) * 8;
+  else
+    b += 4 * nob * 4;
+  return b;
+}
+
+}  // namespace tc
+}  // namespace icnnm_dev

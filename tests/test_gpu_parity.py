@@ -14,6 +14,7 @@ from oracle import icnnm_oracle as O
 pytestmark = pytest.mark.gpu
 
 FIXED = dict(tol_primal=1e-300, tol_change=1e-300)
+ENGINES = ["ffma", "tf32x3"]
 
 
 def _rel(a, b):
@@ -31,36 +32,43 @@ def _rand_orth(k, seed):
 @pytest.mark.parametrize("dims,ks", [((32, 32, 8), (5, 5, 3)), ((7, 5, 9), (3, 2, 4)),
                                      ((5, 4), (3, 3)), ((12,), (5,)), ((3, 3, 3), (3, 3, 3)),
                                      ((20, 33, 17), (9, 1, 5)), ((6, 6, 40), (1, 6, 13))])
-def test_forward_index_map_bit_exact(gpu, dims, ks):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_forward_index_map_bit_exact(gpu, dims, ks, engine):
     """K = I on integer-valued L: A(L) must equal conv_matrix exactly
     (pins the corner-anchored periodic index map, conv_op.cpp:35-46)."""
     rng = np.random.default_rng(1)
     L = rng.integers(-8, 9, size=dims).astype(np.float64)
     k = int(np.prod(ks))
-    out = gpu.BasisConvolver(dims, ks, np.eye(k)).apply(L)
+    out = gpu.BasisConvolver(dims, ks, np.eye(k), engine=engine).apply(L)
     np.testing.assert_array_equal(out, O.conv_matrix(L, ks))
 
 
 @pytest.mark.parametrize("dims,ks", [((32, 32, 8), (5, 5, 3)), ((16, 16, 32), (9, 9, 5)),
-                                     ((9, 7, 11), (3, 4, 2)), ((6, 5), (2, 3))])
-def test_forward_matches_basis_convolver(gpu, dims, ks):
+                                     ((9, 7, 11), (3, 4, 2)), ((6, 5), (2, 3)),
+                                     ((24, 24, 16), (13, 13, 7))])
+@pytest.mark.parametrize("engine", ENGINES)
+def test_forward_matches_basis_convolver(gpu, dims, ks, engine):
     rng = np.random.default_rng(2)
     L = rng.uniform(-1, 1, size=dims)
     k = int(np.prod(ks))
     K = _rand_orth(k, 3)
-    got = gpu.BasisConvolver(dims, ks, K).apply(L)
+    got = gpu.BasisConvolver(dims, ks, K, engine=engine).apply(L)
     ref = O.BasisConvolver(dims, ks, K).apply(L)
-    assert _rel(got, ref) < 1e-5
+    # fp32 FFMA: ~1e-7; TF32x3 (tensor-core fp32 accumulate): ~1e-6 at k ~ 1e3
+    assert _rel(got, ref) < (1e-6 if engine == "ffma" else 1e-5)
 
 
 @pytest.mark.parametrize("dims,ks", [((32, 32, 8), (5, 5, 3)), ((5, 6, 7), (2, 3, 4)),
-                                     ((4, 4), (2, 2)), ((10,), (4,)), ((8, 8, 16), (8, 8, 3))])
-def test_adjoint_bit_exact_on_integers(gpu, dims, ks):
+                                     ((4, 4), (2, 2)), ((10,), (4,)), ((8, 8, 16), (8, 8, 3)),
+                                     ((20, 20, 16), (9, 9, 5))])
+@pytest.mark.parametrize("engine", ENGINES)
+def test_adjoint_bit_exact_on_integers(gpu, dims, ks, engine):
     """conv_adjoint (conv_op.cpp:57-77) on integer W: exact in fp32."""
     rng = np.random.default_rng(4)
     m, k = int(np.prod(dims)), int(np.prod(ks))
     W = rng.integers(-4, 5, size=(m, k)).astype(np.float64)
-    np.testing.assert_array_equal(gpu.conv_adjoint(W, ks, dims), O.conv_adjoint(W, ks, dims))
+    np.testing.assert_array_equal(gpu.conv_adjoint(W, ks, dims, engine=engine),
+                                  O.conv_adjoint(W, ks, dims))
 
 
 def test_adjointness_and_composition(gpu):
@@ -163,7 +171,8 @@ def test_learn_basis_matches_oracle(gpu):
         if ref.eigenvalues[start] > 1e-6 * s1:
             b = got.K[:, start:end]
             v = ref.K[:, start:end]
-            assert np.linalg.norm(b @ b.T - v @ v.T) < 1e-6
+            # eigenvector sensitivity ~ eps * lambda_1 / gap
+            assert np.linalg.norm(b @ b.T - v @ v.T) < 1e-5
         start = end
 
 
@@ -212,7 +221,8 @@ def _oracle_basis(B):
     return O.EigenBasis(tuple(B.kernel_shape), B.K, B.eigenvalues, B.degenerate)
 
 
-def test_solve_config1_full_parity(gpu):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_solve_config1_full_parity(gpu, engine):
     """BASELINE config 1 (32x32x8, 5x5x3, 200 iterations): GPU vs oracle."""
     from paper_2604_17001_b200 import synth
     w = synth.WORKLOADS[1]
@@ -220,7 +230,8 @@ def test_solve_config1_full_parity(gpu):
     mask = w.mask()
     B = gpu.learn_ensemble_basis(w.training(), w.kernel)
     M = X * mask
-    Lg, rg = gpu.icnnm_solve(M, mask, B, gpu.SolverConfig(max_iters=w.iters, **FIXED))
+    Lg, rg = gpu.icnnm_solve(M, mask, B, gpu.SolverConfig(max_iters=w.iters, engine=engine,
+                                                          **FIXED))
     Lo, ro = O.icnnm_solve(M, mask, _oracle_basis(B),
                            O.SolverConfig(max_iters=w.iters, **FIXED))
     assert rg.iterations == w.iters and rg.termination == "max_iters"
@@ -228,21 +239,29 @@ def test_solve_config1_full_parity(gpu):
     assert abs(synth.psnr(X, Lg) - O.psnr(X, Lo)) <= 0.01
     np.testing.assert_allclose(rg.objective, ro.objective, rtol=1e-4)
     np.testing.assert_allclose(rg.l_change, ro.l_change, rtol=1e-2, atol=1e-6)
-    # residual trace is an fp32 identity estimate: checked while resolvable
-    np.testing.assert_allclose(rg.primal_residual[:3], ro.primal_residual[:3], rtol=2e-2)
+    # residual trace: fp32 identity estimate, exact while the
+    # gap is resolvable, NaN below the fp32 floor -- never a spurious value
+    res = np.array(rg.primal_residual)
+    ok = ~np.isnan(res)
+    assert ok[0]
+    np.testing.assert_allclose(res[0], ro.primal_residual[0], rtol=2e-3)
+    assert np.all(res[ok] < 1.0)
 
 
 @pytest.mark.parametrize("dims,ks,iters,rate", [((24, 20, 16), (5, 3, 3), 150, 0.3),
                                                 ((16, 16, 32), (9, 9, 5), 60, 0.2),
-                                                ((20, 24), (4, 5), 100, 0.5)])
-def test_solve_small_parity(gpu, dims, ks, iters, rate):
+                                                ((20, 24), (4, 5), 100, 0.5),
+                                                ((32, 32, 24), (13, 13, 7), 40, 0.3)])
+@pytest.mark.parametrize("engine", ENGINES)
+def test_solve_small_parity(gpu, dims, ks, iters, rate, engine):
     from paper_2604_17001_b200 import synth
     full = dims if len(dims) == 3 else (1,) + tuple(dims)
     X = synth.synth_video(*full, 8, 2, 11).reshape(dims)
     refs = [synth.synth_video(*full, 8, 2, 100 + i).reshape(dims) for i in range(3)]
     mask = synth.reference_bernoulli_mask(dims, rate, 9)
     B = gpu.learn_ensemble_basis(refs, ks)
-    Lg, rg = gpu.icnnm_solve(X * mask, mask, B, gpu.SolverConfig(max_iters=iters, **FIXED))
+    Lg, rg = gpu.icnnm_solve(X * mask, mask, B, gpu.SolverConfig(max_iters=iters, engine=engine,
+                                                                  **FIXED))
     Lo, _ = O.icnnm_solve(X * mask, mask, _oracle_basis(B),
                           O.SolverConfig(max_iters=iters, **FIXED))
     assert _rel(Lg, Lo) <= 1e-4
@@ -333,7 +352,8 @@ def test_handle_api_equals_one_shot(gpu):
     assert r2.iterations == r3.iterations == 50
 
 
-def test_sharded_virtual_slabs_match_unsharded(gpu):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_sharded_virtual_slabs_match_unsharded(gpu, engine):
     """H-sharded iteration (halo exchange + norm all-reduce) with G virtual
     slabs on one device equals the unsharded solve."""
     from paper_2604_17001_b200 import synth
@@ -341,7 +361,7 @@ def test_sharded_virtual_slabs_match_unsharded(gpu):
     mask = synth.synth_mask(48, 16, 16, synth.MASK_IID, 0.3, 22)
     mask[20:30, 3:9, 4:12] = 0.0  # a missing box crossing slab boundaries
     B = gpu.learn_ensemble_basis([synth.synth_video(48, 16, 16, 8, 2, 23)], (5, 3, 3))
-    cfg = gpu.SolverConfig(max_iters=60, **FIXED)
+    cfg = gpu.SolverConfig(max_iters=60, engine=engine, **FIXED)
     L1, r1 = gpu.icnnm_solve(X * mask, mask, B, cfg)
     Lo, _ = O.icnnm_solve(X * mask, mask, _oracle_basis(B), O.SolverConfig(max_iters=60, **FIXED))
     assert _rel(L1, Lo) < 1e-4
