@@ -127,6 +127,10 @@ int64_t icnnm_solver_device_bytes(icnnm_solver_t h);
  * out[0]=forward, out[1]=adjoint, out[2]=update, out[3]=coef. */
 int icnnm_solver_set_profile(icnnm_solver_t h, int enable);
 int icnnm_solver_kernel_times(icnnm_solver_t h, double* out_ms4);
+/* tcgen05 pipeline counters of the last run() with set_profile(h, 2):
+ * 2 x 9 cycle sums (forward, adjoint): builder wait/work, MMA wait on A /
+ * B / accumulator, epilogue wait/work, loader wait, MMA-thread total. */
+int icnnm_solver_tc_counters(icnnm_solver_t h, unsigned long long* out18);
 void icnnm_solver_destroy(icnnm_solver_t h);
 
 /* ------------------------------------------------------------------------

@@ -85,6 +85,7 @@ SIGNATURES = {
     "icnnm_solver_set_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "icnnm_solver_kernel_times": (C.c_int, [C.c_void_p, _dp]),
     "icnnm_solver_destroy": (None, [C.c_void_p]),
+    "icnnm_solver_tc_counters": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "icnnm_cuda_conv_forward": (C.c_int, [C.c_int, _lp, _dp, _lp, _dp, C.c_int, _dp]),
     "icnnm_cuda_conv_adjoint": (C.c_int, [C.c_int, _lp, _lp, _dp, C.c_int, _dp]),
     "icnnm_cuda_conv_forward_ex": (C.c_int, [C.c_int, _lp, _dp, _lp, _dp, C.c_int, C.c_int, _dp]),

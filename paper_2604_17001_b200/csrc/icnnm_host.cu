@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -334,8 +335,15 @@ inline int64_t tc_w_elems(const Geo& g, const TcPlan& t) {
 
 void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const float* src,
                       float* W, const float* Bpk, const float* cvec, float* adj, double* norm2,
-                      const IterState* st, cudaStream_t stream) {
+                      const IterState* st, cudaStream_t stream,
+                      unsigned long long* dbg = nullptr) {
   icnnm_dev::tc::TcArgs a{};
+  a.dbg = dbg;
+  static const int skip_env = [] {
+    const char* e = std::getenv("ICNNM_TC_SKIP");  // timing experiments only
+    return e ? std::atoi(e) : 0;
+  }();
+  a.skip = skip_env;
   a.g = gtc;
   a.src = src;
   a.Win = W;
@@ -448,7 +456,9 @@ struct Solver {
   int64_t observed = 0;
   int64_t launches = 0;
   bool profile = false;
+  bool tc_counters = false;
   double prof_ms[4] = {0, 0, 0, 0};
+  DBuf<unsigned long long> dbg;  // 2 x DBG_SLOTS tcgen05 pipeline counters
 
   ~Solver() {
     if (ev0) cudaEventDestroy(ev0);
@@ -602,7 +612,7 @@ void exchange_adj(Solver& S) {
 void launch_fwd(Solver& S, Slab& s, int mode) {
   if (S.engine == ICNNM_ENGINE_TF32X3) {
     launch_tc_kernel(s.gtc, S.tp, true, mode, s.Lt.p, s.W.p, S.BpkF.p, S.cvec.p, s.adj.p, S.red.p,
-                     S.st.p, S.stream);
+                     S.st.p, S.stream, S.tc_counters ? S.dbg.p : nullptr);
     ++S.launches;
     return;
   }
@@ -615,7 +625,8 @@ void launch_fwd(Solver& S, Slab& s, int mode) {
 void launch_adj(Solver& S, Slab& s) {
   if (S.engine == ICNNM_ENGINE_TF32X3) {
     launch_tc_kernel(s.gtc, S.tp, false, 1, s.Lt.p, s.W.p, S.BpkA.p, S.cvec.p, s.adj.p, S.red.p,
-                     S.st.p, S.stream);
+                     S.st.p, S.stream,
+                     S.tc_counters ? S.dbg.p + icnnm_dev::tc::DBG_SLOTS : nullptr);
     ++S.launches;
     return;
   }
@@ -671,6 +682,10 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   st0.max_iters = iters;
   CK(cudaMemcpyAsync(S.st.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, S.stream));
   S.launches = 0;
+  if (S.tc_counters) {
+    if (!S.dbg.p) S.dbg.alloc(2 * icnnm_dev::tc::DBG_SLOTS);
+    CK(cudaMemsetAsync(S.dbg.p, 0, S.dbg.bytes(), S.stream));
+  }
 
   const int64_t WT = p.dims[1] * p.dims[2];
   for (auto& s : S.slabs) {
@@ -949,7 +964,21 @@ int64_t icnnm_solver_device_bytes(icnnm_solver_t h) {
 int icnnm_solver_set_profile(icnnm_solver_t h, int enable) {
   return guard([&] {
     if (!h) invalid("null handle");
-    h->S.profile = enable != 0;
+    h->S.profile = (enable & 1) != 0;
+    h->S.tc_counters = (enable & 2) != 0;
+  });
+}
+
+int icnnm_solver_tc_counters(icnnm_solver_t h, unsigned long long* out) {
+  return guard([&] {
+    if (!h || !out) invalid("null argument");
+    const int n = 2 * icnnm_dev::tc::DBG_SLOTS;
+    if (!h->S.dbg.p) {
+      for (int i = 0; i < n; ++i) out[i] = 0;
+      return;
+    }
+    DeviceScope ds(h->S.device);
+    CK(cudaMemcpy(out, h->S.dbg.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   });
 }
 

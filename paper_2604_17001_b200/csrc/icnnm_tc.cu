@@ -142,6 +142,19 @@ __device__ __forceinline__ uint32_t idesc_tf32(int n) {
          (static_cast<uint32_t>(128 >> 4) << 24);
 }
 
+__device__ __forceinline__ long long clk() { return clock64(); }
+struct Dbg {
+  unsigned long long* p;
+  long long acc[2] = {0, 0};
+  __device__ explicit Dbg(unsigned long long* q) : p(q) {}
+  __device__ void flush(int s0, int s1) {
+    if (p) {
+      atomicAdd(p + s0, static_cast<unsigned long long>(acc[0]));
+      if (s1 >= 0) atomicAdd(p + s1, static_cast<unsigned long long>(acc[1]));
+    }
+  }
+};
+
 __device__ __forceinline__ int wrapi(int x, int n) {
   int r = x % n;
   return r < 0 ? r + n : r;
@@ -247,6 +260,7 @@ icnnm_tc_kernel(TcArgs a) {
     const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
     const uint32_t lane_base = static_cast<uint32_t>(32 * warp) << 16;
     uint32_t cnt = 0;
+    Dbg dbg(lane == 0 ? a.dbg : nullptr);
     for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
       if (FWD) {
         int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
@@ -267,9 +281,12 @@ icnnm_tc_kernel(TcArgs a) {
         for (int kc = 0; kc < nkc; ++kc, ++cnt) {
           const int sa = cnt % SA;
           const uint32_t ph = (cnt / SA) & 1;
+          long long t0c = dbg.p ? clk() : 0;
           mbar_wait(A_empty + sa, ph ^ 1);
           tc_fence_after();
+          long long t1c = dbg.p ? clk() : 0;
           uint32_t hi[32], lo[32];
+          if (!(a.skip & 1)) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             float x;
@@ -288,11 +305,18 @@ icnnm_tc_kernel(TcArgs a) {
           tmem_st32(tbase + lane_base + col, hi);
           tmem_st32(tbase + lane_base + col + 32, lo);
           tmem_wait_st();
+          }
           tc_fence_before();
           mbar_arrive(A_full + sa);
+          if (dbg.p) {
+            long long t2c = clk();
+            dbg.acc[0] += t1c - t0c;
+            dbg.acc[1] += t2c - t1c;
+          }
         }
       }
     }
+    dbg.flush(DBG_BUILD_WAIT, DBG_BUILD_WORK);
   } else if (warp < 8) {
     // ===================== epilogue =====================
     const int ew = warp - 4;
@@ -304,6 +328,7 @@ icnnm_tc_kernel(TcArgs a) {
     float* myob = ob + ew * nob;
     float* myred = red + ew * 32 * 33;
     uint32_t tcount = 0;
+    Dbg dbg(lane == 0 ? a.dbg : nullptr);
     for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
       int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
       const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
@@ -312,9 +337,11 @@ icnnm_tc_kernel(TcArgs a) {
         const int acc = tcount & 1;
         const uint32_t ph = (tcount >> 1) & 1;
         const int wn = (nt == ntn - 1) ? nlast : 128;
+        long long t0c = dbg.p ? clk() : 0;
         mbar_wait(ACC_full + acc, ph);
         tc_fence_after();
-        for (int c0 = 0; c0 < wn; c0 += 32) {
+        long long t1c = dbg.p ? clk() : 0;
+        for (int c0 = 0; c0 < wn && !(a.skip & 2); c0 += 32) {
           uint32_t u[32];
           tmem_ld32(tbase + lane_base + acc * 128 + c0, u);
           tmem_wait_ld();
@@ -350,6 +377,11 @@ icnnm_tc_kernel(TcArgs a) {
         }
         tc_fence_before();
         mbar_arrive(ACC_empty + acc);
+        if (dbg.p) {
+          long long t2c = clk();
+          dbg.acc[0] += t1c - t0c;
+          dbg.acc[1] += t2c - t1c;
+        }
       }
       if (!FWD) {
         // flush this brick's output bricks (one fp32 atomic per entry)
@@ -372,6 +404,7 @@ icnnm_tc_kernel(TcArgs a) {
         named_sync(2, 128);
       }
     }
+    dbg.flush(DBG_EPI_WAIT, DBG_EPI_WORK);
     if (FWD && a.norm2 != nullptr) {
       named_sync(2, 128);
       for (int j = row; j < g.kp; j += 128)
@@ -382,6 +415,7 @@ icnnm_tc_kernel(TcArgs a) {
     if (lane == 0) {
       uint32_t cnt = 0, bcnt = 0, tcount = 0;
       const uint32_t bs0 = smem_u32(Bst);
+      long long wa = 0, wb = 0, wacc = 0, tstart = a.dbg ? clk() : 0;
       for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
         for (int nt = 0; nt < ntn; ++nt, ++tcount) {
           const int acc = tcount & 1;
@@ -389,13 +423,22 @@ icnnm_tc_kernel(TcArgs a) {
           const int wn = (nt == ntn - 1) ? nlast : 128;
           const uint32_t idesc = idesc_tf32(wn);
           const uint32_t dcol = tbase + acc * 128;
+          long long q0 = a.dbg ? clk() : 0;
           mbar_wait(ACC_empty + acc, aph ^ 1);
+          if (a.dbg) wacc += clk() - q0;
           tc_fence_after();
           for (int kc = 0; kc < nkc; ++kc, ++cnt, ++bcnt) {
             const int sa = cnt % SA;
             const int sb = bcnt % SB;
+            long long q1 = a.dbg ? clk() : 0;
             mbar_wait(A_full + sa, (cnt / SA) & 1);
+            long long q2 = a.dbg ? clk() : 0;
             mbar_wait(B_full + sb, (bcnt / SB) & 1);
+            if (a.dbg) {
+              long long q3 = clk();
+              wa += q2 - q1;
+              wb += q3 - q2;
+            }
             tc_fence_after();
             const uint32_t acol = tbase + A_COL0 + sa * 64;
             const uint32_t bhi = bs0 + sb * B_STAGE_BYTES;
@@ -415,25 +458,35 @@ icnnm_tc_kernel(TcArgs a) {
           tc_commit(ACC_full + acc);
         }
       }
+      if (a.dbg) {
+        atomicAdd(a.dbg + DBG_MMA_WAIT_A, static_cast<unsigned long long>(wa));
+        atomicAdd(a.dbg + DBG_MMA_WAIT_B, static_cast<unsigned long long>(wb));
+        atomicAdd(a.dbg + DBG_MMA_WAIT_ACC, static_cast<unsigned long long>(wacc));
+        atomicAdd(a.dbg + DBG_TOTAL, static_cast<unsigned long long>(clk() - tstart));
+      }
     }
     __syncwarp();
   } else {
     // ===================== B loader =====================
     if (lane == 0) {
       uint32_t bcnt = 0;
+      long long wl = 0;
       for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
         for (int nt = 0; nt < ntn; ++nt) {
           const int wn = (nt == ntn - 1) ? nlast : 128;
           const uint32_t bytes = static_cast<uint32_t>(wn) * 256;
           for (int kc = 0; kc < nkc; ++kc, ++bcnt) {
             const int sb = bcnt % SB;
+            long long q0 = a.dbg ? clk() : 0;
             mbar_wait(B_empty + sb, ((bcnt / SB) & 1) ^ 1);
+            if (a.dbg) wl += clk() - q0;
             mbar_arrive_expect_tx(B_full + sb, bytes);
             const float* src = a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4);
             bulk_g2s(reinterpret_cast<uint8_t*>(Bst) + sb * B_STAGE_BYTES, src, bytes, B_full + sb);
           }
         }
       }
+      if (a.dbg) atomicAdd(a.dbg + DBG_LOAD_WAIT, static_cast<unsigned long long>(wl));
     }
     __syncwarp();
   }

@@ -32,7 +32,13 @@ struct TcArgs {
   int nlast;             // width of the last N-tile (multiple of 32)
   int ntj;               // j-tiles of the W layout
   int64_t nbricks;
+  unsigned long long* dbg;  // optional: per-role wait cycles (see DBG_*), or null
+  int skip;                 // timing experiments only: 1 = no build work, 2 = no epilogue work
 };
+
+// dbg slots (cycles summed over CTAs)
+enum { DBG_BUILD_WAIT = 0, DBG_BUILD_WORK, DBG_MMA_WAIT_A, DBG_MMA_WAIT_B, DBG_MMA_WAIT_ACC,
+       DBG_EPI_WAIT, DBG_EPI_WORK, DBG_LOAD_WAIT, DBG_TOTAL, DBG_SLOTS };
 
 template <bool FWD>
 __global__ void icnnm_tc_kernel(TcArgs a);

@@ -1,0 +1,29 @@
+"""Small driver for ncu: one config-C solve with a few iterations."""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_17001_b200 as P
+from paper_2604_17001_b200 import synth
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--engine", default="tf32x3")
+ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--runs", type=int, default=1)
+a = ap.parse_args()
+w = synth.WORKLOADS[a.config]
+X, mask = w.target(), w.mask()
+B = P.learn_ensemble_basis(w.training(), w.kernel)
+S = P.Solver(X.shape, B)
+S.upload(X * mask, mask)
+cfg = P.SolverConfig(max_iters=a.iters, tol_primal=1e-300, tol_change=1e-300, engine=a.engine)
+for _ in range(a.runs):
+    r = S.run(cfg)
+print(f"config {a.config} engine {a.engine}: {a.iters} iters in {r.loop_seconds*1e3:.2f} ms (loop)")
+if os.environ.get("ICNNM_TC_COUNTERS"):
+    S.set_profile(False, tc_counters=True)
+    r = S.run(cfg)
+    import json
+    c = S.tc_counters()
+    for k, d in c.items():
+        tot = max(d["mma_total"], 1)
+        print(k, {n: round(v / tot, 3) for n, v in d.items()}, "(fractions of MMA-thread cycles; builder/epi sums over 4 warps' lane 0)")
