@@ -269,14 +269,19 @@ void pack_basis(const Problem& p, const double* Kcm, std::vector<float>& Krm,
 // tcgen05 engine plan and B packing
 // ---------------------------------------------------------------------------
 struct TcPlan {
-  int kp = 0, ntn = 0, nkc = 0, nlast = 0;
+  int kp = 0, ntn = 0, nkc = 0, nlast = 0, wbase = 0;
+  int width(int nt) const { return std::min(wbase, kp - nt * wbase); }
 };
 
+// N-tiling: tiles of 128 columns (+ a narrower last tile).  Measured on B200
+// (tools/ubench/mma_rate.cu): an M=128 kind::tf32 MMA costs max(64, N/2)
+// cycles, so splitting into narrower balanced tiles gains nothing.
 TcPlan tc_plan(const Problem& p) {
   TcPlan t;
   t.kp = p.kp_tc;
-  t.ntn = (t.kp + icnnm_dev::tc::NTMAX - 1) / icnnm_dev::tc::NTMAX;
-  t.nlast = t.kp - (t.ntn - 1) * icnnm_dev::tc::NTMAX;
+  t.wbase = icnnm_dev::tc::NTMAX;
+  t.ntn = (t.kp + t.wbase - 1) / t.wbase;
+  t.nlast = t.kp - (t.ntn - 1) * t.wbase;
   t.nkc = t.kp / icnnm_dev::tc::KC;
   return t;
 }
@@ -305,13 +310,13 @@ std::vector<float> pack_b_tiles(const Problem& p, const TcPlan& t, const double*
   const int blk = icnnm_dev::tc::B_STAGE_BYTES / 4;
   std::vector<float> out(static_cast<size_t>(t.ntn) * t.nkc * blk, 0.f);
   for (int nt = 0; nt < t.ntn; ++nt) {
-    const int wn = (nt == t.ntn - 1) ? t.nlast : icnnm_dev::tc::NTMAX;
+    const int wn = t.width(nt);
     for (int kc = 0; kc < t.nkc; ++kc) {
       float* base = out.data() + (static_cast<size_t>(nt) * t.nkc + kc) * blk;
       for (int q = 0; q < 4; ++q)
         for (int n = 0; n < wn; ++n)
           for (int k8 = 0; k8 < 8; ++k8) {
-            const int nn = nt * icnnm_dev::tc::NTMAX + n;
+            const int nn = nt * t.wbase + n;
             const int kk = kc * icnnm_dev::tc::KC + q * 8 + k8;
             double x = 0.0;
             if (nn < k && kk < k)
@@ -357,16 +362,23 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   a.ntn = t.ntn;
   a.nkc = t.nkc;
   a.nlast = t.nlast;
+  a.wbase = t.wbase;
   a.ntj = t.ntn;
+  // stage counts that fit in shared memory (227 KB opt-in)
+  a.sb = icnnm_dev::tc::SB;
+  a.ws = icnnm_dev::tc::WS;
+  while (icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws) > 227 * 1024 && a.ws > 2) --a.ws;
+  while (icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws) > 227 * 1024 && a.sb > 2) --a.sb;
   a.nbricks = n_bricks(gtc);
   int dev = 0, nsm = 148;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.nbricks, nsm));
   void* args[] = {&a};
-  const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd);
+  const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws);
+  if (smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
   CK(cudaLaunchKernel(fwd ? icnnm_dev::tc::fwd_kernel_ptr() : icnnm_dev::tc::adj_kernel_ptr(),
-                      dim3(grid), dim3(320), args, smem, stream));
+                      dim3(grid), dim3(icnnm_dev::tc::threads(fwd)), args, smem, stream));
 }
 
 // EigenBasis::validate (spectral.cpp:25-41).
@@ -490,8 +502,8 @@ void solver_alloc(Solver& S) {
     s.L.alloc(s.m_own);
     s.V.alloc(s.m_own);
     s.gtc = tc_geo(s.g, S.tp);
-    check_smem(icnnm_dev::tc::smem_bytes(s.gtc, true));
-    check_smem(icnnm_dev::tc::smem_bytes(s.gtc, false));
+    check_smem(icnnm_dev::tc::smem_bytes(s.gtc, true, 2, 2));
+    check_smem(icnnm_dev::tc::smem_bytes(s.gtc, false, 2, 2));
     s.W.alloc(std::max<int64_t>(n_bricks(s.g) * BM * p.kp, tc_w_elems(s.gtc, S.tp)));
     CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
   }
@@ -1044,7 +1056,7 @@ int icnnm_cuda_conv_forward_ex(int order, const int64_t* dims, const double* L,
     if (engine == ICNNM_ENGINE_TF32X3) {
       TcPlan t = tc_plan(p);
       Geo gt = tc_geo(g, t);
-      check_smem(icnnm_dev::tc::smem_bytes(gt, true));
+      check_smem(icnnm_dev::tc::smem_bytes(gt, true, 2, 2));
       auto bf = pack_b_tiles(p, t, K_colmajor, true);
       DBuf<float> dB(bf.size()), dW(tc_w_elems(gt, t));
       DBuf<double> dn(t.kp);
@@ -1109,7 +1121,7 @@ int icnnm_cuda_conv_adjoint_ex(int order, const int64_t* dims, const int64_t* kd
     if (engine == ICNNM_ENGINE_TF32X3) {
       TcPlan t = tc_plan(p);
       Geo gt = tc_geo(g, t);
-      check_smem(icnnm_dev::tc::smem_bytes(gt, false));
+      check_smem(icnnm_dev::tc::smem_bytes(gt, false, 2, 2));
       std::vector<double> I(static_cast<size_t>(p.k) * p.k, 0.0);
       for (int j = 0; j < p.k; ++j) I[static_cast<size_t>(j) * p.k + j] = 1.0;
       auto ba = pack_b_tiles(p, t, I.data(), false);

@@ -93,6 +93,29 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t d, uint32_t a, uint64_t bdesc
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
+// Issued by one elected lane of a converged warp (the warp-uniform operands
+// stay in uniform registers; no per-MMA divergence).
+__device__ __forceinline__ void tc_mma_ts_elect(uint32_t d, uint32_t a, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ uint32_t f2tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
@@ -160,12 +183,42 @@ __device__ __forceinline__ int wrapi(int x, int n) {
   return r < 0 ? r + n : r;
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};\n" ::"r"(taddr),
+      R8(0), R8(8)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+__device__ __forceinline__ int tile_width(const TcArgs& a, int nt) {
+  const int w = a.g.kp - nt * a.wbase;
+  return w < a.wbase ? w : a.wbase;
+}
+
 // ---------------------------------------------------------------------------
 // The kernel (FWD = forward implicit GEMM, !FWD = adjoint)
+//   warps [0, 8)            builders (two per TMEM lane quadrant, 16 K each)
+//   warps [8, 8 + NEPI)     epilogue (NEPI = 8 forward, 4 adjoint)
+//   warp  8 + NEPI          MMA issuer
+//   warp  9 + NEPI          B loader
 // ---------------------------------------------------------------------------
 template <bool FWD>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(FWD ? 576 : 448, 1)
 icnnm_tc_kernel(TcArgs a) {
+  constexpr int NB = 8;                  // builder warps
+  constexpr int NEPI = FWD ? 8 : 4;      // epilogue warps
+  constexpr int WMMA = NB + NEPI;        // MMA warp
+  constexpr int WLOAD = NB + NEPI + 1;   // loader warp
   const Geo& g = a.g;
   float rr = 0.f;
   if (a.mode == 1) {
@@ -174,44 +227,48 @@ icnnm_tc_kernel(TcArgs a) {
     rr = static_cast<float>(a.st->r);
   }
   extern __shared__ __align__(1024) uint8_t smem[];
-  // ---- carve shared memory ----
   uint8_t* p = smem;
-  float* Bst = reinterpret_cast<float*>(p);             // SB x B_STAGE_BYTES
-  p += SB * B_STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(p);      // 2*SA + 2*SB + 4
+  const int sbn = a.sb, wsn = a.ws;
+  float* Bst = reinterpret_cast<float*>(p);
+  p += sbn * B_STAGE_BYTES;
+  float* Wst = reinterpret_cast<float*>(p);   // adjoint: W-chunk ring
+  if (!FWD) p += wsn * W_STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p);
   uint64_t* A_full = bars;
   uint64_t* A_empty = bars + SA;
   uint64_t* B_full = bars + 2 * SA;
   uint64_t* B_empty = bars + 2 * SA + SB;
   uint64_t* ACC_full = bars + 2 * SA + 2 * SB;
   uint64_t* ACC_empty = ACC_full + 2;
-  p += 128;
+  uint64_t* W_full = ACC_empty + 2;
+  uint64_t* W_empty = W_full + WS;
+  p += 256;  // 26 mbarriers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p);
   p += 16;
-  int* tapoff = reinterpret_cast<int*>(p);              // ktp
+  int* tapoff = reinterpret_cast<int*>(p);
   p += ((g.ktp * 4 + 15) / 16) * 16;
-  float* cs = reinterpret_cast<float*>(p);              // kp
+  float* cs = reinterpret_cast<float*>(p);
   p += ((g.kp * 4 + 15) / 16) * 16;
   const int nob = g.HH * g.HW * g.HT;
-  // FWD: halo (nob) | red scratch 4 x 32 x 33 | nrm (kp doubles)
-  // ADJ: 4 output bricks (4 x nob)
+  const int nobp = ((nob + 3) / 4) * 4;
+  // FWD: halo[2] (2 x nobp) | red (8 x 32 x 33) | nrm (kp doubles)
+  // ADJ: 4 output bricks (4 x nobp)
   float* halo = reinterpret_cast<float*>(p);
-  float* red = halo + ((nob + 3) / 4) * 4;
-  double* nrm = reinterpret_cast<double*>(red + 4 * 32 * 33);
+  float* red = halo + 2 * nobp;
+  double* nrm = reinterpret_cast<double*>(red + NEPI * 32 * 33);
   float* ob = reinterpret_cast<float*>(p);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
 
-  // ---- one-time setup ----
-  if (warp == 8) {
+  if (warp == WMMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
         smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
     for (int i = 0; i < SA; ++i) {
-      mbar_init(A_full + i, 128);
+      mbar_init(A_full + i, NB * 32);
       mbar_init(A_empty + i, 1);
     }
     for (int i = 0; i < SB; ++i) {
@@ -220,7 +277,11 @@ icnnm_tc_kernel(TcArgs a) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(ACC_full + i, 1);
-      mbar_init(ACC_empty + i, 128);
+      mbar_init(ACC_empty + i, NEPI * 32);
+    }
+    for (int i = 0; i < WS; ++i) {
+      mbar_init(W_full + i, 1);
+      mbar_init(W_empty + i, NB * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -240,7 +301,7 @@ icnnm_tc_kernel(TcArgs a) {
   if (FWD) {
     for (int j = tid; j < g.kp; j += blockDim.x) nrm[j] = 0.0;
   } else {
-    for (int e = tid; e < 4 * nob; e += blockDim.x) ob[e] = 0.f;
+    for (int e = tid; e < 4 * nobp; e += blockDim.x) ob[e] = 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -248,66 +309,74 @@ icnnm_tc_kernel(TcArgs a) {
   const uint32_t tbase = *tmem_slot;
 
   const int nbr = static_cast<int>(a.nbricks);
-  const int ntn = a.ntn;                 // N-tiles per brick
-  const int nkc = a.nkc;                 // K-chunks per tile
-  const int nlast = a.nlast;             // width of the last N-tile
+  const int ntn = a.ntn;
+  const int nkc = a.nkc;
 
-  if (warp < 4) {
+  if (warp < NB && !(a.skip & 8)) {
     // ===================== builders =====================
-    const int row = tid;                 // TMEM lane / voxel of the brick
-    const int v = row;
-    const int vt = v % g.bt, vw = (v / g.bt) % g.bw, vh = v / (g.bt * g.bw);
+    const int quad = warp & 3, half = warp >> 2;
+    const int row = 32 * quad + lane;
+    const int bt_tid = tid;                       // 0..255
+    const int vt = row % g.bt, vw = (row / g.bt) % g.bw, vh = row / (g.bt * g.bw);
     const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
-    const uint32_t lane_base = static_cast<uint32_t>(32 * warp) << 16;
+    const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
     uint32_t cnt = 0;
     Dbg dbg(lane == 0 ? a.dbg : nullptr);
-    for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
-      if (FWD) {
-        int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
-        const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
-        named_sync(1, 128);  // previous brick fully built
-        for (int e = tid; e < nob; e += 128) {
-          int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
-          int hs = h0 - (g.kh - 1) + aa + g.hoff;
-          hs = g.wrapH ? wrapi(hs, g.Hsrc) : (hs < 0 ? 0 : (hs >= g.Hsrc ? g.Hsrc - 1 : hs));
-          int ws = wrapi(w0 - (g.kw - 1) + bb, g.W);
-          int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
-          halo[e] = __ldg(a.src + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts);
-        }
-        named_sync(1, 128);
+    auto issue_halo = [&](float* dst, int b) {
+      int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
+      const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
+      for (int e = bt_tid; e < nob; e += NB * 32) {
+        int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
+        int hs = h0 - (g.kh - 1) + aa + g.hoff;
+        hs = g.wrapH ? wrapi(hs, g.Hsrc) : (hs < 0 ? 0 : (hs >= g.Hsrc ? g.Hsrc - 1 : hs));
+        int ws = wrapi(w0 - (g.kw - 1) + bb, g.W);
+        int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
+        cp_async4(dst + e, a.src + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts);
       }
-      const float* Wrow = FWD ? nullptr : a.Win + static_cast<size_t>(b) * a.ntj * 128 * 128 + row;
+      cp_async_commit();
+    };
+    if (FWD) {
+      if (blockIdx.x < nbr) issue_halo(halo, blockIdx.x);
+    }
+    int iter = 0;
+    for (int b = blockIdx.x; b < nbr; b += gridDim.x, ++iter) {
+      const float* hcur = halo + (iter & 1) * nobp;
+      if (FWD) {
+        cp_async_wait_all();
+        named_sync(1, NB * 32);  // this brick's halo landed; previous brick fully built
+        if (b + static_cast<int>(gridDim.x) < nbr)
+          issue_halo(halo + ((iter + 1) & 1) * nobp, b + gridDim.x);
+      }
       for (int nt = 0; nt < ntn; ++nt) {
         for (int kc = 0; kc < nkc; ++kc, ++cnt) {
           const int sa = cnt % SA;
           const uint32_t ph = (cnt / SA) & 1;
+          const int wsi = cnt % wsn;
+          const uint32_t wph = (cnt / wsn) & 1;
           long long t0c = dbg.p ? clk() : 0;
           mbar_wait(A_empty + sa, ph ^ 1);
+          if (!FWD) mbar_wait(W_full + wsi, wph);
           tc_fence_after();
           long long t1c = dbg.p ? clk() : 0;
-          uint32_t hi[32], lo[32];
           if (!(a.skip & 1)) {
+            uint32_t hi[16], lo[16];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            float x;
-            const int q = kc * KC + i;
-            if (FWD) {
-              x = halo[hidx - tapoff[q]];
-            } else {
-              const int jt = q >> 7, jj = q & 127;
-              x = __ldg(Wrow + (static_cast<size_t>(jt) * 128 + jj) * 128) * cs[q];
+            for (int i = 0; i < 16; ++i) {
+              const int q = kc * KC + 16 * half + i;
+              const float x = FWD ? hcur[hidx - tapoff[q]]
+                                  : Wst[wsi * (W_STAGE_BYTES / 4) + (16 * half + i) * 128 + row] * cs[q];
+              const uint32_t h = f2tf32(x);
+              hi[i] = h;
+              lo[i] = __float_as_uint(x - __uint_as_float(h));
             }
-            const uint32_t h = f2tf32(x);
-            hi[i] = h;
-            lo[i] = __float_as_uint(x - __uint_as_float(h));
-          }
-          const uint32_t col = A_COL0 + sa * 64;
-          tmem_st32(tbase + lane_base + col, hi);
-          tmem_st32(tbase + lane_base + col + 32, lo);
-          tmem_wait_st();
+            const uint32_t col = A_COL0 + sa * 64 + 16 * half;
+            tmem_st16(tbase + lane_base + col, hi);
+            tmem_st16(tbase + lane_base + col + 32, lo);
+            tmem_wait_st();
           }
           tc_fence_before();
           mbar_arrive(A_full + sa);
+          if (!FWD) mbar_arrive(W_empty + wsi);
           if (dbg.p) {
             long long t2c = clk();
             dbg.acc[0] += t1c - t0c;
@@ -317,16 +386,18 @@ icnnm_tc_kernel(TcArgs a) {
       }
     }
     dbg.flush(DBG_BUILD_WAIT, DBG_BUILD_WORK);
-  } else if (warp < 8) {
+  } else if (warp < NB) {
+  } else if (warp < NB + NEPI && !(a.skip & 32)) {
     // ===================== epilogue =====================
-    const int ew = warp - 4;
-    const int row = 32 * ew + lane;
-    const uint32_t lane_base = static_cast<uint32_t>(32 * ew) << 16;
-    const int v = row;
-    const int vt = v % g.bt, vw = (v / g.bt) % g.bw, vh = v / (g.bt * g.bw);
+    const int ew = warp - NB;
+    const int quad = ew & 3, half = ew >> 2;     // half in {0} (adjoint) or {0,1} (forward)
+    const int row = 32 * quad + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
+    const int vt = row % g.bt, vw = (row / g.bt) % g.bw, vh = row / (g.bt * g.bw);
     const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
-    float* myob = ob + ew * nob;
+    float* myob = ob + quad * nobp;
     float* myred = red + ew * 32 * 33;
+    constexpr int NHALF = NEPI / 4;
     uint32_t tcount = 0;
     Dbg dbg(lane == 0 ? a.dbg : nullptr);
     for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
@@ -336,24 +407,30 @@ icnnm_tc_kernel(TcArgs a) {
       for (int nt = 0; nt < ntn; ++nt, ++tcount) {
         const int acc = tcount & 1;
         const uint32_t ph = (tcount >> 1) & 1;
-        const int wn = (nt == ntn - 1) ? nlast : 128;
+        const int wn = tile_width(a, nt);
         long long t0c = dbg.p ? clk() : 0;
         mbar_wait(ACC_full + acc, ph);
         tc_fence_after();
         long long t1c = dbg.p ? clk() : 0;
-        for (int c0 = 0; c0 < wn && !(a.skip & 2); c0 += 32) {
+        for (int c0 = 32 * half; c0 < wn && !(a.skip & 2); c0 += 32 * NHALF) {
           uint32_t u[32];
           tmem_ld32(tbase + lane_base + acc * 128 + c0, u);
           tmem_wait_ld();
+          const int ncol = (wn - c0) < 32 ? (wn - c0) : 32;
           if (FWD) {
-            float* wp = a.Wout + ((static_cast<size_t>(b) * a.ntj + nt) * 128 + c0) * 128 + row;
-            const int j0 = nt * 128 + c0;
+            const int j0 = nt * a.wbase + c0;
+            float* wp = a.Wout + ((static_cast<size_t>(b) * a.ntj + (j0 >> 7)) * 128 + (j0 & 127)) * 128 + row;
+            float wo[32];
+            if (a.mode == 1) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) wo[i] = (i < ncol) ? wp[static_cast<size_t>(i) * 128] : 0.f;
+            }
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               float w = __uint_as_float(u[i]);
-              if (a.mode == 1) w = fmaf(rr * cs[j0 + i], wp[static_cast<size_t>(i) * 128], w);
-              w = valid ? w : 0.f;
-              if (c0 + i < wn) wp[static_cast<size_t>(i) * 128] = w;
+              if (a.mode == 1) w = fmaf(rr * cs[j0 + i], wo[i], w);
+              w = (valid && i < ncol) ? w : 0.f;
+              if (i < ncol) wp[static_cast<size_t>(i) * 128] = w;
               myred[i * 33 + lane] = w * w;
             }
             __syncwarp();
@@ -361,13 +438,13 @@ icnnm_tc_kernel(TcArgs a) {
 #pragma unroll 8
             for (int i = 0; i < 32; ++i) s += myred[lane * 33 + i];
             __syncwarp();
-            if (c0 + lane < wn) atomicAdd(nrm + j0 + lane, static_cast<double>(s));
+            if (lane < ncol) atomicAdd(nrm + j0 + lane, static_cast<double>(s));
           } else {
-            const int s0 = nt * 128 + c0;
+            const int s0 = nt * a.wbase + c0;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const int s = s0 + i;
-              if (s < g.k) {
+              if (i < ncol && s < g.k) {
                 float* o = myob + (hidx - tapoff[s]);
                 *o += __uint_as_float(u[i]);
               }
@@ -384,14 +461,13 @@ icnnm_tc_kernel(TcArgs a) {
         }
       }
       if (!FWD) {
-        // flush this brick's output bricks (one fp32 atomic per entry)
-        named_sync(2, 128);
+        named_sync(2, NEPI * 32);
         for (int e = row; e < nob; e += 128) {
-          float s = ob[e] + ob[nob + e] + ob[2 * nob + e] + ob[3 * nob + e];
+          float s = ob[e] + ob[nobp + e] + ob[2 * nobp + e] + ob[3 * nobp + e];
           ob[e] = 0.f;
-          ob[nob + e] = 0.f;
-          ob[2 * nob + e] = 0.f;
-          ob[3 * nob + e] = 0.f;
+          ob[nobp + e] = 0.f;
+          ob[2 * nobp + e] = 0.f;
+          ob[3 * nobp + e] = 0.f;
           if (s == 0.f) continue;
           int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
           int hs = h0 - (g.kh - 1) + aa + g.hoff;
@@ -401,18 +477,19 @@ icnnm_tc_kernel(TcArgs a) {
           int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
           atomicAdd(a.adj + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts, s);
         }
-        named_sync(2, 128);
+        named_sync(2, NEPI * 32);
       }
     }
     dbg.flush(DBG_EPI_WAIT, DBG_EPI_WORK);
     if (FWD && a.norm2 != nullptr) {
-      named_sync(2, 128);
-      for (int j = row; j < g.kp; j += 128)
+      named_sync(2, NEPI * 32);
+      for (int j = ew * 32 + lane; j < g.kp; j += NEPI * 32)
         if (nrm[j] != 0.0) atomicAdd(a.norm2 + j, nrm[j]);
     }
-  } else if (warp == 8) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
+  } else if (warp < NB + NEPI) {
+  } else if (warp == WMMA) {
+    // ===================== MMA issuer (converged warp, elected lane issues) =====================
+    {
       uint32_t cnt = 0, bcnt = 0, tcount = 0;
       const uint32_t bs0 = smem_u32(Bst);
       long long wa = 0, wb = 0, wacc = 0, tstart = a.dbg ? clk() : 0;
@@ -420,20 +497,20 @@ icnnm_tc_kernel(TcArgs a) {
         for (int nt = 0; nt < ntn; ++nt, ++tcount) {
           const int acc = tcount & 1;
           const uint32_t aph = (tcount >> 1) & 1;
-          const int wn = (nt == ntn - 1) ? nlast : 128;
+          const int wn = tile_width(a, nt);
           const uint32_t idesc = idesc_tf32(wn);
           const uint32_t dcol = tbase + acc * 128;
           long long q0 = a.dbg ? clk() : 0;
-          mbar_wait(ACC_empty + acc, aph ^ 1);
+          if (!(a.skip & 32)) mbar_wait(ACC_empty + acc, aph ^ 1);
           if (a.dbg) wacc += clk() - q0;
           tc_fence_after();
           for (int kc = 0; kc < nkc; ++kc, ++cnt, ++bcnt) {
             const int sa = cnt % SA;
-            const int sb = bcnt % SB;
+            const int sb = bcnt % sbn;
             long long q1 = a.dbg ? clk() : 0;
-            mbar_wait(A_full + sa, (cnt / SA) & 1);
+            if (!(a.skip & 8)) mbar_wait(A_full + sa, (cnt / SA) & 1);
             long long q2 = a.dbg ? clk() : 0;
-            mbar_wait(B_full + sb, (bcnt / SB) & 1);
+            if (!(a.skip & 16)) mbar_wait(B_full + sb, (bcnt / sbn) & 1);
             if (a.dbg) {
               long long q3 = clk();
               wa += q2 - q1;
@@ -448,17 +525,17 @@ icnnm_tc_kernel(TcArgs a) {
               const uint64_t dh = bdesc(bhi + q * wn * 32);
               const uint64_t dl = bdesc(blo + q * wn * 32);
               const uint32_t first = (kc == 0 && q == 0) ? 0u : 1u;
-              tc_mma_ts(dcol, acol + q * 8, dh, idesc, first);
-              tc_mma_ts(dcol, acol + 32 + q * 8, dh, idesc, 1u);
-              tc_mma_ts(dcol, acol + q * 8, dl, idesc, 1u);
+              tc_mma_ts_elect(dcol, acol + q * 8, dh, idesc, first);
+              tc_mma_ts_elect(dcol, acol + 32 + q * 8, dh, idesc, 1u);
+              tc_mma_ts_elect(dcol, acol + q * 8, dl, idesc, 1u);
             }
-            tc_commit(A_empty + sa);
-            tc_commit(B_empty + sb);
+            if (!(a.skip & 8)) tc_commit_elect(A_empty + sa);
+            if (!(a.skip & 16)) tc_commit_elect(B_empty + sb);
           }
-          tc_commit(ACC_full + acc);
+          if (!(a.skip & 32)) tc_commit_elect(ACC_full + acc);
         }
       }
-      if (a.dbg) {
+      if (a.dbg && lane == 0) {
         atomicAdd(a.dbg + DBG_MMA_WAIT_A, static_cast<unsigned long long>(wa));
         atomicAdd(a.dbg + DBG_MMA_WAIT_B, static_cast<unsigned long long>(wb));
         atomicAdd(a.dbg + DBG_MMA_WAIT_ACC, static_cast<unsigned long long>(wacc));
@@ -468,18 +545,22 @@ icnnm_tc_kernel(TcArgs a) {
     __syncwarp();
   } else {
     // ===================== B loader =====================
-    if (lane == 0) {
+    if (lane == 0 && !(a.skip & 16)) {
       uint32_t bcnt = 0;
       long long wl = 0;
       for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
         for (int nt = 0; nt < ntn; ++nt) {
-          const int wn = (nt == ntn - 1) ? nlast : 128;
+          const int wn = tile_width(a, nt);
           const uint32_t bytes = static_cast<uint32_t>(wn) * 256;
           for (int kc = 0; kc < nkc; ++kc, ++bcnt) {
-            const int sb = bcnt % SB;
+            const int sb = bcnt % sbn;
             long long q0 = a.dbg ? clk() : 0;
-            mbar_wait(B_empty + sb, ((bcnt / SB) & 1) ^ 1);
+            mbar_wait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
             if (a.dbg) wl += clk() - q0;
+            if (a.skip & 4) {
+              mbar_arrive(B_full + sb);  // timing experiment: no B traffic
+              continue;
+            }
             mbar_arrive_expect_tx(B_full + sb, bytes);
             const float* src = a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4);
             bulk_g2s(reinterpret_cast<uint8_t*>(Bst) + sb * B_STAGE_BYTES, src, bytes, B_full + sb);
@@ -488,13 +569,31 @@ icnnm_tc_kernel(TcArgs a) {
       }
       if (a.dbg) atomicAdd(a.dbg + DBG_LOAD_WAIT, static_cast<unsigned long long>(wl));
     }
+    if (!FWD && lane == 1) {
+      // adjoint: stream W chunks (32 columns x 128 rows, 16 KB contiguous in
+      // the [brick][jt][jj][row] layout) ahead of the builders
+      uint32_t wcnt = 0;
+      for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+        for (int nt = 0; nt < ntn; ++nt) {
+          for (int kc = 0; kc < nkc; ++kc, ++wcnt) {
+            const int wsi = wcnt % wsn;
+            mbar_wait(W_empty + wsi, ((wcnt / wsn) & 1) ^ 1);
+            mbar_arrive_expect_tx(W_full + wsi, W_STAGE_BYTES);
+            const int j0 = kc * KC;
+            const float* src = a.Win + ((static_cast<size_t>(b) * a.ntj + (j0 >> 7)) * 128 + (j0 & 127)) * 128;
+            bulk_g2s(reinterpret_cast<uint8_t*>(Wst) + wsi * W_STAGE_BYTES, src, W_STAGE_BYTES,
+                     W_full + wsi);
+          }
+        }
+      }
+    }
     __syncwarp();
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 8) {
+  if (warp == WMMA) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
   }
 }

@@ -11,7 +11,9 @@ namespace tc {
 
 constexpr int KC = 32;                         // K per chunk (4 MMA K-steps of 8)
 constexpr int SA = 4;                          // TMEM A stages (64 columns each)
-constexpr int SB = 3;                          // SMEM B stages
+constexpr int SB = 3;                          // SMEM B stages (max; runtime a.sb)
+constexpr int WS = 4;                          // adjoint: SMEM W-chunk stages (max; runtime a.ws)
+constexpr int W_STAGE_BYTES = 128 * KC * 4;    // 16 KB: 32 columns x 128 rows
 constexpr int NTMAX = 128;                     // accumulator width (N per tile)
 constexpr int B_STAGE_BYTES = NTMAX * KC * 4 * 2;  // hi + lo = 32 KB
 constexpr int A_COL0 = 256;                    // TMEM columns 0..255: 2 accumulators
@@ -29,11 +31,14 @@ struct TcArgs {
   int mode;              // 0: plain operator, 1: ADMM iteration
   int ntn;               // N-tiles per brick
   int nkc;               // K-chunks per N-tile
-  int nlast;             // width of the last N-tile (multiple of 32)
+  int nlast;             // width of the last N-tile (multiple of 16)
+  int wbase;             // width of the other N-tiles (multiple of 16, <= 128)
   int ntj;               // j-tiles of the W layout
   int64_t nbricks;
   unsigned long long* dbg;  // optional: per-role wait cycles (see DBG_*), or null
   int skip;                 // timing experiments only: 1 = no build work, 2 = no epilogue work
+  int sb;                   // B stages used (<= SB)
+  int ws;                   // adjoint W stages used (<= WS)
 };
 
 // dbg slots (cycles summed over CTAs)
@@ -46,15 +51,18 @@ __global__ void icnnm_tc_kernel(TcArgs a);
 void* fwd_kernel_ptr();
 void* adj_kernel_ptr();
 
-inline size_t smem_bytes(const Geo& g, bool fwd) {
+inline int threads(bool fwd) { return fwd ? 576 : 448; }
+
+inline size_t smem_bytes(const Geo& g, bool fwd, int sb = SB, int ws = WS) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
-  size_t b = static_cast<size_t>(SB) * B_STAGE_BYTES + 128 + 16;
+  const size_t nobp = ((nob + 3) / 4) * 4;
+  size_t b = static_cast<size_t>(sb) * B_STAGE_BYTES + (fwd ? 0 : static_cast<size_t>(ws) * W_STAGE_BYTES) + 256 + 16;
   b += ((g.ktp * 4 + 15) / 16) * 16;
   b += ((g.kp * 4 + 15) / 16) * 16;
   if (fwd)
-    b += ((nob + 3) / 4) * 16 + 4 * 32 * 33 * 4 + static_cast<size_t>(g.kp) * 8;
+    b += 2 * nobp * 4 + 8 * 32 * 33 * 4 + static_cast<size_t>(g.kp) * 8;
   else
-    b += 4 * nob * 4;
+    b += 4 * nobp * 4;
   return b;
 }
 

@@ -24,6 +24,15 @@ if os.environ.get("ICNNM_TC_COUNTERS"):
     r = S.run(cfg)
     import json
     c = S.tc_counters()
+    nsm = 148
+    nb = (X.size // 128)
+    ntn = (w.k + 31) // 32 * 32
+    import math
+    nt_tiles = math.ceil(ntn / 128); nkc = ntn // 32
+    mmas = nb * nt_tiles * nkc * 12
     for k, d in c.items():
         tot = max(d["mma_total"], 1)
+        print(k, "MMA-thread cycles per CTA per launch: %.0f" % (tot / nsm / a.iters),
+              "cycles per MMA issued: %.1f" % (tot / (mmas * a.iters)),
+              "kernel time per launch (ms):", S.kernel_times_ms() if False else "")
         print(k, {n: round(v / tot, 3) for n, v in d.items()}, "(fractions of MMA-thread cycles; builder/epi sums over 4 warps' lane 0)")
