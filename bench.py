@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--engine", default="ffma")
+    ap.add_argument("--engine", default="tf32x3", choices=["tf32x3", "ffma"])
     ap.add_argument("--iters", type=int, default=0, help="override iterations per solve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -105,6 +105,45 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
                 "samples": len(self.rows)}
+
+
+def measure_tf32_peak(dev: int) -> float:
+    """Dense TF32 tensor throughput (cuBLAS 8192^3, best of 5) on this GPU --
+    the denominator of the TF32x3 engine's roofline (MEASURED_PEAKS.json has
+    only bf16)."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=f"cuda:{dev}")
+        b = torch.randn(n, n, device=f"cuda:{dev}")
+        for _ in range(2):
+            a @ b
+        best = 0.0
+        for _ in range(5):
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+            a @ b
+            s1.record()
+            s1.synchronize()
+            best = max(best, 2 * n ** 3 / (s0.elapsed_time(s1) * 1e-3) / 1e12)
+        del a, b
+        return best
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def load_ncu_traffic(engine: str):
+    """dram bytes per launch of the dominant kernels from the committed ncu
+    --set full capture (profiles/ncu_summary_*.json), if present."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary_latest.json")) as f:
+            d = json.load(f)
+        return d.get(engine)
+    except Exception:
+        return None
 
 
 def load_peaks():
@@ -249,13 +288,29 @@ def main():
     line = None
     if rank == 0:
         peaks = load_peaks()
-        ffma_peak = P.probe_ffma_tflops(dev)
         k = w.k
         flops_fwd = 2.0 * w.m * k * k            # algorithmic, per launch
         flops_adj = 2.0 * w.m * k * k
         dom = "forward" if kt["forward"] >= kt["adjoint"] else "adjoint"
         t_dom = kt[dom] * 1e-3
         achieved = (flops_fwd if dom == "forward" else flops_adj) / t_dom / 1e12
+        if args.engine == "tf32x3":
+            tf32 = measure_tf32_peak(dev)
+            roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": tf32 / 3.0,
+                    "unit": "TFLOP/s", "frac": achieved / (tf32 / 3.0),
+                    "peak_source": "measured dense TF32 (cuBLAS 8192^3 burst, %.0f TFLOP/s) / 3 "
+                                   "tensor MMAs per fp32 product" % tf32,
+                    "tensor_pipe_frac": 3.0 * achieved / tf32}
+        else:
+            ffma_peak = P.probe_ffma_tflops(dev)
+            roof = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": ffma_peak,
+                    "unit": "TFLOP/s", "frac": achieved / ffma_peak,
+                    "peak_source": "measured FFMA probe (icnnm_probe_ffma_tflops)"}
+        traffic = load_ncu_traffic(args.engine)
+        roof["traffic"] = traffic.get(dom) if isinstance(traffic, dict) else None
+        roof["algorithmic_bytes"] = (8.0 if dom == "forward" else 4.0) * w.m * k
+        roof["per_launch_ms"] = kt
+        roof["flops_per_launch"] = flops_fwd
         e2e = None
         if not args.no_e2e:
             e2e_t = []
@@ -287,11 +342,7 @@ def main():
                            w.m * ((k + 63) // 64 * 64) * 4 / 1e9),
                        "parallelism": f"batch split x{world} (independent tensors)"},
             "psnr_db": psnr,
-            "roofline": {"bound": "fp32", "kernel": dom, "achieved": achieved,
-                         "peak": ffma_peak, "unit": "TFLOP/s", "frac": achieved / ffma_peak,
-                         "traffic": None,
-                         "peak_source": "measured FFMA probe (icnnm_probe_ffma_tflops)",
-                         "per_launch_ms": kt, "flops_per_launch": flops_fwd},
+            "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
