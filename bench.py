@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--iters", type=int, default=0, help="override iterations per solve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dims", type=int, nargs=3, default=None,
+                    help="scaled run of the config's recipe (parity / smoke only)")
     return ap.parse_args()
 
 
@@ -202,7 +204,7 @@ def run_reference(args):
     return 0
 
 
-def cpu_baseline_sample(w, X, mask, B, budget_s=20.0):
+def cpu_baseline_sample(w, M, mask, B, budget_s=20.0):
     """Oracle (port) on 1 core, bounded sample of the same workload."""
     os.environ["ICNNM_ORACLE_THREADS"] = "1"
     from threadpoolctl import threadpool_limits
@@ -210,7 +212,7 @@ def cpu_baseline_sample(w, X, mask, B, budget_s=20.0):
     O.WORKERS = 1
     with threadpool_limits(limits=1):
         ob = O.EigenBasis(B.kernel_shape, B.K, B.eigenvalues)
-        s = O.AdmmSolver(X * mask, mask, ob,
+        s = O.AdmmSolver(M, mask, ob,
                          O.SolverConfig(max_iters=w.iters, tol_primal=1e-300, tol_change=1e-300),
                          validate_basis=False)
         t0 = time.perf_counter()
@@ -226,6 +228,25 @@ def cpu_baseline_sample(w, X, mask, B, budget_s=20.0):
                       f"(1 thread, {dt:.1f} s)"}
 
 
+def setup_dist(world, local):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return dist
+    return None
+
+
+def max_over_ranks(dist, dev, x):
+    if not dist:
+        return x
+    import torch
+    t = torch.tensor([x], device=f"cuda:{dev}", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -233,51 +254,65 @@ def main():
 
     rank, world, local = dist_env()
     import torch
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = setup_dist(world, local)
     import paper_2604_17001_b200 as P
     from paper_2604_17001_b200 import synth
 
     w = synth.WORKLOADS[args.config]
+    if args.dims:
+        w = synth.scaled(w, tuple(args.dims))
     iters = args.iters or w.iters
     dev = local
-    # per-rank independent tensor (batch split, weak scaling)
-    X = w.target(b=rank)
-    mask = w.mask()
-    M = X * mask
-    B = P.learn_ensemble_basis(w.training(), w.kernel, device=dev)
     cfg = P.SolverConfig(max_iters=iters, tol_primal=1e-300, tol_change=1e-300,
                          engine=args.engine)
-    S = P.Solver(X.shape, B, device=dev)
-    S.upload(M, mask)
+    B = P.learn_ensemble_basis(w.training(), w.kernel, device=dev)
+
+    if args.config == 5:
+        return bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist)
+
+    # batch of tensors for this rank: cfg 4 splits the 64-tensor batch over
+    # the ranks (strong scaling); cfgs 1-3 give every rank its own tensor
+    # (independent replicas, weak scaling)
+    if args.config == 4:
+        nb = w.batch
+        mine = list(range(rank, nb, world))
+        scaling, units_total = "strong", nb
+    else:
+        mine = [rank]
+        scaling, units_total = "weak", world
+    mask = w.mask()
+    targets = {b: w.target(b=b) for b in mine}
+    S = P.Solver(w.dims, B, device=dev)
+
+    def step():
+        t = 0.0
+        n = 0
+        for b in mine:
+            S.upload(targets[b] * mask, mask)
+            rep = S.run(cfg)
+            t += rep.device_seconds
+            n += S.last_launches
+        return t, n
 
     for _ in range(args.warmup):
-        S.run(cfg)
+        step()
     torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
-
     dev_s = []
     launches = 0
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
-            rep = S.run(cfg)
-            dev_s.append(rep.device_seconds)
-            launches += S.last_launches
+            t, n = step()
+            dev_s.append(t)
+            launches += n
     torch.cuda.synchronize(dev)
-    t_local = float(sum(dev_s))
-    t_max = t_local
+    t_max = max_over_ranks(dist, dev, float(sum(dev_s)))
     if dist:
-        t = torch.tensor([t_local], device=f"cuda:{dev}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
         dist.barrier()
-    value = w.m * iters * args.steps * world / t_max
+    value = w.m * iters * args.steps * units_total / t_max
     L = S.download()
-    psnr = synth.psnr(X, L)
+    psnr = synth.psnr(targets[mine[-1]], L)
 
     # per-kernel times (live, CUDA events on the solver stream) for roofline
     S.set_profile(True)
@@ -285,76 +320,137 @@ def main():
     kt = S.kernel_times_ms()
     S.set_profile(False)
 
-    line = None
     if rank == 0:
-        peaks = load_peaks()
-        k = w.k
-        flops_fwd = 2.0 * w.m * k * k            # algorithmic, per launch
-        flops_adj = 2.0 * w.m * k * k
-        dom = "forward" if kt["forward"] >= kt["adjoint"] else "adjoint"
-        t_dom = kt[dom] * 1e-3
-        achieved = (flops_fwd if dom == "forward" else flops_adj) / t_dom / 1e12
-        if args.engine == "tf32x3":
-            tf32 = measure_tf32_peak(dev)
-            roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": tf32 / 3.0,
-                    "unit": "TFLOP/s", "frac": achieved / (tf32 / 3.0),
-                    "peak_source": "measured dense TF32 (cuBLAS 8192^3 burst, %.0f TFLOP/s) / 3 "
-                                   "tensor MMAs per fp32 product" % tf32,
-                    "tensor_pipe_frac": 3.0 * achieved / tf32}
-        else:
-            ffma_peak = P.probe_ffma_tflops(dev)
-            roof = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": ffma_peak,
-                    "unit": "TFLOP/s", "frac": achieved / ffma_peak,
-                    "peak_source": "measured FFMA probe (icnnm_probe_ffma_tflops)"}
-        traffic = load_ncu_traffic(args.engine)
-        roof["traffic"] = traffic.get(dom) if isinstance(traffic, dict) else None
-        roof["algorithmic_bytes"] = (8.0 if dom == "forward" else 4.0) * w.m * k
-        roof["per_launch_ms"] = kt
-        roof["flops_per_launch"] = flops_fwd
-        e2e = None
-        if not args.no_e2e:
-            e2e_t = []
-            for _ in range(max(1, min(args.steps, 3))):
-                Mh = np.ascontiguousarray(M)
-                t0 = time.perf_counter()
-                Lh, r = P.icnnm_solve(Mh, mask, B, cfg, device=dev)
-                e2e_t.append(time.perf_counter() - t0)
-            te = float(np.mean(e2e_t))
-            e2e = {"value": w.m * iters / te, "unit": UNIT,
-                   "h2d_bytes_per_step": int(M.nbytes + mask.nbytes + B.K.nbytes),
-                   "d2h_bytes_per_step": int(Lh.nbytes + 3 * 8 * iters),
-                   "path": "icnnm_cuda_solve C ABI, host f64 buffers, incl. validation, "
-                           "allocation, H2D, solve, D2H"}
-        cpu = None
-        if not args.no_cpu_baseline:
-            cpu = cpu_baseline_sample(w, X, mask, B)
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (BASELINE.json generator, seeded)",
-            "config": {"workload": f"BASELINE config {args.config}: {w.dims[0]}x{w.dims[1]}x"
-                                   f"{w.dims[2]} kernel {w.kernel[0]}x{w.kernel[1]}x"
-                                   f"{w.kernel[2]} (k={k}), {iters} iterations per step",
-                       "engine": args.engine, "step": "one full ICNNM solve from HBM",
-                       "l2": "inputs larger than L2 (W state %.2f GB)" % (
-                           w.m * ((k + 63) // 64 * 64) * 4 / 1e9),
-                       "parallelism": f"batch split x{world} (independent tensors)"},
-            "psnr_db": psnr,
-            "roofline": roof,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "hbm_peak_gbs": peaks.get("hbm_gbs"),
-        }
-        print(json.dumps(line), flush=True)
+        report_line(args, P, w, B, cfg, iters, dev, world, value, t_max, kt, psnr, launches,
+                    clk, scaling, mask, targets[mine[0]] * mask)
     S.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
+    """BASELINE config 5: one tensor H-sharded over the ranks (halo exchange +
+    one NCCL all-reduce per iteration), strong scaling."""
+    import torch
+    import paper_2604_17001_b200 as P
+    from paper_2604_17001_b200 import synth
+    local_slabs = 1
+    if world == 1:
+        need = w.m * ((w.k + 127) // 128 * 128) * 4
+        if need > 150e9:
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": 1,
+                                  "unavailable": "config 5 W state (%.0f GB) exceeds one B200; "
+                                                 "run with --gpus >= 2 or --dims" % (need / 1e9)}))
+            return 0
+    nid = None
+    if world > 1:
+        obj = [P.dist_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    X = w.target()
+    mask = w.mask()
+    M = X * mask
+    times = []
+    with ClockSampler(dev) as clk:
+        for it in range(args.warmup + args.steps):
+            if dist:
+                dist.barrier()
+            row0, rows, rep = P.sharded_solve(M, mask, B, cfg, local_slabs=local_slabs,
+                                              world=world, rank=rank, nccl_id=nid, device=dev)
+            if it >= args.warmup:
+                times.append(rep.device_seconds)
+    t_max = max_over_ranks(dist, dev, float(sum(times)))
+    value = w.m * iters * args.steps / t_max
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (BASELINE.json generator, seeded)",
+                "config": {"workload": "BASELINE config 5 %s kernel %s, %d iterations, H-sharded "
+                                       "over %d ranks" % ("x".join(map(str, w.dims)),
+                                                          "x".join(map(str, w.kernel)), iters, world),
+                           "engine": args.engine, "parallelism": f"H-shard x{world}"},
+                "psnr_db_own_rows": synth.psnr(X[row0:row0 + rows.shape[0]], rows),
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def report_line(args, P, w, B, cfg, iters, dev, world, value, t_max, kt, psnr, launches, clk,
+                scaling, mask, M):
+    import numpy as np
+    from paper_2604_17001_b200 import synth
+    peaks = load_peaks()
+    k = w.k
+    flops = 2.0 * w.m * k * k            # algorithmic, per launch (either contraction)
+    dom = "forward" if kt["forward"] >= kt["adjoint"] else "adjoint"
+    achieved = flops / (kt[dom] * 1e-3) / 1e12
+    if args.engine == "tf32x3":
+        tf32 = measure_tf32_peak(dev)
+        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": tf32 / 3.0,
+                "unit": "TFLOP/s", "frac": achieved / (tf32 / 3.0),
+                "peak_source": "measured dense TF32 (cuBLAS 8192^3 burst, %.0f TFLOP/s) / 3 "
+                               "tensor MMAs per fp32 product" % tf32,
+                "tensor_pipe_frac": 3.0 * achieved / tf32}
+    else:
+        ffma_peak = P.probe_ffma_tflops(dev)
+        roof = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": ffma_peak,
+                "unit": "TFLOP/s", "frac": achieved / ffma_peak,
+                "peak_source": "measured FFMA probe (icnnm_probe_ffma_tflops)"}
+    traffic = load_ncu_traffic(args.engine) if args.config == 2 else None
+    roof["traffic"] = traffic.get(dom) if isinstance(traffic, dict) else None
+    roof["algorithmic_bytes"] = (8.0 if dom == "forward" else 4.0) * w.m * k
+    roof["per_launch_ms"] = kt
+    roof["flops_per_launch"] = flops
+    e2e = None
+    if not args.no_e2e:
+        e2e_t = []
+        for _ in range(max(1, min(args.steps, 3))):
+            Mh = np.ascontiguousarray(M)
+            t0 = time.perf_counter()
+            Lh, r = P.icnnm_solve(Mh, mask, B, cfg, device=dev)
+            e2e_t.append(time.perf_counter() - t0)
+        te = float(np.mean(e2e_t))
+        e2e = {"value": w.m * iters / te * (world if args.config != 4 else 1), "unit": UNIT,
+               "h2d_bytes_per_step": int(M.nbytes + mask.nbytes + B.K.nbytes),
+               "d2h_bytes_per_step": int(Lh.nbytes + 3 * 8 * iters),
+               "path": "icnnm_cuda_solve C ABI on host f64 buffers (validation, allocation, "
+                       "H2D, solve, D2H inside the timed region); one tensor per rank"}
+    cpu = None
+    if not args.no_cpu_baseline and w.m * k <= 3e8:
+        cpu = cpu_baseline_sample(w, M, mask, B)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (BASELINE.json generator, seeded)",
+        "config": {"workload": f"BASELINE config {args.config}: {w.dims[0]}x{w.dims[1]}x"
+                               f"{w.dims[2]} kernel {w.kernel[0]}x{w.kernel[1]}x"
+                               f"{w.kernel[2]} (k={k}), {iters} iterations per solve",
+                   "engine": args.engine,
+                   "step": "one full ICNNM solve from HBM" + (
+                       " per tensor of the rank's share of the 64-tensor batch"
+                       if args.config == 4 else ""),
+                   "l2": "inputs larger than L2 (W state %.2f GB)" % (
+                       w.m * ((k + 127) // 128 * 128) * 4 / 1e9),
+                   "parallelism": ("batch split x%d (no communication)" % world)},
+        "psnr_db": psnr,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "hbm_peak_gbs": peaks.get("hbm_gbs"),
+    }
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

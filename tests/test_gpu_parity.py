@@ -374,3 +374,53 @@ def test_sharded_virtual_slabs_match_unsharded(gpu, engine):
         assert row0 == 0 and rows.shape == X.shape
         assert _rel(rows, L1) < 1e-5, G
         np.testing.assert_allclose(rep.objective, r1.objective, rtol=1e-5)
+
+
+# --------------------------------------------------------------------------
+# BASELINE recipes at oracle-feasible sizes (same generator, mask kind and
+# kernel box as configs 3-5; SURVEY §8c parity plan for the large configs)
+# --------------------------------------------------------------------------
+def _recipe(cfg, dims, iters):
+    from paper_2604_17001_b200 import synth
+    w = synth.scaled(synth.WORKLOADS[cfg], dims, iters=iters, n_train=3)
+    if cfg == 3:   # frames 0..(5/6 T) observed, the tail missing (40 of 48)
+        mask = synth.synth_mask(*dims, synth.MASK_T_PREFIX, int(dims[2] * 40 / 48), 0)
+    elif cfg == 5:
+        mask = synth.synth_mask(*dims, synth.MASK_IID_BOXES, 0.3, 3005, n_boxes=2)
+    else:
+        mask = w.mask()
+    return w, w.target(), mask
+
+
+@pytest.mark.parametrize("cfg,dims,iters", [(3, (24, 24, 24), 30), (4, (32, 32, 16), 60),
+                                            (5, (32, 24, 18), 40)])
+@pytest.mark.parametrize("engine", ENGINES)
+def test_recipe_parity(gpu, cfg, dims, iters, engine):
+    from paper_2604_17001_b200 import synth
+    w, X, mask = _recipe(cfg, dims, iters)
+    B = gpu.learn_ensemble_basis(w.training(), w.kernel)
+    Lg, _ = gpu.icnnm_solve(X * mask, mask, B, gpu.SolverConfig(max_iters=iters, engine=engine,
+                                                                **FIXED))
+    Lo, _ = O.icnnm_solve(X * mask, mask, _oracle_basis(B),
+                          O.SolverConfig(max_iters=iters, **FIXED))
+    assert _rel(Lg, Lo) <= 1e-4
+    miss = mask == 0
+    assert _rel(Lg[miss], Lo[miss]) <= 1e-3          # the recovered (unobserved) entries
+    assert abs(synth.psnr(X, Lg) - O.psnr(X, Lo)) <= 0.01
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config5_sharded_recipe(gpu, engine):
+    """Config 5's kernel (9x9x9) and mask recipe, H-sharded over 2 and 4 virtual
+    slabs, against the fp64 oracle and the unsharded GPU solve."""
+    from paper_2604_17001_b200 import synth
+    w, X, mask = _recipe(5, (48, 24, 20), 30)
+    B = gpu.learn_ensemble_basis(w.training(), w.kernel)
+    cfg = gpu.SolverConfig(max_iters=30, engine=engine, **FIXED)
+    L1, _ = gpu.icnnm_solve(X * mask, mask, B, cfg)
+    Lo, _ = O.icnnm_solve(X * mask, mask, _oracle_basis(B), O.SolverConfig(max_iters=30, **FIXED))
+    assert _rel(L1, Lo) <= 1e-4
+    for G in (2, 4):
+        _, rows, _ = gpu.sharded_solve(X * mask, mask, B, cfg, local_slabs=G)
+        assert _rel(rows, Lo) <= 1e-4, G
+        assert _rel(rows, L1) <= 1e-5, G
