@@ -59,7 +59,10 @@ typedef struct icnnm_solver_config {
   double tol_change;    /* 1e-8                                       */
   double rank_tol;      /* 1e-8 (unused by the solver, as upstream)   */
   int init_fill;        /* ICNNM_INIT_ZERO | ICNNM_INIT_MEAN          */
-  int engine;           /* ICNNM_ENGINE_* (extension; default FFMA)   */
+  int engine;           /* ICNNM_ENGINE_* (extension; default TF32X3) */
+  int exact_residual;   /* extension: 1 = exact primal_residual trace
+                           (one extra forward contraction per iteration);
+                           0 = fp32 identity estimate (NaN once unresolved) */
 } icnnm_solver_config;
 
 /* Mirror of icnnm::SolveReport (solver.hpp:46-52).  objective and
@@ -261,6 +264,28 @@ void icnnm_rng_normal(icnnm_rng_t r, double mean, double stddev, int64_t n,
 /* bernoulli_mask(dims, rate, seed) of mask.cpp:49-59 (flat, m entries). */
 int icnnm_reference_bernoulli_mask(int64_t m, double rate, uint64_t seed,
                                    double* out);
+
+/* ------------------------------------------------------------------------
+ * Reference file formats (tensor_io.cpp:86-128, report_io.cpp:39-68), used
+ * by the GPU CLI drop-in (bin: paper_2604_17001_b200/icnnm_b200).
+ * ---------------------------------------------------------------------- */
+const char* icnnm_io_last_error(void);
+int icnnm_write_tnsr(const char* path, int order, const int64_t* dims,
+                     const double* values);
+/* values == NULL: header only (order, dims16[0..order)) */
+int icnnm_read_tnsr(const char* path, int* order, int64_t* dims16,
+                    double* values);
+int icnnm_write_ebas(const char* path, int order, const int64_t* kdims,
+                     const double* eigenvalues, const double* K_colmajor);
+/* eigenvalues/K NULL: header only */
+int icnnm_read_ebas(const char* path, int* order, int64_t* kdims16,
+                    double* eigenvalues, double* K_colmajor);
+/* solver_config_from_json: flat object, absent keys keep the defaults,
+ * "theta0": null = automatic; validates (SolverConfig::validate). */
+int icnnm_config_from_json(const char* text, icnnm_solver_config* cfg);
+/* solve_report_to_json; returns the byte length, writes <= cap bytes. */
+int64_t icnnm_report_to_json(const icnnm_solve_report* rep, char* out,
+                             int64_t cap);
 
 /* ------------------------------------------------------------------------
  * Probes used by bench.py for roofline denominators (device microbenches).

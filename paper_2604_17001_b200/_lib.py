@@ -45,6 +45,7 @@ class SolverConfigC(C.Structure):
         ("rank_tol", C.c_double),
         ("init_fill", C.c_int),
         ("engine", C.c_int),
+        ("exact_residual", C.c_int),
     ]
 
 
@@ -114,6 +115,13 @@ SIGNATURES = {
     "icnnm_rng_normal": (None, [C.c_void_p, C.c_double, C.c_double, C.c_int64, _dp]),
     "icnnm_reference_bernoulli_mask": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, _dp]),
     "icnnm_probe_ffma_tflops": (C.c_int, [C.c_int, _dp]),
+    "icnnm_io_last_error": (C.c_char_p, []),
+    "icnnm_write_tnsr": (C.c_int, [C.c_char_p, C.c_int, _lp, _dp]),
+    "icnnm_read_tnsr": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), _lp, _dp]),
+    "icnnm_write_ebas": (C.c_int, [C.c_char_p, C.c_int, _lp, _dp, _dp]),
+    "icnnm_read_ebas": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), _lp, _dp, _dp]),
+    "icnnm_config_from_json": (C.c_int, [C.c_char_p, C.POINTER(SolverConfigC)]),
+    "icnnm_report_to_json": (C.c_int64, [C.POINTER(SolveReportC), C.c_char_p, C.c_int64]),
 }
 
 _lib = None
@@ -149,6 +157,18 @@ def check(status: int) -> None:
         raise InvalidArgument(msg)
     if status == ICNNM_CUDA_ERROR:
         raise CudaError(msg)
+    raise IcnnmError(msg)
+
+
+CLI_PATH = os.path.join(_HERE, "icnnm_b200")
+
+
+def check_io(status: int) -> None:
+    if status == ICNNM_OK:
+        return
+    msg = lib().icnnm_io_last_error().decode(errors="replace")
+    if status == ICNNM_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
     raise IcnnmError(msg)
 
 

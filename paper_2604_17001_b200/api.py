@@ -50,7 +50,8 @@ class SolverConfig:
     tol_change: float = 1e-8
     rank_tol: float = 1e-8
     init_fill: str = "zero"
-    engine: str = "ffma"
+    engine: str = "tf32x3"
+    exact_residual: bool = False
 
     def to_c(self) -> SolverConfigC:
         if self.init_fill not in ("zero", "mean"):
@@ -69,6 +70,7 @@ class SolverConfig:
         c.rank_tol = float(self.rank_tol)
         c.init_fill = 0 if self.init_fill == "zero" else 1
         c.engine = ENGINES[self.engine]
+        c.exact_residual = 1 if self.exact_residual else 0
         return c
 
     def validate(self) -> None:

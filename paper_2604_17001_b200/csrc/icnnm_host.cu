@@ -438,6 +438,7 @@ struct Slab {
   int64_t m_own = 0;            // rows * W * T
   int64_t halo_elems = 0;       // (kh-1) * W * T (slab mode)
   DBuf<float> Lt, adj, pm, mask, W;
+  DBuf<float> Lr;                 // exact-residual mode: L_{t+1} (fp32, with halo rows)
   DBuf<double> L, V;
 };
 
@@ -452,6 +453,7 @@ struct Solver {
   TcPlan tp;
   DBuf<float> BpkF, BpkA;        // tcgen05 engine: packed B tiles (fwd / adj)
   int engine = ICNNM_ENGINE_FFMA;  // engine of the current run
+  bool exact_res = false;          // exact primal residual (one extra forward / iteration)
   DBuf<double> red;              // norm2 (kp) | update slot (8)
   DBuf<double> theta;
   DBuf<IterState> st;
@@ -567,7 +569,7 @@ void solver_upload(Solver& S, const double* M, const double* mask) {
 }
 
 // L~ halo exchange: slab g's last kh-1 own rows -> slab g+1's halo rows.
-void exchange_lt(Solver& S) {
+void exchange_lt(Solver& S, DBuf<float> Slab::*buf = &Slab::Lt) {
   if (!S.sharded) return;
   const size_t he = S.slabs[0].halo_elems;
   if (he == 0) return;
@@ -576,17 +578,17 @@ void exchange_lt(Solver& S) {
     for (int i = 0; i < nl; ++i) {
       const Slab& src = S.slabs[i];
       Slab& dst = S.slabs[(i + 1) % nl];
-      CK(cudaMemcpyAsync(dst.Lt.p, src.Lt.p + src.m_own, he * sizeof(float),
+      CK(cudaMemcpyAsync((dst.*buf).p, (src.*buf).p + src.m_own, he * sizeof(float),
                          cudaMemcpyDeviceToDevice, S.stream));
     }
     return;
   }
   // local neighbours first, then the process boundary through the comm.
   for (int i = 0; i + 1 < nl; ++i)
-    CK(cudaMemcpyAsync(S.slabs[i + 1].Lt.p, S.slabs[i].Lt.p + S.slabs[i].m_own,
+    CK(cudaMemcpyAsync((S.slabs[i + 1].*buf).p, (S.slabs[i].*buf).p + S.slabs[i].m_own,
                        he * sizeof(float), cudaMemcpyDeviceToDevice, S.stream));
   const Slab& last = S.slabs[nl - 1];
-  S.comm->shift_forward(last.Lt.p + last.m_own, S.slabs[0].Lt.p, he, S.stream);
+  S.comm->shift_forward((last.*buf).p + last.m_own, (S.slabs[0].*buf).p, he, S.stream);
 }
 
 // Adjoint reverse halo: slab g's halo partials -> added to slab g-1's last rows.
@@ -621,16 +623,20 @@ void exchange_adj(Solver& S) {
   add(last.adj.p + last.m_own, S.xfer_recv.p);
 }
 
+int engine_kp(const Solver& S);
+
 void launch_fwd(Solver& S, Slab& s, int mode) {
+  // mode 2 (exact residual): forward on L_{t+1}, epilogue sums the gap into slot[5]
+  const float* src = mode == 2 ? s.Lr.p : s.Lt.p;
+  double* acc = mode == 2 ? S.red.p + engine_kp(S) + 5 : S.red.p;
   if (S.engine == ICNNM_ENGINE_TF32X3) {
-    launch_tc_kernel(s.gtc, S.tp, true, mode, s.Lt.p, s.W.p, S.BpkF.p, S.cvec.p, s.adj.p, S.red.p,
+    launch_tc_kernel(s.gtc, S.tp, true, mode, src, s.W.p, S.BpkF.p, S.cvec.p, s.adj.p, acc,
                      S.st.p, S.stream, S.tc_counters ? S.dbg.p : nullptr);
     ++S.launches;
     return;
   }
   icnnm_dev::icnnm_fwd_ffma<<<static_cast<unsigned>(n_bricks(s.g)), 128, fwd_smem(s.g),
-                              S.stream>>>(s.g, s.Lt.p, S.Krm.p, s.W.p, S.cvec.p, S.st.p,
-                                          S.red.p, mode);
+                              S.stream>>>(s.g, src, S.Krm.p, s.W.p, S.cvec.p, S.st.p, acc, mode);
   CKL();
   ++S.launches;
 }
@@ -648,7 +654,7 @@ void launch_adj(Solver& S, Slab& s) {
   ++S.launches;
 }
 
-inline int engine_kp(const Solver& S) {
+int engine_kp(const Solver& S) {
   return S.engine == ICNNM_ENGINE_TF32X3 ? S.tp.kp : S.p.kp;
 }
 
@@ -668,7 +674,11 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   if (!S.uploaded) invalid("solve: no problem uploaded");
   const Problem& p = S.p;
   S.engine = cfg.engine;
+  S.exact_res = cfg.exact_residual != 0;
   const int kpe = engine_kp(S);
+  if (S.exact_res)
+    for (auto& s : S.slabs)
+      if (!s.Lr.p) s.Lr.alloc(s.Lt.n);
   const int iters = cfg.max_iters;
   const double kd = static_cast<double>(p.k);
   // theta schedule exactly as solver.cpp:88-91,126 (fp64, sequential).
@@ -719,17 +729,23 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   auto iteration = [&]() {
     icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
                                                     S.stats.p, p.k, kpe, kd, res_scale,
-                                                    cfg.tol_primal, cfg.tol_change, floor_rel);
+                                                    cfg.tol_primal, cfg.tol_change, floor_rel,
+                                                    S.exact_res ? 1 : 0);
     CKL();
     for (auto& s : S.slabs) launch_adj(S, s);
     exchange_adj(S);
     for (auto& s : S.slabs) {
       icnnm_dev::icnnm_update<<<grid_for(s.m_own, 256, 148 * 8), 256, 0, S.stream>>>(
           s.m_own, S.st.p, cfg.lambda, kd, s.adj.p + s.halo_elems, s.L.p, s.V.p, s.pm.p,
-          s.mask.p, s.Lt.p + s.halo_elems, S.red.p + kpe);
+          s.mask.p, s.Lt.p + s.halo_elems, S.red.p + kpe,
+          S.exact_res ? s.Lr.p + s.halo_elems : nullptr);
       CKL();
     }
     exchange_lt(S);
+    if (S.exact_res) {
+      exchange_lt(S, &Slab::Lr);
+      for (auto& s : S.slabs) launch_fwd(S, s, 2);
+    }
     for (auto& s : S.slabs) launch_fwd(S, s, 1);
     allreduce_red(S);
   };
@@ -746,7 +762,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
       icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
                                                       S.stats.p, p.k, kpe, kd, res_scale,
                                                       cfg.tol_primal, cfg.tol_change,
-                                                      floor_rel);
+                                                      floor_rel, S.exact_res ? 1 : 0);
       CK(cudaEventRecord(e[1], S.stream));
       for (auto& s : S.slabs) launch_adj(S, s);
       exchange_adj(S);
@@ -754,9 +770,14 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
       for (auto& s : S.slabs) {
         icnnm_dev::icnnm_update<<<grid_for(s.m_own, 256, 148 * 8), 256, 0, S.stream>>>(
             s.m_own, S.st.p, cfg.lambda, kd, s.adj.p + s.halo_elems, s.L.p, s.V.p, s.pm.p,
-            s.mask.p, s.Lt.p + s.halo_elems, S.red.p + kpe);
+            s.mask.p, s.Lt.p + s.halo_elems, S.red.p + kpe,
+            S.exact_res ? s.Lr.p + s.halo_elems : nullptr);
       }
       exchange_lt(S);
+      if (S.exact_res) {
+        exchange_lt(S, &Slab::Lr);
+        for (auto& s : S.slabs) launch_fwd(S, s, 2);
+      }
       CK(cudaEventRecord(e[3], S.stream));
       for (auto& s : S.slabs) launch_fwd(S, s, 1);
       allreduce_red(S);
@@ -803,7 +824,8 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   // final coef: moves the last update slot into stats, evaluates the stop test.
   icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
                                                   S.stats.p, p.k, kpe, kd, res_scale,
-                                                  cfg.tol_primal, cfg.tol_change, floor_rel);
+                                                  cfg.tol_primal, cfg.tol_change, floor_rel,
+                                                  S.exact_res ? 1 : 0);
   CKL();
   ++S.launches;
   CK(cudaEventRecord(S.ev1, S.stream));
@@ -834,9 +856,9 @@ void fill_report(const Solver& S, const icnnm_solver_config& cfg, const RunResul
   int term = ICNNM_TERM_MAX_ITERS;
   for (int it = 0; it < executed; ++it) {
     const IterStats& q = R.stats[it];
-    const double gap2 = q.z2 - 2.0 * q.ip + kd * q.ln2;
+    const double gap2 = S.exact_res ? q.gap2 : q.z2 - 2.0 * q.ip + kd * q.ln2;
     const double res = std::sqrt(std::max(gap2, 0.0)) / res_scale;
-    const bool res_ok = gap2 > 1e-5 * (q.z2 + kd * q.ln2);
+    const bool res_ok = S.exact_res || gap2 > 1e-5 * (q.z2 + kd * q.ln2);
     const double lc = std::sqrt(q.dl2) / std::max(std::sqrt(q.l2o), 1e-300);
     if (rep->objective) rep->objective[it] = q.l21 + 0.5 * cfg.lambda * kd * q.fit;
     // Below the fp32 floor the identity cannot resolve the gap: report NaN
@@ -892,7 +914,8 @@ void icnnm_default_config(icnnm_solver_config* c) {
   c->tol_change = 1e-8;
   c->rank_tol = 1e-8;
   c->init_fill = ICNNM_INIT_ZERO;
-  c->engine = ICNNM_ENGINE_FFMA;
+  c->engine = ICNNM_ENGINE_TF32X3;
+  c->exact_residual = 0;
 }
 
 int icnnm_validate_config(const icnnm_solver_config* cfg) {

@@ -85,6 +85,7 @@ icnnm_fwd_ffma(Geo g, const float* __restrict__ Lt, const float* __restrict__ Kr
     if (!st->active || st->it >= st->max_iters - 1) return;
     r = static_cast<float>(st->r);
   }
+  if (mode == 2 && !st->active) return;  // exact residual: ||(1-c)W_t - A(L_{t+1})K||^2
   extern __shared__ float4 smem4[];
   float* Ks = reinterpret_cast<float*>(smem4);           // 2 * BK * BN
   int* tapoff = reinterpret_cast<int*>(Ks + 2 * BK * BN);  // ktp
@@ -169,8 +170,25 @@ icnnm_fwd_ffma(Geo g, const float* __restrict__ Lt, const float* __restrict__ Kr
       __syncthreads();
     }
 
-    // epilogue: W_new = acc + r c W_old, masked voxels -> 0, column norms.
     const int col0 = nt * BN + cg * 8;
+    if (mode == 2) {
+      float g2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool valid = rowvalid && (t0 + vt0 + i < g.T);
+        const float* wp = Wm + (static_cast<size_t>(blk) * BM + v0 + i) * g.kp + col0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float gap = (1.f - cvec[col0 + j]) * wp[j] - acc[i][j];
+          g2 = valid ? fmaf(gap, gap, g2) : g2;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) g2 += __shfl_xor_sync(0xffffffffu, g2, o);
+      if (lane == 0) atomicAdd(norm2, static_cast<double>(g2));
+      continue;
+    }
+    // epilogue: W_new = acc + r c W_old, masked voxels -> 0, column norms.
     float cr[8];
     if (mode == 1) {
       float4 c0 = *reinterpret_cast<const float4*>(cvec + col0);
@@ -397,7 +415,8 @@ __device__ __forceinline__ void block_reduce_add(double (&v)[N], double* dst) {
 __global__ void icnnm_coef(IterState* st, const double* __restrict__ theta,
                            double* __restrict__ red, float* __restrict__ cvec,
                            IterStats* __restrict__ stats, int k, int kp, double kd,
-                           double res_scale, double tol_p, double tol_c, double floor_rel) {
+                           double res_scale, double tol_p, double tol_c, double floor_rel,
+                           int exact) {
   // red = [norm2 (kp) | update slot (dl2, l2o, fit, ip, ln2) | pad]
   __shared__ int go;
   __shared__ int cur;
@@ -408,11 +427,13 @@ __global__ void icnnm_coef(IterState* st, const double* __restrict__ theta,
       IterStats& p = stats[it - 1];
       double* slot = red + kp;
       p.dl2 = slot[0]; p.l2o = slot[1]; p.fit = slot[2]; p.ip = slot[3]; p.ln2 = slot[4];
+      p.gap2 = slot[5];
       for (int q = 0; q < 8; ++q) slot[q] = 0.0;
-      double gap2 = p.z2 - 2.0 * p.ip + kd * p.ln2;
+      double gap2 = exact ? p.gap2 : p.z2 - 2.0 * p.ip + kd * p.ln2;
       double scale2 = p.z2 + kd * p.ln2;
       double res = sqrt(fmax(gap2, 0.0)) / res_scale;
-      bool res_ok = gap2 > floor_rel * scale2;  // below the floor: unresolved in fp32
+      // identity form: below the floor the gap is unresolved in fp32
+      bool res_ok = exact ? true : gap2 > floor_rel * scale2;
       double lc = sqrt(p.dl2) / fmax(sqrt(p.l2o), 1e-300);
       if ((res_ok && res < tol_p) || lc < tol_c) {
         g = 0;
@@ -461,7 +482,7 @@ __global__ void __launch_bounds__(256)
 icnnm_update(int64_t m, const IterState* __restrict__ st, double lambda, double kd,
              float* __restrict__ adj, double* __restrict__ L, double* __restrict__ V,
              const float* __restrict__ pm, const float* __restrict__ mask,
-             float* __restrict__ Lt, double* __restrict__ slot) {
+             float* __restrict__ Lt, double* __restrict__ slot, float* __restrict__ Lr) {
   if (!st->active) return;
   const double th = st->theta;
   const double r = st->r;
@@ -478,6 +499,7 @@ icnnm_update(int64_t m, const IterState* __restrict__ st, double lambda, double 
     const double v = V[i];
     L[i] = ln;
     Lt[i] = static_cast<float>(ln + r * d);
+    if (Lr != nullptr) Lr[i] = static_cast<float>(ln);
     adj[i] = 0.f;
     V[i] = r * (kd * lo - a - kd * ln);
     const double f = mk * (ln - p);

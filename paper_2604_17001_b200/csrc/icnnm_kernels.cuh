@@ -55,7 +55,7 @@ struct IterStats {
   double fit;   // ||mask (L_{t+1} - M)||^2
   double ip;    // <k L_t - V_t - adj_t, L_{t+1}>   (= <Z_t, A(L_{t+1})K>)
   double ln2;   // ||L_{t+1}||^2
-  double pad;
+  double gap2;  // exact ||Z_t - A(L_{t+1})K||^2 (exact_residual mode), else 0
 };
 
 }  // namespace icnnm_dev
@@ -70,10 +70,10 @@ __global__ void icnnm_adj_ffma(Geo g, const float* Wm, const float* KT, const fl
                                float* adj, const IterState* st, int mode);
 __global__ void icnnm_coef(IterState* st, const double* theta, double* red, float* cvec,
                            IterStats* stats, int k, int kp, double kd, double res_scale,
-                           double tol_p, double tol_c, double floor_rel);
+                           double tol_p, double tol_c, double floor_rel, int exact);
 __global__ void icnnm_update(int64_t m, const IterState* st, double lambda, double kd,
                              float* adj, double* L, double* V, const float* pm,
-                             const float* mask, float* Lt, double* slot);
+                             const float* mask, float* Lt, double* slot, float* Lr);
 __global__ void icnnm_add_rows(int64_t n, float* dst, float* src);
 __global__ void icnnm_setup(int64_t m, const double* M, const double* msk, int mean_fill,
                             double mean, float* pm, float* maskf, double* L, double* V,

@@ -226,6 +226,7 @@ icnnm_tc_kernel(TcArgs a) {
     if (FWD && a.st->it >= a.st->max_iters - 1) return;
     rr = static_cast<float>(a.st->r);
   }
+  if (a.mode == 2 && !a.st->active) return;  // forward on L_{t+1}: exact residual only
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* p = smem;
   const int sbn = a.sb, wsn = a.ws;
@@ -295,7 +296,7 @@ icnnm_tc_kernel(TcArgs a) {
   }
   for (int j = tid; j < g.kp; j += blockDim.x) {
     float c = 1.f;
-    if (a.mode == 1) c = a.cvec[j];
+    if (a.mode >= 1) c = a.cvec[j];
     cs[j] = (j < g.k) ? c : 0.f;
   }
   if (FWD) {
@@ -398,6 +399,7 @@ icnnm_tc_kernel(TcArgs a) {
     float* myob = ob + quad * nobp;
     float* myred = red + ew * 32 * 33;
     constexpr int NHALF = NEPI / 4;
+    float gacc = 0.f;  // mode 2: this thread's share of ||(1-c)W - A(L)K||^2
     uint32_t tcount = 0;
     Dbg dbg(lane == 0 ? a.dbg : nullptr);
     for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
@@ -417,7 +419,18 @@ icnnm_tc_kernel(TcArgs a) {
           tmem_ld32(tbase + lane_base + acc * 128 + c0, u);
           tmem_wait_ld();
           const int ncol = (wn - c0) < 32 ? (wn - c0) : 32;
-          if (FWD) {
+          if (FWD && a.mode == 2) {
+            const int j0 = nt * a.wbase + c0;
+            const float* wp = a.Wout + ((static_cast<size_t>(b) * a.ntj + (j0 >> 7)) * 128 + (j0 & 127)) * 128 + row;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (i < ncol && valid) {
+                const float gap = (1.f - cs[j0 + i]) * wp[static_cast<size_t>(i) * 128] -
+                                  __uint_as_float(u[i]);
+                gacc = fmaf(gap, gap, gacc);
+              }
+            }
+          } else if (FWD) {
             const int j0 = nt * a.wbase + c0;
             float* wp = a.Wout + ((static_cast<size_t>(b) * a.ntj + (j0 >> 7)) * 128 + (j0 & 127)) * 128 + row;
             float wo[32];
@@ -481,7 +494,11 @@ icnnm_tc_kernel(TcArgs a) {
       }
     }
     dbg.flush(DBG_EPI_WAIT, DBG_EPI_WORK);
-    if (FWD && a.norm2 != nullptr) {
+    if (FWD && a.mode == 2) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, o);
+      if (lane == 0) atomicAdd(a.norm2, static_cast<double>(gacc));
+    } else if (FWD && a.norm2 != nullptr) {
       named_sync(2, NEPI * 32);
       for (int j = ew * 32 + lane; j < g.kp; j += NEPI * 32)
         if (nrm[j] != 0.0) atomicAdd(a.norm2 + j, nrm[j]);

@@ -424,3 +424,78 @@ def test_config5_sharded_recipe(gpu, engine):
         _, rows, _ = gpu.sharded_solve(X * mask, mask, B, cfg, local_slabs=G)
         assert _rel(rows, Lo) <= 1e-4, G
         assert _rel(rows, L1) <= 1e-5, G
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_exact_residual_trace(gpu, engine):
+    """exact_residual=True reproduces the reference's primal_residual trace
+    (solver.cpp:123-124) while it is above the fp32 resolution floor."""
+    from paper_2604_17001_b200 import synth
+    w = synth.WORKLOADS[1]
+    X, mask = w.target(), w.mask()
+    B = gpu.learn_ensemble_basis(w.training(), w.kernel)
+    Lg, rg = gpu.icnnm_solve(X * mask, mask, B,
+                             gpu.SolverConfig(max_iters=120, engine=engine, exact_residual=True,
+                                              **FIXED))
+    Lo, ro = O.icnnm_solve(X * mask, mask, _oracle_basis(B),
+                           O.SolverConfig(max_iters=120, **FIXED))
+    assert _rel(Lg, Lo) <= 1e-4
+    rgv, rov = np.array(rg.primal_residual), np.array(ro.primal_residual)
+    assert not np.any(np.isnan(rgv))
+    sel = rov > 1e-4
+    assert sel.sum() > 10
+    np.testing.assert_allclose(rgv[sel], rov[sel], rtol=2e-2)
+    assert np.all(rgv[~sel] < 2e-4)
+
+
+def test_exact_residual_stops_like_reference(gpu):
+    """With the reference's default tolerances the exact residual drives the
+    stopping test (solver.cpp:136-139) on the cosine recovery case."""
+    L0 = np.cos(2 * np.pi * np.arange(32) / 8)
+    B = gpu.learn_ensemble_basis([L0], (8,))
+    mask = gpu.synth.reference_bernoulli_mask((32,), 0.75, 5)
+    cfg = gpu.SolverConfig(exact_residual=True, tol_primal=1e-5)
+    L, rep = gpu.icnnm_solve(L0 * mask, mask, B, cfg)
+    Lo, ro = O.icnnm_solve(L0 * mask, mask, _oracle_basis(B), O.SolverConfig(tol_primal=1e-5))
+    assert rep.termination == "converged" and ro.termination == "converged"
+    assert abs(rep.iterations - ro.iterations) <= 3
+    assert _rel(L, L0) < 1e-3
+
+
+def test_cli_learn_complete_end_to_end(gpu, tmp_path):
+    """GPU drop-in of the reference CLI's learn + complete
+    (tools/icnnm_cli.cpp:151-166) on the reference's file formats."""
+    import json
+    import subprocess
+    from paper_2604_17001_b200 import io as pio, synth
+    from paper_2604_17001_b200._lib import CLI_PATH
+    w = synth.WORKLOADS[1]
+    X, mask = w.target(), w.mask()
+    refs = w.training()
+    paths = []
+    for i, r in enumerate(refs):
+        p = str(tmp_path / f"ref{i}.tnsr")
+        pio.write_tnsr(p, r)
+        paths.append(p)
+    ebas = str(tmp_path / "basis.ebas")
+    out = subprocess.run([CLI_PATH, "learn", "--refs", *paths, "--kernel", "5,5,3", "--out", ebas],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    B = pio.read_ebas(ebas)
+    Bp = gpu.learn_ensemble_basis(refs, w.kernel)
+    np.testing.assert_array_equal(B.K, Bp.K)
+    pio.write_tnsr(str(tmp_path / "M.tnsr"), X * mask)
+    pio.write_tnsr(str(tmp_path / "mask.tnsr"), mask)
+    (tmp_path / "cfg.json").write_text(json.dumps({"max_iters": 50, "tol_primal": 1e-300,
+                                                   "tol_change": 1e-300}))
+    out = subprocess.run([CLI_PATH, "complete", "--input", str(tmp_path / "M.tnsr"), "--mask",
+                          str(tmp_path / "mask.tnsr"), "--basis", ebas, "--config",
+                          str(tmp_path / "cfg.json"), "--out", str(tmp_path / "L.tnsr"),
+                          "--report", str(tmp_path / "rep.json")], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    L = pio.read_tnsr(str(tmp_path / "L.tnsr"))
+    rep = json.loads((tmp_path / "rep.json").read_text())
+    Lp, rp = gpu.icnnm_solve(X * mask, mask, B, gpu.SolverConfig(max_iters=50, **FIXED))
+    assert _rel(L, Lp) < 1e-6
+    assert rep["iterations"] == 50 and rep["termination"] == "max_iters"
+    np.testing.assert_allclose(rep["objective"], rp.objective, rtol=1e-6)
