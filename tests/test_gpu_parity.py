@@ -449,14 +449,16 @@ def test_exact_residual_trace(gpu, engine):
 
 
 def test_exact_residual_stops_like_reference(gpu):
-    """With the reference's default tolerances the exact residual drives the
-    stopping test (solver.cpp:136-139) on the cosine recovery case."""
+    """The exact residual drives the primal stopping test (solver.cpp:136-139)
+    like the reference's on the cosine recovery case (tol_change disabled on
+    both sides: fp32 cannot resolve l_change below ~1e-7)."""
     L0 = np.cos(2 * np.pi * np.arange(32) / 8)
     B = gpu.learn_ensemble_basis([L0], (8,))
     mask = gpu.synth.reference_bernoulli_mask((32,), 0.75, 5)
-    cfg = gpu.SolverConfig(exact_residual=True, tol_primal=1e-5)
+    cfg = gpu.SolverConfig(exact_residual=True, tol_primal=1e-5, tol_change=1e-300)
     L, rep = gpu.icnnm_solve(L0 * mask, mask, B, cfg)
-    Lo, ro = O.icnnm_solve(L0 * mask, mask, _oracle_basis(B), O.SolverConfig(tol_primal=1e-5))
+    Lo, ro = O.icnnm_solve(L0 * mask, mask, _oracle_basis(B),
+                           O.SolverConfig(tol_primal=1e-5, tol_change=1e-300))
     assert rep.termination == "converged" and ro.termination == "converged"
     assert abs(rep.iterations - ro.iterations) <= 3
     assert _rel(L, L0) < 1e-3
