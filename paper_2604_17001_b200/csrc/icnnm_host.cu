@@ -305,6 +305,15 @@ inline float tf32_rna(float x) {
 // Pre-packed B tiles in the UMMA canonical SWIZZLE_NONE K-major layout, hi and
 // lo TF32 parts: [nt][kc] blocks of 32 KB = [hl][q][n/8][k/4][n%8][k%4].
 // forward: B(n=j, k=s) = K[s][j];  adjoint: B(n=s, k=j) = K[s][j].
+// Adjoint N order (icnnm_tc.cu tapoff): n = (sw*kt + st)*kh + sh -> tap s.
+inline int adj_tap(const Problem& p, int n) {
+  const int kh = static_cast<int>(p.kd[0]), kw = static_cast<int>(p.kd[1]),
+            kt = static_cast<int>(p.kd[2]);
+  (void)kw;
+  const int sh = n % kh, q = n / kh, st = q % kt, sw = q / kt;
+  return (sh * kw + sw) * kt + st;
+}
+
 std::vector<float> pack_b_tiles(const Problem& p, const TcPlan& t, const double* Kcm, bool fwd) {
   const int k = p.k;
   const int blk = icnnm_dev::tc::B_STAGE_BYTES / 4;
@@ -320,7 +329,8 @@ std::vector<float> pack_b_tiles(const Problem& p, const TcPlan& t, const double*
             const int kk = kc * icnnm_dev::tc::KC + q * 8 + k8;
             double x = 0.0;
             if (nn < k && kk < k)
-              x = fwd ? Kcm[static_cast<size_t>(nn) * k + kk] : Kcm[static_cast<size_t>(kk) * k + nn];
+              x = fwd ? Kcm[static_cast<size_t>(nn) * k + kk]
+                      : Kcm[static_cast<size_t>(kk) * k + adj_tap(p, nn)];
             const float xf = static_cast<float>(x);
             const float hi = tf32_rna(xf);
             const float lo = xf - hi;
@@ -367,6 +377,9 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   // stage counts that fit in shared memory (227 KB opt-in)
   a.sb = icnnm_dev::tc::SB;
   a.ws = icnnm_dev::tc::WS;
+  // shrink W stages to 3, then B stages to 3, then both to 2 until it fits
+  while (icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws) > 227 * 1024 && a.ws > 3) --a.ws;
+  while (icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws) > 227 * 1024 && a.sb > 3) --a.sb;
   while (icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws) > 227 * 1024 && a.ws > 2) --a.ws;
   while (icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws) > 227 * 1024 && a.sb > 2) --a.sb;
   a.nbricks = n_bricks(gtc);

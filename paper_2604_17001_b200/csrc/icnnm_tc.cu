@@ -289,7 +289,21 @@ icnnm_tc_kernel(TcArgs a) {
   for (int s = tid; s < g.ktp; s += blockDim.x) {
     int off = 0;
     if (s < g.k) {
-      int st = s % g.kt, q = s / g.kt, sw = q % g.kw, sh = q / g.kw;
+      int st, sw, sh;
+      if (FWD) {
+        st = s % g.kt;
+        const int q = s / g.kt;
+        sw = q % g.kw;
+        sh = q / g.kw;
+      } else {
+        // adjoint N order: sh fastest (see tap_perm in the host): within a
+        // warp the 32 rows share vh, so taps with different sh never hit the
+        // same output cell -> the col2im scatter can batch them hazard-free
+        sh = s % g.kh;
+        const int q = s / g.kh;
+        st = q % g.kt;
+        sw = q / g.kt;
+      }
       off = (sh * g.HW + sw) * g.HT + st;
     }
     tapoff[s] = off;
@@ -302,7 +316,7 @@ icnnm_tc_kernel(TcArgs a) {
   if (FWD) {
     for (int j = tid; j < g.kp; j += blockDim.x) nrm[j] = 0.0;
   } else {
-    for (int e = tid; e < 4 * nobp; e += blockDim.x) ob[e] = 0.f;
+    for (int e = tid; e < 4 * (nobp + 32); e += blockDim.x) ob[e] = 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -396,7 +410,8 @@ icnnm_tc_kernel(TcArgs a) {
     const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
     const int vt = row % g.bt, vw = (row / g.bt) % g.bw, vh = row / (g.bt * g.bw);
     const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
-    float* myob = ob + quad * nobp;
+    const int obs = nobp + 32;             // output-brick stride (+32 scratch)
+    float* myob = ob + quad * obs;
     float* myred = red + ew * 32 * 33;
     constexpr int NHALF = NEPI / 4;
     float gacc = 0.f;  // mode 2: this thread's share of ||(1-c)W - A(L)K||^2
@@ -454,14 +469,36 @@ icnnm_tc_kernel(TcArgs a) {
             if (lane < ncol) atomicAdd(nrm + j0 + lane, static_cast<double>(s));
           } else {
             const int s0 = nt * a.wbase + c0;
+            if (g.kh >= 4) {
+              // batches of 4 consecutive N columns = 4 distinct sh: no hazards
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int s = s0 + i;
-              if (i < ncol && s < g.k) {
-                float* o = myob + (hidx - tapoff[s]);
-                *o += __uint_as_float(u[i]);
+              for (int i = 0; i < 32; i += 4) {
+                float* o[4];
+                float v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const int sidx = s0 + i + q;
+                  const bool ok = (i + q < ncol) && sidx < g.k;
+                  o[q] = myob + (ok ? hidx - tapoff[sidx] : nobp + lane);  // per-lane scratch
+                  v[q] = ok ? __uint_as_float(u[i + q]) : 0.f;
+                }
+                float x[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) x[q] = *o[q];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) *o[q] = x[q] + v[q];
+                __syncwarp();
               }
-              __syncwarp();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const int sidx = s0 + i;
+                if (i < ncol && sidx < g.k) {
+                  float* o = myob + (hidx - tapoff[sidx]);
+                  *o += __uint_as_float(u[i]);
+                }
+                __syncwarp();
+              }
             }
           }
         }
@@ -476,11 +513,11 @@ icnnm_tc_kernel(TcArgs a) {
       if (!FWD) {
         named_sync(2, NEPI * 32);
         for (int e = row; e < nob; e += 128) {
-          float s = ob[e] + ob[nobp + e] + ob[2 * nobp + e] + ob[3 * nobp + e];
+          float s = ob[e] + ob[obs + e] + ob[2 * obs + e] + ob[3 * obs + e];
           ob[e] = 0.f;
-          ob[nobp + e] = 0.f;
-          ob[2 * nobp + e] = 0.f;
-          ob[3 * nobp + e] = 0.f;
+          ob[obs + e] = 0.f;
+          ob[2 * obs + e] = 0.f;
+          ob[3 * obs + e] = 0.f;
           if (s == 0.f) continue;
           int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
           int hs = h0 - (g.kh - 1) + aa + g.hoff;

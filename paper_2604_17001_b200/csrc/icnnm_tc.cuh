@@ -11,7 +11,7 @@ namespace tc {
 
 constexpr int KC = 32;                         // K per chunk (4 MMA K-steps of 8)
 constexpr int SA = 4;                          // TMEM A stages (64 columns each)
-constexpr int SB = 3;                          // SMEM B stages (max; runtime a.sb)
+constexpr int SB = 4;                          // SMEM B stages (max; runtime a.sb)
 constexpr int WS = 4;                          // adjoint: SMEM W-chunk stages (max; runtime a.ws)
 constexpr int W_STAGE_BYTES = 128 * KC * 4;    // 16 KB: 32 columns x 128 rows
 constexpr int NTMAX = 128;                     // accumulator width (N per tile)
@@ -62,7 +62,7 @@ inline size_t smem_bytes(const Geo& g, bool fwd, int sb = SB, int ws = WS) {
   if (fwd)
     b += 2 * nobp * 4 + 8 * 32 * 33 * 4 + static_cast<size_t>(g.kp) * 8;
   else
-    b += 4 * nobp * 4;
+    b += 4 * (nobp + 32) * 4;
   return b;
 }
 
