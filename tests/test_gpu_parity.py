@@ -501,3 +501,29 @@ def test_cli_learn_complete_end_to_end(gpu, tmp_path):
     assert _rel(L, Lp) < 1e-6
     assert rep["iterations"] == 50 and rep["termination"] == "max_iters"
     np.testing.assert_allclose(rep["objective"], rp.objective, rtol=1e-6)
+
+
+# --------------------------------------------------------------------------
+# Full-size BASELINE config 2 against the committed fp64-oracle golden
+# (tests/golden/cfg2_it300.npz, oracle/gen_golden.py; the basis K is stored
+# with the golden so both sides use identical bits)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config2_full_size_golden(gpu, engine):
+    import os
+    from paper_2604_17001_b200 import synth
+    path = os.path.join(os.path.dirname(__file__), "golden", "cfg2_it300.npz")
+    gd = np.load(path)
+    w = synth.WORKLOADS[2]
+    assert tuple(gd["dims"]) == w.dims and tuple(gd["kernel"]) == w.kernel
+    X, mask = w.target(), w.mask()
+    B = gpu.EigenBasis(tuple(int(x) for x in gd["kernel"]), gd["K"], gd["eigenvalues"])
+    L, rep = gpu.icnnm_solve(X * mask, mask, B,
+                             gpu.SolverConfig(max_iters=int(gd["iters"]), engine=engine, **FIXED))
+    Lo = gd["L"].astype(np.float64)
+    assert rep.iterations == 300
+    assert _rel(L, Lo) <= 1e-4
+    miss = mask == 0
+    assert _rel(L[miss], Lo[miss]) <= 1e-3
+    assert abs(synth.psnr(X, L) - float(gd["psnr"])) <= 0.01
+    np.testing.assert_allclose(rep.objective, gd["objective"], rtol=1e-4)

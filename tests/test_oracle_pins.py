@@ -334,3 +334,28 @@ def test_certified_exact_recovery(case):                 # :178-209
     B = O.learn_ensemble_basis([L0], ks)
     L, rep = O.icnnm_solve(L0 * mask, mask, B, O.SolverConfig())
     assert O.rel_l2(L, L0) < 1e-3 and rep.iterations <= 1000
+
+
+def test_golden_cfg2_fixture_matches_oracle():
+    """The committed config-2 golden was produced by this oracle
+    (oracle/gen_golden.py): its basis is the oracle's learned basis and its
+    first objective values are reproduced by re-running the oracle."""
+    import os
+    from threadpoolctl import threadpool_limits
+    path = os.path.join(os.path.dirname(__file__), "golden", "cfg2_it300.npz")
+    gd = np.load(path)
+    w = synth.WORKLOADS[2]
+    X, mask = w.target(), w.mask()
+    nthr = os.cpu_count() or 1
+    O.WORKERS = nthr
+    try:
+        with threadpool_limits(limits=nthr):
+            B = O.learn_ensemble_basis(w.training(), w.kernel)
+            np.testing.assert_allclose(B.eigenvalues, gd["eigenvalues"], rtol=1e-10)
+            s = O.AdmmSolver(X * mask, mask, O.EigenBasis(w.kernel, gd["K"], gd["eigenvalues"]),
+                             O.SolverConfig(max_iters=300, tol_primal=1e-300, tol_change=1e-300))
+            s.step()
+    finally:
+        O.WORKERS = 1
+    np.testing.assert_allclose(s.report.objective[0], gd["objective"][0], rtol=1e-12)
+    assert abs(O.psnr(X, gd["L"].astype(np.float64)) - float(gd["psnr"])) < 1e-4
