@@ -808,23 +808,26 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     S.prof_ms[3] = acc[3] / iters;
     for (auto& x : e) cudaEventDestroy(x);
   } else {
+    // Capture U iterations per graph so the device never waits on the host
+    // between iterations; replays past max_iters are no-ops (coef deactivates).
+    const int U = std::min(iters, 32);
     cudaGraph_t graph;
     cudaGraphExec_t exec;
     const int64_t before = S.launches;
     CK(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeThreadLocal));
-    iteration();
+    for (int u = 0; u < U; ++u) iteration();
     CK(cudaStreamEndCapture(S.stream, &graph));
-    const int64_t per_iter = S.launches - before + 1 /*coef*/ +
+    const int64_t per_iter = (S.launches - before) / U + 1 /*coef*/ +
                              static_cast<int64_t>(S.slabs.size()) /*update*/;
     S.launches = before;
     CK(cudaGraphInstantiate(&exec, graph, 0));
     const bool may_stop = !(cfg.tol_primal <= 1e-200 && cfg.tol_change <= 1e-200);
     IterState* hst = nullptr;
     CK(cudaMallocHost(&hst, sizeof(IterState)));
-    for (int it = 0; it < iters; ++it) {
+    for (int it = 0; it < iters; it += U) {
       CK(cudaGraphLaunch(exec, S.stream));
-      S.launches += per_iter;
-      if (may_stop && (it % 32) == 31) {
+      S.launches += per_iter * std::min(U, iters - it);
+      if (may_stop && it + U < iters) {
         CK(cudaMemcpyAsync(hst, S.st.p, sizeof(IterState), cudaMemcpyDeviceToHost, S.stream));
         CK(cudaStreamSynchronize(S.stream));
         if (!hst->active) break;
@@ -1250,8 +1253,15 @@ void gram_lags_accumulate(const Problem& p, const double* dX, double* dR, cudaSt
   check_smem(smem);
   const int nb = ((H + bh - 1) / bh) * ((W + bw - 1) / bw) * ((T + bt - 1) / bt);
   dim3 grid(2 * kh - 1, std::max(1, std::min(nb, 1184 / (2 * kh - 1) + 1)));
-  icnnm_dev::icnnm_gram_lags<<<grid, 256, smem, s>>>(H, W, T, kh, kw, kt, bh, bw, bt, dX, dR);
+  const int64_t nR = static_cast<int64_t>(2 * kh - 1) * nl;
+  DBuf<double> part(static_cast<size_t>(grid.y) * nR);
+  icnnm_dev::icnnm_gram_lags<<<grid, 256, smem, s>>>(H, W, T, kh, kw, kt, bh, bw, bt, dX,
+                                                     part.p);
   CKL();
+  icnnm_dev::icnnm_gram_reduce<<<grid_for(nR, 256), 256, 0, s>>>(nR, static_cast<int>(grid.y),
+                                                                 part.p, dR);
+  CKL();
+  CK(cudaStreamSynchronize(s));
 }
 
 // G[s,t] = R[(s - t)] over the kernel box (spectral.cpp:62-79).

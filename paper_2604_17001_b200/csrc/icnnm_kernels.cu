@@ -587,10 +587,24 @@ icnnm_gram_lags(int H, int W, int T, int kh, int kw, int kt, int bh, int bw, int
       }
     }
   }
+  // deterministic: one partial per (dh, CTA-row); icnnm_gram_reduce sums them
+  // in a fixed order, so learn_basis is bit-reproducible run to run
 #pragma unroll
   for (int p = 0; p < GRAM_LPT; ++p) {
     const int l = threadIdx.x + p * blockDim.x;
-    if (l < nl) atomicAdd(R + static_cast<size_t>(blockIdx.x) * nl + l, acc[p]);
+    if (l < nl)
+      R[(static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * nl + l] = acc[p];
+  }
+}
+
+// R_out[i] += sum_y partial[y][i] (fixed order)
+__global__ void icnnm_gram_reduce(int64_t n, int ny, const double* __restrict__ partial,
+                                  double* __restrict__ R_out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int y = 0; y < ny; ++y) s += partial[static_cast<size_t>(y) * n + i];
+    R_out[i] += s;
   }
 }
 

@@ -80,6 +80,7 @@ __global__ void icnnm_setup(int64_t m, const double* M, const double* msk, int m
                             float* Lt);
 __global__ void icnnm_gram_lags(int H, int W, int T, int kh, int kw, int kt, int bh, int bw,
                                 int bt, const double* X, double* R);
+__global__ void icnnm_gram_reduce(int64_t n, int ny, const double* partial, double* R_out);
 __global__ void icnnm_colnorm2(int64_t rows, int64_t cols, const double* W, double* out);
 __global__ void icnnm_colscale(int64_t rows, int64_t cols, const double* W, const double* n2,
                                double tau, double* Z);

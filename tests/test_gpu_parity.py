@@ -180,6 +180,16 @@ def test_learn_basis_matches_oracle(gpu):
         start = end
 
 
+def test_learn_basis_is_deterministic(gpu):
+    from paper_2604_17001_b200 import synth
+    w = synth.WORKLOADS[1]
+    refs = w.training()
+    a = gpu.learn_ensemble_basis(refs, w.kernel)
+    b = gpu.learn_ensemble_basis(refs, w.kernel)
+    np.testing.assert_array_equal(a.K, b.K)
+    np.testing.assert_array_equal(a.eigenvalues, b.eigenvalues)
+
+
 def test_learn_basis_degenerate_and_errors(gpu):
     b = gpu.learn_ensemble_basis([np.zeros((4, 4))], (2, 2))
     assert b.degenerate and np.array_equal(b.K, np.eye(4))
@@ -485,7 +495,8 @@ def test_cli_learn_complete_end_to_end(gpu, tmp_path):
     assert out.returncode == 0, out.stderr
     B = pio.read_ebas(ebas)
     Bp = gpu.learn_ensemble_basis(refs, w.kernel)
-    np.testing.assert_array_equal(B.K, Bp.K)
+    np.testing.assert_array_equal(B.K, Bp.K)          # deterministic Gram reduction
+    np.testing.assert_array_equal(B.eigenvalues, Bp.eigenvalues)
     pio.write_tnsr(str(tmp_path / "M.tnsr"), X * mask)
     pio.write_tnsr(str(tmp_path / "mask.tnsr"), mask)
     (tmp_path / "cfg.json").write_text(json.dumps({"max_iters": 50, "tol_primal": 1e-300,
