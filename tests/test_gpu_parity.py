@@ -538,3 +538,45 @@ def test_config2_full_size_golden(gpu, engine):
     assert _rel(L[miss], Lo[miss]) <= 1e-3
     assert abs(synth.psnr(X, L) - float(gd["psnr"])) <= 0.01
     np.testing.assert_allclose(rep.objective, gd["objective"], rtol=1e-4)
+
+
+# --------------------------------------------------------------------------
+# tcgen05 engine edge cases: N-tile boundaries (k around 128/256, partial last
+# tile), partial bricks, T < 8, order 1/2, kernel box = whole tensor
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("dims,ks", [((12, 11, 10), (4, 4, 8)),     # k=128: exactly one tile
+                                     ((12, 11, 10), (1, 11, 9)),    # k=99
+                                     ((14, 9, 17), (3, 3, 15)),     # k=135: 128 + 7
+                                     ((10, 9, 20), (2, 8, 16)),     # k=256: two full tiles
+                                     ((9, 9, 7), (9, 9, 4)),        # kernel spans H and W
+                                     ((5, 3, 3), (5, 3, 3)),        # kernel = whole tensor
+                                     ((40, 3), (7, 3)),             # order 2, T < 8
+                                     ((50,), (33,))])               # order 1, k=33
+@pytest.mark.parametrize("engine", ENGINES)
+def test_operator_edge_cases(gpu, dims, ks, engine):
+    rng = np.random.default_rng(7)
+    k = int(np.prod(ks))
+    Li = rng.integers(-8, 9, size=dims).astype(np.float64)
+    np.testing.assert_array_equal(gpu.BasisConvolver(dims, ks, np.eye(k), engine=engine).apply(Li),
+                                  O.conv_matrix(Li, ks))
+    W = rng.integers(-4, 5, size=(Li.size, k)).astype(np.float64)
+    np.testing.assert_array_equal(gpu.conv_adjoint(W, ks, dims, engine=engine),
+                                  O.conv_adjoint(W, ks, dims))
+    L = rng.uniform(-1, 1, size=dims)
+    K = _rand_orth(k, 11)
+    got = gpu.BasisConvolver(dims, ks, K, engine=engine).apply(L)
+    assert _rel(got, O.BasisConvolver(dims, ks, K).apply(L)) < 1e-5
+
+
+@pytest.mark.parametrize("dims,ks,iters", [((14, 9, 17), (3, 3, 15), 40), ((10, 9, 20), (2, 8, 16), 30),
+                                           ((40, 3), (7, 3), 60), ((50,), (33,), 80)])
+@pytest.mark.parametrize("engine", ENGINES)
+def test_solve_edge_cases(gpu, dims, ks, iters, engine):
+    rng = np.random.default_rng(3)
+    base = np.cos(np.linspace(0, 6, int(np.prod(dims)))).reshape(dims)
+    X = base + 0.05 * rng.standard_normal(dims)
+    mask = gpu.synth.reference_bernoulli_mask(dims, 0.6, 4)
+    B = gpu.learn_ensemble_basis([base + 0.05 * rng.standard_normal(dims)], ks)
+    Lg, _ = gpu.icnnm_solve(X * mask, mask, B, gpu.SolverConfig(max_iters=iters, engine=engine, **FIXED))
+    Lo, _ = O.icnnm_solve(X * mask, mask, _oracle_basis(B), O.SolverConfig(max_iters=iters, **FIXED))
+    assert _rel(Lg, Lo) <= 1e-4
