@@ -129,7 +129,7 @@ struct Problem {
   int64_t m = 0;
   int k = 0;
   int kp = 0;     // FFMA engine column padding (multiple of 64)
-  int kp_tc = 0;  // tcgen05 engine padding (multiple of 32)
+  int kp_tc = 0;  // tcgen05 engine padding (multiple of KC = 16)
 };
 
 inline int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -269,21 +269,38 @@ void pack_basis(const Problem& p, const double* Kcm, std::vector<float>& Krm,
 // tcgen05 engine plan and B packing
 // ---------------------------------------------------------------------------
 struct TcPlan {
-  int kp = 0, ntn = 0, nkc = 0, nlast = 0, wbase = 0;
+  int kp = 0, ntn = 0, nkc = 0, nlast = 0, wbase = 0, sa = 0;
   int width(int nt) const { return std::min(wbase, kp - nt * wbase); }
 };
 
-// N-tiling: tiles of 128 columns (+ a narrower last tile).  Measured on B200
-// (tools/ubench/mma_rate.cu): an M=128 kind::tf32 MMA costs max(64, N/2)
-// cycles, so splitting into narrower balanced tiles gains nothing.
+// N-tiling of kp columns into ntn tiles of width <= NTMAX (multiples of 16),
+// minimising the measured MMA cost: an M=128 kind::tf32 MMA takes
+// max(64, N/2) cycles on B200 (tools/ubench/mma_rate.cu), so few wide tiles
+// beat many narrow ones (k=405: 2x208 instead of 128+128+128+32 = -19% MMA
+// time, half the MMA instructions).  TMEM: 2 accumulators of wbase columns +
+// sa A stages of 2*KC columns <= 512.
 TcPlan tc_plan(const Problem& p) {
-  TcPlan t;
-  t.kp = p.kp_tc;
-  t.wbase = icnnm_dev::tc::NTMAX;
-  t.ntn = (t.kp + t.wbase - 1) / t.wbase;
-  t.nlast = t.kp - (t.ntn - 1) * t.wbase;
-  t.nkc = t.kp / icnnm_dev::tc::KC;
-  return t;
+  TcPlan best;
+  const int kp = p.kp_tc;
+  double best_cost = 1e300;
+  const int n0 = (kp + icnnm_dev::tc::NTMAX - 1) / icnnm_dev::tc::NTMAX;
+  for (int ntn = n0; ntn <= n0 + 8; ++ntn) {
+    const int wb = static_cast<int>(roundup((kp + ntn - 1) / ntn, 16));
+    if (wb > icnnm_dev::tc::NTMAX) continue;
+    const int nt_eff = (kp + wb - 1) / wb;
+    double cost = 0;
+    for (int i = 0; i < nt_eff; ++i) cost += std::max(64.0, std::min(wb, kp - i * wb) / 2.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best.kp = kp;
+      best.ntn = nt_eff;
+      best.wbase = wb;
+      best.nlast = kp - (nt_eff - 1) * wb;
+    }
+  }
+  best.nkc = kp / icnnm_dev::tc::KC;
+  best.sa = std::min(icnnm_dev::tc::SA, (512 - 2 * best.wbase) / (2 * icnnm_dev::tc::KC));
+  return best;
 }
 
 Geo tc_geo(const Geo& g, const TcPlan& t) {
@@ -322,7 +339,7 @@ std::vector<float> pack_b_tiles(const Problem& p, const TcPlan& t, const double*
     const int wn = t.width(nt);
     for (int kc = 0; kc < t.nkc; ++kc) {
       float* base = out.data() + (static_cast<size_t>(nt) * t.nkc + kc) * blk;
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < icnnm_dev::tc::KC / 8; ++q)
         for (int n = 0; n < wn; ++n)
           for (int k8 = 0; k8 < 8; ++k8) {
             const int nn = nt * t.wbase + n;
@@ -337,7 +354,7 @@ std::vector<float> pack_b_tiles(const Problem& p, const TcPlan& t, const double*
             const size_t off = static_cast<size_t>(q) * (8 * wn) + (n / 8) * 64 + (k8 / 4) * 32 +
                                (n % 8) * 4 + (k8 % 4);
             base[off] = hi;
-            base[32 * wn + off] = lo;
+            base[(icnnm_dev::tc::KC / 8) * 8 * wn + off] = lo;
           }
     }
   }
@@ -345,7 +362,7 @@ std::vector<float> pack_b_tiles(const Problem& p, const TcPlan& t, const double*
 }
 
 inline int64_t tc_w_elems(const Geo& g, const TcPlan& t) {
-  return n_bricks(g) * static_cast<int64_t>(t.ntn) * 128 * 128;
+  return n_bricks(g) * static_cast<int64_t>(t.kp) * 128;
 }
 
 void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const float* src,
@@ -373,7 +390,8 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   a.nkc = t.nkc;
   a.nlast = t.nlast;
   a.wbase = t.wbase;
-  a.ntj = t.ntn;
+  a.accw = t.wbase;
+  a.sa = t.sa;
   // stage counts that fit in shared memory (227 KB opt-in)
   a.sb = icnnm_dev::tc::SB;
   a.ws = icnnm_dev::tc::WS;
@@ -1112,7 +1130,7 @@ int icnnm_cuda_conv_forward_ex(int order, const int64_t* dims, const double* L,
             const int64_t b = r / BM, v = r % BM;
             for (int j = 0; j < p.k; ++j)
               out[static_cast<size_t>(j) * p.m + flat] =
-                  Wh[((static_cast<size_t>(b) * t.ntn + j / 128) * 128 + (j % 128)) * 128 + v];
+                  Wh[(static_cast<size_t>(b) * t.kp + j) * 128 + v];
           }
       return;
     }
@@ -1172,7 +1190,7 @@ int icnnm_cuda_conv_adjoint_ex(int order, const int64_t* dims, const int64_t* kd
             const int64_t r = brick_row(gt, h, w, tt);
             const int64_t b = r / BM, v = r % BM;
             for (int j = 0; j < p.k; ++j)
-              Wt[((static_cast<size_t>(b) * t.ntn + j / 128) * 128 + (j % 128)) * 128 + v] =
+              Wt[(static_cast<size_t>(b) * t.kp + j) * 128 + v] =
                   static_cast<float>(Wcm[static_cast<size_t>(j) * p.m + flat]);
           }
       DBuf<float> dB(ba.size()), dW(Wt.size());

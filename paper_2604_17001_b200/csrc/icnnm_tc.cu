@@ -16,13 +16,14 @@
 //                         B from SMEM via a SWIZZLE_NONE K-major descriptor)
 //   warp 9     loader   : cp.async.bulk of host-pre-packed B tiles (UMMA
 //                         canonical layout) into a 3-stage SMEM ring
-// TMEM: two 128-column accumulators (epilogue of tile i overlaps MMAs of
-// tile i+1) + four 64-column A stages = 512 columns.
+// TMEM: two accumulators of accw <= 208 columns (epilogue of tile i overlaps
+// the MMAs of tile i+1) + sa A stages of 2*KC columns (hi | lo).
 //
 // Forward  (a)+(b): D[v, j] = sum_s L~[v - s] K[s, j]          (N = columns j)
 // Adjoint  (c)    : D[v, s] = sum_j W[v, j] c_j K[s, j]        (N = taps s)
-// W layout (this engine): [brick][jt][jj][row], jt = j / 128, jj = j % 128,
-// so epilogue/builder threads (one per row) access it coalesced.
+// W layout (this engine): [brick][j][row] (column-major per brick), so
+// epilogue/builder threads (one per row) access it coalesced and any column
+// range of a brick is one contiguous block.
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -183,6 +184,12 @@ __device__ __forceinline__ int wrapi(int x, int n) {
   return r < 0 ? r + n : r;
 }
 
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+      R8(0)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -213,12 +220,12 @@ __device__ __forceinline__ int tile_width(const TcArgs& a, int nt) {
 //   warp  9 + NEPI          B loader
 // ---------------------------------------------------------------------------
 template <bool FWD>
-__global__ void __launch_bounds__(FWD ? 576 : 448, 1)
+__global__ void __launch_bounds__(FWD ? 576 : 480, 1)
 icnnm_tc_kernel(TcArgs a) {
   constexpr int NB = 8;                  // builder warps
   constexpr int NEPI = FWD ? 8 : 4;      // epilogue warps
   constexpr int WMMA = NB + NEPI;        // MMA warp
-  constexpr int WLOAD = NB + NEPI + 1;   // loader warp
+  constexpr int WLOAD = NB + NEPI + 1;   // B loader warp (adjoint: + W loader warp after it)
   const Geo& g = a.g;
   float rr = 0.f;
   if (a.mode == 1) {
@@ -229,7 +236,8 @@ icnnm_tc_kernel(TcArgs a) {
   if (a.mode == 2 && !a.st->active) return;  // forward on L_{t+1}: exact residual only
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* p = smem;
-  const int sbn = a.sb, wsn = a.ws;
+  const int sbn = a.sb, wsn = a.ws, san = a.sa;
+  const uint32_t a_col0 = 2u * static_cast<uint32_t>(a.accw);
   float* Bst = reinterpret_cast<float*>(p);
   p += sbn * B_STAGE_BYTES;
   float* Wst = reinterpret_cast<float*>(p);   // adjoint: W-chunk ring
@@ -364,8 +372,8 @@ icnnm_tc_kernel(TcArgs a) {
       }
       for (int nt = 0; nt < ntn; ++nt) {
         for (int kc = 0; kc < nkc; ++kc, ++cnt) {
-          const int sa = cnt % SA;
-          const uint32_t ph = (cnt / SA) & 1;
+          const int sa = cnt % san;
+          const uint32_t ph = (cnt / san) & 1;
           const int wsi = cnt % wsn;
           const uint32_t wph = (cnt / wsn) & 1;
           long long t0c = dbg.p ? clk() : 0;
@@ -374,19 +382,19 @@ icnnm_tc_kernel(TcArgs a) {
           tc_fence_after();
           long long t1c = dbg.p ? clk() : 0;
           if (!(a.skip & 1)) {
-            uint32_t hi[16], lo[16];
+            uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int q = kc * KC + 16 * half + i;
+            for (int i = 0; i < 8; ++i) {
+              const int q = kc * KC + 8 * half + i;
               const float x = FWD ? hcur[hidx - tapoff[q]]
-                                  : Wst[wsi * (W_STAGE_BYTES / 4) + (16 * half + i) * 128 + row] * cs[q];
+                                  : Wst[wsi * (W_STAGE_BYTES / 4) + (8 * half + i) * 128 + row] * cs[q];
               const uint32_t h = f2tf32(x);
               hi[i] = h;
               lo[i] = __float_as_uint(x - __uint_as_float(h));
             }
-            const uint32_t col = A_COL0 + sa * 64 + 16 * half;
-            tmem_st16(tbase + lane_base + col, hi);
-            tmem_st16(tbase + lane_base + col + 32, lo);
+            const uint32_t col = a_col0 + sa * (2 * KC) + 8 * half;
+            tmem_st8(tbase + lane_base + col, hi);
+            tmem_st8(tbase + lane_base + col + KC, lo);
             tmem_wait_st();
           }
           tc_fence_before();
@@ -431,12 +439,12 @@ icnnm_tc_kernel(TcArgs a) {
         long long t1c = dbg.p ? clk() : 0;
         for (int c0 = 32 * half; c0 < wn && !(a.skip & 2); c0 += 32 * NHALF) {
           uint32_t u[32];
-          tmem_ld32(tbase + lane_base + acc * 128 + c0, u);
+          tmem_ld32(tbase + lane_base + acc * a.accw + c0, u);
           tmem_wait_ld();
           const int ncol = (wn - c0) < 32 ? (wn - c0) : 32;
           if (FWD && a.mode == 2) {
             const int j0 = nt * a.wbase + c0;
-            const float* wp = a.Wout + ((static_cast<size_t>(b) * a.ntj + (j0 >> 7)) * 128 + (j0 & 127)) * 128 + row;
+            const float* wp = a.Wout + (static_cast<size_t>(b) * g.kp + j0) * 128 + row;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               if (i < ncol && valid) {
@@ -447,7 +455,7 @@ icnnm_tc_kernel(TcArgs a) {
             }
           } else if (FWD) {
             const int j0 = nt * a.wbase + c0;
-            float* wp = a.Wout + ((static_cast<size_t>(b) * a.ntj + (j0 >> 7)) * 128 + (j0 & 127)) * 128 + row;
+            float* wp = a.Wout + (static_cast<size_t>(b) * g.kp + j0) * 128 + row;
             float wo[32];
             if (a.mode == 1) {
 #pragma unroll
@@ -553,16 +561,16 @@ icnnm_tc_kernel(TcArgs a) {
           const uint32_t aph = (tcount >> 1) & 1;
           const int wn = tile_width(a, nt);
           const uint32_t idesc = idesc_tf32(wn);
-          const uint32_t dcol = tbase + acc * 128;
+          const uint32_t dcol = tbase + acc * a.accw;
           long long q0 = a.dbg ? clk() : 0;
           if (!(a.skip & 32)) mbar_wait(ACC_empty + acc, aph ^ 1);
           if (a.dbg) wacc += clk() - q0;
           tc_fence_after();
           for (int kc = 0; kc < nkc; ++kc, ++cnt, ++bcnt) {
-            const int sa = cnt % SA;
+            const int sa = cnt % san;
             const int sb = bcnt % sbn;
             long long q1 = a.dbg ? clk() : 0;
-            if (!(a.skip & 8)) mbar_wait(A_full + sa, (cnt / SA) & 1);
+            if (!(a.skip & 8)) mbar_wait(A_full + sa, (cnt / san) & 1);
             long long q2 = a.dbg ? clk() : 0;
             if (!(a.skip & 16)) mbar_wait(B_full + sb, (bcnt / sbn) & 1);
             if (a.dbg) {
@@ -571,16 +579,16 @@ icnnm_tc_kernel(TcArgs a) {
               wb += q3 - q2;
             }
             tc_fence_after();
-            const uint32_t acol = tbase + A_COL0 + sa * 64;
+            const uint32_t acol = tbase + a_col0 + sa * (2 * KC);
             const uint32_t bhi = bs0 + sb * B_STAGE_BYTES;
-            const uint32_t blo = bhi + wn * 128;
+            const uint32_t blo = bhi + wn * (KC / 8) * 32;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < KC / 8; ++q) {
               const uint64_t dh = bdesc(bhi + q * wn * 32);
               const uint64_t dl = bdesc(blo + q * wn * 32);
               const uint32_t first = (kc == 0 && q == 0) ? 0u : 1u;
               tc_mma_ts_elect(dcol, acol + q * 8, dh, idesc, first);
-              tc_mma_ts_elect(dcol, acol + 32 + q * 8, dh, idesc, 1u);
+              tc_mma_ts_elect(dcol, acol + KC + q * 8, dh, idesc, 1u);
               tc_mma_ts_elect(dcol, acol + q * 8, dl, idesc, 1u);
             }
             if (!(a.skip & 8)) tc_commit_elect(A_empty + sa);
@@ -597,7 +605,7 @@ icnnm_tc_kernel(TcArgs a) {
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp == WLOAD) {
     // ===================== B loader =====================
     if (lane == 0 && !(a.skip & 16)) {
       uint32_t bcnt = 0;
@@ -605,7 +613,7 @@ icnnm_tc_kernel(TcArgs a) {
       for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
         for (int nt = 0; nt < ntn; ++nt) {
           const int wn = tile_width(a, nt);
-          const uint32_t bytes = static_cast<uint32_t>(wn) * 256;
+          const uint32_t bytes = static_cast<uint32_t>(wn) * KC * 8;
           for (int kc = 0; kc < nkc; ++kc, ++bcnt) {
             const int sb = bcnt % sbn;
             long long q0 = a.dbg ? clk() : 0;
@@ -623,9 +631,11 @@ icnnm_tc_kernel(TcArgs a) {
       }
       if (a.dbg) atomicAdd(a.dbg + DBG_LOAD_WAIT, static_cast<unsigned long long>(wl));
     }
-    if (!FWD && lane == 1) {
-      // adjoint: stream W chunks (32 columns x 128 rows, 16 KB contiguous in
-      // the [brick][jt][jj][row] layout) ahead of the builders
+    __syncwarp();
+  } else if (!FWD && warp == WLOAD + 1) {
+    if (lane == 0) {
+      // adjoint: stream W chunks (16 columns x 128 rows, 8 KB contiguous in the
+      // [brick][j][row] layout) ahead of the builders
       uint32_t wcnt = 0;
       for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
         for (int nt = 0; nt < ntn; ++nt) {
@@ -633,8 +643,7 @@ icnnm_tc_kernel(TcArgs a) {
             const int wsi = wcnt % wsn;
             mbar_wait(W_empty + wsi, ((wcnt / wsn) & 1) ^ 1);
             mbar_arrive_expect_tx(W_full + wsi, W_STAGE_BYTES);
-            const int j0 = kc * KC;
-            const float* src = a.Win + ((static_cast<size_t>(b) * a.ntj + (j0 >> 7)) * 128 + (j0 & 127)) * 128;
+            const float* src = a.Win + (static_cast<size_t>(b) * g.kp + kc * KC) * 128;
             bulk_g2s(reinterpret_cast<uint8_t*>(Wst) + wsi * W_STAGE_BYTES, src, W_STAGE_BYTES,
                      W_full + wsi);
           }

@@ -9,14 +9,13 @@
 namespace icnnm_dev {
 namespace tc {
 
-constexpr int KC = 32;                         // K per chunk (4 MMA K-steps of 8)
-constexpr int SA = 4;                          // TMEM A stages (64 columns each)
+constexpr int KC = 16;                         // K per chunk (2 MMA K-steps of 8)
+constexpr int SA = 4;                          // TMEM A stages (max; runtime a.sa), 2*KC columns each
 constexpr int SB = 4;                          // SMEM B stages (max; runtime a.sb)
 constexpr int WS = 4;                          // adjoint: SMEM W-chunk stages (max; runtime a.ws)
-constexpr int W_STAGE_BYTES = 128 * KC * 4;    // 16 KB: 32 columns x 128 rows
-constexpr int NTMAX = 128;                     // accumulator width (N per tile)
-constexpr int B_STAGE_BYTES = NTMAX * KC * 4 * 2;  // hi + lo = 32 KB
-constexpr int A_COL0 = 256;                    // TMEM columns 0..255: 2 accumulators
+constexpr int W_STAGE_BYTES = 128 * KC * 4;    // 8 KB: 16 columns x 128 rows
+constexpr int NTMAX = 208;                     // max accumulator width (N per tile)
+constexpr int B_STAGE_BYTES = 256 * KC * 4 * 2;    // hi + lo, up to 256 rows = 32 KB
 
 struct TcArgs {
   Geo g;                 // kp = ktp = roundup(k, 32)
@@ -32,8 +31,9 @@ struct TcArgs {
   int ntn;               // N-tiles per brick
   int nkc;               // K-chunks per N-tile
   int nlast;             // width of the last N-tile (multiple of 16)
-  int wbase;             // width of the other N-tiles (multiple of 16, <= 128)
-  int ntj;               // j-tiles of the W layout
+  int wbase;             // width of the other N-tiles (multiple of 16, <= NTMAX)
+  int accw;              // TMEM accumulator width (= wbase): acc0 @0, acc1 @accw, A @2*accw
+  int sa;                // A stages used (<= SA, limited by TMEM)
   int64_t nbricks;
   unsigned long long* dbg;  // optional: per-role wait cycles (see DBG_*), or null
   int skip;                 // timing experiments only: 1 = no build work, 2 = no epilogue work
@@ -51,7 +51,7 @@ __global__ void icnnm_tc_kernel(TcArgs a);
 void* fwd_kernel_ptr();
 void* adj_kernel_ptr();
 
-inline int threads(bool fwd) { return fwd ? 576 : 448; }
+inline int threads(bool fwd) { return fwd ? 576 : 480; }
 
 inline size_t smem_bytes(const Geo& g, bool fwd, int sb = SB, int ws = WS) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
