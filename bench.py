@@ -284,6 +284,8 @@ def main():
     targets = {b: w.target(b=b) for b in mine}
     S = P.Solver(w.dims, B, device=dev)
 
+    loops = []
+
     def step():
         t = 0.0
         n = 0
@@ -291,6 +293,7 @@ def main():
             S.upload(targets[b] * mask, mask)
             rep = S.run(cfg)
             t += rep.device_seconds
+            loops.append(rep.loop_seconds)
             n += S.last_launches
         return t, n
 
@@ -322,7 +325,9 @@ def main():
 
     if rank == 0:
         report_line(args, P, w, B, cfg, iters, dev, world, value, t_max, kt, psnr, launches,
-                    clk, scaling, mask, targets[mine[0]] * mask)
+                    clk, scaling, mask, targets[mine[0]] * mask,
+                    extra={"step_device_s": [round(x, 5) for x in dev_s],
+                           "loop_s": [round(x, 5) for x in loops[-args.steps:]]})
     S.close()
     if dist:
         dist.barrier()
@@ -384,7 +389,7 @@ def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
 
 
 def report_line(args, P, w, B, cfg, iters, dev, world, value, t_max, kt, psnr, launches, clk,
-                scaling, mask, M):
+                scaling, mask, M, extra=None):
     import numpy as np
     from paper_2604_17001_b200 import synth
     peaks = load_peaks()
@@ -450,6 +455,8 @@ def report_line(args, P, w, B, cfg, iters, dev, world, value, t_max, kt, psnr, l
         "clocks": clk.summary(),
         "hbm_peak_gbs": peaks.get("hbm_gbs"),
     }
+    if extra:
+        line["timing_detail"] = extra
     print(json.dumps(line), flush=True)
 
 
