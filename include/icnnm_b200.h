@@ -191,6 +191,80 @@ int icnnm_cuda_objective(int order, const int64_t* dims, const double* L,
                          double lambda, int device, double* out);
 
 /* ------------------------------------------------------------------------
+ * Recovery-theory diagnostics (`analyze`), replacing
+ * /root/reference/proj/core/include/icnnm/analysis.hpp:25-99 and
+ * core/src/analysis.cpp.  Matrix-free on the GPU in fp64: the m x k
+ * convolution matrix the reference builds for its SVD (analysis.cpp:111-135)
+ * is never formed.  `evals` may be NULL (the reference's basis_from_matrix
+ * test bases carry zero eigenvalues); when given it is validated like
+ * EigenBasis::validate (spectral.cpp:25-41).  rank_tol default: 1e-8
+ * (kDefaultRankTol, spectral.hpp:25).
+ * ---------------------------------------------------------------------- */
+#define ICNNM_DEFAULT_RANK_TOL 1e-8
+
+/* ConvCoherence (analysis.hpp:62-67). */
+typedef struct icnnm_conv_coherence {
+  double mu1, mu2, tau;
+  int64_t rank;
+} icnnm_conv_coherence;
+
+/* ThresholdInputs / Thresholds (analysis.hpp:72-93). */
+typedef struct icnnm_threshold_inputs {
+  int64_t r_K;
+  double alpha_K, mu_K_I, mu1, mu2;
+  int64_t r0, k, m;
+  double rho0;
+} icnnm_threshold_inputs;
+
+typedef struct icnnm_threshold_values {
+  double rho_min_noiseless, rho_min_noisy, error_bound_factor, cnnm_bound,
+      icnnm_ideal_bound;
+  int certified;
+} icnnm_threshold_values;
+
+/* RecoveryDiagnostics (analysis.hpp:29-44).  support_I: caller-owned array
+ * of k entries (or NULL); the first r_K are written. */
+typedef struct icnnm_recovery_diagnostics {
+  int64_t r_K;
+  int64_t* support_I;
+  double alpha_K, mu_K_I, mu1, mu2, tau;
+  int64_t r0;
+  double rho0, rho_min_noiseless, rho_min_noisy, error_bound_factor, cnnm_bound,
+      icnnm_ideal_bound;
+  int certified;
+} icnnm_recovery_diagnostics;
+
+/* sigma^K_i = ||A(L0) K_i|| for i < k (relative_eigenvalues,
+ * analysis.cpp:29-38). */
+int icnnm_cuda_relative_eigenvalues(int order, const int64_t* dims, const double* L0,
+                                    const int64_t* kdims, const double* K_colmajor,
+                                    const double* evals, int device, double* sigma);
+/* relative_conv_rank (analysis.hpp:45-51): r_K and the support (k entries). */
+int icnnm_cuda_relative_conv_rank(int order, const int64_t* dims, const double* L0,
+                                  const int64_t* kdims, const double* K_colmajor,
+                                  const double* evals, double rank_tol, int device,
+                                  int64_t* r_K, int64_t* support);
+/* spectral_corr_coeff (analysis.hpp:53-57); r_K = 0 is an error. */
+int icnnm_cuda_spectral_corr_coeff(int order, const int64_t* dims, const double* L0,
+                                   const int64_t* kdims, const double* K_colmajor,
+                                   const double* evals, double rank_tol, int device,
+                                   double* alpha);
+/* active_coherence (analysis.hpp:59-60); host only. */
+int icnnm_active_coherence(int64_t k, const double* K_colmajor, int64_t n_support,
+                           const int64_t* support, double* out);
+/* conv_coherence (analysis.hpp:68-70); zero tensor is an error. */
+int icnnm_cuda_conv_coherence(int order, const int64_t* dims, const double* L0,
+                              const int64_t* kdims, double rank_tol, int device,
+                              icnnm_conv_coherence* out);
+/* thresholds (analysis.hpp:94); host only. */
+int icnnm_thresholds(const icnnm_threshold_inputs* in, icnnm_threshold_values* out);
+/* analyze_recovery (analysis.hpp:96-99). */
+int icnnm_cuda_analyze_recovery(int order, const int64_t* dims, const double* L0,
+                                const int64_t* kdims, const double* K_colmajor,
+                                const double* evals, const double* mask, double rank_tol,
+                                int device, icnnm_recovery_diagnostics* out);
+
+/* ------------------------------------------------------------------------
  * Sharded solve of one large tensor, split over H into G slabs (one slab per
  * rank of a NCCL communicator, optionally several virtual slabs per process;
  * BASELINE config 5).  Periodic halos of kh-1 rows travel from rank g-1 to g
@@ -286,6 +360,10 @@ int icnnm_config_from_json(const char* text, icnnm_solver_config* cfg);
 /* solve_report_to_json; returns the byte length, writes <= cap bytes. */
 int64_t icnnm_report_to_json(const icnnm_solve_report* rep, char* out,
                              int64_t cap);
+/* diagnostics_to_json (report_io.cpp:70-88): same contract as
+ * icnnm_report_to_json. */
+int64_t icnnm_diagnostics_to_json(const icnnm_recovery_diagnostics* d, char* out,
+                                  int64_t cap);
 
 /* ------------------------------------------------------------------------
  * Probes used by bench.py for roofline denominators (device microbenches).

@@ -392,3 +392,207 @@ def psnr(ref, est, peak: float = 1.0) -> float:
 
 def rel_l2(a, b) -> float:
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+# ---------------------------------------------------------------------------
+# Recovery-theory diagnostics (core/src/analysis.cpp) and the spectrum /
+# generator helpers its tests use.
+# ---------------------------------------------------------------------------
+DEFAULT_RANK_TOL = 1e-8  # kDefaultRankTol (spectral.hpp:25)
+
+
+@dataclasses.dataclass
+class ConvSpectrum:
+    singular_values: np.ndarray
+    eigenvectors: np.ndarray
+    rank: int
+    degenerate: bool
+
+
+def conv_spectrum(L: np.ndarray, ks, tol: float = DEFAULT_RANK_TOL) -> ConvSpectrum:
+    """conv_spectrum (spectral.cpp:102-131): Gram eigen-decomposition with the
+    k*eps*lambda_1 backward-error floor on the rank cut."""
+    validate_kernel(ks, L.shape)
+    k = int(np.prod(ks))
+    if np.linalg.norm(L) == 0.0:
+        return ConvSpectrum(np.zeros(k), np.eye(k), 0, True)
+    w, V = psd_eig_sorted(conv_gram(L, ks))
+    floor = k * np.finfo(float).eps * w[0]
+    cut = max(tol * tol * w[0], floor)
+    return ConvSpectrum(np.sqrt(w), V, int(np.sum(w > cut)), False)
+
+
+def synth_low_conv_rank(dims, ks, target_rank: int, rng) -> np.ndarray:
+    """synth_low_conv_rank (synth.cpp:27-93).  `rng` is an mt19937_64 stream
+    seeded like the reference (uniform / uniform_int draws in the same order)."""
+    dims = tuple(int(d) for d in dims)
+    validate_kernel(ks, dims)
+    k = int(np.prod(ks))
+    if target_rank < 1 or target_rank > k:
+        raise ValueError("synth_low_conv_rank: infeasible target rank")
+    if target_rank >= k:
+        return rng.uniform(-1.0, 1.0, int(np.prod(dims))).reshape(dims)
+    if target_rank == 1:
+        c = 0.0
+        while abs(c) < 0.1:
+            c = float(rng.uniform(-1.0, 1.0, 1)[0])
+        return np.full(dims, c)
+    use_dc = target_rank % 2 != 0
+    n_cos = (target_rank - 1 if use_dc else target_rank) // 2
+    out = np.zeros(dims)
+    used = set()
+    if use_dc:
+        out[...] = float(rng.uniform(0.5, 1.5, 1)[0])
+        used.add((0,) * len(dims))
+    grids = np.meshgrid(*[np.arange(d) for d in dims], indexing="ij")
+    for _ in range(n_cos):
+        for attempt in itertools.count():
+            if attempt > 1000:
+                raise RuntimeError("synth_low_conv_rank: frequency sampling stuck")
+            f = [int(rng.uniform_int(0, d - 1, 1)[0]) for d in dims]
+            canon = tuple(min(fj, d - fj) for fj, d in zip(f, dims))
+            if any(fj != 0 for fj in f) and canon not in used:
+                used.add(canon)
+                break
+        A = float(rng.uniform(0.5, 1.5, 1)[0])
+        phi = float(rng.uniform(0.0, 2.0 * np.pi, 1)[0])
+        arg = np.full(dims, phi)
+        for fj, d, g in zip(f, dims, grids):
+            arg = arg + 2.0 * np.pi * fj * g / d
+        out += A * np.cos(arg)
+    if conv_spectrum(out, ks, 1e-8).rank > target_rank:
+        raise RuntimeError("synth_low_conv_rank: rank check failed")
+    return out
+
+
+def relative_eigenvalues(L0: np.ndarray, basis: EigenBasis) -> np.ndarray:
+    """relative_eigenvalues (analysis.cpp:29-38): ||L0 * kernel_i||_F."""
+    basis.validate()
+    validate_kernel(basis.kernel_shape, L0.shape)
+    k = basis.K.shape[0]
+    return np.array([np.linalg.norm(circular_convolve(L0, basis.K[:, i].reshape(basis.kernel_shape)))
+                     for i in range(k)])
+
+
+def support_from(sigma: np.ndarray, rank_tol: float) -> List[int]:
+    """support_from (analysis.cpp:40-49)."""
+    smax = float(np.max(sigma))
+    if smax == 0:
+        return []
+    return [i for i in range(len(sigma)) if sigma[i] > rank_tol * smax]
+
+
+def power_iteration_top_eig(S: np.ndarray) -> float:
+    """power_iteration_top_eig (analysis.cpp:51-69)."""
+    n = S.shape[0]
+    v = np.ones(n) / np.sqrt(float(n))
+    eig = 0.0
+    for it in range(10000):
+        w = S @ v
+        nw = np.linalg.norm(w)
+        if nw == 0:
+            return 0.0
+        w = w / nw
+        new_eig = float(w @ (S @ w))
+        done = abs(new_eig - eig) <= 1e-10 * max(1.0, abs(new_eig))
+        eig = new_eig
+        v = w
+        if done and it > 0:
+            break
+    return eig
+
+
+def relative_conv_rank(L0, basis: EigenBasis, rank_tol: float = DEFAULT_RANK_TOL):
+    """relative_conv_rank (analysis.cpp:71-77)."""
+    sup = support_from(relative_eigenvalues(L0, basis), rank_tol)
+    return len(sup), sup
+
+
+def spectral_corr_coeff(L0, basis: EigenBasis, rank_tol: float = DEFAULT_RANK_TOL) -> float:
+    """spectral_corr_coeff (analysis.cpp:79-96)."""
+    sigma = relative_eigenvalues(L0, basis)
+    sup = support_from(sigma, rank_tol)
+    if not sup:
+        raise ValueError("spectral_corr_coeff: r_K = 0, undefined")
+    G = conv_gram(L0, basis.kernel_shape)
+    KD = basis.K[:, sup] / sigma[sup]
+    S = KD.T @ G @ KD
+    return float(np.sqrt(max(0.0, power_iteration_top_eig(S))))
+
+
+def active_coherence(basis: EigenBasis, support_I: Sequence[int]) -> float:
+    """active_coherence (analysis.cpp:98-109)."""
+    if len(support_I) == 0:
+        raise ValueError("active_coherence: empty support")
+    k = basis.K.shape[0]
+    rows = np.sum(basis.K[:, list(support_I)] ** 2, axis=1)
+    return k / len(support_I) * float(np.max(rows))
+
+
+@dataclasses.dataclass
+class ConvCoherence:
+    mu1: float
+    mu2: float
+    tau: float
+    rank: int
+
+
+def conv_coherence(L0: np.ndarray, ks, rank_tol: float = DEFAULT_RANK_TOL) -> ConvCoherence:
+    """conv_coherence (analysis.cpp:111-135): thin SVD of the dense conv matrix."""
+    if np.linalg.norm(L0) == 0:
+        raise ValueError("conv_coherence: zero tensor")
+    A = conv_matrix(L0, ks)
+    U, s, Vt = np.linalg.svd(A, full_matrices=False)
+    r = int(np.sum(s > rank_tol * s[0]))
+    m, k = A.shape
+    mu1 = m / r * float(np.max(np.sum(U[:, :r] ** 2, axis=1)))
+    mu2 = k / r * float(np.max(np.sum(Vt[:r, :].T ** 2, axis=1)))
+    return ConvCoherence(mu1, mu2, float(s[0] / s[r - 1]), r)
+
+
+@dataclasses.dataclass
+class ThresholdInputs:
+    r_K: int = 0
+    alpha_K: float = 0.0
+    mu_K_I: float = 0.0
+    mu1: float = 0.0
+    mu2: float = 0.0
+    r0: int = 0
+    k: int = 0
+    m: int = 0
+    rho0: float = 0.0
+
+
+def thresholds(inp: ThresholdInputs) -> dict:
+    """thresholds (analysis.cpp:137-153)."""
+    a2 = inp.alpha_K ** 2
+    k, m, rk, r0 = float(inp.k), float(inp.m), float(inp.r_K), float(inp.r0)
+    t = dict(
+        rho_min_noiseless=1.0 - k / ((1.0 + a2) * inp.mu_K_I * rk * m),
+        rho_min_noisy=1.0 - 0.64 * k / ((0.64 + a2) * inp.mu_K_I * rk * m),
+        error_bound_factor=(18.0 * np.sqrt(k) + 2.0) * (inp.alpha_K + np.sqrt(1.0 + a2)) / inp.alpha_K,
+        icnnm_ideal_bound=1.0 - 0.5 * k / (inp.mu2 * r0 * m),
+        cnnm_bound=1.0 - 0.25 * k / (max(inp.mu1, inp.mu2) * r0 * m),
+    )
+    t["certified"] = inp.rho0 > t["rho_min_noiseless"]
+    return t
+
+
+def analyze_recovery(L0, basis: EigenBasis, mask, rank_tol: float = DEFAULT_RANK_TOL) -> dict:
+    """analyze_recovery (analysis.cpp:155-185)."""
+    if mask.shape != L0.shape:
+        raise ValueError("analyze_recovery: mask dims != target dims")
+    if np.any((mask != 0.0) & (mask != 1.0)):
+        raise ValueError("SamplingMask: entries must be 0 or 1")
+    rk, sup = relative_conv_rank(L0, basis, rank_tol)
+    if rk == 0:
+        raise ValueError("analyze_recovery: zero target, diagnostics undefined")
+    d = dict(r_K=rk, support_I=sup)
+    d["alpha_K"] = spectral_corr_coeff(L0, basis, rank_tol)
+    d["mu_K_I"] = active_coherence(basis, sup)
+    cc = conv_coherence(L0, basis.kernel_shape, rank_tol)
+    d.update(mu1=cc.mu1, mu2=cc.mu2, tau=cc.tau, r0=cc.rank)
+    d["rho0"] = int(np.sum(mask) + 0.5) / mask.size
+    d.update(thresholds(ThresholdInputs(rk, d["alpha_K"], d["mu_K_I"], cc.mu1, cc.mu2, cc.rank,
+                                        basis.K.shape[0], L0.size, d["rho0"])))
+    return d

@@ -62,6 +62,33 @@ class SolveReportC(C.Structure):
     ]
 
 
+class ConvCoherenceC(C.Structure):
+    _fields_ = [("mu1", C.c_double), ("mu2", C.c_double), ("tau", C.c_double),
+                ("rank", C.c_int64)]
+
+
+class ThresholdInputsC(C.Structure):
+    _fields_ = [("r_K", C.c_int64), ("alpha_K", C.c_double), ("mu_K_I", C.c_double),
+                ("mu1", C.c_double), ("mu2", C.c_double), ("r0", C.c_int64),
+                ("k", C.c_int64), ("m", C.c_int64), ("rho0", C.c_double)]
+
+
+class ThresholdValuesC(C.Structure):
+    _fields_ = [("rho_min_noiseless", C.c_double), ("rho_min_noisy", C.c_double),
+                ("error_bound_factor", C.c_double), ("cnnm_bound", C.c_double),
+                ("icnnm_ideal_bound", C.c_double), ("certified", C.c_int)]
+
+
+class RecoveryDiagnosticsC(C.Structure):
+    _fields_ = [("r_K", C.c_int64), ("support_I", C.POINTER(C.c_int64)),
+                ("alpha_K", C.c_double), ("mu_K_I", C.c_double), ("mu1", C.c_double),
+                ("mu2", C.c_double), ("tau", C.c_double), ("r0", C.c_int64),
+                ("rho0", C.c_double), ("rho_min_noiseless", C.c_double),
+                ("rho_min_noisy", C.c_double), ("error_bound_factor", C.c_double),
+                ("cnnm_bound", C.c_double), ("icnnm_ideal_bound", C.c_double),
+                ("certified", C.c_int)]
+
+
 _dp = C.POINTER(C.c_double)
 _lp = C.POINTER(C.c_int64)
 
@@ -122,6 +149,21 @@ SIGNATURES = {
     "icnnm_read_ebas": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), _lp, _dp, _dp]),
     "icnnm_config_from_json": (C.c_int, [C.c_char_p, C.POINTER(SolverConfigC)]),
     "icnnm_report_to_json": (C.c_int64, [C.POINTER(SolveReportC), C.c_char_p, C.c_int64]),
+    "icnnm_diagnostics_to_json": (C.c_int64, [C.POINTER(RecoveryDiagnosticsC), C.c_char_p,
+                                              C.c_int64]),
+    "icnnm_cuda_relative_eigenvalues": (C.c_int, [C.c_int, _lp, _dp, _lp, _dp, _dp, C.c_int,
+                                                  _dp]),
+    "icnnm_cuda_relative_conv_rank": (C.c_int, [C.c_int, _lp, _dp, _lp, _dp, _dp, C.c_double,
+                                                C.c_int, _lp, _lp]),
+    "icnnm_cuda_spectral_corr_coeff": (C.c_int, [C.c_int, _lp, _dp, _lp, _dp, _dp, C.c_double,
+                                                 C.c_int, _dp]),
+    "icnnm_active_coherence": (C.c_int, [C.c_int64, _dp, C.c_int64, _lp, _dp]),
+    "icnnm_cuda_conv_coherence": (C.c_int, [C.c_int, _lp, _dp, _lp, C.c_double, C.c_int,
+                                            C.POINTER(ConvCoherenceC)]),
+    "icnnm_thresholds": (C.c_int, [C.POINTER(ThresholdInputsC), C.POINTER(ThresholdValuesC)]),
+    "icnnm_cuda_analyze_recovery": (C.c_int, [C.c_int, _lp, _dp, _lp, _dp, _dp, _dp,
+                                              C.c_double, C.c_int,
+                                              C.POINTER(RecoveryDiagnosticsC)]),
 }
 
 _lib = None

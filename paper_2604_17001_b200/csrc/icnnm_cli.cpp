@@ -1,5 +1,6 @@
 // icnnm_b200 — GPU drop-in for the reference CLI's `learn` and `complete`
-// subcommands (/root/reference/proj/tools/icnnm_cli.cpp:151-166), same flags,
+// subcommands (/root/reference/proj/tools/icnnm_cli.cpp:151-166) and of
+// `analyze` (:100-108, :174-179), same flags,
 // same TNSR/EBAS files and JSON config/report, errors as {"error": ...} on
 // stderr with exit code 1 (:202-210).  Extensions: --engine, --device,
 // --exact-residual.
@@ -7,6 +8,8 @@
 //   icnnm_b200 learn --refs a.tnsr b.tnsr ... --kernel 9,9,5 --out basis.ebas [--normalize]
 //   icnnm_b200 complete --input M.tnsr --mask mask.tnsr --basis basis.ebas
 //                       [--config cfg.json] --out L.tnsr [--report report.json]
+//   icnnm_b200 analyze --target L0.tnsr --basis basis.ebas --mask mask.tnsr
+//                      [--rank-tol 1e-8] --out diagnostics.json
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -82,7 +85,8 @@ int run(int argc, char** argv) {
   if (argc < 2) throw Fail("usage: icnnm_b200 {learn|complete} ...");
   const std::string cmd = argv[1];
   std::vector<std::string> refs;
-  std::string kernel, out, in, mask, basis, config, report, engine;
+  std::string kernel, out, in, mask, basis, config, report, engine, target;
+  double rank_tol = ICNNM_DEFAULT_RANK_TOL;
   bool normalize = false, exact = false;
   int device = 0;
   for (int i = 2; i < argc; ++i) {
@@ -104,6 +108,13 @@ int run(int argc, char** argv) {
     else if (a == "--engine") engine = next();
     else if (a == "--device") device = std::atoi(next().c_str());
     else if (a == "--exact-residual") exact = true;
+    else if (a == "--target") target = next();
+    else if (a == "--rank-tol") {
+      const std::string v = next();
+      char* end = nullptr;
+      rank_tol = std::strtod(v.c_str(), &end);
+      if (*end != '\0') throw Fail("bad value for --rank-tol: " + v);
+    }
     else throw Fail("unknown option: " + a);
   }
   if (cmd == "learn") {
@@ -180,7 +191,38 @@ int run(int argc, char** argv) {
     }
     return 0;
   }
-  throw Fail("unknown subcommand: " + cmd + " (the GPU CLI implements learn and complete)");
+  if (cmd == "analyze") {
+    if (target.empty() || basis.empty() || mask.empty() || out.empty())
+      throw Fail("analyze: --target, --basis, --mask and --out are required");
+    Tensor L0 = read_tensor(target), W = read_tensor(mask);
+    for (double v : W.v)
+      if (v != 0.0 && v != 1.0) throw Fail("SamplingMask: entries must be 0 or 1");
+    if (W.dims != L0.dims) throw Fail("analyze_recovery: mask dims != target dims");
+    int order = 0;
+    int64_t kd[16];
+    check(icnnm_read_ebas(basis.c_str(), &order, kd, nullptr, nullptr), icnnm_io_last_error);
+    int64_t k = 1;
+    for (int j = 0; j < order; ++j) k *= kd[j];
+    std::vector<double> ev(k), K(k * k);
+    check(icnnm_read_ebas(basis.c_str(), &order, kd, ev.data(), K.data()), icnnm_io_last_error);
+    if (order != static_cast<int>(L0.dims.size())) throw Fail("KernelShape: order mismatch with tensor");
+    std::vector<int64_t> support(k);
+    icnnm_recovery_diagnostics d{};
+    d.support_I = support.data();
+    check(icnnm_cuda_analyze_recovery(order, L0.dims.data(), L0.v.data(), kd, K.data(), ev.data(),
+                                      W.v.data(), rank_tol, device, &d),
+          icnnm_last_error);
+    const int64_t n = icnnm_diagnostics_to_json(&d, nullptr, 0);
+    std::string js(static_cast<size_t>(n) + 1, '\0');
+    icnnm_diagnostics_to_json(&d, &js[0], n + 1);
+    js.resize(static_cast<size_t>(n));
+    std::ofstream os(out);
+    if (!os) throw Fail("cannot create file: " + out);
+    os << js;
+    return 0;
+  }
+  throw Fail("unknown subcommand: " + cmd +
+             " (the GPU CLI implements learn, complete and analyze)");
 }
 
 }  // namespace

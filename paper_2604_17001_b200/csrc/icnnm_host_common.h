@@ -1,0 +1,146 @@
+// Host-side helpers shared by the C-ABI translation units (icnnm_host.cu,
+// icnnm_analysis.cu): error classes, device buffers, problem geometry.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/icnnm_b200.h"
+#include "icnnm_kernels.cuh"
+
+using icnnm_dev::BK;
+using icnnm_dev::BM;
+using icnnm_dev::BN;
+using icnnm_dev::Geo;
+
+namespace icnnm_host {
+
+// ---------------------------------------------------------------------------
+// Errors
+// ---------------------------------------------------------------------------
+struct Error {
+  int code;
+  std::string msg;
+};
+extern thread_local std::string g_last_error;
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+[[noreturn]] inline void invalid(const std::string& msg) { fail(ICNNM_INVALID_ARGUMENT, msg); }
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      ::icnnm_host::fail(ICNNM_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define CKL() CK(cudaGetLastError())
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return ICNNM_OK;
+  } catch (const Error& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return ICNNM_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ICNNM_RUNTIME_ERROR;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Device buffers
+// ---------------------------------------------------------------------------
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) {
+      cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+      if (e != cudaSuccess) {
+        p = nullptr;
+        fail(ICNNM_CUDA_ERROR, "cudaMalloc(" + std::to_string(count * sizeof(T)) +
+                                   " bytes): " + cudaGetErrorString(e));
+      }
+    }
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+  ~DBuf() { release(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+};
+
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    CK(cudaGetDevice(&prev));
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (dev < 0 || dev >= n)
+      invalid("device index " + std::to_string(dev) + " out of range (" + std::to_string(n) +
+              " devices)");
+    CK(cudaSetDevice(dev));
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Problem geometry
+// ---------------------------------------------------------------------------
+struct Problem {
+  int order = 0;
+  int64_t dims[3] = {1, 1, 1};   // H, W, T
+  int64_t kd[3] = {1, 1, 1};     // kh, kw, kt
+  int64_t m = 0;
+  int k = 0;
+  int kp = 0;     // FFMA engine column padding (multiple of 64)
+  int kp_tc = 0;  // tcgen05 engine padding (multiple of KC = 16)
+};
+
+inline int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+inline int pow2ceil(int64_t x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+Problem make_problem(int order, const int64_t* dims, const int64_t* kdims);
+Geo make_geo(const Problem& p, int64_t rows, bool wrap);
+inline int64_t n_bricks(const Geo& g) {
+  return static_cast<int64_t>(g.nbh) * g.nbw * g.nbt;
+}
+void check_smem(size_t need);
+void set_smem_attrs();
+void validate_basis(int k, const double* K, const double* evals);
+inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 16) {
+  int64_t b = (n + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, max_blocks)));
+}
+void gram_lags_accumulate(const Problem& p, const double* dX, double* dR, cudaStream_t s);
+void gram_from_lags(const Problem& p, const std::vector<double>& R, double* G);
+
+}  // namespace icnnm_host
+
+extern "C" int icnnm_host_symeig_impl(int n, const double* G, double* evals, double* evecs);

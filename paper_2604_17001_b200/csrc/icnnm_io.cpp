@@ -264,4 +264,39 @@ int64_t icnnm_report_to_json(const icnnm_solve_report* rep, char* out, int64_t c
   return static_cast<int64_t>(s.size());
 }
 
+// diagnostics_to_json (report_io.cpp:70-88); keys in the order nlohmann's
+// std::map-backed object dumps them (alphabetical).
+int64_t icnnm_diagnostics_to_json(const icnnm_recovery_diagnostics* d, char* out, int64_t cap) {
+  if (!d) return -1;
+  std::ostringstream os;
+  os.precision(17);
+  auto num = [&](double v) {
+    if (std::isfinite(v)) os << v; else os << "null";
+  };
+  os << "{\n  \"alpha_K\": "; num(d->alpha_K);
+  os << ",\n  \"certified\": " << (d->certified ? "true" : "false");
+  os << ",\n  \"cnnm_bound\": "; num(d->cnnm_bound);
+  os << ",\n  \"error_bound_factor\": "; num(d->error_bound_factor);
+  os << ",\n  \"icnnm_ideal_bound\": "; num(d->icnnm_ideal_bound);
+  os << ",\n  \"mu1\": "; num(d->mu1);
+  os << ",\n  \"mu2\": "; num(d->mu2);
+  os << ",\n  \"mu_K_I\": "; num(d->mu_K_I);
+  os << ",\n  \"r0\": " << d->r0;
+  os << ",\n  \"r_K\": " << d->r_K;
+  os << ",\n  \"rho0\": "; num(d->rho0);
+  os << ",\n  \"rho_min_noiseless\": "; num(d->rho_min_noiseless);
+  os << ",\n  \"rho_min_noisy\": "; num(d->rho_min_noisy);
+  os << ",\n  \"support_I\": [";
+  for (int64_t i = 0; d->support_I && i < d->r_K; ++i) os << (i ? ", " : "") << d->support_I[i];
+  os << "],\n  \"tau\": "; num(d->tau);
+  os << "\n}";
+  const std::string s = os.str();
+  if (out && cap > 0) {
+    const int64_t n = std::min<int64_t>(cap - 1, static_cast<int64_t>(s.size()));
+    std::memcpy(out, s.data(), n);
+    out[n] = '\0';
+  }
+  return static_cast<int64_t>(s.size());
+}
+
 }  // extern "C"
