@@ -191,6 +191,20 @@ int icnnm_cuda_objective(int order, const int64_t* dims, const double* L,
                          double lambda, int device, double* out);
 
 /* ------------------------------------------------------------------------
+ * CNNM baseline.  Replaces
+ *   std::pair<DenseTensor,SolveReport> cnnm_solve(const DenseTensor& M_obs,
+ *     const SamplingMask& mask, const KernelShape& ks, const SolverConfig&)
+ * (solver.hpp:71-75, solver.cpp:161-170): the same ADMM loop with K = I and
+ * singular-value thresholding (svt, solver.cpp:52-57) as the Z-update, in
+ * fp64 on the GPU (Gram + cuSOLVER eigensolve + DGEMM per iteration).
+ * cfg->engine and cfg->exact_residual are ignored (the trace is exact).
+ * ---------------------------------------------------------------------- */
+int icnnm_cuda_cnnm_solve(int order, const int64_t* dims, const double* M_obs,
+                          const double* mask, const int64_t* kdims,
+                          const icnnm_solver_config* cfg, int device, double* L_out,
+                          icnnm_solve_report* report);
+
+/* ------------------------------------------------------------------------
  * Recovery-theory diagnostics (`analyze`), replacing
  * /root/reference/proj/core/include/icnnm/analysis.hpp:25-99 and
  * core/src/analysis.cpp.  Matrix-free on the GPU in fp64: the m x k

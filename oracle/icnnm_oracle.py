@@ -280,12 +280,15 @@ class SolveReport:
 
 
 class AdmmSolver:
-    """admm_solve (solver.cpp:62-146) with the prox_l21 Z-update, literally;
-    setup in __init__ (:66-102), one loop body per step() (:108-139)."""
+    """admm_solve (solver.cpp:62-146) with the prox_l21 Z-update (or, for
+    cnnm_solve, svt), literally; setup in __init__ (:66-102), one loop body
+    per step() (:108-139)."""
 
     def __init__(self, M_obs: np.ndarray, mask: np.ndarray, basis: EigenBasis,
-                 cfg: Optional[SolverConfig] = None, validate_basis: bool = True):
+                 cfg: Optional[SolverConfig] = None, validate_basis: bool = True,
+                 z_update=None):
         cfg = cfg or SolverConfig()
+        self.z_update = z_update or (lambda Xt, tau: _prox_l21_t(Xt, tau)[0])
         if validate_basis:
             basis.validate()                                     # solver.cpp:156
         cfg.validate()                                           # :66
@@ -327,7 +330,7 @@ class AdmmSolver:
         """One iteration; returns True when the stopping test fires."""
         cfg, k, theta = self.cfg, self.k, self.theta
         flat = (k, -1)
-        self.Z, _ = _prox_l21_t(self.AKL - self.Y / theta, 1.0 / theta)  # :108
+        self.Z = self.z_update(self.AKL - self.Y / theta, 1.0 / theta)  # :108
         # WK = (Y + theta Z) K^T  -> transposed: K (Y + theta Z)^T      (:110)
         WKt = (self.basis.K @ (self.Y + theta * self.Z).reshape(flat)).reshape(self.AKL.shape)
         adj = conv_adjoint_t(WKt, self.ks, self.dims)            # :111
@@ -361,6 +364,36 @@ def icnnm_solve(M_obs: np.ndarray, mask: np.ndarray, basis: EigenBasis,
     """icnnm_solve (solver.cpp:150-159)."""
     s = AdmmSolver(M_obs, mask, basis, cfg, validate_basis)
     for _ in range(s.cfg.max_iters):                             # :107
+        if s.step():
+            break
+    s.report.wall_time_seconds = time.perf_counter() - s.t_start
+    return s.L, s.report
+
+
+def svt(W: np.ndarray, tau: float) -> np.ndarray:
+    """svt (solver.cpp:52-57): U max(S - tau, 0) V^T of a thin SVD."""
+    if tau < 0:
+        raise ValueError("svt: tau must be >= 0")
+    U, S, Vt = np.linalg.svd(W, full_matrices=False)
+    return (U * np.maximum(S - tau, 0.0)) @ Vt
+
+
+def _svt_t(Wt: np.ndarray, tau: float) -> np.ndarray:
+    # transposed storage (k, *dims): svt(W^T) = svt(W)^T
+    k = Wt.shape[0]
+    return svt(Wt.reshape(k, -1), tau).reshape(Wt.shape)
+
+
+def cnnm_solve(M_obs: np.ndarray, mask: np.ndarray, ks, cfg: Optional[SolverConfig] = None
+               ) -> Tuple[np.ndarray, SolveReport]:
+    """cnnm_solve (solver.cpp:161-170): the shared ADMM loop with K = I and
+    the singular-value-thresholding Z-update (the CNNM baseline)."""
+    ks = tuple(int(d) for d in ks)
+    k = int(np.prod(ks))
+    validate_kernel(ks, M_obs.shape)
+    s = AdmmSolver(M_obs, mask, EigenBasis(ks, np.eye(k), np.zeros(k)), cfg,
+                   validate_basis=False, z_update=_svt_t)
+    for _ in range(s.cfg.max_iters):
         if s.step():
             break
     s.report.wall_time_seconds = time.perf_counter() - s.t_start

@@ -6,15 +6,15 @@ package is the Python mirror of the reference's solver/operator interface.
 """
 from ._lib import IcnnmError, InvalidArgument, CudaError, LIB_PATH, lib
 from .api import (SolverConfig, SolveReport, EigenBasis, Solver, BasisConvolver,
-                  icnnm_solve, learn_ensemble_basis, conv_adjoint, prox_l21, conv_gram,
+                  icnnm_solve, cnnm_solve, learn_ensemble_basis, conv_adjoint, prox_l21, conv_gram,
                   objective_icnnm, symeig, sharded_solve, shard_plan, dist_unique_id,
                   device_count, probe_ffma_tflops)
-from . import synth
+from . import synth, analysis
 
 __all__ = [
     "IcnnmError", "InvalidArgument", "CudaError", "LIB_PATH", "lib",
     "SolverConfig", "SolveReport", "EigenBasis", "Solver", "BasisConvolver",
-    "icnnm_solve", "learn_ensemble_basis", "conv_adjoint", "prox_l21", "conv_gram",
+    "icnnm_solve", "cnnm_solve", "learn_ensemble_basis", "conv_adjoint", "prox_l21", "conv_gram",
     "objective_icnnm", "symeig", "sharded_solve", "shard_plan", "dist_unique_id",
-    "device_count", "probe_ffma_tflops", "synth",
+    "device_count", "probe_ffma_tflops", "synth", "analysis",
 ]

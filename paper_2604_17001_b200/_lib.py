@@ -149,6 +149,8 @@ SIGNATURES = {
     "icnnm_read_ebas": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), _lp, _dp, _dp]),
     "icnnm_config_from_json": (C.c_int, [C.c_char_p, C.POINTER(SolverConfigC)]),
     "icnnm_report_to_json": (C.c_int64, [C.POINTER(SolveReportC), C.c_char_p, C.c_int64]),
+    "icnnm_cuda_cnnm_solve": (C.c_int, [C.c_int, _lp, _dp, _dp, _lp, C.POINTER(SolverConfigC),
+                                        C.c_int, _dp, C.POINTER(SolveReportC)]),
     "icnnm_diagnostics_to_json": (C.c_int64, [C.POINTER(RecoveryDiagnosticsC), C.c_char_p,
                                               C.c_int64]),
     "icnnm_cuda_relative_eigenvalues": (C.c_int, [C.c_int, _lp, _dp, _lp, _dp, _dp, C.c_int,

@@ -414,6 +414,26 @@ def sharded_solve(M_obs, mask, basis: EigenBasis, cfg: Optional[SolverConfig] = 
     return r0.value, rows.copy(), _report_from_c(rep, obj, res, lc)
 
 
+def cnnm_solve(M_obs, mask, kernel_shape, cfg: Optional[SolverConfig] = None,
+               device: int = 0) -> Tuple[np.ndarray, SolveReport]:
+    """cnnm_solve (solver.cpp:161-170): the CNNM baseline (K = I, SVT
+    Z-update) on the GPU in fp64."""
+    cfg = cfg or SolverConfig()
+    M, W = _f64(M_obs), _f64(mask)
+    if M.shape != W.shape:
+        raise InvalidArgument("solve: mask dims != observation dims")
+    kernel_shape = tuple(int(d) for d in kernel_shape)
+    if len(kernel_shape) != M.ndim:
+        raise InvalidArgument("KernelShape: order mismatch with tensor")
+    c = cfg.to_c()
+    out = np.empty_like(M)
+    rep, obj, res, lc = _report_buffers(max(int(cfg.max_iters), 1))
+    check(lib().icnnm_cuda_cnnm_solve(M.ndim, lptr(_dims(M.shape)), dptr(M), dptr(W),
+                                      lptr(_dims(kernel_shape)), C.byref(c), device, dptr(out),
+                                      C.byref(rep)))
+    return out, _report_from_c(rep, obj, res, lc)
+
+
 def device_count() -> int:
     return int(lib().icnnm_device_count())
 

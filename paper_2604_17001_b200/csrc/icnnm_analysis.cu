@@ -12,15 +12,20 @@
 //   alpha_K^2   = top eig of (K_I D)^T G (K_I D)    conv Gram (icnnm_gram_lags),
 //                                                   icnnm_dgemm_tn, host power
 //                                                   iteration (:51-69, :79-96)
-//   conv_coherence: G = V S^2 V^T (host symeig); s_i = ||A(L0) v_i|| (column
-//                 norms, so small singular values are not squared away);
-//                 mu2 from the rows of V_r; mu1 = m/r max_v ||(A V_r S_r^-1)_v||^2
-//                 (icnnm_conv64, row-norm epilogue) (:111-135)
+//   conv_coherence: streaming TSQR of A(L0) (row blocks gathered on the GPU
+//                 by icnnm_im2col64, cuSOLVER geqrf), SVD of the k x k R
+//                 (cuSOLVER gesvd) -> s, V, both backward stable like the
+//                 reference's BDCSVD (a Gram eigensolve would square the
+//                 condition number and lose the singular vectors near the
+//                 1e-8 rank cut); mu2 from the rows of V_r;
+//                 mu1 = m/r max_v ||(A V_r S_r^-1)_v||^2 (icnnm_conv64,
+//                 row-norm epilogue) (:111-135)
 //   thresholds, active coherence: closed forms on the host (:98-109, :137-153)
 //
 // Everything is fp64: these are one-time diagnostics whose rank decisions use
 // a 1e-8 relative tolerance (spectral.hpp:25), below fp32 resolution.
 #include <cuda_runtime.h>
+#include <cusolverDn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -198,6 +203,30 @@ icnnm_conv64(Geo g, int np, const double* __restrict__ L, const double* __restri
       part[blk] = m;
     }
   }
+}
+
+// Rows [row0, row0 + rows) of the convolution matrix A(L) (conv_op.cpp:35-46),
+// column-major with leading dimension ld, written at out + off:
+//   out[off + i + ld * s] = L[(v - s) mod dims],  v = row0 + i (natural order).
+__global__ void icnnm_im2col64(int H, int W, int T, int kh, int kw, int kt, int64_t row0,
+                               int rows, const double* __restrict__ L, double* __restrict__ out,
+                               int64_t ld, int64_t off) {
+  const int s = blockIdx.y;
+  const int st = s % kt, q = s / kt, sw = q % kw, sh = q / kw;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+    const int64_t v = row0 + i;
+    const int t = static_cast<int>(v % T);
+    const int64_t r = v / T;
+    const int w = static_cast<int>(r % W), h = static_cast<int>(r / W);
+    const int hs = wrap64(h - sh, H), ws = wrap64(w - sw, W), ts = wrap64(t - st, T);
+    out[off + i + ld * s] = L[(static_cast<int64_t>(hs) * W + ws) * T + ts];
+  }
+}
+
+// Zero the strictly lower triangle of the leading k x k block (ld rows).
+__global__ void icnnm_keep_upper(int k, int64_t ld, double* __restrict__ A) {
+  const int c = blockIdx.x;
+  for (int r = c + 1 + threadIdx.x; r < k; r += blockDim.x) A[r + ld * c] = 0.0;
 }
 
 // C[M x N] = A^T B with A (K x M), B (K x N), C (M x N), all column-major,
@@ -415,19 +444,89 @@ double alpha_from(const Problem& p, const std::vector<double>& G, const double* 
   return std::sqrt(std::max(0.0, power_iteration_top_eig(S, r)));
 }
 
-void conv_coherence_impl(const Problem& p, const double* L0, Conv64& conv,
-                         const std::vector<double>& G, double rank_tol, icnnm_conv_coherence* out) {
+#define CKS(x)                                                                     \
+  do {                                                                             \
+    cusolverStatus_t st_ = (x);                                                    \
+    if (st_ != CUSOLVER_STATUS_SUCCESS)                                            \
+      ::icnnm_host::fail(ICNNM_CUDA_ERROR, std::string(#x) + ": cusolver status " + \
+                                               std::to_string(static_cast<int>(st_)));  \
+  } while (0)
+
+struct Cusolver {
+  cusolverDnHandle_t h = nullptr;
+  Cusolver() { CKS(cusolverDnCreate(&h)); }
+  ~Cusolver() {
+    if (h) cusolverDnDestroy(h);
+  }
+};
+
+// Singular values (descending) and right singular vectors V (k x k,
+// column-major, column i <-> s[i]) of the m x k convolution matrix A(L0):
+// streaming TSQR  [R; A_b] = Q R'  over row blocks A_b gathered on the GPU,
+// then the SVD of the final R.  Device memory: (k + rows_b) x k doubles.
+void conv_svd(const Problem& p, const double* dL0, std::vector<double>& s,
+              std::vector<double>& V) {
+  const int k = p.k;
+  const int64_t m = p.m;
+  const int64_t budget_rows = std::max<int64_t>(4 * k, (int64_t(1) << 28) / k);  // 2 GB
+  const int rows_b = static_cast<int>(std::min<int64_t>(m, budget_rows));
+  const int64_t ld = static_cast<int64_t>(k) + rows_b;
+  if (ld > (int64_t(1) << 31) - 1) invalid("conv_coherence: block too large");
+  Cusolver cs;
+  DBuf<double> Wb(static_cast<size_t>(ld) * k), tau(k);
+  DBuf<int> info(1);
+  int lwork = 0;
+  CKS(cusolverDnDgeqrf_bufferSize(cs.h, static_cast<int>(ld), k, Wb.p, static_cast<int>(ld),
+                                  &lwork));
+  DBuf<double> work(std::max(lwork, 1));
+  CK(cudaMemset(Wb.p, 0, Wb.bytes()));  // R_0 = 0
+  const int H = static_cast<int>(p.dims[0]), W = static_cast<int>(p.dims[1]),
+            T = static_cast<int>(p.dims[2]);
+  for (int64_t row0 = 0; row0 < m; row0 += rows_b) {
+    const int rows = static_cast<int>(std::min<int64_t>(rows_b, m - row0));
+    if (rows < rows_b)  // last partial block: zero rows contribute nothing
+      CK(cudaMemset2D(Wb.p + k + rows, sizeof(double) * ld, 0, sizeof(double) * (rows_b - rows),
+                      k));
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>((rows + 255) / 256, 4096)),
+              static_cast<unsigned>(k));
+    icnnm_dev::icnnm_im2col64<<<grid, 256>>>(H, W, T, static_cast<int>(p.kd[0]),
+                                             static_cast<int>(p.kd[1]), static_cast<int>(p.kd[2]),
+                                             row0, rows, dL0, Wb.p, ld, k);
+    CKL();
+    CKS(cusolverDnDgeqrf(cs.h, static_cast<int>(ld), k, Wb.p, static_cast<int>(ld), tau.p,
+                         work.p, lwork, info.p));
+    icnnm_dev::icnnm_keep_upper<<<k, 128>>>(k, ld, Wb.p);
+    CKL();
+  }
+  int hinfo = 0;
+  CK(cudaMemcpy(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (hinfo != 0) fail(ICNNM_RUNTIME_ERROR, "conv_coherence: QR failed");
+  // SVD of R (k x k, leading block of Wb).
+  DBuf<double> R(static_cast<size_t>(k) * k), S(k), VT(static_cast<size_t>(k) * k);
+  CK(cudaMemcpy2D(R.p, sizeof(double) * k, Wb.p, sizeof(double) * ld, sizeof(double) * k, k,
+                  cudaMemcpyDeviceToDevice));
+  int lw2 = 0;
+  CKS(cusolverDnDgesvd_bufferSize(cs.h, k, k, &lw2));
+  DBuf<double> work2(std::max(lw2, 1)), rwork(k);
+  CKS(cusolverDnDgesvd(cs.h, 'N', 'A', k, k, R.p, k, S.p, nullptr, 1, VT.p, k, work2.p, lw2,
+                       rwork.p, info.p));
+  CK(cudaMemcpy(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (hinfo != 0) fail(ICNNM_RUNTIME_ERROR, "conv_coherence: SVD did not converge");
+  s.resize(k);
+  std::vector<double> vt(static_cast<size_t>(k) * k);
+  CK(cudaMemcpy(s.data(), S.p, S.bytes(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(vt.data(), VT.p, VT.bytes(), cudaMemcpyDeviceToHost));
+  V.assign(static_cast<size_t>(k) * k, 0.0);
+  for (int i = 0; i < k; ++i)      // V[:, i] = row i of VT
+    for (int j = 0; j < k; ++j) V[static_cast<size_t>(i) * k + j] = vt[i + static_cast<size_t>(k) * j];
+}
+
+void conv_coherence_impl(const Problem& p, const double* L0, Conv64& conv, double rank_tol,
+                         icnnm_conv_coherence* out) {
   if (tensor_norm2(p, L0) == 0) invalid("conv_coherence: zero tensor");
   const int k = p.k;
-  std::vector<double> lam(k), V(static_cast<size_t>(k) * k);
-  if (icnnm_host_symeig_impl(k, G.data(), lam.data(), V.data()) != 0)
-    fail(ICNNM_RUNTIME_ERROR, "eigensolver did not converge");
-  std::vector<double> s2 = conv.colnorm2(V.data(), k);
-  std::vector<int> idx(k);
-  std::iota(idx.begin(), idx.end(), 0);
-  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return s2[a] > s2[b]; });
-  std::vector<double> s(k);
-  for (int i = 0; i < k; ++i) s[i] = std::sqrt(s2[idx[i]]);
+  std::vector<double> s, V;
+  conv_svd(p, conv.dL.p, s, V);
   int r = 0;
   for (int i = 0; i < k; ++i)
     if (s[i] > rank_tol * s[0]) ++r;
@@ -436,7 +535,7 @@ void conv_coherence_impl(const Problem& p, const double* L0, Conv64& conv,
   for (int j = 0; j < k; ++j) {
     double acc = 0;
     for (int i = 0; i < r; ++i) {
-      const double v = V[static_cast<size_t>(idx[i]) * k + j];
+      const double v = V[static_cast<size_t>(i) * k + j];
       acc += v * v;
     }
     vmax = std::max(vmax, acc);
@@ -444,7 +543,7 @@ void conv_coherence_impl(const Problem& p, const double* L0, Conv64& conv,
   std::vector<double> Us(static_cast<size_t>(k) * r);
   for (int i = 0; i < r; ++i)
     for (int j = 0; j < k; ++j)
-      Us[static_cast<size_t>(i) * k + j] = V[static_cast<size_t>(idx[i]) * k + j] / s[i];
+      Us[static_cast<size_t>(i) * k + j] = V[static_cast<size_t>(i) * k + j] / s[i];
   const double umax = conv.rowmax(Us.data(), r);
   out->rank = r;
   out->mu1 = static_cast<double>(p.m) / r * umax;
@@ -563,7 +662,7 @@ int icnnm_cuda_conv_coherence(int order, const int64_t* dims, const double* L0,
     DeviceScope ds(device);
     if (tensor_norm2(p, L0) == 0) invalid("conv_coherence: zero tensor");
     Conv64 conv(p, L0);
-    conv_coherence_impl(p, L0, conv, conv_gram_host(p, conv.dL.p), rank_tol, out);
+    conv_coherence_impl(p, L0, conv, rank_tol, out);
   });
 }
 
@@ -599,7 +698,7 @@ int icnnm_cuda_analyze_recovery(int order, const int64_t* dims, const double* L0
     d->alpha_K = alpha_from(p, G, K, sigma, sup);
     d->mu_K_I = active_coherence_impl(p.k, K, d->r_K, sup.data());
     icnnm_conv_coherence cc{};
-    conv_coherence_impl(p, L0, conv, G, rank_tol, &cc);
+    conv_coherence_impl(p, L0, conv, rank_tol, &cc);
     d->mu1 = cc.mu1;
     d->mu2 = cc.mu2;
     d->tau = cc.tau;

@@ -359,3 +359,32 @@ def test_golden_cfg2_fixture_matches_oracle():
         O.WORKERS = 1
     np.testing.assert_allclose(s.report.objective[0], gd["objective"][0], rtol=1e-12)
     assert abs(O.psnr(X, gd["L"].astype(np.float64)) - float(gd["psnr"])) < 1e-4
+
+
+# --- CNNM baseline (solver.cpp:52-57,161-170) ---------------------------------------
+def test_cnnm_fully_observed_and_cosine_recovery():     # test_solver.cpp:151-168
+    M = Rng(35).random_tensor((8, 8))
+    L, _ = O.cnnm_solve(M, np.ones_like(M), (3, 3), O.SolverConfig(max_iters=300))
+    assert O.rel_l2(L, M) < 1e-3
+    L0 = _cos(32, 8)
+    mask = synth.reference_bernoulli_mask((32,), 0.75, 5)
+    L2, _ = O.cnnm_solve(L0, mask, (8,), O.SolverConfig())
+    assert O.rel_l2(L2, L0) < 1e-3
+
+
+def test_exact_basis_icnnm_and_cnnm_agree():            # test_solver.cpp:170-193
+    L0 = _cos(32, 8)
+    B = O.learn_ensemble_basis([L0], (8,))
+    mask = synth.reference_bernoulli_mask((32,), 0.75, 11)
+    li, _ = O.icnnm_solve(L0, mask, B, O.SolverConfig())
+    lc, _ = O.cnnm_solve(L0, mask, (8,), O.SolverConfig())
+    assert np.linalg.norm(li - lc) / np.linalg.norm(L0) < 1e-4
+    obj_i = O.objective_icnnm(li, L0, mask, B, 1000.0)
+    nuc = float(np.sum(np.linalg.svd(O.conv_matrix(lc, (8,)), compute_uv=False)))
+    obj_c = nuc + 0.5 * 1000.0 * 8.0 * float(np.sum(((lc - L0) * mask) ** 2))
+    assert abs(obj_i - obj_c) / obj_c < 1e-5
+
+
+def test_svt_rejects_negative_tau():
+    with pytest.raises(ValueError):
+        O.svt(np.eye(3), -1.0)
