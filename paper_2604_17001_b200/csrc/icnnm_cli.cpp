@@ -1,6 +1,6 @@
 // icnnm_b200 — GPU drop-in for the reference CLI's `learn` and `complete`
 // subcommands (/root/reference/proj/tools/icnnm_cli.cpp:151-166) and of
-// `analyze` (:100-108, :174-179), same flags,
+// `cnnm` (:91-98, :167-173) and `analyze` (:100-108, :174-179), same flags,
 // same TNSR/EBAS files and JSON config/report, errors as {"error": ...} on
 // stderr with exit code 1 (:202-210).  Extensions: --engine, --device,
 // --exact-residual.
@@ -8,8 +8,11 @@
 //   icnnm_b200 learn --refs a.tnsr b.tnsr ... --kernel 9,9,5 --out basis.ebas [--normalize]
 //   icnnm_b200 complete --input M.tnsr --mask mask.tnsr --basis basis.ebas
 //                       [--config cfg.json] --out L.tnsr [--report report.json]
+//   icnnm_b200 cnnm --input M.tnsr --mask mask.tnsr --kernel 9,9,5
+//                   [--config cfg.json] --out L.tnsr [--report report.json]
 //   icnnm_b200 analyze --target L0.tnsr --basis basis.ebas --mask mask.tnsr
 //                      [--rank-tol 1e-8] --out diagnostics.json
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -149,19 +152,32 @@ int run(int argc, char** argv) {
           icnnm_io_last_error);
     return 0;
   }
-  if (cmd == "complete") {
-    if (in.empty() || mask.empty() || basis.empty() || out.empty())
-      throw Fail("complete: --input, --mask, --basis and --out are required");
+  if (cmd == "complete" || cmd == "cnnm") {
+    const bool cn = cmd == "cnnm";
+    if (in.empty() || mask.empty() || (cn ? kernel.empty() : basis.empty()) || out.empty())
+      throw Fail(cn ? "cnnm: --input, --mask, --kernel and --out are required"
+                    : "complete: --input, --mask, --basis and --out are required");
     Tensor M = read_tensor(in), W = read_tensor(mask);
-    if (M.dims != W.dims) throw Fail("solve: mask dims != observation dims");
+    for (double v : W.v)
+      if (v != 0.0 && v != 1.0) throw Fail("SamplingMask: entries must be 0 or 1");
     int order = 0;
     int64_t kd[16];
-    check(icnnm_read_ebas(basis.c_str(), &order, kd, nullptr, nullptr), icnnm_io_last_error);
-    int64_t k = 1;
-    for (int j = 0; j < order; ++j) k *= kd[j];
-    std::vector<double> ev(k), K(k * k);
-    check(icnnm_read_ebas(basis.c_str(), &order, kd, ev.data(), K.data()), icnnm_io_last_error);
+    std::vector<double> ev, K;
+    if (cn) {
+      const std::vector<int64_t> kv = parse_dims(kernel);
+      order = static_cast<int>(kv.size());
+      if (order > 16) throw Fail("bad dims: " + kernel);
+      std::copy(kv.begin(), kv.end(), kd);
+    } else {
+      check(icnnm_read_ebas(basis.c_str(), &order, kd, nullptr, nullptr), icnnm_io_last_error);
+      int64_t k = 1;
+      for (int j = 0; j < order; ++j) k *= kd[j];
+      ev.resize(k);
+      K.resize(k * k);
+      check(icnnm_read_ebas(basis.c_str(), &order, kd, ev.data(), K.data()), icnnm_io_last_error);
+    }
     if (order != static_cast<int>(M.dims.size())) throw Fail("KernelShape: order mismatch with tensor");
+    if (M.dims != W.dims) throw Fail("solve: mask dims != observation dims");
     icnnm_solver_config cfg;
     if (!config.empty())
       check(icnnm_config_from_json(read_text(config).c_str(), &cfg), icnnm_io_last_error);
@@ -176,9 +192,14 @@ int run(int argc, char** argv) {
     rep.objective = obj.data();
     rep.primal_residual = res.data();
     rep.l_change = lc.data();
-    check(icnnm_cuda_solve(order, M.dims.data(), M.v.data(), W.v.data(), kd, K.data(), ev.data(),
-                           &cfg, device, L.data(), &rep),
-          icnnm_last_error);
+    if (cn)
+      check(icnnm_cuda_cnnm_solve(order, M.dims.data(), M.v.data(), W.v.data(), kd, &cfg, device,
+                                  L.data(), &rep),
+            icnnm_last_error);
+    else
+      check(icnnm_cuda_solve(order, M.dims.data(), M.v.data(), W.v.data(), kd, K.data(),
+                             ev.data(), &cfg, device, L.data(), &rep),
+            icnnm_last_error);
     check(icnnm_write_tnsr(out.c_str(), order, M.dims.data(), L.data()), icnnm_io_last_error);
     if (!report.empty()) {
       const int64_t n = icnnm_report_to_json(&rep, nullptr, 0);
@@ -222,7 +243,7 @@ int run(int argc, char** argv) {
     return 0;
   }
   throw Fail("unknown subcommand: " + cmd +
-             " (the GPU CLI implements learn, complete and analyze)");
+             " (the GPU CLI implements learn, complete, cnnm and analyze)");
 }
 
 }  // namespace
