@@ -266,6 +266,11 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
     return e ? std::atoi(e) : 0;
   }();
   a.skip = skip_env;
+  static const int bsplit_env = [] {
+    const char* e = std::getenv("ICNNM_TC_BSPLIT");  // A/B experiments only
+    return e ? std::atoi(e) : 0;
+  }();
+  a.bsplit = bsplit_env;
   a.g = gtc;
   a.src = src;
   a.Win = W;

@@ -276,8 +276,9 @@ icnnm_tc_kernel(TcArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
+    const int nbuild = a.bsplit ? NB * 32 : (NB / 2) * 32;  // builder arrivals per chunk
     for (int i = 0; i < SA; ++i) {
-      mbar_init(A_full + i, NB * 32);
+      mbar_init(A_full + i, nbuild);
       mbar_init(A_empty + i, 1);
     }
     for (int i = 0; i < SB; ++i) {
@@ -290,7 +291,7 @@ icnnm_tc_kernel(TcArgs a) {
     }
     for (int i = 0; i < WS; ++i) {
       mbar_init(W_full + i, 1);
-      mbar_init(W_empty + i, NB * 32);
+      mbar_init(W_empty + i, nbuild);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -372,6 +373,10 @@ icnnm_tc_kernel(TcArgs a) {
       }
       for (int nt = 0; nt < ntn; ++nt) {
         for (int kc = 0; kc < nkc; ++kc, ++cnt) {
+          // bsplit = 0: group `half` owns the chunks with cnt % 2 == half and
+          // builds all KC columns, so each warp has two chunk periods of MMA
+          // time to cover its TMEM-store round trip.
+          if (!a.bsplit && static_cast<int>(cnt & 1u) != half) continue;
           const int sa = cnt % san;
           const uint32_t ph = (cnt / san) & 1;
           const int wsi = cnt % wsn;
@@ -382,19 +387,37 @@ icnnm_tc_kernel(TcArgs a) {
           tc_fence_after();
           long long t1c = dbg.p ? clk() : 0;
           if (!(a.skip & 1)) {
-            uint32_t hi[8], lo[8];
+            const uint32_t col = a_col0 + sa * (2 * KC);
+            if (a.bsplit) {
+              uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int q = kc * KC + 8 * half + i;
-              const float x = FWD ? hcur[hidx - tapoff[q]]
-                                  : Wst[wsi * (W_STAGE_BYTES / 4) + (8 * half + i) * 128 + row] * cs[q];
-              const uint32_t h = f2tf32(x);
-              hi[i] = h;
-              lo[i] = __float_as_uint(x - __uint_as_float(h));
+              for (int i = 0; i < 8; ++i) {
+                const int q = kc * KC + 8 * half + i;
+                const float x = FWD ? hcur[hidx - tapoff[q]]
+                                    : Wst[wsi * (W_STAGE_BYTES / 4) + (8 * half + i) * 128 + row] * cs[q];
+                const uint32_t h = f2tf32(x);
+                hi[i] = h;
+                lo[i] = __float_as_uint(x - __uint_as_float(h));
+              }
+              tmem_st8(tbase + lane_base + col + 8 * half, hi);
+              tmem_st8(tbase + lane_base + col + 8 * half + KC, lo);
+            } else {
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {  // two 8-column halves, one wait::st
+                uint32_t hi[8], lo[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const int q = kc * KC + 8 * hh + i;
+                  const float x = FWD ? hcur[hidx - tapoff[q]]
+                                      : Wst[wsi * (W_STAGE_BYTES / 4) + (8 * hh + i) * 128 + row] * cs[q];
+                  const uint32_t h = f2tf32(x);
+                  hi[i] = h;
+                  lo[i] = __float_as_uint(x - __uint_as_float(h));
+                }
+                tmem_st8(tbase + lane_base + col + 8 * hh, hi);
+                tmem_st8(tbase + lane_base + col + 8 * hh + KC, lo);
+              }
             }
-            const uint32_t col = a_col0 + sa * (2 * KC) + 8 * half;
-            tmem_st8(tbase + lane_base + col, hi);
-            tmem_st8(tbase + lane_base + col + KC, lo);
             tmem_wait_st();
           }
           tc_fence_before();

@@ -39,6 +39,8 @@ struct TcArgs {
   int skip;                 // timing experiments only: 1 = no build work, 2 = no epilogue work
   int sb;                   // B stages used (<= SB)
   int ws;                   // adjoint W stages used (<= WS)
+  int bsplit;               // A build: 0 = the two 4-warp groups own alternate K-chunks
+                            // (16 columns each); 1 = both groups split every chunk
 };
 
 // dbg slots (cycles summed over CTAs)
