@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--engine", default="tf32x3", choices=["tf32x3", "ffma"])
+    ap.add_argument("--engine", default="tf32x3", choices=["tf32x3", "f16x3", "ffma"])
     ap.add_argument("--iters", type=int, default=0, help="override iterations per solve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -135,6 +135,28 @@ def measure_tf32_peak(dev: int) -> float:
         return best
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def measure_f16_peak(dev: int) -> float:
+    """Dense fp16 tensor throughput (cuBLAS 8192^3, best of 5): fallback
+    denominator of the F16x3 engine when MEASURED_PEAKS.json is absent."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, device=f"cuda:{dev}", dtype=torch.float16)
+    b = torch.randn(n, n, device=f"cuda:{dev}", dtype=torch.float16)
+    for _ in range(2):
+        a @ b
+    best = 0.0
+    for _ in range(5):
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record()
+        a @ b
+        s1.record()
+        s1.synchronize()
+        best = max(best, 2 * n ** 3 / (s0.elapsed_time(s1) * 1e-3) / 1e12)
+    del a, b
+    return best
 
 
 def load_ncu_traffic(engine: str):
@@ -404,6 +426,16 @@ def report_line(args, P, w, B, cfg, iters, dev, world, value, t_max, kt, psnr, l
                 "peak_source": "measured dense TF32 (cuBLAS 8192^3 burst, %.0f TFLOP/s) / 3 "
                                "tensor MMAs per fp32 product" % tf32,
                 "tensor_pipe_frac": 3.0 * achieved / tf32}
+    elif args.engine == "f16x3":
+        f16 = peaks.get("bf16_tflops")
+        src = "MEASURED_PEAKS.json dense bf16 (burst)"
+        if not f16:
+            f16, src = measure_f16_peak(dev), "measured dense fp16 (cuBLAS 8192^3 burst)"
+        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": f16 / 3.0,
+                "unit": "TFLOP/s", "frac": achieved / (f16 / 3.0),
+                "peak_source": "%s %.0f TFLOP/s / 3 kind::f16 MMAs per fp32 product "
+                               "(kind::f16 runs at the bf16 rate)" % (src, f16),
+                "tensor_pipe_frac": 3.0 * achieved / f16}
     else:
         ffma_peak = P.probe_ffma_tflops(dev)
         roof = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": ffma_peak,

@@ -46,6 +46,8 @@ extern "C" {
 /* GEMM engine of the two per-iteration contractions. */
 #define ICNNM_ENGINE_FFMA 0     /* exact fp32 FFMA implicit GEMM            */
 #define ICNNM_ENGINE_TF32X3 1   /* tcgen05 kind::tf32, 3-term split (sm_100a) */
+#define ICNNM_ENGINE_F16X3 2    /* tcgen05 kind::f16, 3-term split of power-of-2
+                                   scaled operands (sm_100a; half the MMA time) */
 
 /* Field-for-field mirror of icnnm::SolverConfig (solver.hpp:29-43). */
 typedef struct icnnm_solver_config {

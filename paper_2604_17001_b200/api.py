@@ -35,7 +35,7 @@ import numpy as np
 from ._lib import (SolveReportC, SolverConfigC, check, dptr, lib, lptr,
                    InvalidArgument)
 
-ENGINES = {"ffma": 0, "tf32x3": 1}
+ENGINES = {"ffma": 0, "tf32x3": 1, "f16x3": 2}
 
 
 @dataclasses.dataclass

@@ -5,6 +5,7 @@
 // validation rules and error classes follow solver.cpp:26-40,66-72,
 // tensor.hpp:100-107,115-121 and spectral.cpp:25-41; the ADMM loop is the
 // restated form of solver.cpp:62-146 documented in DESIGN.md §2.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -127,10 +128,12 @@ void set_smem_attrs() {
   set_max_dyn_smem(icnnm_dev::icnnm_fwd_ffma, optin);
   set_max_dyn_smem(icnnm_dev::icnnm_adj_ffma, optin);
   set_max_dyn_smem(icnnm_dev::icnnm_gram_lags, optin);
-  CK(cudaFuncSetAttribute(icnnm_dev::tc::fwd_kernel_ptr(),
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-  CK(cudaFuncSetAttribute(icnnm_dev::tc::adj_kernel_ptr(),
-                          cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  for (bool f16 : {false, true}) {
+    CK(cudaFuncSetAttribute(icnnm_dev::tc::fwd_kernel_ptr(f16),
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    CK(cudaFuncSetAttribute(icnnm_dev::tc::adj_kernel_ptr(f16),
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  }
   done_dev = dev;
 }
 
@@ -160,8 +163,14 @@ void pack_basis(const Problem& p, const double* Kcm, std::vector<float>& Krm,
 // ---------------------------------------------------------------------------
 struct TcPlan {
   int kp = 0, ntn = 0, nkc = 0, nlast = 0, wbase = 0, sa = 0;
+  bool f16 = false;        // F16x3 engine (kind::f16) instead of TF32x3
+  float bunscale = 1.f;    // F16x3: inverse of B's power-of-2 scale
   int width(int nt) const { return std::min(wbase, kp - nt * wbase); }
 };
+
+inline bool is_tc(int engine) {
+  return engine == ICNNM_ENGINE_TF32X3 || engine == ICNNM_ENGINE_F16X3;
+}
 
 // N-tiling of kp columns into ntn tiles of width <= NTMAX (multiples of 16),
 // minimising the measured MMA cost: an M=128 kind::tf32 MMA takes
@@ -169,8 +178,9 @@ struct TcPlan {
 // beat many narrow ones (k=405: 2x208 instead of 128+128+128+32 = -19% MMA
 // time, half the MMA instructions).  TMEM: 2 accumulators of wbase columns +
 // sa A stages of 2*KC columns <= 512.
-TcPlan tc_plan(const Problem& p) {
+TcPlan tc_plan(const Problem& p, bool f16 = false) {
   TcPlan best;
+  best.f16 = f16;
   const int kp = p.kp_tc;
   double best_cost = 1e300;
   const int n0 = (kp + icnnm_dev::tc::NTMAX - 1) / icnnm_dev::tc::NTMAX;
@@ -189,7 +199,8 @@ TcPlan tc_plan(const Problem& p) {
     }
   }
   best.nkc = kp / icnnm_dev::tc::KC;
-  best.sa = std::min(icnnm_dev::tc::SA, (512 - 2 * best.wbase) / (2 * icnnm_dev::tc::KC));
+  const int stage_cols = f16 ? icnnm_dev::tc::KC : 2 * icnnm_dev::tc::KC;
+  best.sa = std::min(icnnm_dev::tc::SA, (512 - 2 * best.wbase) / stage_cols);
   return best;
 }
 
@@ -221,7 +232,45 @@ inline int adj_tap(const Problem& p, int n) {
   return (sh * kw + sw) * kt + st;
 }
 
-std::vector<float> pack_b_tiles(const Problem& p, const TcPlan& t, const double* Kcm, bool fwd) {
+// F16x3 B tiles: per (nt, kc) block [hl][n/8][k/8][n%8][k%8] halves of
+// s * B (s = 2^eB puts max|K| below 2^14), hi = rn_f16(s x), lo = rn_f16(s x - hi);
+// the lo block starts wn * 16 halves after hi.  Same block stride as TF32x3.
+std::vector<float> pack_b_tiles_f16(const Problem& p, TcPlan& t, const double* Kcm, bool fwd) {
+  const int k = p.k;
+  double amax = 0.0;
+  for (size_t i = 0; i < static_cast<size_t>(k) * k; ++i) amax = std::max(amax, std::fabs(Kcm[i]));
+  int ex = 0;
+  if (amax > 0) std::frexp(amax, &ex);
+  const int eb = 14 - ex;
+  t.bunscale = static_cast<float>(std::ldexp(1.0, -eb));
+  const int blk = icnnm_dev::tc::B_STAGE_BYTES / 4;
+  std::vector<float> out(static_cast<size_t>(t.ntn) * t.nkc * blk, 0.f);
+  for (int nt = 0; nt < t.ntn; ++nt) {
+    const int wn = t.width(nt);
+    for (int kc = 0; kc < t.nkc; ++kc) {
+      __half* base = reinterpret_cast<__half*>(out.data() + (static_cast<size_t>(nt) * t.nkc + kc) * blk);
+      for (int n = 0; n < wn; ++n)
+        for (int k16 = 0; k16 < icnnm_dev::tc::KC; ++k16) {
+          const int nn = nt * t.wbase + n;
+          const int kk = kc * icnnm_dev::tc::KC + k16;
+          double x = 0.0;
+          if (nn < k && kk < k)
+            x = fwd ? Kcm[static_cast<size_t>(nn) * k + kk]
+                    : Kcm[static_cast<size_t>(kk) * k + adj_tap(p, nn)];
+          const float xs = static_cast<float>(std::ldexp(x, eb));
+          const __half hi = __float2half_rn(xs);
+          const __half lo = __float2half_rn(xs - __half2float(hi));
+          const size_t off = (n / 8) * 128 + (k16 / 8) * 64 + (n % 8) * 8 + (k16 % 8);
+          base[off] = hi;
+          base[static_cast<size_t>(wn) * 16 + off] = lo;
+        }
+    }
+  }
+  return out;
+}
+
+std::vector<float> pack_b_tiles(const Problem& p, TcPlan& t, const double* Kcm, bool fwd) {
+  if (t.f16) return pack_b_tiles_f16(p, t, Kcm, fwd);
   const int k = p.k;
   const int blk = icnnm_dev::tc::B_STAGE_BYTES / 4;
   std::vector<float> out(static_cast<size_t>(t.ntn) * t.nkc * blk, 0.f);
@@ -258,8 +307,10 @@ inline int64_t tc_w_elems(const Geo& g, const TcPlan& t) {
 void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const float* src,
                       float* W, const float* Bpk, const float* cvec, float* adj, double* norm2,
                       const IterState* st, cudaStream_t stream,
-                      unsigned long long* dbg = nullptr) {
+                      unsigned long long* dbg = nullptr, float amax = 0.f) {
   icnnm_dev::tc::TcArgs a{};
+  a.bunscale = t.bunscale;
+  a.amax = amax;
   a.dbg = dbg;
   static const int skip_env = [] {
     const char* e = std::getenv("ICNNM_TC_SKIP");  // timing experiments only
@@ -287,14 +338,27 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   a.wbase = t.wbase;
   a.accw = t.wbase;
   a.sa = t.sa;
-  // stage counts that fit in shared memory (227 KB opt-in)
-  a.sb = icnnm_dev::tc::SB;
-  a.ws = icnnm_dev::tc::WS;
-  // shrink W stages to 3, then B stages to 3, then both to 2 until it fits
-  while (icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws) > 227 * 1024 && a.ws > 3) --a.ws;
-  while (icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws) > 227 * 1024 && a.sb > 3) --a.sb;
-  while (icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws) > 227 * 1024 && a.ws > 2) --a.ws;
-  while (icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws) > 227 * 1024 && a.sb > 2) --a.sb;
+  // deepest (B, W) stage counts that fit in shared memory (227 KB opt-in).
+  // W depth is even: the two builder groups own alternate K-chunks, so with an
+  // even ring each W stage is only ever consumed by one group.  With an odd
+  // ring consecutive uses of a stage alternate between groups, and a group
+  // running two uses ahead (possible with F16x3's 6 A stages) would pass its
+  // parity wait on the previous fill.
+  static const int pri[][2] = {{6, 4}, {5, 4}, {4, 4}, {3, 4}, {4, 2}, {3, 2}, {2, 2}};
+  static const int sb_cap = [] {
+    const char* e = std::getenv("ICNNM_TC_SB");  // A/B experiments only
+    return e ? std::atoi(e) : icnnm_dev::tc::SB;
+  }();
+  a.sb = 2;
+  a.ws = 2;
+  for (const auto& c : pri) {
+    if (c[0] > sb_cap) continue;
+    if (icnnm_dev::tc::smem_bytes(gtc, fwd, c[0], c[1]) <= 227 * 1024) {
+      a.sb = c[0];
+      a.ws = c[1];
+      break;
+    }
+  }
   a.nbricks = n_bricks(gtc);
   int dev = 0, nsm = 148;
   CK(cudaGetDevice(&dev));
@@ -303,7 +367,7 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   void* args[] = {&a};
   const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws);
   if (smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
-  CK(cudaLaunchKernel(fwd ? icnnm_dev::tc::fwd_kernel_ptr() : icnnm_dev::tc::adj_kernel_ptr(),
+  CK(cudaLaunchKernel(fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16) : icnnm_dev::tc::adj_kernel_ptr(t.f16),
                       dim3(grid), dim3(icnnm_dev::tc::threads(fwd)), args, smem, stream));
 }
 
@@ -345,7 +409,7 @@ void validate_cfg(const icnnm_solver_config* c) {
     invalid("SolverConfig: tolerances must be > 0");
   if (c->init_fill != ICNNM_INIT_ZERO && c->init_fill != ICNNM_INIT_MEAN)
     invalid("SolverConfig: init_fill must be 'zero' or 'mean'");
-  if (c->engine != ICNNM_ENGINE_FFMA && c->engine != ICNNM_ENGINE_TF32X3)
+  if (c->engine != ICNNM_ENGINE_FFMA && !is_tc(c->engine))
     invalid("SolverConfig: unknown engine");
 }
 
@@ -372,8 +436,9 @@ struct Solver {
   std::vector<Slab> slabs;
   std::unique_ptr<Comm> comm;    // cross-process exchange (world > 1)
   DBuf<float> Krm, KT, cvec;
-  TcPlan tp;
-  DBuf<float> BpkF, BpkA;        // tcgen05 engine: packed B tiles (fwd / adj)
+  TcPlan tp, tp16;               // tcgen05 engines: TF32x3 / F16x3 plans
+  DBuf<float> BpkF, BpkA;        // TF32x3: packed B tiles (fwd / adj)
+  DBuf<float> BpkF16, BpkA16;    // F16x3: packed B tiles (fwd / adj)
   int engine = ICNNM_ENGINE_FFMA;  // engine of the current run
   bool exact_res = false;          // exact primal residual (one extra forward / iteration)
   DBuf<double> red;              // norm2 (kp) | update slot (8)
@@ -412,6 +477,7 @@ void solver_alloc(Solver& S) {
   CK(cudaEventCreate(&S.evs));
   set_smem_attrs();
   S.tp = tc_plan(p);
+  S.tp16 = tc_plan(p, true);
   const int64_t WT = p.dims[1] * p.dims[2];
   for (auto& s : S.slabs) {
     s.g = make_geo(p, s.rows, !S.sharded);
@@ -440,10 +506,16 @@ void solver_alloc(Solver& S) {
   {
     auto bf = pack_b_tiles(p, S.tp, S.K.data(), true);
     auto ba = pack_b_tiles(p, S.tp, S.K.data(), false);
+    auto hf = pack_b_tiles(p, S.tp16, S.K.data(), true);
+    auto ha = pack_b_tiles(p, S.tp16, S.K.data(), false);
     S.BpkF.alloc(bf.size());
     S.BpkA.alloc(ba.size());
+    S.BpkF16.alloc(hf.size());
+    S.BpkA16.alloc(ha.size());
     CK(cudaMemcpyAsync(S.BpkF.p, bf.data(), S.BpkF.bytes(), cudaMemcpyHostToDevice, S.stream));
     CK(cudaMemcpyAsync(S.BpkA.p, ba.data(), S.BpkA.bytes(), cudaMemcpyHostToDevice, S.stream));
+    CK(cudaMemcpyAsync(S.BpkF16.p, hf.data(), S.BpkF16.bytes(), cudaMemcpyHostToDevice, S.stream));
+    CK(cudaMemcpyAsync(S.BpkA16.p, ha.data(), S.BpkA16.bytes(), cudaMemcpyHostToDevice, S.stream));
     CK(cudaStreamSynchronize(S.stream));
   }
   const int kpmax = std::max(p.kp, S.tp.kp);
@@ -547,13 +619,25 @@ void exchange_adj(Solver& S) {
 
 int engine_kp(const Solver& S);
 
+// Debugging only: ICNNM_F16_OFF=1 runs the F16x3 engine's adjoint in TF32x3,
+// =2 its forward (isolates a kernel when bisecting a failure).
+inline int f16_debug_mask() {
+  static const int m = [] {
+    const char* e = std::getenv("ICNNM_F16_OFF");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
 void launch_fwd(Solver& S, Slab& s, int mode) {
   // mode 2 (exact residual): forward on L_{t+1}, epilogue sums the gap into slot[5]
   const float* src = mode == 2 ? s.Lr.p : s.Lt.p;
   double* acc = mode == 2 ? S.red.p + engine_kp(S) + 5 : S.red.p;
-  if (S.engine == ICNNM_ENGINE_TF32X3) {
-    launch_tc_kernel(s.gtc, S.tp, true, mode, src, s.W.p, S.BpkF.p, S.cvec.p, s.adj.p, acc,
-                     S.st.p, S.stream, S.tc_counters ? S.dbg.p : nullptr);
+  if (is_tc(S.engine)) {
+    const bool f16 = S.engine == ICNNM_ENGINE_F16X3 && !(f16_debug_mask() & 2);
+    launch_tc_kernel(s.gtc, f16 ? S.tp16 : S.tp, true, mode, src, s.W.p,
+                     f16 ? S.BpkF16.p : S.BpkF.p, S.cvec.p, s.adj.p, acc, S.st.p, S.stream,
+                     S.tc_counters ? S.dbg.p : nullptr);
     ++S.launches;
     return;
   }
@@ -563,9 +647,10 @@ void launch_fwd(Solver& S, Slab& s, int mode) {
   ++S.launches;
 }
 void launch_adj(Solver& S, Slab& s) {
-  if (S.engine == ICNNM_ENGINE_TF32X3) {
-    launch_tc_kernel(s.gtc, S.tp, false, 1, s.Lt.p, s.W.p, S.BpkA.p, S.cvec.p, s.adj.p, S.red.p,
-                     S.st.p, S.stream,
+  if (is_tc(S.engine)) {
+    const bool f16 = S.engine == ICNNM_ENGINE_F16X3 && !(f16_debug_mask() & 1);
+    launch_tc_kernel(s.gtc, f16 ? S.tp16 : S.tp, false, 1, s.Lt.p, s.W.p,
+                     f16 ? S.BpkA16.p : S.BpkA.p, S.cvec.p, s.adj.p, S.red.p, S.st.p, S.stream,
                      S.tc_counters ? S.dbg.p + icnnm_dev::tc::DBG_SLOTS : nullptr);
     ++S.launches;
     return;
@@ -577,7 +662,7 @@ void launch_adj(Solver& S, Slab& s) {
 }
 
 int engine_kp(const Solver& S) {
-  return S.engine == ICNNM_ENGINE_TF32X3 ? S.tp.kp : S.p.kp;
+  return is_tc(S.engine) ? S.tp.kp : S.p.kp;
 }
 
 void allreduce_red(Solver& S) {
@@ -993,7 +1078,7 @@ int icnnm_cuda_conv_forward_ex(int order, const int64_t* dims, const double* L,
   return guard([&] {
     Problem p = make_problem(order, dims, kdims);
     if (!L || !K_colmajor || !out) invalid("null argument");
-    if (engine != ICNNM_ENGINE_FFMA && engine != ICNNM_ENGINE_TF32X3) invalid("unknown engine");
+    if (engine != ICNNM_ENGINE_FFMA && !is_tc(engine)) invalid("unknown engine");
     DeviceScope ds(device);
     set_smem_attrs();
     Geo g = make_geo(p, p.dims[0], true);
@@ -1001,8 +1086,8 @@ int icnnm_cuda_conv_forward_ex(int order, const int64_t* dims, const double* L,
     std::vector<float> Lf(L, L + p.m);
     DBuf<float> dL(p.m);
     CK(cudaMemcpy(dL.p, Lf.data(), dL.bytes(), cudaMemcpyHostToDevice));
-    if (engine == ICNNM_ENGINE_TF32X3) {
-      TcPlan t = tc_plan(p);
+    if (is_tc(engine)) {
+      TcPlan t = tc_plan(p, engine == ICNNM_ENGINE_F16X3);
       Geo gt = tc_geo(g, t);
       check_smem(icnnm_dev::tc::smem_bytes(gt, true, 2, 2));
       auto bf = pack_b_tiles(p, t, K_colmajor, true);
@@ -1059,21 +1144,22 @@ int icnnm_cuda_conv_adjoint_ex(int order, const int64_t* dims, const int64_t* kd
   return guard([&] {
     Problem p = make_problem(order, dims, kdims);
     if (!Wcm || !out) invalid("null argument");
-    if (engine != ICNNM_ENGINE_FFMA && engine != ICNNM_ENGINE_TF32X3) invalid("unknown engine");
+    if (engine != ICNNM_ENGINE_FFMA && !is_tc(engine)) invalid("unknown engine");
     DeviceScope ds(device);
     set_smem_attrs();
     Geo g = make_geo(p, p.dims[0], true);
     const int64_t H = p.dims[0], Wd = p.dims[1], T = p.dims[2];
     DBuf<float> dadj(p.m);
     CK(cudaMemset(dadj.p, 0, dadj.bytes()));
-    if (engine == ICNNM_ENGINE_TF32X3) {
-      TcPlan t = tc_plan(p);
+    if (is_tc(engine)) {
+      TcPlan t = tc_plan(p, engine == ICNNM_ENGINE_F16X3);
       Geo gt = tc_geo(g, t);
       check_smem(icnnm_dev::tc::smem_bytes(gt, false, 2, 2));
       std::vector<double> I(static_cast<size_t>(p.k) * p.k, 0.0);
       for (int j = 0; j < p.k; ++j) I[static_cast<size_t>(j) * p.k + j] = 1.0;
       auto ba = pack_b_tiles(p, t, I.data(), false);
       std::vector<float> Wt(tc_w_elems(gt, t), 0.f);
+      float wmax = 0.f;  // F16x3 operand scale bound (mode 0: no shrink factors)
       for (int64_t h = 0; h < H; ++h)
         for (int64_t w = 0; w < Wd; ++w)
           for (int64_t tt = 0; tt < T; ++tt) {
@@ -1081,13 +1167,17 @@ int icnnm_cuda_conv_adjoint_ex(int order, const int64_t* dims, const int64_t* kd
             const int64_t r = brick_row(gt, h, w, tt);
             const int64_t b = r / BM, v = r % BM;
             for (int j = 0; j < p.k; ++j)
-              Wt[(static_cast<size_t>(b) * t.kp + j) * 128 + v] =
-                  static_cast<float>(Wcm[static_cast<size_t>(j) * p.m + flat]);
+            {
+              const float x = static_cast<float>(Wcm[static_cast<size_t>(j) * p.m + flat]);
+              Wt[(static_cast<size_t>(b) * t.kp + j) * 128 + v] = x;
+              wmax = std::max(wmax, std::fabs(x));
+            }
           }
       DBuf<float> dB(ba.size()), dW(Wt.size());
       CK(cudaMemcpy(dB.p, ba.data(), dB.bytes(), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(dW.p, Wt.data(), dW.bytes(), cudaMemcpyHostToDevice));
-      launch_tc_kernel(gt, t, false, 0, nullptr, dW.p, dB.p, nullptr, dadj.p, nullptr, nullptr, 0);
+      launch_tc_kernel(gt, t, false, 0, nullptr, dW.p, dB.p, nullptr, dadj.p, nullptr, nullptr, 0,
+                       nullptr, wmax);
     } else {
       check_smem(adj_smem(g));
       // W (m x k column-major) -> brick-ordered rows; K = I.

@@ -35,7 +35,9 @@ extern thread_local std::string g_last_error;
   do {                                                                                \
     cudaError_t e_ = (x);                                                             \
     if (e_ != cudaSuccess)                                                            \
-      ::icnnm_host::fail(ICNNM_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+      ::icnnm_host::fail(ICNNM_CUDA_ERROR, std::string(#x) + " (" + __FILE__ + ":" +      \
+                                               std::to_string(__LINE__) + "): " +             \
+                                               cudaGetErrorString(e_));                       \
   } while (0)
 #define CKL() CK(cudaGetLastError())
 

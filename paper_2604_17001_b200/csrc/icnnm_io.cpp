@@ -217,6 +217,7 @@ int icnnm_config_from_json(const char* text, icnnm_solver_config* cfg) {
       else return io_fail("SolverConfig: init_fill must be 'zero' or 'mean'", ICNNM_INVALID_ARGUMENT);
     } else if (key == "engine") {
       if (sval == "tf32x3") cfg->engine = ICNNM_ENGINE_TF32X3;
+      else if (sval == "f16x3") cfg->engine = ICNNM_ENGINE_F16X3;
       else if (sval == "ffma") cfg->engine = ICNNM_ENGINE_FFMA;
       else return io_fail("SolverConfig: unknown engine", ICNNM_INVALID_ARGUMENT);
     } else if (key == "exact_residual") {

@@ -456,6 +456,7 @@ __global__ void icnnm_coef(IterState* st, const double* __restrict__ theta,
   const double th = theta[cur];
   const double tau = 1.0 / th;
   double acc[2] = {0.0, 0.0};
+  double amax = 0.0;  // max_j c_j n_j = max_j min(n_j, tau) bounds |W_vj c_j|
   for (int j = threadIdx.x; j < kp; j += blockDim.x) {
     double n = sqrt(red[j]);
     red[j] = 0.0;
@@ -465,8 +466,21 @@ __global__ void icnnm_coef(IterState* st, const double* __restrict__ theta,
       c = static_cast<float>(cd);
       acc[0] += fmax(0.0, n - tau);
       acc[1] += (1.0 - cd) * (1.0 - cd) * n * n;
+      amax = fmax(amax, fmin(n, tau));
     }
     cvec[j] = c;
+  }
+  {
+    __shared__ double wmax[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = amax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, wmax[w]);
+      st->adj_amax = m;
+    }
   }
   block_reduce_add<2>(acc, &stats[cur].l21);
 }

@@ -44,6 +44,7 @@ struct IterState {
   int pad0;
   double theta;    // theta_it
   double r;        // theta_it / theta_{it+1}
+  double adj_amax; // max_j min(n_j, 1/theta) >= |W_vj c_j|: F16x3 adjoint operand scale
 };
 
 // Per-iteration reductions (fp64).

@@ -1,23 +1,32 @@
 // ICNNM forward / adjoint contractions on the 5th-gen tensor cores (sm_100a).
 //
-// Engine ICNNM_ENGINE_TF32X3: each fp32 GEMM is computed as three tcgen05
-// kind::tf32 MMAs per K-step with fp32 accumulation in TMEM,
-//     D += A_hi B_hi + A_lo B_hi + A_hi B_lo,     x_hi = rna_tf32(x), x_lo = x - x_hi,
-// which keeps ~22 mantissa bits of every product (the parity study in
-// DESIGN.md §5 shows 1-term TF32 misses the 1e-4 tolerance).
+// Each fp32 GEMM is computed from a hi/lo split of both operands with fp32
+// accumulation in TMEM, three MMAs per K-step:
+//     D += A_hi B_hi + A_lo B_hi + A_hi B_lo
+// Engine ICNNM_ENGINE_TF32X3: x_hi = rna_tf32(x), x_lo = x - x_hi,
+//   tcgen05.mma kind::tf32 (K = 8 per MMA).
+// Engine ICNNM_ENGINE_F16X3: x_hi = rn_f16(s x), x_lo = rn_f16(s x - x_hi) with a
+//   power-of-2 scale s that puts max|x| below 2^14, tcgen05.mma kind::f16
+//   (K = 16 per MMA at the same cycle cost: half the MMA time).  Both keep
+//   ~22 mantissa bits of every product.  Scales: B (the basis)
+//   once on the host; forward A per brick from the max of the brick's halo
+//   (builders -> epilogue through a ring of mbarrier-guarded slots); adjoint A
+//   from the bound |W_vj c_j| <= min(n_j, 1/theta) computed by the coef kernel.
 //
-// Kernel shape (persistent, one CTA per SM, 320 threads):
-//   warps 0-3  builders : im2col / scaled-W rows -> hi/lo split -> tcgen05.st
-//                         into a TMEM A-stage (row = TMEM lane = voxel)
-//   warps 4-7  epilogue : tcgen05.ld the accumulator; forward: W update +
+// Kernel shape (persistent, one CTA per SM, 576 (forward) / 480 (adjoint) threads):
+//   warps 0-7  builders : im2col / scaled-W rows -> hi/lo split -> tcgen05.st
+//                         into a TMEM A-stage (row = TMEM lane = voxel); the two
+//                         4-warp groups own alternate K-chunks
+//   warps 8..  epilogue : tcgen05.ld the accumulator; forward: W update +
 //                         column norms; adjoint: col2im into per-warp SMEM
 //                         output bricks, flushed with one atomic per entry
-//   warp 8     MMA      : one elected thread issues tcgen05.mma (A from TMEM,
+//   next warp  MMA      : one elected thread issues tcgen05.mma (A from TMEM,
 //                         B from SMEM via a SWIZZLE_NONE K-major descriptor)
-//   warp 9     loader   : cp.async.bulk of host-pre-packed B tiles (UMMA
-//                         canonical layout) into a 3-stage SMEM ring
+//   next warp  loader   : cp.async.bulk of host-pre-packed B tiles (UMMA
+//                         canonical layout) into an SMEM ring; the adjoint has
+//                         one more warp streaming W chunks
 // TMEM: two accumulators of accw <= 208 columns (epilogue of tile i overlaps
-// the MMAs of tile i+1) + sa A stages of 2*KC columns (hi | lo).
+// the MMAs of tile i+1) + sa A stages (tf32: 2*KC columns, f16: KC columns).
 //
 // Forward  (a)+(b): D[v, j] = sum_s L~[v - s] K[s, j]          (N = columns j)
 // Adjoint  (c)    : D[v, s] = sum_j W[v, j] c_j K[s, j]        (N = taps s)
@@ -117,6 +126,38 @@ __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
       "}\n" ::"r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tc_mma_f16_elect(uint32_t d, uint32_t a, uint64_t bdesc,
+                                                 uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// {lo16 = rn_f16(x0), hi16 = rn_f16(x1)}: element 2i in the low half
+__device__ __forceinline__ uint32_t pack_f16x2(float x0, float x1) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(x1), "f"(x0));
+  return r;
+}
+__device__ __forceinline__ void unpack_f16x2(uint32_t h, float& x0, float& x1) {
+  asm("{\n.reg .f16 a, b;\nmov.b32 {a, b}, %2;\ncvt.f32.f16 %0, a;\ncvt.f32.f16 %1, b;\n}\n"
+      : "=f"(x0), "=f"(x1)
+      : "r"(h));
+}
+// Power-of-2 scale putting values of magnitude <= amax below 2^14 (f16 max 65504).
+__device__ __forceinline__ float f16_scale(float amax) {
+  if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
+  int ex;
+  frexpf(amax, &ex);  // amax < 2^ex
+  int e = 14 - ex;
+  e = e > 126 ? 126 : e;
+  return ldexpf(1.f, e);
+}
 __device__ __forceinline__ uint32_t f2tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
@@ -163,6 +204,11 @@ __device__ __forceinline__ uint64_t bdesc(uint32_t saddr) {
 // kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M=128.
 __device__ __forceinline__ uint32_t idesc_tf32(int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(128 >> 4) << 24);
+}
+// kind::f16 instruction descriptor: D f32, A/B f16, both K-major, M=128.
+__device__ __forceinline__ uint32_t idesc_f16(int n) {
+  return (1u << 4) | (static_cast<uint32_t>(n >> 3) << 17) |
          (static_cast<uint32_t>(128 >> 4) << 24);
 }
 
@@ -219,9 +265,11 @@ __device__ __forceinline__ int tile_width(const TcArgs& a, int nt) {
 //   warp  8 + NEPI          MMA issuer
 //   warp  9 + NEPI          B loader
 // ---------------------------------------------------------------------------
-template <bool FWD>
+template <bool FWD, bool F16>
 __global__ void __launch_bounds__(FWD ? 576 : 480, 1)
 icnnm_tc_kernel(TcArgs a) {
+  constexpr int ASC = F16 ? KC : 2 * KC;  // TMEM columns per A stage
+  constexpr int ALO = ASC / 2;            // column offset of the lo half
   constexpr int NB = 8;                  // builder warps
   constexpr int NEPI = FWD ? 8 : 4;      // epilogue warps
   constexpr int WMMA = NB + NEPI;        // MMA warp
@@ -251,7 +299,10 @@ icnnm_tc_kernel(TcArgs a) {
   uint64_t* ACC_empty = ACC_full + 2;
   uint64_t* W_full = ACC_empty + 2;
   uint64_t* W_empty = W_full + WS;
-  p += 256;  // 26 mbarriers
+  uint64_t* SC_full = W_empty + WS;   // F16x3 forward: per-brick scale slots
+  float* sc_ring = reinterpret_cast<float*>(SC_full + NSC);
+  float* wmax = sc_ring + NSC;        // 2 x 8 builder-warp maxima
+  p += 512;  // 2*SA + 2*SB + 4 + 2*WS + NSC mbarriers, NSC scales, 16 maxima
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p);
   p += 16;
   int* tapoff = reinterpret_cast<int*>(p);
@@ -276,7 +327,7 @@ icnnm_tc_kernel(TcArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
-    const int nbuild = a.bsplit ? NB * 32 : (NB / 2) * 32;  // builder arrivals per chunk
+    const int nbuild = (a.bsplit && !F16) ? NB * 32 : (NB / 2) * 32;  // builder arrivals / chunk
     for (int i = 0; i < SA; ++i) {
       mbar_init(A_full + i, nbuild);
       mbar_init(A_empty + i, 1);
@@ -293,6 +344,7 @@ icnnm_tc_kernel(TcArgs a) {
       mbar_init(W_full + i, 1);
       mbar_init(W_empty + i, nbuild);
     }
+    for (int i = 0; i < NSC; ++i) mbar_init(SC_full + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int s = tid; s < g.ktp; s += blockDim.x) {
@@ -317,9 +369,15 @@ icnnm_tc_kernel(TcArgs a) {
     }
     tapoff[s] = off;
   }
+  // cs[j]: forward mode 1: r c_j (the W_old weight); mode 2: c_j; adjoint:
+  // c_j (mode 1) or 1, times the F16x3 operand scale
+  const float fscale_adj =
+      (F16 && !FWD) ? f16_scale(a.mode >= 1 ? static_cast<float>(a.st->adj_amax) : a.amax) : 1.f;
   for (int j = tid; j < g.kp; j += blockDim.x) {
     float c = 1.f;
     if (a.mode >= 1) c = a.cvec[j];
+    if (FWD && a.mode == 1) c *= rr;
+    if (!FWD) c *= fscale_adj;
     cs[j] = (j < g.k) ? c : 0.f;
   }
   if (FWD) {
@@ -362,21 +420,41 @@ icnnm_tc_kernel(TcArgs a) {
     if (FWD) {
       if (blockIdx.x < nbr) issue_halo(halo, blockIdx.x);
     }
+    // F16x3 operand scale: forward per brick (the halo is prescaled in place);
+    // adjoint: folded into cs
     int iter = 0;
     for (int b = blockIdx.x; b < nbr; b += gridDim.x, ++iter) {
-      const float* hcur = halo + (iter & 1) * nobp;
+      float* hcur = halo + (iter & 1) * nobp;
       if (FWD) {
         cp_async_wait_all();
         named_sync(1, NB * 32);  // this brick's halo landed; previous brick fully built
         if (b + static_cast<int>(gridDim.x) < nbr)
           issue_halo(halo + ((iter + 1) & 1) * nobp, b + gridDim.x);
+        if (F16) {
+          float mx = 0.f;
+          for (int e = bt_tid; e < nob; e += NB * 32) mx = fmaxf(mx, fabsf(hcur[e]));
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          if (lane == 0) wmax[(iter & 1) * 8 + warp] = mx;
+          named_sync(1, NB * 32);
+          float bm = 0.f;
+#pragma unroll
+          for (int w = 0; w < NB; ++w) bm = fmaxf(bm, wmax[(iter & 1) * 8 + w]);
+          const float fscale = f16_scale(bm);
+          for (int e = bt_tid; e < nob; e += NB * 32) hcur[e] *= fscale;
+          if (bt_tid == 0) {  // the epilogue unscales this brick by 2^-(eA + eB)
+            sc_ring[iter % NSC] = a.bunscale / fscale;
+            mbar_arrive(SC_full + iter % NSC);
+          }
+          named_sync(1, NB * 32);  // halo scaled
+        }
       }
       for (int nt = 0; nt < ntn; ++nt) {
         for (int kc = 0; kc < nkc; ++kc, ++cnt) {
           // bsplit = 0: group `half` owns the chunks with cnt % 2 == half and
           // builds all KC columns, so each warp has two chunk periods of MMA
           // time to cover its TMEM-store round trip.
-          if (!a.bsplit && static_cast<int>(cnt & 1u) != half) continue;
+          if ((F16 || !a.bsplit) && static_cast<int>(cnt & 1u) != half) continue;
           const int sa = cnt % san;
           const uint32_t ph = (cnt / san) & 1;
           const int wsi = cnt % wsn;
@@ -387,8 +465,27 @@ icnnm_tc_kernel(TcArgs a) {
           tc_fence_after();
           long long t1c = dbg.p ? clk() : 0;
           if (!(a.skip & 1)) {
-            const uint32_t col = a_col0 + sa * (2 * KC);
-            if (a.bsplit) {
+            const uint32_t col = a_col0 + sa * ASC;
+            if (F16) {
+              // 16 K values -> 8 f16x2 words hi | 8 words lo (element 2i in the low half)
+              uint32_t hi[8], lo[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                float x[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  const int q = kc * KC + 2 * i + u;
+                  x[u] = FWD ? hcur[hidx - tapoff[q]]
+                             : Wst[wsi * (W_STAGE_BYTES / 4) + (2 * i + u) * 128 + row] * cs[q];
+                }
+                hi[i] = pack_f16x2(x[0], x[1]);
+                float h0, h1;
+                unpack_f16x2(hi[i], h0, h1);
+                lo[i] = pack_f16x2(x[0] - h0, x[1] - h1);
+              }
+              tmem_st8(tbase + lane_base + col, hi);
+              tmem_st8(tbase + lane_base + col + ALO, lo);
+            } else if (a.bsplit) {
               uint32_t hi[8], lo[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -448,10 +545,35 @@ icnnm_tc_kernel(TcArgs a) {
     float gacc = 0.f;  // mode 2: this thread's share of ||(1-c)W - A(L)K||^2
     uint32_t tcount = 0;
     Dbg dbg(lane == 0 ? a.dbg : nullptr);
-    for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+    float us_adj = 1.f;  // F16x3 adjoint: 2^-(eA + eB)
+    if (F16 && !FWD)
+      us_adj = a.bunscale / f16_scale(a.mode >= 1 ? static_cast<float>(a.st->adj_amax) : a.amax);
+    // forward modes 1/2 read W_old: stream each brick's contiguous W block
+    // (kp x 128 floats) into L2 one brick ahead so the epilogue's loads hit L2
+    const bool pf = FWD && a.mode >= 1 && ew == 0 && lane == 0 && !(a.skip & 64);
+    auto prefetch_w = [&](int bb) {
+      if (bb >= nbr) return;
+      const char* base = reinterpret_cast<const char*>(a.Wout + static_cast<size_t>(bb) * g.kp * 128);
+      const uint32_t total = static_cast<uint32_t>(g.kp) * 128u * 4u;
+      for (uint32_t off = 0; off < total; off += 32768u) {
+        const uint32_t sz = total - off < 32768u ? total - off : 32768u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base + off), "r"(sz)
+                     : "memory");
+      }
+    };
+    if (pf) prefetch_w(blockIdx.x);
+    uint32_t biter = 0;
+    for (int b = blockIdx.x; b < nbr; b += gridDim.x, ++biter) {
+      if (pf) prefetch_w(b + gridDim.x);
       int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
       const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
       const bool valid = (h0 + vh < g.H) && (w0 + vw < g.W) && (t0 + vt < g.T);
+      const bool bfull = (h0 + g.bh <= g.H) && (w0 + g.bw <= g.W) && (t0 + g.bt <= g.T);
+      float us = us_adj;
+      if (F16 && FWD) {  // this brick's scale, published by the builders
+        mbar_wait(SC_full + biter % NSC, (biter / NSC) & 1);
+        us = sc_ring[biter % NSC];
+      }
       for (int nt = 0; nt < ntn; ++nt, ++tcount) {
         const int acc = tcount & 1;
         const uint32_t ph = (tcount >> 1) & 1;
@@ -465,39 +587,77 @@ icnnm_tc_kernel(TcArgs a) {
           tmem_ld32(tbase + lane_base + acc * a.accw + c0, u);
           tmem_wait_ld();
           const int ncol = (wn - c0) < 32 ? (wn - c0) : 32;
+          // accumulator -> fp32 product (F16x3: undo the operand scales)
+          auto accv = [&](int i) { return F16 ? __uint_as_float(u[i]) * us : __uint_as_float(u[i]); };
           if (FWD && a.mode == 2) {
             const int j0 = nt * a.wbase + c0;
             const float* wp = a.Wout + (static_cast<size_t>(b) * g.kp + j0) * 128 + row;
+            float wo[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) wo[i] = (i < ncol) ? wp[static_cast<size_t>(i) * 128] : 0.f;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-              if (i < ncol && valid) {
-                const float gap = (1.f - cs[j0 + i]) * wp[static_cast<size_t>(i) * 128] -
-                                  __uint_as_float(u[i]);
-                gacc = fmaf(gap, gap, gacc);
-              }
+              const float gap = (1.f - cs[j0 + i]) * wo[i] - accv(i);
+              gacc = (i < ncol && valid) ? fmaf(gap, gap, gacc) : gacc;
             }
           } else if (FWD) {
             const int j0 = nt * a.wbase + c0;
             float* wp = a.Wout + (static_cast<size_t>(b) * g.kp + j0) * 128 + row;
-            float wo[32];
-            if (a.mode == 1) {
+            if (ncol == 32 && bfull) {
+              // fast path (whole brick inside the tensor, full 32 columns):
+              // W = acc (* us) + (r c_j) W_old, r c_j read 4 at a time
+              float w[32];
+              if (a.mode == 1) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) wo[i] = (i < ncol) ? wp[static_cast<size_t>(i) * 128] : 0.f;
-            }
+                for (int i = 0; i < 32; ++i) w[i] = wp[static_cast<size_t>(i) * 128];
+                const float4* c4 = reinterpret_cast<const float4*>(cs + j0);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              float w = __uint_as_float(u[i]);
-              if (a.mode == 1) w = fmaf(rr * cs[j0 + i], wo[i], w);
-              w = (valid && i < ncol) ? w : 0.f;
-              if (i < ncol) wp[static_cast<size_t>(i) * 128] = w;
-              myred[i * 33 + lane] = w * w;
+                for (int q = 0; q < 8; ++q) {
+                  const float4 cc = c4[q];
+                  const float cq[4] = {cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+                  for (int r4 = 0; r4 < 4; ++r4) {
+                    const int i = 4 * q + r4;
+                    w[i] = F16 ? fmaf(__uint_as_float(u[i]), us, cq[r4] * w[i])
+                               : fmaf(cq[r4], w[i], __uint_as_float(u[i]));
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) w[i] = accv(i);
+              }
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                wp[static_cast<size_t>(i) * 128] = w[i];
+                myred[i * 33 + lane] = w[i];
+              }
+            } else {
+              // general path: W_old loads issued together as predicated loads
+              // (a load inside the compute loop becomes a branch per element and
+              // serialises 32 HBM round trips)
+              float wo[32];
+              if (a.mode == 1) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) wo[i] = (i < ncol) ? wp[static_cast<size_t>(i) * 128] : 0.f;
+              }
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                float w = accv(i);
+                if (a.mode == 1) w = fmaf(cs[j0 + i], wo[i], w);
+                w = (valid && i < ncol) ? w : 0.f;
+                if (i < ncol) wp[static_cast<size_t>(i) * 128] = w;
+                myred[i * 33 + lane] = w;
+              }
             }
             __syncwarp();
-            float s = 0.f;
+            float sq = 0.f;
 #pragma unroll 8
-            for (int i = 0; i < 32; ++i) s += myred[lane * 33 + i];
+            for (int i = 0; i < 32; ++i) {
+              const float x = myred[lane * 33 + i];
+              sq = fmaf(x, x, sq);
+            }
             __syncwarp();
-            if (lane < ncol) atomicAdd(nrm + j0 + lane, static_cast<double>(s));
+            if (lane < ncol) atomicAdd(nrm + j0 + lane, static_cast<double>(sq));
           } else {
             const int s0 = nt * a.wbase + c0;
             if (g.kh >= 4) {
@@ -517,7 +677,7 @@ icnnm_tc_kernel(TcArgs a) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) x[q] = *o[q];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) *o[q] = x[q] + v[q];
+                for (int q = 0; q < 4; ++q) *o[q] = F16 ? fmaf(v[q], us, x[q]) : x[q] + v[q];
                 __syncwarp();
               }
             } else {
@@ -526,7 +686,7 @@ icnnm_tc_kernel(TcArgs a) {
                 const int sidx = s0 + i;
                 if (i < ncol && sidx < g.k) {
                   float* o = myob + (hidx - tapoff[sidx]);
-                  *o += __uint_as_float(u[i]);
+                  *o += accv(i);
                 }
                 __syncwarp();
               }
@@ -583,7 +743,7 @@ icnnm_tc_kernel(TcArgs a) {
           const int acc = tcount & 1;
           const uint32_t aph = (tcount >> 1) & 1;
           const int wn = tile_width(a, nt);
-          const uint32_t idesc = idesc_tf32(wn);
+          const uint32_t idesc = F16 ? idesc_f16(wn) : idesc_tf32(wn);
           const uint32_t dcol = tbase + acc * a.accw;
           long long q0 = a.dbg ? clk() : 0;
           if (!(a.skip & 32)) mbar_wait(ACC_empty + acc, aph ^ 1);
@@ -602,17 +762,26 @@ icnnm_tc_kernel(TcArgs a) {
               wb += q3 - q2;
             }
             tc_fence_after();
-            const uint32_t acol = tbase + a_col0 + sa * (2 * KC);
+            const uint32_t acol = tbase + a_col0 + sa * ASC;
             const uint32_t bhi = bs0 + sb * B_STAGE_BYTES;
-            const uint32_t blo = bhi + wn * (KC / 8) * 32;
+            if (F16) {
+              // one K-step of 16: B hi | lo blocks of wn x 16 halves (wn * 32 B each)
+              const uint64_t dh = bdesc(bhi);
+              const uint64_t dl = bdesc(bhi + wn * 32);
+              tc_mma_f16_elect(dcol, acol, dh, idesc, kc == 0 ? 0u : 1u);
+              tc_mma_f16_elect(dcol, acol + ALO, dh, idesc, 1u);
+              tc_mma_f16_elect(dcol, acol, dl, idesc, 1u);
+            } else {
+              const uint32_t blo = bhi + wn * (KC / 8) * 32;
 #pragma unroll
-            for (int q = 0; q < KC / 8; ++q) {
-              const uint64_t dh = bdesc(bhi + q * wn * 32);
-              const uint64_t dl = bdesc(blo + q * wn * 32);
-              const uint32_t first = (kc == 0 && q == 0) ? 0u : 1u;
-              tc_mma_ts_elect(dcol, acol + q * 8, dh, idesc, first);
-              tc_mma_ts_elect(dcol, acol + KC + q * 8, dh, idesc, 1u);
-              tc_mma_ts_elect(dcol, acol + q * 8, dl, idesc, 1u);
+              for (int q = 0; q < KC / 8; ++q) {
+                const uint64_t dh = bdesc(bhi + q * wn * 32);
+                const uint64_t dl = bdesc(blo + q * wn * 32);
+                const uint32_t first = (kc == 0 && q == 0) ? 0u : 1u;
+                tc_mma_ts_elect(dcol, acol + q * 8, dh, idesc, first);
+                tc_mma_ts_elect(dcol, acol + ALO + q * 8, dh, idesc, 1u);
+                tc_mma_ts_elect(dcol, acol + q * 8, dl, idesc, 1u);
+              }
             }
             if (!(a.skip & 8)) tc_commit_elect(A_empty + sa);
             if (!(a.skip & 16)) tc_commit_elect(B_empty + sb);
@@ -636,7 +805,7 @@ icnnm_tc_kernel(TcArgs a) {
       for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
         for (int nt = 0; nt < ntn; ++nt) {
           const int wn = tile_width(a, nt);
-          const uint32_t bytes = static_cast<uint32_t>(wn) * KC * 8;
+          const uint32_t bytes = static_cast<uint32_t>(wn) * KC * (F16 ? 4 : 8);
           for (int kc = 0; kc < nkc; ++kc, ++bcnt) {
             const int sb = bcnt % sbn;
             long long q0 = a.dbg ? clk() : 0;
@@ -684,11 +853,19 @@ icnnm_tc_kernel(TcArgs a) {
   }
 }
 
-template __global__ void icnnm_tc_kernel<true>(TcArgs);
-template __global__ void icnnm_tc_kernel<false>(TcArgs);
+template __global__ void icnnm_tc_kernel<true, false>(TcArgs);
+template __global__ void icnnm_tc_kernel<false, false>(TcArgs);
+template __global__ void icnnm_tc_kernel<true, true>(TcArgs);
+template __global__ void icnnm_tc_kernel<false, true>(TcArgs);
 
-void* fwd_kernel_ptr() { return reinterpret_cast<void*>(&icnnm_tc_kernel<true>); }
-void* adj_kernel_ptr() { return reinterpret_cast<void*>(&icnnm_tc_kernel<false>); }
+void* fwd_kernel_ptr(bool f16) {
+  return f16 ? reinterpret_cast<void*>(&icnnm_tc_kernel<true, true>)
+             : reinterpret_cast<void*>(&icnnm_tc_kernel<true, false>);
+}
+void* adj_kernel_ptr(bool f16) {
+  return f16 ? reinterpret_cast<void*>(&icnnm_tc_kernel<false, true>)
+             : reinterpret_cast<void*>(&icnnm_tc_kernel<false, false>);
+}
 
 }  // namespace tc
 }  // namespace icnnm_dev

@@ -1,5 +1,5 @@
-// tcgen05 (TF32x3) engine of the two ICNNM contractions: shared host/device
-// declarations.  See icnnm_tc.cu for the kernel design.
+// tcgen05 engines (TF32x3, F16x3) of the two ICNNM contractions: shared
+// host/device declarations.  See icnnm_tc.cu for the kernel design.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -9,9 +9,11 @@
 namespace icnnm_dev {
 namespace tc {
 
-constexpr int KC = 16;                         // K per chunk (2 MMA K-steps of 8)
-constexpr int SA = 4;                          // TMEM A stages (max; runtime a.sa), 2*KC columns each
-constexpr int SB = 4;                          // SMEM B stages (max; runtime a.sb)
+constexpr int KC = 16;                         // K per chunk (tf32: 2 MMA K-steps of 8; f16: 1 of 16)
+constexpr int SA = 6;                          // TMEM A stages (max; runtime a.sa); tf32: 2*KC
+                                               // columns each, f16: KC columns (2 halves / column)
+constexpr int NSC = 8;                         // F16x3 forward: per-brick scale ring
+constexpr int SB = 6;                          // SMEM B stages (max; runtime a.sb)
 constexpr int WS = 4;                          // adjoint: SMEM W-chunk stages (max; runtime a.ws)
 constexpr int W_STAGE_BYTES = 128 * KC * 4;    // 8 KB: 16 columns x 128 rows
 constexpr int NTMAX = 208;                     // max accumulator width (N per tile)
@@ -40,25 +42,27 @@ struct TcArgs {
   int sb;                   // B stages used (<= SB)
   int ws;                   // adjoint W stages used (<= WS)
   int bsplit;               // A build: 0 = the two 4-warp groups own alternate K-chunks
-                            // (16 columns each); 1 = both groups split every chunk
+                            // (16 columns each); 1 = both groups split every chunk (TF32x3)
+  float bunscale;           // F16x3: 2^-eB, the inverse of the power-of-2 scale of B
+  float amax;               // F16x3 adjoint, mode 0: bound on |W| (mode 1: st->adj_amax)
 };
 
 // dbg slots (cycles summed over CTAs)
 enum { DBG_BUILD_WAIT = 0, DBG_BUILD_WORK, DBG_MMA_WAIT_A, DBG_MMA_WAIT_B, DBG_MMA_WAIT_ACC,
        DBG_EPI_WAIT, DBG_EPI_WORK, DBG_LOAD_WAIT, DBG_TOTAL, DBG_SLOTS };
 
-template <bool FWD>
+template <bool FWD, bool F16>
 __global__ void icnnm_tc_kernel(TcArgs a);
 
-void* fwd_kernel_ptr();
-void* adj_kernel_ptr();
+void* fwd_kernel_ptr(bool f16);
+void* adj_kernel_ptr(bool f16);
 
 inline int threads(bool fwd) { return fwd ? 576 : 480; }
 
 inline size_t smem_bytes(const Geo& g, bool fwd, int sb = SB, int ws = WS) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
   const size_t nobp = ((nob + 3) / 4) * 4;
-  size_t b = static_cast<size_t>(sb) * B_STAGE_BYTES + (fwd ? 0 : static_cast<size_t>(ws) * W_STAGE_BYTES) + 256 + 16;
+  size_t b = static_cast<size_t>(sb) * B_STAGE_BYTES + (fwd ? 0 : static_cast<size_t>(ws) * W_STAGE_BYTES) + 512 + 16;
   b += ((g.ktp * 4 + 15) / 16) * 16;
   b += ((g.kp * 4 + 15) / 16) * 16;
   if (fwd)

@@ -14,7 +14,7 @@ from oracle import icnnm_oracle as O
 pytestmark = pytest.mark.gpu
 
 FIXED = dict(tol_primal=1e-300, tol_change=1e-300)
-ENGINES = ["ffma", "tf32x3"]
+ENGINES = ["ffma", "tf32x3", "f16x3"]
 
 
 def _rel(a, b):
