@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--engine", default="tf32x3", choices=["tf32x3", "f16x3", "ffma"])
+    ap.add_argument("--engine", default="f16x3", choices=["f16x3", "tf32x3", "ffma"])
     ap.add_argument("--iters", type=int, default=0, help="override iterations per solve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

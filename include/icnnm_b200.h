@@ -61,7 +61,7 @@ typedef struct icnnm_solver_config {
   double tol_change;    /* 1e-8                                       */
   double rank_tol;      /* 1e-8 (unused by the solver, as upstream)   */
   int init_fill;        /* ICNNM_INIT_ZERO | ICNNM_INIT_MEAN          */
-  int engine;           /* ICNNM_ENGINE_* (extension; default TF32X3) */
+  int engine;           /* ICNNM_ENGINE_* (extension; default F16X3) */
   int exact_residual;   /* extension: 1 = exact primal_residual trace
                            (one extra forward contraction per iteration);
                            0 = fp32 identity estimate (NaN once unresolved) */

@@ -50,7 +50,7 @@ class SolverConfig:
     tol_change: float = 1e-8
     rank_tol: float = 1e-8
     init_fill: str = "zero"
-    engine: str = "tf32x3"
+    engine: str = "f16x3"
     exact_residual: bool = False
 
     def to_c(self) -> SolverConfigC:

@@ -346,8 +346,10 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   // parity wait on the previous fill.
   static const int pri[][2] = {{6, 4}, {5, 4}, {4, 4}, {3, 4}, {4, 2}, {3, 2}, {2, 2}};
   static const int sb_cap = [] {
-    const char* e = std::getenv("ICNNM_TC_SB");  // A/B experiments only
-    return e ? std::atoi(e) : icnnm_dev::tc::SB;
+    // 4 B stages measured faster than 5-6 (more SMEM leaves less L1):
+    // profiles/README_r1.md; ICNNM_TC_SB overrides for A/B experiments
+    const char* e = std::getenv("ICNNM_TC_SB");
+    return e ? std::atoi(e) : 4;
   }();
   a.sb = 2;
   a.ws = 2;
@@ -924,7 +926,7 @@ void icnnm_default_config(icnnm_solver_config* c) {
   c->tol_change = 1e-8;
   c->rank_tol = 1e-8;
   c->init_fill = ICNNM_INIT_ZERO;
-  c->engine = ICNNM_ENGINE_TF32X3;
+  c->engine = ICNNM_ENGINE_F16X3;
   c->exact_residual = 0;
 }
 

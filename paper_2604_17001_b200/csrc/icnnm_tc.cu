@@ -78,6 +78,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
@@ -266,14 +281,14 @@ __device__ __forceinline__ int tile_width(const TcArgs& a, int nt) {
 //   warp  9 + NEPI          B loader
 // ---------------------------------------------------------------------------
 template <bool FWD, bool F16>
-__global__ void __launch_bounds__(FWD ? 576 : 480, 1)
+__global__ void __launch_bounds__(FWD ? 608 : 480, 1)
 icnnm_tc_kernel(TcArgs a) {
   constexpr int ASC = F16 ? KC : 2 * KC;  // TMEM columns per A stage
   constexpr int ALO = ASC / 2;            // column offset of the lo half
   constexpr int NB = 8;                  // builder warps
   constexpr int NEPI = FWD ? 8 : 4;      // epilogue warps
   constexpr int WMMA = NB + NEPI;        // MMA warp
-  constexpr int WLOAD = NB + NEPI + 1;   // B loader warp (adjoint: + W loader warp after it)
+  constexpr int WLOAD = NB + NEPI + 1;   // B loader warp; W loader warp after it
   const Geo& g = a.g;
   float rr = 0.f;
   if (a.mode == 1) {
@@ -288,8 +303,8 @@ icnnm_tc_kernel(TcArgs a) {
   const uint32_t a_col0 = 2u * static_cast<uint32_t>(a.accw);
   float* Bst = reinterpret_cast<float*>(p);
   p += sbn * B_STAGE_BYTES;
-  float* Wst = reinterpret_cast<float*>(p);   // adjoint: W-chunk ring
-  if (!FWD) p += wsn * W_STAGE_BYTES;
+  float* Wst = reinterpret_cast<float*>(p);   // adjoint: W-chunk ring; forward: W-group ring
+  p += wsn * (FWD ? WO_STAGE_BYTES : W_STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p);
   uint64_t* A_full = bars;
   uint64_t* A_empty = bars + SA;
@@ -311,11 +326,10 @@ icnnm_tc_kernel(TcArgs a) {
   p += ((g.kp * 4 + 15) / 16) * 16;
   const int nob = g.HH * g.HW * g.HT;
   const int nobp = ((nob + 3) / 4) * 4;
-  // FWD: halo[2] (2 x nobp) | red (8 x 32 x 33) | nrm (kp doubles)
+  // FWD: halo[2] (2 x nobp) | nrm (kp doubles)
   // ADJ: 4 output bricks (4 x nobp)
   float* halo = reinterpret_cast<float*>(p);
-  float* red = halo + 2 * nobp;
-  double* nrm = reinterpret_cast<double*>(red + NEPI * 32 * 33);
+  double* nrm = reinterpret_cast<double*>(halo + 2 * nobp);
   float* ob = reinterpret_cast<float*>(p);
 
   const int tid = threadIdx.x;
@@ -342,7 +356,7 @@ icnnm_tc_kernel(TcArgs a) {
     }
     for (int i = 0; i < WS; ++i) {
       mbar_init(W_full + i, 1);
-      mbar_init(W_empty + i, nbuild);
+      mbar_init(W_empty + i, FWD ? 4 * 32 : nbuild);  // forward: the half's 4 epilogue warps
     }
     for (int i = 0; i < NSC; ++i) mbar_init(SC_full + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -540,31 +554,16 @@ icnnm_tc_kernel(TcArgs a) {
     const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
     const int obs = nobp + 32;             // output-brick stride (+32 scratch)
     float* myob = ob + quad * obs;
-    float* myred = red + ew * 32 * 33;
     constexpr int NHALF = NEPI / 4;
+    uint32_t gbase = 0;  // forward: W-group ring slot of the current tile's first group
     float gacc = 0.f;  // mode 2: this thread's share of ||(1-c)W - A(L)K||^2
     uint32_t tcount = 0;
     Dbg dbg(lane == 0 ? a.dbg : nullptr);
     float us_adj = 1.f;  // F16x3 adjoint: 2^-(eA + eB)
     if (F16 && !FWD)
       us_adj = a.bunscale / f16_scale(a.mode >= 1 ? static_cast<float>(a.st->adj_amax) : a.amax);
-    // forward modes 1/2 read W_old: stream each brick's contiguous W block
-    // (kp x 128 floats) into L2 one brick ahead so the epilogue's loads hit L2
-    const bool pf = FWD && a.mode >= 1 && ew == 0 && lane == 0 && !(a.skip & 64);
-    auto prefetch_w = [&](int bb) {
-      if (bb >= nbr) return;
-      const char* base = reinterpret_cast<const char*>(a.Wout + static_cast<size_t>(bb) * g.kp * 128);
-      const uint32_t total = static_cast<uint32_t>(g.kp) * 128u * 4u;
-      for (uint32_t off = 0; off < total; off += 32768u) {
-        const uint32_t sz = total - off < 32768u ? total - off : 32768u;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(base + off), "r"(sz)
-                     : "memory");
-      }
-    };
-    if (pf) prefetch_w(blockIdx.x);
     uint32_t biter = 0;
     for (int b = blockIdx.x; b < nbr; b += gridDim.x, ++biter) {
-      if (pf) prefetch_w(b + gridDim.x);
       int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
       const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
       const bool valid = (h0 + vh < g.H) && (w0 + vw < g.W) && (t0 + vt < g.T);
@@ -582,83 +581,92 @@ icnnm_tc_kernel(TcArgs a) {
         mbar_wait(ACC_full + acc, ph);
         tc_fence_after();
         long long t1c = dbg.p ? clk() : 0;
-        for (int c0 = 32 * half; c0 < wn && !(a.skip & 2); c0 += 32 * NHALF) {
-          uint32_t u[32];
-          tmem_ld32(tbase + lane_base + acc * a.accw + c0, u);
-          tmem_wait_ld();
-          const int ncol = (wn - c0) < 32 ? (wn - c0) : 32;
-          // accumulator -> fp32 product (F16x3: undo the operand scales)
-          auto accv = [&](int i) { return F16 ? __uint_as_float(u[i]) * us : __uint_as_float(u[i]); };
-          if (FWD && a.mode == 2) {
-            const int j0 = nt * a.wbase + c0;
-            const float* wp = a.Wout + (static_cast<size_t>(b) * g.kp + j0) * 128 + row;
-            float wo[32];
+        if (FWD) {
+          // forward: the W group (32 columns x 128 rows) is staged in SMEM by
+          // the W loader (mode 1/2: W_old), updated in place, reduced for the
+          // column norms and written back with one bulk store
+          const int ng = (wn + 31) / 32, ngp = ng + (ng & 1);  // even: one half per stage
+          for (int gq = half; gq < ngp; gq += 2) {
+            const uint32_t gsl = gbase + gq;
+            const int wsl = static_cast<int>(gsl % wsn);
+            mbar_wait(W_full + wsl, (gsl / wsn) & 1);
+            if (gq < ng && !(a.skip & 2)) {
+              const int c0 = 32 * gq;
+              const int ncol = (wn - c0) < 32 ? (wn - c0) : 32;
+              const int j0 = nt * a.wbase + c0;
+              float* st = Wst + wsl * (WO_STAGE_BYTES / 4);
+              uint32_t u[32];
+              tmem_ld32(tbase + lane_base + acc * a.accw + c0, u);
+              tmem_wait_ld();
+              auto accv = [&](int i) {
+                return F16 ? __uint_as_float(u[i]) * us : __uint_as_float(u[i]);
+              };
+              if (a.mode == 2) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) wo[i] = (i < ncol) ? wp[static_cast<size_t>(i) * 128] : 0.f;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float gap = (1.f - cs[j0 + i]) * wo[i] - accv(i);
-              gacc = (i < ncol && valid) ? fmaf(gap, gap, gacc) : gacc;
-            }
-          } else if (FWD) {
-            const int j0 = nt * a.wbase + c0;
-            float* wp = a.Wout + (static_cast<size_t>(b) * g.kp + j0) * 128 + row;
-            if (ncol == 32 && bfull) {
-              // fast path (whole brick inside the tensor, full 32 columns):
-              // W = acc (* us) + (r c_j) W_old, r c_j read 4 at a time
-              float w[32];
-              if (a.mode == 1) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) w[i] = wp[static_cast<size_t>(i) * 128];
-                const float4* c4 = reinterpret_cast<const float4*>(cs + j0);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  const float4 cc = c4[q];
-                  const float cq[4] = {cc.x, cc.y, cc.z, cc.w};
-#pragma unroll
-                  for (int r4 = 0; r4 < 4; ++r4) {
-                    const int i = 4 * q + r4;
-                    w[i] = F16 ? fmaf(__uint_as_float(u[i]), us, cq[r4] * w[i])
-                               : fmaf(cq[r4], w[i], __uint_as_float(u[i]));
-                  }
+                for (int i = 0; i < 32; ++i) {
+                  const float gap = (1.f - cs[j0 + i]) * st[i * 128 + row] - accv(i);
+                  gacc = (i < ncol && valid) ? fmaf(gap, gap, gacc) : gacc;
                 }
               } else {
+                if (ncol == 32 && bfull) {
+                  const float4* c4 = reinterpret_cast<const float4*>(cs + j0);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) w[i] = accv(i);
-              }
+                  for (int q = 0; q < 8; ++q) {
+                    const float4 cc = c4[q];
+                    const float cq[4] = {cc.x, cc.y, cc.z, cc.w};
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                wp[static_cast<size_t>(i) * 128] = w[i];
-                myred[i * 33 + lane] = w[i];
-              }
-            } else {
-              // general path: W_old loads issued together as predicated loads
-              // (a load inside the compute loop becomes a branch per element and
-              // serialises 32 HBM round trips)
-              float wo[32];
-              if (a.mode == 1) {
+                    for (int r4 = 0; r4 < 4; ++r4) {
+                      const int i = 4 * q + r4;
+                      float w = accv(i);
+                      if (a.mode == 1) w = fmaf(cq[r4], st[i * 128 + row], w);
+                      st[i * 128 + row] = w;
+                    }
+                  }
+                } else {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) wo[i] = (i < ncol) ? wp[static_cast<size_t>(i) * 128] : 0.f;
-              }
+                  for (int i = 0; i < 32; ++i) {
+                    float w = accv(i);
+                    if (a.mode == 1) w = fmaf(cs[j0 + i], st[i * 128 + row], w);
+                    st[i * 128 + row] = (valid && i < ncol) ? w : 0.f;
+                  }
+                }
+                fence_proxy_async_smem();   // the bulk store reads these writes
+                named_sync(3 + half, 128);
+                // column norms: thread t of the half sums a quarter column
+                const int t = quad * 32 + lane;
+                const int col = t >> 2, qr = t & 3;
+                const float4* p4 = reinterpret_cast<const float4*>(st + col * 128 + qr * 32);
+                float sq = 0.f;
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                float w = accv(i);
-                if (a.mode == 1) w = fmaf(cs[j0 + i], wo[i], w);
-                w = (valid && i < ncol) ? w : 0.f;
-                if (i < ncol) wp[static_cast<size_t>(i) * 128] = w;
-                myred[i * 33 + lane] = w;
+                for (int k4 = 0; k4 < 8; ++k4) {
+                  const float4 v = p4[k4];
+                  sq = fmaf(v.x, v.x, sq);
+                  sq = fmaf(v.y, v.y, sq);
+                  sq = fmaf(v.z, v.z, sq);
+                  sq = fmaf(v.w, v.w, sq);
+                }
+                sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+                sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+                if (qr == 0 && col < ncol) atomicAdd(nrm + j0 + col, static_cast<double>(sq));
+                if (t == 0) {
+                  bulk_s2g(a.Wout + (static_cast<size_t>(b) * g.kp + j0) * 128, st,
+                           static_cast<uint32_t>(ncol) * 512u);
+                  bulk_wait_read();  // the stage may be refilled after this
+                }
               }
             }
-            __syncwarp();
-            float sq = 0.f;
-#pragma unroll 8
-            for (int i = 0; i < 32; ++i) {
-              const float x = myred[lane * 33 + i];
-              sq = fmaf(x, x, sq);
-            }
-            __syncwarp();
-            if (lane < ncol) atomicAdd(nrm + j0 + lane, static_cast<double>(sq));
-          } else {
+            mbar_arrive(W_empty + wsl);
+          }
+          gbase += static_cast<uint32_t>(ngp);
+        } else {
+          for (int c0 = 32 * half; c0 < wn && !(a.skip & 2); c0 += 32 * NHALF) {
+            uint32_t u[32];
+            tmem_ld32(tbase + lane_base + acc * a.accw + c0, u);
+            tmem_wait_ld();
+            const int ncol = (wn - c0) < 32 ? (wn - c0) : 32;
+            auto accv = [&](int i) {
+              return F16 ? __uint_as_float(u[i]) * us : __uint_as_float(u[i]);
+            };
             const int s0 = nt * a.wbase + c0;
             if (g.kh >= 4) {
               // batches of 4 consecutive N columns = 4 distinct sh: no hazards
@@ -722,6 +730,7 @@ icnnm_tc_kernel(TcArgs a) {
       }
     }
     dbg.flush(DBG_EPI_WAIT, DBG_EPI_WORK);
+    if (FWD && quad == 0 && lane == 0) bulk_wait_all();  // W stores complete before exit
     if (FWD && a.mode == 2) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, o);
@@ -822,6 +831,35 @@ icnnm_tc_kernel(TcArgs a) {
         }
       }
       if (a.dbg) atomicAdd(a.dbg + DBG_LOAD_WAIT, static_cast<unsigned long long>(wl));
+    }
+    __syncwarp();
+  } else if (FWD && warp == WLOAD + 1) {
+    if (lane == 0) {
+      // forward: stream W groups (32 columns x 128 rows, 16 KB contiguous in
+      // the [brick][j][row] layout) into the ring ahead of the epilogue; mode 0
+      // has no W_old (the slot is only handed over).  Tiles are padded to an
+      // even number of groups so that each stage serves one epilogue half.
+      uint32_t gs = 0;
+      for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+        for (int nt = 0; nt < ntn; ++nt) {
+          const int wn = tile_width(a, nt);
+          const int ng = (wn + 31) / 32, ngp = ng + (ng & 1);
+          for (int gq = 0; gq < ngp; ++gq, ++gs) {
+            const int wsl = static_cast<int>(gs % wsn);
+            mbar_wait(W_empty + wsl, ((gs / wsn) & 1) ^ 1);
+            if (gq < ng && a.mode >= 1 && !(a.skip & 2)) {
+              const int ncol = (wn - 32 * gq) < 32 ? (wn - 32 * gq) : 32;
+              const uint32_t bytes = static_cast<uint32_t>(ncol) * 512u;
+              mbar_arrive_expect_tx(W_full + wsl, bytes);
+              bulk_g2s(reinterpret_cast<uint8_t*>(Wst) + wsl * WO_STAGE_BYTES,
+                       a.Wout + (static_cast<size_t>(b) * g.kp + nt * a.wbase + 32 * gq) * 128,
+                       bytes, W_full + wsl);
+            } else {
+              mbar_arrive(W_full + wsl);
+            }
+          }
+        }
+      }
     }
     __syncwarp();
   } else if (!FWD && warp == WLOAD + 1) {

@@ -15,7 +15,8 @@ constexpr int SA = 6;                          // TMEM A stages (max; runtime a.
 constexpr int NSC = 8;                         // F16x3 forward: per-brick scale ring
 constexpr int SB = 6;                          // SMEM B stages (max; runtime a.sb)
 constexpr int WS = 4;                          // adjoint: SMEM W-chunk stages (max; runtime a.ws)
-constexpr int W_STAGE_BYTES = 128 * KC * 4;    // 8 KB: 16 columns x 128 rows
+constexpr int W_STAGE_BYTES = 128 * KC * 4;    // adjoint: 8 KB W chunk, 16 columns x 128 rows
+constexpr int WO_STAGE_BYTES = 128 * 32 * 4;   // forward: 16 KB W group, 32 columns x 128 rows
 constexpr int NTMAX = 208;                     // max accumulator width (N per tile)
 constexpr int B_STAGE_BYTES = 256 * KC * 4 * 2;    // hi + lo, up to 256 rows = 32 KB
 
@@ -57,16 +58,17 @@ __global__ void icnnm_tc_kernel(TcArgs a);
 void* fwd_kernel_ptr(bool f16);
 void* adj_kernel_ptr(bool f16);
 
-inline int threads(bool fwd) { return fwd ? 576 : 480; }
+inline int threads(bool fwd) { return fwd ? 608 : 480; }
 
 inline size_t smem_bytes(const Geo& g, bool fwd, int sb = SB, int ws = WS) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
   const size_t nobp = ((nob + 3) / 4) * 4;
-  size_t b = static_cast<size_t>(sb) * B_STAGE_BYTES + (fwd ? 0 : static_cast<size_t>(ws) * W_STAGE_BYTES) + 512 + 16;
+  size_t b = static_cast<size_t>(sb) * B_STAGE_BYTES +
+             static_cast<size_t>(ws) * (fwd ? WO_STAGE_BYTES : W_STAGE_BYTES) + 512 + 16;
   b += ((g.ktp * 4 + 15) / 16) * 16;
   b += ((g.kp * 4 + 15) / 16) * 16;
   if (fwd)
-    b += 2 * nobp * 4 + 8 * 32 * 33 * 4 + static_cast<size_t>(g.kp) * 8;
+    b += 2 * nobp * 4 + static_cast<size_t>(g.kp) * 8;
   else
     b += 4 * (nobp + 32) * 4;
   return b;

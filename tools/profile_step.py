@@ -6,7 +6,7 @@ from paper_2604_17001_b200 import synth
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
-ap.add_argument("--engine", default="tf32x3")
+ap.add_argument("--engine", default="f16x3")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--runs", type=int, default=1)
 a = ap.parse_args()
