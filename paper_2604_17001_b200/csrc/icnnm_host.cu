@@ -204,10 +204,29 @@ TcPlan tc_plan(const Problem& p, bool f16 = false) {
   return best;
 }
 
+// tcgen05 engine geometry.  When T is a multiple of 32 the brick is
+// 2 x 2 x 32 so that each warp's 32 TMEM lanes are 32 consecutive t: the
+// builders' halo gathers and the adjoint's col2im scatter then hit 32
+// consecutive words (conflict-free) instead of two 16-runs one halo row apart.
 Geo tc_geo(const Geo& g, const TcPlan& t) {
   Geo q = g;
   q.kp = t.kp;
   q.ktp = t.kp;
+  static const bool bt32 = [] {
+    const char* e = std::getenv("ICNNM_TC_BT32");  // A/B experiments only
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (bt32 && g.T % 32 == 0 && g.W >= 2 && g.H >= 2) {
+    q.bt = 32;
+    q.bw = 2;
+    q.bh = BM / (q.bt * q.bw);
+    q.nbh = (q.H + q.bh - 1) / q.bh;
+    q.nbw = (q.W + q.bw - 1) / q.bw;
+    q.nbt = (q.T + q.bt - 1) / q.bt;
+    q.HH = q.bh + q.kh - 1;
+    q.HW = q.bw + q.kw - 1;
+    q.HT = q.bt + q.kt - 1;
+  }
   return q;
 }
 

@@ -632,22 +632,21 @@ icnnm_tc_kernel(TcArgs a) {
                 }
                 fence_proxy_async_smem();   // the bulk store reads these writes
                 named_sync(3 + half, 128);
-                // column norms: thread t of the half sums a quarter column
-                const int t = quad * 32 + lane;
-                const int col = t >> 2, qr = t & 3;
-                const float4* p4 = reinterpret_cast<const float4*>(st + col * 128 + qr * 32);
+                // column norms: lane l sums column l over this warp's 32 rows
+                // (float4 index rotated by lane: conflict-free, 4 wavefronts per
+                // load); the 4 warps of the half add their partials
+                const float* colp = st + lane * 128 + quad * 32;
                 float sq = 0.f;
 #pragma unroll
                 for (int k4 = 0; k4 < 8; ++k4) {
-                  const float4 v = p4[k4];
+                  const float4 v = *reinterpret_cast<const float4*>(colp + ((k4 + lane) & 7) * 4);
                   sq = fmaf(v.x, v.x, sq);
                   sq = fmaf(v.y, v.y, sq);
                   sq = fmaf(v.z, v.z, sq);
                   sq = fmaf(v.w, v.w, sq);
                 }
-                sq += __shfl_xor_sync(0xffffffffu, sq, 1);
-                sq += __shfl_xor_sync(0xffffffffu, sq, 2);
-                if (qr == 0 && col < ncol) atomicAdd(nrm + j0 + col, static_cast<double>(sq));
+                if (lane < ncol) atomicAdd(nrm + j0 + lane, static_cast<double>(sq));
+                const int t = quad * 32 + lane;
                 if (t == 0) {
                   bulk_s2g(a.Wout + (static_cast<size_t>(b) * g.kp + j0) * 128, st,
                            static_cast<uint32_t>(ncol) * 512u);

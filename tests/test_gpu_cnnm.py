@@ -135,6 +135,8 @@ def test_cli_cnnm_matches_api(gpu, tmp_path):
     L = pio.read_tnsr(str(tmp_path / "L.tnsr"))
     rep = json.loads((tmp_path / "rep.json").read_text())
     Lp, rp = gpu.cnnm_solve(X * mask, mask, w.kernel, gpu.SolverConfig(max_iters=30, **FIXED))
-    np.testing.assert_array_equal(L, Lp)
+    # cuBLAS / cuSOLVER are not bit-reproducible across processes (algorithm
+    # selection), so the CLI and the in-process call agree to fp64 rounding
+    np.testing.assert_allclose(L, Lp, rtol=1e-12, atol=1e-14)
     assert rep["iterations"] == 30
     np.testing.assert_allclose(rep["objective"], rp.objective, rtol=1e-12)
