@@ -204,17 +204,20 @@ TcPlan tc_plan(const Problem& p, bool f16 = false) {
   return best;
 }
 
-// tcgen05 engine geometry.  When T is a multiple of 32 the brick is
-// 2 x 2 x 32 so that each warp's 32 TMEM lanes are 32 consecutive t: the
-// builders' halo gathers and the adjoint's col2im scatter then hit 32
-// consecutive words (conflict-free) instead of two 16-runs one halo row apart.
+// tcgen05 engine geometry.  ICNNM_TC_BT32=1 (experiment, off by default)
+// uses 2 x 2 x 32 bricks when T is a multiple of 32, so that each warp's 32
+// TMEM lanes are 32 consecutive t: halo gathers and the adjoint's col2im
+// scatter become conflict-free (SMEM bank conflicts -65% / -83%), but the
+// larger halo (3600 vs 2400 words per brick at config 2) and output-brick
+// flush cost more than the conflicts did (forward +7%, adjoint +14%;
+// profiles/README_r1.md).
 Geo tc_geo(const Geo& g, const TcPlan& t) {
   Geo q = g;
   q.kp = t.kp;
   q.ktp = t.kp;
   static const bool bt32 = [] {
-    const char* e = std::getenv("ICNNM_TC_BT32");  // A/B experiments only
-    return !(e && std::atoi(e) == 0);
+    const char* e = std::getenv("ICNNM_TC_BT32");
+    return e && std::atoi(e) == 1;
   }();
   if (bt32 && g.T % 32 == 0 && g.W >= 2 && g.H >= 2) {
     q.bt = 32;
