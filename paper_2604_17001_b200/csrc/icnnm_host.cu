@@ -344,6 +344,11 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
     return e ? std::atoi(e) : 0;
   }();
   a.bsplit = bsplit_env;
+  static const int bpair_env = [] {
+    const char* e = std::getenv("ICNNM_TC_BPAIR");  // A/B experiments
+    return e ? std::atoi(e) : 0;
+  }();
+  a.bpair = bpair_env;
   a.g = gtc;
   a.src = src;
   a.Win = W;

@@ -436,6 +436,10 @@ icnnm_tc_kernel(TcArgs a) {
     }
     // F16x3 operand scale: forward per brick (the halo is prescaled in place);
     // adjoint: folded into cs
+    // (the held chunk c and the next owned chunk c+2 must use different A and
+    // W stages: sa >= 3 always; the adjoint's W ring needs 4)
+    const bool pair = (F16 || !a.bsplit) && a.bpair && san >= 3 && (FWD || wsn >= 4);
+    int pend_sa = -1, pend_wsi = 0;
     int iter = 0;
     for (int b = blockIdx.x; b < nbr; b += gridDim.x, ++iter) {
       float* hcur = halo + (iter & 1) * nobp;
@@ -480,6 +484,19 @@ icnnm_tc_kernel(TcArgs a) {
           long long t1c = dbg.p ? clk() : 0;
           if (!(a.skip & 1)) {
             const uint32_t col = a_col0 + sa * ASC;
+            // the chunk's 16 tap offsets (forward) or c_j factors (adjoint), 4 vector loads
+            int tq[KC];
+            float cq[KC];
+#pragma unroll
+            for (int v4 = 0; v4 < KC / 4; ++v4) {
+              if (FWD) {
+                const int4 t4 = reinterpret_cast<const int4*>(tapoff + kc * KC)[v4];
+                tq[4 * v4] = t4.x; tq[4 * v4 + 1] = t4.y; tq[4 * v4 + 2] = t4.z; tq[4 * v4 + 3] = t4.w;
+              } else {
+                const float4 c4 = reinterpret_cast<const float4*>(cs + kc * KC)[v4];
+                cq[4 * v4] = c4.x; cq[4 * v4 + 1] = c4.y; cq[4 * v4 + 2] = c4.z; cq[4 * v4 + 3] = c4.w;
+              }
+            }
             if (F16) {
               // 16 K values -> 8 f16x2 words hi | 8 words lo (element 2i in the low half)
               uint32_t hi[8], lo[8];
@@ -488,9 +505,8 @@ icnnm_tc_kernel(TcArgs a) {
                 float x[2];
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                  const int q = kc * KC + 2 * i + u;
-                  x[u] = FWD ? hcur[hidx - tapoff[q]]
-                             : Wst[wsi * (W_STAGE_BYTES / 4) + (2 * i + u) * 128 + row] * cs[q];
+                  x[u] = FWD ? hcur[hidx - tq[2 * i + u]]
+                             : Wst[wsi * (W_STAGE_BYTES / 4) + (2 * i + u) * 128 + row] * cq[2 * i + u];
                 }
                 hi[i] = pack_f16x2(x[0], x[1]);
                 float h0, h1;
@@ -518,9 +534,8 @@ icnnm_tc_kernel(TcArgs a) {
                 uint32_t hi[8], lo[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                  const int q = kc * KC + 8 * hh + i;
-                  const float x = FWD ? hcur[hidx - tapoff[q]]
-                                      : Wst[wsi * (W_STAGE_BYTES / 4) + (8 * hh + i) * 128 + row] * cs[q];
+                  const float x = FWD ? hcur[hidx - tq[8 * hh + i]]
+                                      : Wst[wsi * (W_STAGE_BYTES / 4) + (8 * hh + i) * 128 + row] * cq[8 * hh + i];
                   const uint32_t h = f2tf32(x);
                   hi[i] = h;
                   lo[i] = __float_as_uint(x - __uint_as_float(h));
@@ -529,17 +544,42 @@ icnnm_tc_kernel(TcArgs a) {
                 tmem_st8(tbase + lane_base + col + 8 * hh + KC, lo);
               }
             }
-            tmem_wait_st();
+            if (!pair) tmem_wait_st();
           }
-          tc_fence_before();
-          mbar_arrive(A_full + sa);
-          if (!FWD) mbar_arrive(W_empty + wsi);
+          if (pair) {
+            // pairing: hand over the previous owned chunk together with this
+            // one after a single wait::st (its store latency overlapped this
+            // chunk's gathers); the last chunk of a brick is flushed below
+            if (pend_sa >= 0) {
+              if (!(a.skip & 1)) tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(A_full + pend_sa);
+              if (!FWD) mbar_arrive(W_empty + pend_wsi);
+              mbar_arrive(A_full + sa);
+              if (!FWD) mbar_arrive(W_empty + wsi);
+              pend_sa = -1;
+            } else {
+              pend_sa = sa;
+              pend_wsi = wsi;
+            }
+          } else {
+            tc_fence_before();
+            mbar_arrive(A_full + sa);
+            if (!FWD) mbar_arrive(W_empty + wsi);
+          }
           if (dbg.p) {
             long long t2c = clk();
             dbg.acc[0] += t1c - t0c;
             dbg.acc[1] += t2c - t1c;
           }
         }
+      }
+      if (pair && pend_sa >= 0) {  // flush the brick's last owned chunk
+        if (!(a.skip & 1)) tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(A_full + pend_sa);
+        if (!FWD) mbar_arrive(W_empty + pend_wsi);
+        pend_sa = -1;
       }
     }
     dbg.flush(DBG_BUILD_WAIT, DBG_BUILD_WORK);

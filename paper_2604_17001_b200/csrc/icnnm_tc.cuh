@@ -46,6 +46,7 @@ struct TcArgs {
                             // (16 columns each); 1 = both groups split every chunk (TF32x3)
   float bunscale;           // F16x3: 2^-eB, the inverse of the power-of-2 scale of B
   float amax;               // F16x3 adjoint, mode 0: bound on |W| (mode 1: st->adj_amax)
+  int bpair;                // builders hand over owned chunks in pairs (one wait::st)
 };
 
 // dbg slots (cycles summed over CTAs)
