@@ -12,6 +12,8 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libicnnm_b200.so")
+# A/B kernel experiments only: load another build of the same C ABI
+LIB_PATH = os.environ.get("ICNNM_LIB_AB") or LIB_PATH
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "icnnm_b200.h")
 
 ICNNM_OK = 0

@@ -17,6 +17,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "../../include/icnnm_b200.h"
@@ -365,13 +366,38 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   a.wbase = t.wbase;
   a.accw = t.wbase;
   a.sa = t.sa;
+  // Tile groups (icnnm_tc.cu tg_seq): pairs of N-tiles share every built A
+  // chunk (half the A-operand builds and, in the adjoint, half the W-chunk
+  // loads).  The skew needs spare A stages beyond D, so it is used only when
+  // the plan leaves at least 4 (F16x3 at k = 405: 6 stages).  Measured on the
+  // same box (config 2, profiles/ab_r1/README.md): the adjoint gains (0.76 ->
+  // 0.73 ms), the forward loses (0.70 -> 0.77 ms: its heavier epilogue is no
+  // longer hidden behind the other tile's MMAs), so only the adjoint pairs.
+  // ICNNM_TC_GRP / ICNNM_TC_SKEW override both kernels for A/B experiments.
+  static const int grp_env = [] {
+    const char* e = std::getenv("ICNNM_TC_GRP");
+    return e ? std::atoi(e) : -1;
+  }();
+  static const int skew_env = [] {
+    const char* e = std::getenv("ICNNM_TC_SKEW");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool can_pair = t.ntn >= 2 && t.sa >= 4;
+  a.grp = grp_env >= 0 ? grp_env : ((can_pair && !fwd) ? 2 : 1);
+  a.skew = skew_env >= 0 ? skew_env : std::max(0, t.sa - 2);
   // deepest (B, W) stage counts that fit in shared memory (227 KB opt-in).
   // W depth is even: the two builder groups own alternate K-chunks, so with an
   // even ring each W stage is only ever consumed by one group.  With an odd
   // ring consecutive uses of a stage alternate between groups, and a group
   // running two uses ahead (possible with F16x3's 6 A stages) would pass its
   // parity wait on the previous fill.
-  static const int pri[][2] = {{6, 4}, {5, 4}, {4, 4}, {3, 4}, {4, 2}, {3, 2}, {2, 2}};
+  // F16x3 B stages are 16 KB (half the TF32 stage), which leaves room for
+  // an 8-deep forward W-group ring: a 208-column tile has 8 W groups, so the
+  // whole tile's W_old is in flight before its epilogue starts.
+  static const std::vector<std::array<int, 2>> pri_tf32 = {{6, 4}, {5, 4}, {4, 4}, {3, 4},
+                                                            {4, 2}, {3, 2}, {2, 2}};
+  static const std::vector<std::array<int, 2>> pri_f16 = {{6, 8}, {4, 8}, {4, 6}, {4, 4},
+                                                           {3, 4}, {4, 2}, {3, 2}, {2, 2}};
   static const int sb_cap = [] {
     // 4 B stages measured faster than 5-6 (more SMEM leaves less L1):
     // profiles/README_r1.md; ICNNM_TC_SB overrides for A/B experiments
@@ -380,9 +406,13 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   }();
   a.sb = 2;
   a.ws = 2;
-  for (const auto& c : pri) {
-    if (c[0] > sb_cap) continue;
-    if (icnnm_dev::tc::smem_bytes(gtc, fwd, c[0], c[1]) <= 227 * 1024) {
+  static const int ws_cap = [] {
+    const char* e = std::getenv("ICNNM_TC_WS");  // A/B experiments
+    return e ? std::atoi(e) : icnnm_dev::tc::WS;
+  }();
+  for (const auto& c : (t.f16 ? pri_f16 : pri_tf32)) {
+    if (c[0] > sb_cap || c[1] > ws_cap) continue;
+    if (icnnm_dev::tc::smem_bytes(gtc, fwd, c[0], c[1], t.f16) <= 227 * 1024) {
       a.sb = c[0];
       a.ws = c[1];
       break;
@@ -394,7 +424,7 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.nbricks, nsm));
   void* args[] = {&a};
-  const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws);
+  const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16);
   if (smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
   CK(cudaLaunchKernel(fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16) : icnnm_dev::tc::adj_kernel_ptr(t.f16),
                       dim3(grid), dim3(icnnm_dev::tc::threads(fwd)), args, smem, stream));
@@ -521,8 +551,8 @@ void solver_alloc(Solver& S) {
     s.L.alloc(s.m_own);
     s.V.alloc(s.m_own);
     s.gtc = tc_geo(s.g, S.tp);
-    check_smem(icnnm_dev::tc::smem_bytes(s.gtc, true, 2, 2));
-    check_smem(icnnm_dev::tc::smem_bytes(s.gtc, false, 2, 2));
+    check_smem(icnnm_dev::tc::smem_bytes(s.gtc, true, 2, 2, false));
+    check_smem(icnnm_dev::tc::smem_bytes(s.gtc, false, 2, 2, false));
     s.W.alloc(std::max<int64_t>(n_bricks(s.g) * BM * p.kp, tc_w_elems(s.gtc, S.tp)));
     CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
   }
@@ -730,36 +760,6 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
 
   S.theta.alloc(iters + 1);
   S.stats.alloc(iters);
-  CK(cudaEventRecord(S.evs, S.stream));
-  CK(cudaMemcpyAsync(S.theta.p, th.data(), th.size() * sizeof(double), cudaMemcpyHostToDevice,
-                     S.stream));
-  CK(cudaMemsetAsync(S.stats.p, 0, S.stats.bytes(), S.stream));
-  CK(cudaMemsetAsync(S.red.p, 0, S.red.bytes(), S.stream));
-  IterState st0{};
-  st0.active = 1;
-  st0.max_iters = iters;
-  CK(cudaMemcpyAsync(S.st.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, S.stream));
-  S.launches = 0;
-  if (S.tc_counters) {
-    if (!S.dbg.p) S.dbg.alloc(2 * icnnm_dev::tc::DBG_SLOTS);
-    CK(cudaMemsetAsync(S.dbg.p, 0, S.dbg.bytes(), S.stream));
-  }
-
-  const int64_t WT = p.dims[1] * p.dims[2];
-  for (auto& s : S.slabs) {
-    const int64_t off = s.row0 * WT;
-    icnnm_dev::icnnm_setup<<<grid_for(s.m_own, 256), 256, 0, S.stream>>>(
-        s.m_own, S.Mstage.p + off, S.maskstage.p + off, cfg.init_fill == ICNNM_INIT_MEAN,
-        mean, s.pm.p, s.mask.p, s.L.p, s.V.p, s.Lt.p + s.halo_elems);
-    CKL();
-    ++S.launches;
-    CK(cudaMemsetAsync(s.W.p, 0, s.W.bytes(), S.stream));
-    CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
-  }
-  exchange_lt(S);
-  for (auto& s : S.slabs) launch_fwd(S, s, 0);
-  allreduce_red(S);
-
   // One ADMM iteration as a graph: coef -> adjoint -> update -> forward.
   const double floor_rel = 1e-5;
   auto iteration = [&]() {
@@ -785,6 +785,54 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     for (auto& s : S.slabs) launch_fwd(S, s, 1);
     allreduce_red(S);
   };
+
+
+  // Capture U iterations per graph so the device never waits on the host
+  // between iterations; replays past max_iters are no-ops (coef deactivates).
+  // Capture and instantiation are host work: they happen before the run's
+  // first event so that the device time of the solve never includes them.
+  const int U = std::min(iters, 32);
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t per_iter = 0;
+  if (S.tc_counters && !S.dbg.p) S.dbg.alloc(2 * icnnm_dev::tc::DBG_SLOTS);  // captured pointer
+  IterState* hst = nullptr;
+  if (!S.profile) {
+    CK(cudaMallocHost(&hst, sizeof(IterState)));
+    const int64_t before = S.launches;
+    CK(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeThreadLocal));
+    for (int u = 0; u < U; ++u) iteration();
+    CK(cudaStreamEndCapture(S.stream, &graph));
+    per_iter = (S.launches - before) / U + 1 /*coef*/ +
+               static_cast<int64_t>(S.slabs.size()) /*update*/;
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+  }
+  CK(cudaEventRecord(S.evs, S.stream));
+  CK(cudaMemcpyAsync(S.theta.p, th.data(), th.size() * sizeof(double), cudaMemcpyHostToDevice,
+                     S.stream));
+  CK(cudaMemsetAsync(S.stats.p, 0, S.stats.bytes(), S.stream));
+  CK(cudaMemsetAsync(S.red.p, 0, S.red.bytes(), S.stream));
+  IterState st0{};
+  st0.active = 1;
+  st0.max_iters = iters;
+  CK(cudaMemcpyAsync(S.st.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, S.stream));
+  S.launches = 0;
+  if (S.tc_counters) CK(cudaMemsetAsync(S.dbg.p, 0, S.dbg.bytes(), S.stream));
+
+  const int64_t WT = p.dims[1] * p.dims[2];
+  for (auto& s : S.slabs) {
+    const int64_t off = s.row0 * WT;
+    icnnm_dev::icnnm_setup<<<grid_for(s.m_own, 256), 256, 0, S.stream>>>(
+        s.m_own, S.Mstage.p + off, S.maskstage.p + off, cfg.init_fill == ICNNM_INIT_MEAN,
+        mean, s.pm.p, s.mask.p, s.L.p, s.V.p, s.Lt.p + s.halo_elems);
+    CKL();
+    ++S.launches;
+    CK(cudaMemsetAsync(s.W.p, 0, s.W.bytes(), S.stream));
+    CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
+  }
+  exchange_lt(S);
+  for (auto& s : S.slabs) launch_fwd(S, s, 0);
+  allreduce_red(S);
 
   const int64_t setup_launches = S.launches;
   CK(cudaEventRecord(S.ev0, S.stream));
@@ -831,22 +879,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     S.prof_ms[3] = acc[3] / iters;
     for (auto& x : e) cudaEventDestroy(x);
   } else {
-    // Capture U iterations per graph so the device never waits on the host
-    // between iterations; replays past max_iters are no-ops (coef deactivates).
-    const int U = std::min(iters, 32);
-    cudaGraph_t graph;
-    cudaGraphExec_t exec;
-    const int64_t before = S.launches;
-    CK(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeThreadLocal));
-    for (int u = 0; u < U; ++u) iteration();
-    CK(cudaStreamEndCapture(S.stream, &graph));
-    const int64_t per_iter = (S.launches - before) / U + 1 /*coef*/ +
-                             static_cast<int64_t>(S.slabs.size()) /*update*/;
-    S.launches = before;
-    CK(cudaGraphInstantiate(&exec, graph, 0));
     const bool may_stop = !(cfg.tol_primal <= 1e-200 && cfg.tol_change <= 1e-200);
-    IterState* hst = nullptr;
-    CK(cudaMallocHost(&hst, sizeof(IterState)));
     for (int it = 0; it < iters; it += U) {
       CK(cudaGraphLaunch(exec, S.stream));
       S.launches += per_iter * std::min(U, iters - it);
@@ -1118,7 +1151,7 @@ int icnnm_cuda_conv_forward_ex(int order, const int64_t* dims, const double* L,
     if (is_tc(engine)) {
       TcPlan t = tc_plan(p, engine == ICNNM_ENGINE_F16X3);
       Geo gt = tc_geo(g, t);
-      check_smem(icnnm_dev::tc::smem_bytes(gt, true, 2, 2));
+      check_smem(icnnm_dev::tc::smem_bytes(gt, true, 2, 2, t.f16));
       auto bf = pack_b_tiles(p, t, K_colmajor, true);
       DBuf<float> dB(bf.size()), dW(tc_w_elems(gt, t));
       DBuf<double> dn(t.kp);
@@ -1183,7 +1216,7 @@ int icnnm_cuda_conv_adjoint_ex(int order, const int64_t* dims, const int64_t* kd
     if (is_tc(engine)) {
       TcPlan t = tc_plan(p, engine == ICNNM_ENGINE_F16X3);
       Geo gt = tc_geo(g, t);
-      check_smem(icnnm_dev::tc::smem_bytes(gt, false, 2, 2));
+      check_smem(icnnm_dev::tc::smem_bytes(gt, false, 2, 2, t.f16));
       std::vector<double> I(static_cast<size_t>(p.k) * p.k, 0.0);
       for (int j = 0; j < p.k; ++j) I[static_cast<size_t>(j) * p.k + j] = 1.0;
       auto ba = pack_b_tiles(p, t, I.data(), false);

@@ -33,6 +33,7 @@
 // W layout (this engine): [brick][j][row] (column-major per brick), so
 // epilogue/builder threads (one per row) access it coalesced and any column
 // range of a brick is one contiguous block.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -273,6 +274,44 @@ __device__ __forceinline__ int tile_width(const TcArgs& a, int nt) {
   return w < a.wbase ? w : a.wbase;
 }
 
+// Tile-group MMA schedule.  The A operand of a K-chunk depends only on
+// (brick, chunk), so the MMAs of a group of gsz (1 or 2) N-tiles share each
+// built A stage: the builders build every chunk once per group instead of once
+// per tile.  The two tiles of a group accumulate in acc0/acc1 at the same
+// time, so the schedule is skewed to keep the epilogue overlapped: the first
+// D chunks go to tile 0 alone (tile 1's accumulator is still being drained by
+// the epilogue of the previous group), then tile 1 catches up on them, the body
+// alternates (0,c),(1,c), and the last D chunks again go to tile 0 first so
+// that its accumulator completes D chunk periods before tile 1's.  A stage of
+// chunk c is released after its last use; D <= sa keeps the ring live.
+__device__ __forceinline__ void tg_seq(int i, int gsz, int nkc, int D, int& t, int& c) {
+  if (gsz == 1) {
+    t = 0;
+    c = i;
+    return;
+  }
+  if (i < D) {
+    t = 0;
+    c = i;
+    return;
+  }
+  if (i < 2 * D) {
+    t = 1;
+    c = i - D;
+    return;
+  }
+  int j = i - 2 * D;
+  const int nb = 2 * (nkc - 2 * D);
+  if (j < nb) {
+    t = j & 1;
+    c = D + (j >> 1);
+    return;
+  }
+  j -= nb;
+  t = j < D ? 0 : 1;
+  c = nkc - D + (j < D ? j : j - D);
+}
+
 // ---------------------------------------------------------------------------
 // The kernel (FWD = forward implicit GEMM, !FWD = adjoint)
 //   warps [0, 8)            builders (two per TMEM lane quadrant, 16 K each)
@@ -289,6 +328,7 @@ icnnm_tc_kernel(TcArgs a) {
   constexpr int NEPI = FWD ? 8 : 4;      // epilogue warps
   constexpr int WMMA = NB + NEPI;        // MMA warp
   constexpr int WLOAD = NB + NEPI + 1;   // B loader warp; W loader warp after it
+  constexpr int BSTG = F16 ? B_STAGE_F16 : B_STAGE_BYTES;  // SMEM B stage stride
   const Geo& g = a.g;
   float rr = 0.f;
   if (a.mode == 1) {
@@ -302,7 +342,7 @@ icnnm_tc_kernel(TcArgs a) {
   const int sbn = a.sb, wsn = a.ws, san = a.sa;
   const uint32_t a_col0 = 2u * static_cast<uint32_t>(a.accw);
   float* Bst = reinterpret_cast<float*>(p);
-  p += sbn * B_STAGE_BYTES;
+  p += sbn * BSTG;
   float* Wst = reinterpret_cast<float*>(p);   // adjoint: W-chunk ring; forward: W-group ring
   p += wsn * (FWD ? WO_STAGE_BYTES : W_STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p);
@@ -317,7 +357,7 @@ icnnm_tc_kernel(TcArgs a) {
   uint64_t* SC_full = W_empty + WS;   // F16x3 forward: per-brick scale slots
   float* sc_ring = reinterpret_cast<float*>(SC_full + NSC);
   float* wmax = sc_ring + NSC;        // 2 x 8 builder-warp maxima
-  p += 512;  // 2*SA + 2*SB + 4 + 2*WS + NSC mbarriers, NSC scales, 16 maxima
+  p += BAR_BYTES;  // 2*SA + 2*SB + 4 + 2*WS + NSC mbarriers, NSC scales, 16 maxima
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p);
   p += 16;
   int* tapoff = reinterpret_cast<int*>(p);
@@ -407,6 +447,11 @@ icnnm_tc_kernel(TcArgs a) {
   const int nbr = static_cast<int>(a.nbricks);
   const int ntn = a.ntn;
   const int nkc = a.nkc;
+  const int grp = a.grp > 1 ? 2 : 1;          // N-tiles sharing each A chunk
+  const int ngrp = (ntn + grp - 1) / grp;
+  int skew = a.skew < nkc / 2 ? a.skew : nkc / 2;
+  skew = skew < san ? skew : san;
+  skew = skew < 0 ? 0 : skew;
 
   if (warp < NB && !(a.skip & 8)) {
     // ===================== builders =====================
@@ -459,7 +504,15 @@ icnnm_tc_kernel(TcArgs a) {
 #pragma unroll
           for (int w = 0; w < NB; ++w) bm = fmaxf(bm, wmax[(iter & 1) * 8 + w]);
           const float fscale = f16_scale(bm);
-          for (int e = bt_tid; e < nob; e += NB * 32) hcur[e] *= fscale;
+          // prescale and pre-split in place: word = rn_f16(x) | rn_f16(x - hi) << 16,
+          // so each chunk's build is gathers + byte permutes (same bits as
+          // splitting per chunk, once per halo element instead of once per tap)
+          uint32_t* hw = reinterpret_cast<uint32_t*>(hcur);
+          for (int e = bt_tid; e < nob; e += NB * 32) {
+            const float x = hcur[e] * fscale;
+            const float xh = __half2float(__float2half_rn(x));
+            hw[e] = pack_f16x2(x, x - xh);
+          }
           if (bt_tid == 0) {  // the epilogue unscales this brick by 2^-(eA + eB)
             sc_ring[iter % NSC] = a.bunscale / fscale;
             mbar_arrive(SC_full + iter % NSC);
@@ -467,7 +520,7 @@ icnnm_tc_kernel(TcArgs a) {
           named_sync(1, NB * 32);  // halo scaled
         }
       }
-      for (int nt = 0; nt < ntn; ++nt) {
+      for (int gi = 0; gi < ngrp; ++gi) {
         for (int kc = 0; kc < nkc; ++kc, ++cnt) {
           // bsplit = 0: group `half` owns the chunks with cnt % 2 == half and
           // builds all KC columns, so each warp has two chunk periods of MMA
@@ -497,7 +550,19 @@ icnnm_tc_kernel(TcArgs a) {
                 cq[4 * v4] = c4.x; cq[4 * v4 + 1] = c4.y; cq[4 * v4 + 2] = c4.z; cq[4 * v4 + 3] = c4.w;
               }
             }
-            if (F16) {
+            if (F16 && FWD) {
+              // pre-split halo words {hi, lo}: hi pair = low halves, lo pair = high halves
+              const uint32_t* hw = reinterpret_cast<const uint32_t*>(hcur);
+              uint32_t hi[8], lo[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const uint32_t w0 = hw[hidx - tq[2 * i]], w1 = hw[hidx - tq[2 * i + 1]];
+                hi[i] = __byte_perm(w0, w1, 0x5410);
+                lo[i] = __byte_perm(w0, w1, 0x7632);
+              }
+              tmem_st8(tbase + lane_base + col, hi);
+              tmem_st8(tbase + lane_base + col + ALO, lo);
+            } else if (F16) {
               // 16 K values -> 8 f16x2 words hi | 8 words lo (element 2i in the low half)
               uint32_t hi[8], lo[8];
 #pragma unroll
@@ -783,58 +848,88 @@ icnnm_tc_kernel(TcArgs a) {
   } else if (warp == WMMA) {
     // ===================== MMA issuer (converged warp, elected lane issues) =====================
     {
-      uint32_t cnt = 0, bcnt = 0, tcount = 0;
+      uint32_t cnt = 0, tcount = 0;
+      int sb = 0;
+      uint32_t bph = 0;
       const uint32_t bs0 = smem_u32(Bst);
       long long wa = 0, wb = 0, wacc = 0, tstart = a.dbg ? clk() : 0;
-      for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
-        for (int nt = 0; nt < ntn; ++nt, ++tcount) {
-          const int acc = tcount & 1;
-          const uint32_t aph = (tcount >> 1) & 1;
-          const int wn = tile_width(a, nt);
-          const uint32_t idesc = F16 ? idesc_f16(wn) : idesc_tf32(wn);
-          const uint32_t dcol = tbase + acc * a.accw;
+      // MMAs of chunk kc into tile t of the current group (acc = tile parity)
+      uint32_t idesc_t[2], dcol_t[2];
+      int wn_t[2];
+      auto issue = [&](int t, int kc, bool first_use, bool last_use) {
+        if (kc == 0) {
+          const uint32_t tci = tcount + static_cast<uint32_t>(t);
           long long q0 = a.dbg ? clk() : 0;
-          if (!(a.skip & 32)) mbar_wait(ACC_empty + acc, aph ^ 1);
+          if (!(a.skip & 32)) mbar_wait(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
           if (a.dbg) wacc += clk() - q0;
-          tc_fence_after();
-          for (int kc = 0; kc < nkc; ++kc, ++cnt, ++bcnt) {
-            const int sa = cnt % san;
-            const int sb = bcnt % sbn;
-            long long q1 = a.dbg ? clk() : 0;
-            if (!(a.skip & 8)) mbar_wait(A_full + sa, (cnt / san) & 1);
-            long long q2 = a.dbg ? clk() : 0;
-            if (!(a.skip & 16)) mbar_wait(B_full + sb, (bcnt / sbn) & 1);
-            if (a.dbg) {
-              long long q3 = clk();
-              wa += q2 - q1;
-              wb += q3 - q2;
-            }
-            tc_fence_after();
-            const uint32_t acol = tbase + a_col0 + sa * ASC;
-            const uint32_t bhi = bs0 + sb * B_STAGE_BYTES;
-            if (F16) {
-              // one K-step of 16: B hi | lo blocks of wn x 16 halves (wn * 32 B each)
-              const uint64_t dh = bdesc(bhi);
-              const uint64_t dl = bdesc(bhi + wn * 32);
-              tc_mma_f16_elect(dcol, acol, dh, idesc, kc == 0 ? 0u : 1u);
-              tc_mma_f16_elect(dcol, acol + ALO, dh, idesc, 1u);
-              tc_mma_f16_elect(dcol, acol, dl, idesc, 1u);
-            } else {
-              const uint32_t blo = bhi + wn * (KC / 8) * 32;
+        }
+        const uint32_t ci = cnt + static_cast<uint32_t>(kc);
+        const int sa = static_cast<int>(ci % static_cast<uint32_t>(san));
+        long long q1 = a.dbg ? clk() : 0;
+        if (first_use && !(a.skip & 8)) mbar_wait(A_full + sa, (ci / san) & 1);
+        long long q2 = a.dbg ? clk() : 0;
+        if (!(a.skip & 16)) mbar_wait(B_full + sb, bph);
+        if (a.dbg) {
+          long long q3 = clk();
+          wa += q2 - q1;
+          wb += q3 - q2;
+        }
+        tc_fence_after();
+        const uint32_t acol = tbase + a_col0 + sa * ASC;
+        const uint32_t bhi = bs0 + sb * BSTG;
+        const uint32_t dcol = dcol_t[t], idesc = idesc_t[t];
+        const int wn = wn_t[t];
+        if (F16) {
+          // one K-step of 16: B hi | lo blocks of wn x 16 halves (wn * 32 B each)
+          const uint64_t dh = bdesc(bhi);
+          const uint64_t dl = bdesc(bhi + wn * 32);
+          tc_mma_f16_elect(dcol, acol, dh, idesc, kc == 0 ? 0u : 1u);
+          tc_mma_f16_elect(dcol, acol + ALO, dh, idesc, 1u);
+          tc_mma_f16_elect(dcol, acol, dl, idesc, 1u);
+        } else {
+          const uint32_t blo = bhi + wn * (KC / 8) * 32;
 #pragma unroll
-              for (int q = 0; q < KC / 8; ++q) {
-                const uint64_t dh = bdesc(bhi + q * wn * 32);
-                const uint64_t dl = bdesc(blo + q * wn * 32);
-                const uint32_t first = (kc == 0 && q == 0) ? 0u : 1u;
-                tc_mma_ts_elect(dcol, acol + q * 8, dh, idesc, first);
-                tc_mma_ts_elect(dcol, acol + ALO + q * 8, dh, idesc, 1u);
-                tc_mma_ts_elect(dcol, acol + q * 8, dl, idesc, 1u);
-              }
-            }
-            if (!(a.skip & 8)) tc_commit_elect(A_empty + sa);
-            if (!(a.skip & 16)) tc_commit_elect(B_empty + sb);
+          for (int q = 0; q < KC / 8; ++q) {
+            const uint64_t dh = bdesc(bhi + q * wn * 32);
+            const uint64_t dl = bdesc(blo + q * wn * 32);
+            const uint32_t first = (kc == 0 && q == 0) ? 0u : 1u;
+            tc_mma_ts_elect(dcol, acol + q * 8, dh, idesc, first);
+            tc_mma_ts_elect(dcol, acol + ALO + q * 8, dh, idesc, 1u);
+            tc_mma_ts_elect(dcol, acol + q * 8, dl, idesc, 1u);
           }
-          if (!(a.skip & 32)) tc_commit_elect(ACC_full + acc);
+        }
+        if (last_use && !(a.skip & 8)) tc_commit_elect(A_empty + sa);
+        if (!(a.skip & 16)) tc_commit_elect(B_empty + sb);
+        if (kc == nkc - 1 && !(a.skip & 32))
+          tc_commit_elect(ACC_full + ((tcount + static_cast<uint32_t>(t)) & 1));
+        if (++sb == sbn) {
+          sb = 0;
+          bph ^= 1u;
+        }
+      };
+      for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+        for (int gi = 0; gi < ngrp; ++gi) {
+          const int nt0 = gi * grp;
+          const int gsz = (ntn - nt0) < grp ? (ntn - nt0) : grp;
+          for (int t = 0; t < gsz; ++t) {
+            wn_t[t] = tile_width(a, nt0 + t);
+            idesc_t[t] = F16 ? idesc_f16(wn_t[t]) : idesc_tf32(wn_t[t]);
+            dcol_t[t] = tbase + ((tcount + t) & 1) * a.accw;
+          }
+          if (gsz == 1) {
+            for (int kc = 0; kc < nkc; ++kc) issue(0, kc, true, true);
+          } else {  // the tg_seq order, phase by phase
+            for (int kc = 0; kc < skew; ++kc) issue(0, kc, true, false);
+            for (int kc = 0; kc < skew; ++kc) issue(1, kc, false, true);
+            for (int kc = skew; kc < nkc - skew; ++kc) {
+              issue(0, kc, true, false);
+              issue(1, kc, false, true);
+            }
+            for (int kc = nkc - skew; kc < nkc; ++kc) issue(0, kc, true, false);
+            for (int kc = nkc - skew; kc < nkc; ++kc) issue(1, kc, false, true);
+          }
+          cnt += static_cast<uint32_t>(nkc);
+          tcount += static_cast<uint32_t>(gsz);
         }
       }
       if (a.dbg && lane == 0) {
@@ -851,10 +946,15 @@ icnnm_tc_kernel(TcArgs a) {
       uint32_t bcnt = 0;
       long long wl = 0;
       for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
-        for (int nt = 0; nt < ntn; ++nt) {
-          const int wn = tile_width(a, nt);
-          const uint32_t bytes = static_cast<uint32_t>(wn) * KC * (F16 ? 4 : 8);
-          for (int kc = 0; kc < nkc; ++kc, ++bcnt) {
+        for (int gi = 0; gi < ngrp; ++gi) {
+          const int nt0 = gi * grp;
+          const int gsz = (ntn - nt0) < grp ? (ntn - nt0) : grp;
+          for (int i = 0; i < gsz * nkc; ++i, ++bcnt) {
+            int t, kc;
+            tg_seq(i, gsz, nkc, skew, t, kc);
+            const int nt = nt0 + t;
+            const int wn = tile_width(a, nt);
+            const uint32_t bytes = static_cast<uint32_t>(wn) * KC * (F16 ? 4 : 8);
             const int sb = bcnt % sbn;
             long long q0 = a.dbg ? clk() : 0;
             mbar_wait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
@@ -865,7 +965,7 @@ icnnm_tc_kernel(TcArgs a) {
             }
             mbar_arrive_expect_tx(B_full + sb, bytes);
             const float* src = a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4);
-            bulk_g2s(reinterpret_cast<uint8_t*>(Bst) + sb * B_STAGE_BYTES, src, bytes, B_full + sb);
+            bulk_g2s(reinterpret_cast<uint8_t*>(Bst) + sb * BSTG, src, bytes, B_full + sb);
           }
         }
       }
@@ -907,7 +1007,7 @@ icnnm_tc_kernel(TcArgs a) {
       // [brick][j][row] layout) ahead of the builders
       uint32_t wcnt = 0;
       for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
-        for (int nt = 0; nt < ntn; ++nt) {
+        for (int gi = 0; gi < ngrp; ++gi) {
           for (int kc = 0; kc < nkc; ++kc, ++wcnt) {
             const int wsi = wcnt % wsn;
             mbar_wait(W_empty + wsi, ((wcnt / wsn) & 1) ^ 1);

@@ -14,11 +14,15 @@ constexpr int SA = 6;                          // TMEM A stages (max; runtime a.
                                                // columns each, f16: KC columns (2 halves / column)
 constexpr int NSC = 8;                         // F16x3 forward: per-brick scale ring
 constexpr int SB = 6;                          // SMEM B stages (max; runtime a.sb)
-constexpr int WS = 4;                          // adjoint: SMEM W-chunk stages (max; runtime a.ws)
+constexpr int WS = 8;                          // SMEM W stages (max; runtime a.ws, even)
 constexpr int W_STAGE_BYTES = 128 * KC * 4;    // adjoint: 8 KB W chunk, 16 columns x 128 rows
 constexpr int WO_STAGE_BYTES = 128 * 32 * 4;   // forward: 16 KB W group, 32 columns x 128 rows
 constexpr int NTMAX = 208;                     // max accumulator width (N per tile)
-constexpr int B_STAGE_BYTES = 256 * KC * 4 * 2;    // hi + lo, up to 256 rows = 32 KB
+constexpr int B_STAGE_BYTES = 256 * KC * 4 * 2;    // hi + lo, up to 256 rows = 32 KB (tf32;
+                                                   // also the packed-block stride in global)
+constexpr int B_STAGE_F16 = 256 * KC * 2 * 2;      // f16 hi + lo: 16 KB SMEM stage
+constexpr int BAR_BYTES = 640;                     // mbarriers + scale ring + builder maxima
+inline int b_stage_bytes(bool f16) { return f16 ? B_STAGE_F16 : B_STAGE_BYTES; }
 
 struct TcArgs {
   Geo g;                 // kp = ktp = roundup(k, 32)
@@ -47,6 +51,8 @@ struct TcArgs {
   float bunscale;           // F16x3: 2^-eB, the inverse of the power-of-2 scale of B
   float amax;               // F16x3 adjoint, mode 0: bound on |W| (mode 1: st->adj_amax)
   int bpair;                // builders hand over owned chunks in pairs (one wait::st)
+  int grp;                  // N-tiles per tile group sharing each built A chunk (1 or 2)
+  int skew;                 // tile-group schedule skew D (chunks), see tg_seq
 };
 
 // dbg slots (cycles summed over CTAs)
@@ -61,11 +67,11 @@ void* adj_kernel_ptr(bool f16);
 
 inline int threads(bool fwd) { return fwd ? 608 : 480; }
 
-inline size_t smem_bytes(const Geo& g, bool fwd, int sb = SB, int ws = WS) {
+inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
   const size_t nobp = ((nob + 3) / 4) * 4;
-  size_t b = static_cast<size_t>(sb) * B_STAGE_BYTES +
-             static_cast<size_t>(ws) * (fwd ? WO_STAGE_BYTES : W_STAGE_BYTES) + 512 + 16;
+  size_t b = static_cast<size_t>(sb) * b_stage_bytes(f16) +
+             static_cast<size_t>(ws) * (fwd ? WO_STAGE_BYTES : W_STAGE_BYTES) + BAR_BYTES + 16;
   b += ((g.ktp * 4 + 15) / 16) * 16;
   b += ((g.kp * 4 + 15) / 16) * 16;
   if (fwd)

@@ -336,16 +336,19 @@ def test_certified_exact_recovery(case):                 # :178-209
     assert O.rel_l2(L, L0) < 1e-3 and rep.iterations <= 1000
 
 
-def test_golden_cfg2_fixture_matches_oracle():
-    """The committed config-2 golden was produced by this oracle
-    (oracle/gen_golden.py): its basis is the oracle's learned basis and its
-    first objective values are reproduced by re-running the oracle."""
+@pytest.mark.parametrize("fname,cfgno", [("cfg2_it300.npz", 2), ("cfg4_it200.npz", 4)])
+def test_golden_fixture_matches_oracle(fname, cfgno):
+    """The committed full-size goldens were produced by this oracle
+    (oracle/gen_golden.py): the basis is the oracle's learned basis and the
+    first objective value is reproduced by re-running the oracle."""
     import os
     from threadpoolctl import threadpool_limits
-    path = os.path.join(os.path.dirname(__file__), "golden", "cfg2_it300.npz")
+    path = os.path.join(os.path.dirname(__file__), "golden", fname)
+    if not os.path.exists(path):
+        pytest.skip(f"{fname} not generated")
     gd = np.load(path)
-    w = synth.WORKLOADS[2]
-    X, mask = w.target(), w.mask()
+    w = synth.WORKLOADS[cfgno]
+    X, mask = w.target(b=int(gd["batch_index"])), w.mask()
     nthr = os.cpu_count() or 1
     O.WORKERS = nthr
     try:
@@ -353,7 +356,8 @@ def test_golden_cfg2_fixture_matches_oracle():
             B = O.learn_ensemble_basis(w.training(), w.kernel)
             np.testing.assert_allclose(B.eigenvalues, gd["eigenvalues"], rtol=1e-10)
             s = O.AdmmSolver(X * mask, mask, O.EigenBasis(w.kernel, gd["K"], gd["eigenvalues"]),
-                             O.SolverConfig(max_iters=300, tol_primal=1e-300, tol_change=1e-300))
+                             O.SolverConfig(max_iters=w.iters, tol_primal=1e-300,
+                                            tol_change=1e-300))
             s.step()
     finally:
         O.WORKERS = 1
