@@ -154,6 +154,40 @@ __device__ __forceinline__ void tc_mma_f16_elect(uint32_t d, uint32_t a, uint64_
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
+// One F16x3 K-chunk, issued by one elected lane of the converged MMA warp in a
+// single block: D += A_hi B_hi + A_lo B_hi + A_hi B_lo, then the commits (B
+// stage always; A stage on its last use; accumulator when the tile is done).
+// One elect and one operand hand-off to the uniform datapath per chunk instead
+// of one per instruction (the per-instruction form made the issue loop, not
+// the tensor pipe, the limiter: ~770 cycles per 312-cycle chunk).
+__device__ __forceinline__ void tc_chunk_f16(uint32_t d, uint32_t a, uint32_t alo, uint64_t dh,
+                                             uint64_t dl, uint32_t idesc, uint32_t accum,
+                                             uint32_t bar_b, uint32_t bar_a, uint32_t bar_acc,
+                                             uint32_t flags) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t, qa, qc;\n"
+      ".reg .b32 f;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "setp.eq.b32 t, %6, %6;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "and.b32 f, %10, 1;\n"
+      "setp.ne.b32 qa, f, 0;\n"
+      "and.b32 f, %10, 2;\n"
+      "setp.ne.b32 qc, f, 0;\n"
+      "and.pred qa, qa, e;\n"
+      "and.pred qc, qc, e;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, t;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n"
+      "@qa tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n"
+      "@qc tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n"
+      "}\n" ::"r"(d),
+      "r"(a), "r"(alo), "l"(dh), "l"(dl), "r"(idesc), "r"(accum), "r"(bar_b), "r"(bar_a),
+      "r"(bar_acc), "r"(flags)
+      : "memory");
+}
 // {lo16 = rn_f16(x0), hi16 = rn_f16(x1)}: element 2i in the low half
 __device__ __forceinline__ uint32_t pack_f16x2(float x0, float x1) {
   uint32_t r;
@@ -373,7 +407,9 @@ icnnm_tc_kernel(TcArgs a) {
   float* ob = reinterpret_cast<float*>(p);
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  // warp index through a shuffle: provably warp-uniform, so role branches are
+  // uniform and the MMA issuer's counters can live in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
 
   if (warp == WMMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
@@ -852,21 +888,22 @@ icnnm_tc_kernel(TcArgs a) {
       int sb = 0;
       uint32_t bph = 0;
       const uint32_t bs0 = smem_u32(Bst);
+      const uint32_t bar_af = smem_u32(A_full), bar_ae = smem_u32(A_empty);
+      const uint32_t bar_bf = smem_u32(B_full), bar_be = smem_u32(B_empty);
+      const uint32_t bar_accf = smem_u32(ACC_full);
       long long wa = 0, wb = 0, wacc = 0, tstart = a.dbg ? clk() : 0;
-      // MMAs of chunk kc into tile t of the current group (acc = tile parity)
       uint32_t idesc_t[2], dcol_t[2];
       int wn_t[2];
-      auto issue = [&](int t, int kc, bool first_use, bool last_use) {
+      // MMAs of chunk kc (A stage sa, parity aph) into tile t of the current group
+      auto issue = [&](int t, int kc, int sa, uint32_t aph, bool first_use, bool last_use) {
         if (kc == 0) {
           const uint32_t tci = tcount + static_cast<uint32_t>(t);
           long long q0 = a.dbg ? clk() : 0;
           if (!(a.skip & 32)) mbar_wait(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
           if (a.dbg) wacc += clk() - q0;
         }
-        const uint32_t ci = cnt + static_cast<uint32_t>(kc);
-        const int sa = static_cast<int>(ci % static_cast<uint32_t>(san));
         long long q1 = a.dbg ? clk() : 0;
-        if (first_use && !(a.skip & 8)) mbar_wait(A_full + sa, (ci / san) & 1);
+        if (first_use && !(a.skip & 8)) mbar_wait(A_full + sa, aph);
         long long q2 = a.dbg ? clk() : 0;
         if (!(a.skip & 16)) mbar_wait(B_full + sb, bph);
         if (a.dbg) {
@@ -879,32 +916,54 @@ icnnm_tc_kernel(TcArgs a) {
         const uint32_t bhi = bs0 + sb * BSTG;
         const uint32_t dcol = dcol_t[t], idesc = idesc_t[t];
         const int wn = wn_t[t];
-        if (F16) {
-          // one K-step of 16: B hi | lo blocks of wn x 16 halves (wn * 32 B each)
-          const uint64_t dh = bdesc(bhi);
-          const uint64_t dl = bdesc(bhi + wn * 32);
-          tc_mma_f16_elect(dcol, acol, dh, idesc, kc == 0 ? 0u : 1u);
-          tc_mma_f16_elect(dcol, acol + ALO, dh, idesc, 1u);
-          tc_mma_f16_elect(dcol, acol, dl, idesc, 1u);
+        const bool acc_done = kc == nkc - 1 && !(a.skip & 32);
+        if (F16 && !(a.skip & 24)) {
+          tc_chunk_f16(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + wn * 32), idesc,
+                       kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
+                       bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
+                       (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
         } else {
-          const uint32_t blo = bhi + wn * (KC / 8) * 32;
+          if (F16) {
+            const uint64_t dh = bdesc(bhi);
+            const uint64_t dl = bdesc(bhi + wn * 32);
+            tc_mma_f16_elect(dcol, acol, dh, idesc, kc == 0 ? 0u : 1u);
+            tc_mma_f16_elect(dcol, acol + ALO, dh, idesc, 1u);
+            tc_mma_f16_elect(dcol, acol, dl, idesc, 1u);
+          } else {
+            const uint32_t blo = bhi + wn * (KC / 8) * 32;
 #pragma unroll
-          for (int q = 0; q < KC / 8; ++q) {
-            const uint64_t dh = bdesc(bhi + q * wn * 32);
-            const uint64_t dl = bdesc(blo + q * wn * 32);
-            const uint32_t first = (kc == 0 && q == 0) ? 0u : 1u;
-            tc_mma_ts_elect(dcol, acol + q * 8, dh, idesc, first);
-            tc_mma_ts_elect(dcol, acol + ALO + q * 8, dh, idesc, 1u);
-            tc_mma_ts_elect(dcol, acol + q * 8, dl, idesc, 1u);
+            for (int q = 0; q < KC / 8; ++q) {
+              const uint64_t dh = bdesc(bhi + q * wn * 32);
+              const uint64_t dl = bdesc(blo + q * wn * 32);
+              const uint32_t first = (kc == 0 && q == 0) ? 0u : 1u;
+              tc_mma_ts_elect(dcol, acol + q * 8, dh, idesc, first);
+              tc_mma_ts_elect(dcol, acol + ALO + q * 8, dh, idesc, 1u);
+              tc_mma_ts_elect(dcol, acol + q * 8, dl, idesc, 1u);
+            }
           }
+          if (last_use && !(a.skip & 8)) tc_commit_elect(A_empty + sa);
+          if (!(a.skip & 16)) tc_commit_elect(B_empty + sb);
+          if (acc_done) tc_commit_elect(ACC_full + ((tcount + static_cast<uint32_t>(t)) & 1));
         }
-        if (last_use && !(a.skip & 8)) tc_commit_elect(A_empty + sa);
-        if (!(a.skip & 16)) tc_commit_elect(B_empty + sb);
-        if (kc == nkc - 1 && !(a.skip & 32))
-          tc_commit_elect(ACC_full + ((tcount + static_cast<uint32_t>(t)) & 1));
         if (++sb == sbn) {
           sb = 0;
           bph ^= 1u;
+        }
+      };
+      (void)bar_af;
+      (void)bar_bf;
+      // A-stage (index, parity) of chunk ci, advanced incrementally within a phase
+      struct StageIt {
+        int s;
+        uint32_t ph;
+      };
+      auto stage_of = [&](uint32_t ci) {
+        return StageIt{static_cast<int>(ci % static_cast<uint32_t>(san)), (ci / san) & 1u};
+      };
+      auto next = [&](StageIt& x) {
+        if (++x.s == san) {
+          x.s = 0;
+          x.ph ^= 1u;
         }
       };
       for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
@@ -917,16 +976,21 @@ icnnm_tc_kernel(TcArgs a) {
             dcol_t[t] = tbase + ((tcount + t) & 1) * a.accw;
           }
           if (gsz == 1) {
-            for (int kc = 0; kc < nkc; ++kc) issue(0, kc, true, true);
+            StageIt x = stage_of(cnt);
+            for (int kc = 0; kc < nkc; ++kc, next(x)) issue(0, kc, x.s, x.ph, true, true);
           } else {  // the tg_seq order, phase by phase
-            for (int kc = 0; kc < skew; ++kc) issue(0, kc, true, false);
-            for (int kc = 0; kc < skew; ++kc) issue(1, kc, false, true);
-            for (int kc = skew; kc < nkc - skew; ++kc) {
-              issue(0, kc, true, false);
-              issue(1, kc, false, true);
+            StageIt x = stage_of(cnt);
+            for (int kc = 0; kc < skew; ++kc, next(x)) issue(0, kc, x.s, x.ph, true, false);
+            x = stage_of(cnt);
+            for (int kc = 0; kc < skew; ++kc, next(x)) issue(1, kc, x.s, x.ph, false, true);
+            for (int kc = skew; kc < nkc - skew; ++kc, next(x)) {
+              issue(0, kc, x.s, x.ph, true, false);
+              issue(1, kc, x.s, x.ph, false, true);
             }
-            for (int kc = nkc - skew; kc < nkc; ++kc) issue(0, kc, true, false);
-            for (int kc = nkc - skew; kc < nkc; ++kc) issue(1, kc, false, true);
+            const StageIt y = x;
+            for (int kc = nkc - skew; kc < nkc; ++kc, next(x)) issue(0, kc, x.s, x.ph, true, false);
+            x = y;
+            for (int kc = nkc - skew; kc < nkc; ++kc, next(x)) issue(1, kc, x.s, x.ph, false, true);
           }
           cnt += static_cast<uint32_t>(nkc);
           tcount += static_cast<uint32_t>(gsz);

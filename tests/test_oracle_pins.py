@@ -354,7 +354,10 @@ def test_golden_fixture_matches_oracle(fname, cfgno):
     try:
         with threadpool_limits(limits=nthr):
             B = O.learn_ensemble_basis(w.training(), w.kernel)
-            np.testing.assert_allclose(B.eigenvalues, gd["eigenvalues"], rtol=1e-10)
+            # relative to the spectrum (the tail eigenvalues are round-off sized
+            # and depend on the FFT thread count)
+            np.testing.assert_allclose(B.eigenvalues, gd["eigenvalues"], rtol=1e-10,
+                                       atol=1e-8 * float(np.max(gd["eigenvalues"])))
             s = O.AdmmSolver(X * mask, mask, O.EigenBasis(w.kernel, gd["K"], gd["eigenvalues"]),
                              O.SolverConfig(max_iters=w.iters, tol_primal=1e-300,
                                             tol_change=1e-300))
