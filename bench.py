@@ -104,9 +104,17 @@ class ClockSampler:
             for i, n in enumerate(names):
                 if len(r) > 4 + i and r[4 + i].lower() == "active":
                     reasons.add(n)
+        pw = []
+        for r in self.rows:
+            try:
+                pw.append(float(r[2]))
+            except (ValueError, IndexError):
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+                "samples": len(self.rows),
+                "sm_mhz_min": min(sm) if sm else None,
+                "power_w_max": max(pw) if pw else None}
 
 
 def measure_tf32_peak(dev: int) -> float:

@@ -18,6 +18,8 @@
 #include <stdexcept>
 #include <string>
 #include <array>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "../../include/icnnm_b200.h"
@@ -129,10 +131,10 @@ void set_smem_attrs() {
   set_max_dyn_smem(icnnm_dev::icnnm_fwd_ffma, optin);
   set_max_dyn_smem(icnnm_dev::icnnm_adj_ffma, optin);
   set_max_dyn_smem(icnnm_dev::icnnm_gram_lags, optin);
-  for (bool f16 : {false, true}) {
-    CK(cudaFuncSetAttribute(icnnm_dev::tc::fwd_kernel_ptr(f16),
+  for (int v = 0; v < 3; ++v) {  // tf32x3, f16x3, f16x3 CTA pairs
+    CK(cudaFuncSetAttribute(icnnm_dev::tc::fwd_kernel_ptr(v > 0, v > 1),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    CK(cudaFuncSetAttribute(icnnm_dev::tc::adj_kernel_ptr(f16),
+    CK(cudaFuncSetAttribute(icnnm_dev::tc::adj_kernel_ptr(v > 0, v > 1),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   }
   done_dev = dev;
@@ -391,43 +393,97 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   // ring consecutive uses of a stage alternate between groups, and a group
   // running two uses ahead (possible with F16x3's 6 A stages) would pass its
   // parity wait on the previous fill.
+  // CTA pairs (F16x3): thread-block clusters of 2 on one TPC run cta_group::2
+  // MMAs (M = 256, one per pair): each CTA builds its own brick's A in its own
+  // TMEM but loads only half of every B tile (N split across the pair), so the
+  // B stream -- 13.3 KB per 312-cycle chunk and SM, the largest L2 and SMEM
+  // consumer (and a quarter of the board power, profiles/ab_r1) -- halves.
+  // ICNNM_TC_CS=2 enables (A/B experiments; first measurement: slower, see DESIGN).
+  static const int cs_env = [] {
+    const char* e = std::getenv("ICNNM_TC_CS");
+    return e ? std::atoi(e) : -1;
+  }();
+  a.cs = cs_env >= 0 ? cs_env : 1;  // pairs: opt-in until they beat single CTAs
+  if (!t.f16 || n_bricks(gtc) < 2) a.cs = 1;
+  const bool pairs = a.cs > 1;
   // F16x3 B stages are 16 KB (half the TF32 stage), which leaves room for
   // an 8-deep forward W-group ring: a 208-column tile has 8 W groups, so the
-  // whole tile's W_old is in flight before its epilogue starts.
-  static const std::vector<std::array<int, 2>> pri_tf32 = {{6, 4}, {5, 4}, {4, 4}, {3, 4},
-                                                            {4, 2}, {3, 2}, {2, 2}};
-  static const std::vector<std::array<int, 2>> pri_f16 = {{6, 8}, {4, 8}, {4, 6}, {4, 4},
-                                                           {3, 4}, {4, 2}, {3, 2}, {2, 2}};
-  static const int sb_cap = [] {
-    // 4 B stages measured faster than 5-6 (more SMEM leaves less L1):
-    // profiles/README_r1.md; ICNNM_TC_SB overrides for A/B experiments
+  // whole tile's W_old is in flight before its epilogue starts.  Deepest B
+  // ring up to the cap first, then the deepest even W ring that still fits.
+  static const int sb_env = [] {
+    // 4 B stages measured faster than 5-6 for TF32x3 (more SMEM leaves less L1):
+    // profiles/README_r1.md; CTA pairs hold half-size stages, so twice as many
+    // in the same space.  ICNNM_TC_SB overrides for A/B experiments
     const char* e = std::getenv("ICNNM_TC_SB");
-    return e ? std::atoi(e) : 4;
+    return e ? std::atoi(e) : -1;
   }();
-  a.sb = 2;
-  a.ws = 2;
+  const int sb_cap = sb_env > 0 ? sb_env : (pairs ? 8 : 4);
   static const int ws_cap = [] {
     const char* e = std::getenv("ICNNM_TC_WS");  // A/B experiments
     return e ? std::atoi(e) : icnnm_dev::tc::WS;
   }();
-  for (const auto& c : (t.f16 ? pri_f16 : pri_tf32)) {
-    if (c[0] > sb_cap || c[1] > ws_cap) continue;
-    if (icnnm_dev::tc::smem_bytes(gtc, fwd, c[0], c[1], t.f16) <= 227 * 1024) {
-      a.sb = c[0];
-      a.ws = c[1];
-      break;
-    }
-  }
+  a.sb = 2;
+  a.ws = 2;
+  bool found = false;
+  for (int sbv = std::min(sb_cap, icnnm_dev::tc::SB); sbv >= 2 && !found; --sbv)
+    for (int wsv = std::min(ws_cap, icnnm_dev::tc::WS) & ~1; wsv >= 2 && !found; wsv -= 2)
+      if (icnnm_dev::tc::smem_bytes(gtc, fwd, sbv, wsv, t.f16, pairs) <= 227 * 1024) {
+        a.sb = sbv;
+        a.ws = wsv;
+        found = true;
+      }
   a.nbricks = n_bricks(gtc);
   int dev = 0, nsm = 148;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.nbricks, nsm));
   void* args[] = {&a};
-  const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16);
+  const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16, pairs);
   if (smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
-  CK(cudaLaunchKernel(fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16) : icnnm_dev::tc::adj_kernel_ptr(t.f16),
-                      dim3(grid), dim3(icnnm_dev::tc::threads(fwd)), args, smem, stream));
+  const dim3 block(icnnm_dev::tc::threads(fwd));
+  void* fn = fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16, a.cs > 1)
+                 : icnnm_dev::tc::adj_kernel_ptr(t.f16, a.cs > 1);
+  if (a.cs > 1) {
+    // persistent grid: as many pairs as can be co-resident (pairs live in one GPC)
+    static std::map<std::pair<void*, size_t>, int> max_pairs;
+    static std::mutex mp_mu;
+    std::lock_guard<std::mutex> lk(mp_mu);
+    auto key = std::make_pair(fn, smem);
+    auto it = max_pairs.find(key);
+    if (it == max_pairs.end()) {
+      cudaLaunchConfig_t qc{};
+      cudaLaunchAttribute at{};
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = 2;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      qc.gridDim = dim3(static_cast<unsigned>(nsm));
+      qc.blockDim = block;
+      qc.dynamicSmemBytes = smem;
+      qc.attrs = &at;
+      qc.numAttrs = 1;
+      int n = 0;
+      CK(cudaOccupancyMaxActiveClusters(&n, fn, &qc));
+      it = max_pairs.emplace(key, std::max(1, n)).first;
+    }
+    const int64_t nslot = (a.nbricks + 1) / 2;
+    const unsigned pairs = static_cast<unsigned>(std::min<int64_t>(nslot, it->second));
+    cudaLaunchConfig_t lc{};
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 2;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    lc.gridDim = dim3(2 * pairs);
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = stream;
+    lc.attrs = &at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelExC(&lc, fn, args));
+  } else {
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.nbricks, nsm));
+    CK(cudaLaunchKernel(fn, dim3(grid), block, args, smem, stream));
+  }
 }
 
 // EigenBasis::validate (spectral.cpp:25-41).
@@ -508,6 +564,9 @@ struct Solver {
   DBuf<float> xfer_send, xfer_recv;  // cross-process halo buffers
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
+  double* h_theta = nullptr;  // pinned staging of the theta schedule
+  size_t h_theta_n = 0;
+  IterState* h_st = nullptr;  // pinned: [0] initial state, [1] state readback
   // host copies of the basis (validation happens once at create)
   std::vector<double> K;
   // per-problem scalars (from upload)
@@ -524,6 +583,8 @@ struct Solver {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (evs) cudaEventDestroy(evs);
+    if (h_theta) cudaFreeHost(h_theta);
+    if (h_st) cudaFreeHost(h_st);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -787,56 +848,71 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   };
 
 
-  // Capture U iterations per graph so the device never waits on the host
-  // between iterations; replays past max_iters are no-ops (coef deactivates).
-  // Capture and instantiation are host work: they happen before the run's
-  // first event so that the device time of the solve never includes them.
-  const int U = std::min(iters, 32);
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  int64_t per_iter = 0;
   if (S.tc_counters && !S.dbg.p) S.dbg.alloc(2 * icnnm_dev::tc::DBG_SLOTS);  // captured pointer
-  IterState* hst = nullptr;
-  if (!S.profile) {
-    CK(cudaMallocHost(&hst, sizeof(IterState)));
-    const int64_t before = S.launches;
-    CK(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeThreadLocal));
-    for (int u = 0; u < U; ++u) iteration();
-    CK(cudaStreamEndCapture(S.stream, &graph));
-    per_iter = (S.launches - before) / U + 1 /*coef*/ +
-               static_cast<int64_t>(S.slabs.size()) /*update*/;
-    CK(cudaGraphInstantiate(&exec, graph, 0));
+  // pinned staging of the per-run host inputs (theta schedule, initial state),
+  // so that their uploads are capturable stream operations
+  if (S.h_theta_n < th.size()) {
+    if (S.h_theta) cudaFreeHost(S.h_theta);
+    CK(cudaMallocHost(&S.h_theta, th.size() * sizeof(double)));
+    S.h_theta_n = th.size();
   }
-  CK(cudaEventRecord(S.evs, S.stream));
-  CK(cudaMemcpyAsync(S.theta.p, th.data(), th.size() * sizeof(double), cudaMemcpyHostToDevice,
-                     S.stream));
-  CK(cudaMemsetAsync(S.stats.p, 0, S.stats.bytes(), S.stream));
-  CK(cudaMemsetAsync(S.red.p, 0, S.red.bytes(), S.stream));
+  if (!S.h_st) CK(cudaMallocHost(&S.h_st, 2 * sizeof(IterState)));
+  std::copy(th.begin(), th.end(), S.h_theta);
   IterState st0{};
   st0.active = 1;
   st0.max_iters = iters;
-  CK(cudaMemcpyAsync(S.st.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, S.stream));
-  S.launches = 0;
-  if (S.tc_counters) CK(cudaMemsetAsync(S.dbg.p, 0, S.dbg.bytes(), S.stream));
+  S.h_st[0] = st0;
 
+  // setup of one solve: theta/state upload, L0 = pm (or mean fill), W = A(L0)K
   const int64_t WT = p.dims[1] * p.dims[2];
-  for (auto& s : S.slabs) {
-    const int64_t off = s.row0 * WT;
-    icnnm_dev::icnnm_setup<<<grid_for(s.m_own, 256), 256, 0, S.stream>>>(
-        s.m_own, S.Mstage.p + off, S.maskstage.p + off, cfg.init_fill == ICNNM_INIT_MEAN,
-        mean, s.pm.p, s.mask.p, s.L.p, s.V.p, s.Lt.p + s.halo_elems);
+  // events may be recorded inside a stream capture: "external" records become
+  // event-record nodes of the graph (a plain record would only add an edge)
+  auto record = [&](cudaEvent_t e) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(S.stream, &cs));
+    if (cs == cudaStreamCaptureStatusActive)
+      CK(cudaEventRecordWithFlags(e, S.stream, cudaEventRecordExternal));
+    else
+      CK(cudaEventRecord(e, S.stream));
+  };
+  auto setup = [&]() {
+    record(S.evs);
+    CK(cudaMemcpyAsync(S.theta.p, S.h_theta, th.size() * sizeof(double), cudaMemcpyHostToDevice,
+                       S.stream));
+    CK(cudaMemsetAsync(S.stats.p, 0, S.stats.bytes(), S.stream));
+    CK(cudaMemsetAsync(S.red.p, 0, S.red.bytes(), S.stream));
+    CK(cudaMemcpyAsync(S.st.p, S.h_st, sizeof(IterState), cudaMemcpyHostToDevice, S.stream));
+    if (S.tc_counters) CK(cudaMemsetAsync(S.dbg.p, 0, S.dbg.bytes(), S.stream));
+    for (auto& s : S.slabs) {
+      const int64_t off = s.row0 * WT;
+      icnnm_dev::icnnm_setup<<<grid_for(s.m_own, 256), 256, 0, S.stream>>>(
+          s.m_own, S.Mstage.p + off, S.maskstage.p + off, cfg.init_fill == ICNNM_INIT_MEAN,
+          mean, s.pm.p, s.mask.p, s.L.p, s.V.p, s.Lt.p + s.halo_elems);
+      CKL();
+      ++S.launches;
+      CK(cudaMemsetAsync(s.W.p, 0, s.W.bytes(), S.stream));
+      CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
+    }
+    exchange_lt(S);
+    for (auto& s : S.slabs) launch_fwd(S, s, 0);
+    allreduce_red(S);
+  };
+  // final coef: moves the last update slot into stats, evaluates the stop test.
+  auto finish = [&]() {
+    icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
+                                                    S.stats.p, p.k, kpe, kd, res_scale,
+                                                    cfg.tol_primal, cfg.tol_change, floor_rel,
+                                                    S.exact_res ? 1 : 0);
     CKL();
     ++S.launches;
-    CK(cudaMemsetAsync(s.W.p, 0, s.W.bytes(), S.stream));
-    CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
-  }
-  exchange_lt(S);
-  for (auto& s : S.slabs) launch_fwd(S, s, 0);
-  allreduce_red(S);
+    record(S.ev1);
+  };
 
-  const int64_t setup_launches = S.launches;
-  CK(cudaEventRecord(S.ev0, S.stream));
+  S.launches = 0;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // destroyed after the final sync
   if (S.profile) {
+    setup();
+    CK(cudaEventRecord(S.ev0, S.stream));
     // Per-family timing (serialised, events between launches; diagnostics).
     cudaEvent_t e[5];
     for (auto& x : e) CK(cudaEventCreate(&x));
@@ -878,29 +954,62 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     S.prof_ms[2] = acc[2] / iters;
     S.prof_ms[3] = acc[3] / iters;
     for (auto& x : e) cudaEventDestroy(x);
+    finish();
   } else {
+    // The whole solve -- setup, its events, every iteration, the final coef --
+    // is one CUDA graph (up to GMAX iterations), captured and instantiated
+    // before anything runs: the device time of a solve is one graph launch and
+    // host-side delays (driver locks, scheduling) can never stretch it.
+    // Longer solves replay GMAX-iteration graphs between a head and a tail;
+    // replays past max_iters are no-ops (the coef kernel deactivates), and with
+    // tolerances the host checks the state between replays.
+    constexpr int GMAX = 512;
+    const bool one = iters <= GMAX;
+    const int U = one ? iters : GMAX;
     const bool may_stop = !(cfg.tol_primal <= 1e-200 && cfg.tol_change <= 1e-200);
-    for (int it = 0; it < iters; it += U) {
-      CK(cudaGraphLaunch(exec, S.stream));
-      S.launches += per_iter * std::min(U, iters - it);
-      if (may_stop && it + U < iters) {
-        CK(cudaMemcpyAsync(hst, S.st.p, sizeof(IterState), cudaMemcpyDeviceToHost, S.stream));
-        CK(cudaStreamSynchronize(S.stream));
-        if (!hst->active) break;
+    auto capture = [&](bool head, int n, bool tail) {
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t e = nullptr;
+      CK(cudaStreamBeginCapture(S.stream, cudaStreamCaptureModeThreadLocal));
+      if (head) {
+        setup();
+        record(S.ev0);
       }
+      for (int u = 0; u < n; ++u) iteration();
+      if (tail) finish();
+      CK(cudaStreamEndCapture(S.stream, &g));
+      CK(cudaGraphInstantiate(&e, g, 0));
+      CK(cudaGraphUpload(e, S.stream));
+      cudaGraphDestroy(g);
+      return e;
+    };
+    // launch accounting: capture counts the TC/FFMA launches of one iteration
+    const int64_t l0 = S.launches;
+    cudaGraphExec_t gx = capture(true, U, one);
+    const int64_t captured = S.launches - l0;
+    S.launches = l0;
+    // per iteration: coef + update per slab + the counted engine launches
+    const int64_t setup_l = static_cast<int64_t>(S.slabs.size()) * 2 + (one ? 1 : 0);
+    const int64_t per_iter = (captured - setup_l) / std::max(1, U) + 1 +
+                             static_cast<int64_t>(S.slabs.size());
+    cudaGraphExec_t gr = one ? nullptr : capture(false, U, false);
+    CK(cudaStreamSynchronize(S.stream));  // uploads done; nothing of this solve has run
+    CK(cudaGraphLaunch(gx, S.stream));
+    S.launches += setup_l + per_iter * U;
+    for (int it = U; it < iters; it += U) {
+      if (may_stop) {
+        CK(cudaMemcpyAsync(S.h_st + 1, S.st.p, sizeof(IterState), cudaMemcpyDeviceToHost,
+                           S.stream));
+        CK(cudaStreamSynchronize(S.stream));
+        if (!S.h_st[1].active) break;
+      }
+      CK(cudaGraphLaunch(gr, S.stream));
+      S.launches += per_iter * std::min(U, iters - it);
     }
-    cudaFreeHost(hst);
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
+    if (!one) finish();
+    gexec[0] = gx;
+    gexec[1] = gr;
   }
-  // final coef: moves the last update slot into stats, evaluates the stop test.
-  icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
-                                                  S.stats.p, p.k, kpe, kd, res_scale,
-                                                  cfg.tol_primal, cfg.tol_change, floor_rel,
-                                                  S.exact_res ? 1 : 0);
-  CKL();
-  ++S.launches;
-  CK(cudaEventRecord(S.ev1, S.stream));
   RunResult R;
   R.stats.resize(iters);
   CK(cudaMemcpyAsync(R.stats.data(), S.stats.p, S.stats.bytes(), cudaMemcpyDeviceToHost,
@@ -912,7 +1021,8 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   R.loop_ms = ms;
   CK(cudaEventElapsedTime(&ms, S.evs, S.ev1));
   R.run_ms = ms;
-  (void)setup_launches;
+  for (auto& x : gexec)
+    if (x) cudaGraphExecDestroy(x);
   return R;
 }
 

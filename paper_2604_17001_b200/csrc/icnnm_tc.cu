@@ -79,6 +79,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
                "r"(smem_u32(src)), "r"(bytes)
@@ -141,6 +145,67 @@ __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
       "}\n" ::"r"(smem_u32(bar))
       : "memory");
+}
+// ---- CTA-pair (cta_group::2) primitives ----
+// The address of the same shared-memory object in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// Arrive on a (possibly remote) mbarrier with cluster-scope release.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr)
+               : "memory");
+}
+// Wait whose acquire covers arrivals released by the peer CTA.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// One F16x3 K-chunk of a CTA pair (M = 256: 128 rows from each CTA's TMEM A
+// stage, B split by N between the two CTAs' shared memory), issued by the
+// leader; commits are multicast to the barrier at the same offset in both CTAs.
+__device__ __forceinline__ void tc_chunk_f16_pair(uint32_t d, uint32_t a, uint32_t alo, uint64_t dh,
+                                                  uint64_t dl, uint32_t idesc, uint32_t accum,
+                                                  uint32_t bar_b, uint32_t bar_a, uint32_t bar_acc,
+                                                  uint32_t flags) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t, qa, qc;\n"
+      ".reg .b32 f;\n"
+      ".reg .b16 m;\n"
+      "mov.b16 m, 3;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "setp.eq.b32 t, %6, %6;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "and.b32 f, %10, 1;\n"
+      "setp.ne.b32 qa, f, 0;\n"
+      "and.b32 f, %10, 2;\n"
+      "setp.ne.b32 qc, f, 0;\n"
+      "and.pred qa, qa, e;\n"
+      "and.pred qc, qc, e;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %3, %5, p;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%2], %3, %5, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %4, %5, t;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], m;\n"
+      "@qa tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%8], m;\n"
+      "@qc tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%9], m;\n"
+      "}\n" ::"r"(d),
+      "r"(a), "r"(alo), "l"(dh), "l"(dl), "r"(idesc), "r"(accum), "r"(bar_b), "r"(bar_a),
+      "r"(bar_acc), "r"(flags)
+      : "memory");
+}
+// kind::f16 instruction descriptor for M = 256 (CTA pair): D f32, A/B f16, K-major.
+__device__ __forceinline__ uint32_t idesc_f16_m256(int n) {
+  return (1u << 4) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(256 >> 4) << 24);
 }
 __device__ __forceinline__ void tc_mma_f16_elect(uint32_t d, uint32_t a, uint64_t bdesc,
                                                  uint32_t idesc, uint32_t acc) {
@@ -353,7 +418,7 @@ __device__ __forceinline__ void tg_seq(int i, int gsz, int nkc, int D, int& t, i
 //   warp  8 + NEPI          MMA issuer
 //   warp  9 + NEPI          B loader
 // ---------------------------------------------------------------------------
-template <bool FWD, bool F16>
+template <bool FWD, bool F16, bool PAIR>
 __global__ void __launch_bounds__(FWD ? 608 : 480, 1)
 icnnm_tc_kernel(TcArgs a) {
   constexpr int ASC = F16 ? KC : 2 * KC;  // TMEM columns per A stage
@@ -362,7 +427,7 @@ icnnm_tc_kernel(TcArgs a) {
   constexpr int NEPI = FWD ? 8 : 4;      // epilogue warps
   constexpr int WMMA = NB + NEPI;        // MMA warp
   constexpr int WLOAD = NB + NEPI + 1;   // B loader warp; W loader warp after it
-  constexpr int BSTG = F16 ? B_STAGE_F16 : B_STAGE_BYTES;  // SMEM B stage stride
+  constexpr int BSTG = F16 ? (PAIR ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES;  // B stage stride
   const Geo& g = a.g;
   float rr = 0.f;
   if (a.mode == 1) {
@@ -412,23 +477,31 @@ icnnm_tc_kernel(TcArgs a) {
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
 
   if (warp == WMMA) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
-        smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if (PAIR) {  // both CTAs' warp WMMA: 512 columns in each CTA of the pair
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+          smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+          smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
   }
   if (tid == 0) {
     const int nbuild = (a.bsplit && !F16) ? NB * 32 : (NB / 2) * 32;  // builder arrivals / chunk
+    // PAIR: the leader's A_full / ACC_empty count one arrival per warp of both
+    // CTAs; its B_full the local expect_tx plus the peer's relayed arrival
     for (int i = 0; i < SA; ++i) {
-      mbar_init(A_full + i, nbuild);
+      mbar_init(A_full + i, PAIR ? 2 * (NB / 2) : nbuild);
       mbar_init(A_empty + i, 1);
     }
     for (int i = 0; i < SB; ++i) {
-      mbar_init(B_full + i, 1);
+      mbar_init(B_full + i, (PAIR && (blockIdx.x & 1u) == 0) ? 2 : 1);
       mbar_init(B_empty + i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(ACC_full + i, 1);
-      mbar_init(ACC_empty + i, NEPI * 32);
+      mbar_init(ACC_empty + i, PAIR ? 2 * NEPI : NEPI * 32);
     }
     for (int i = 0; i < WS; ++i) {
       mbar_init(W_full + i, 1);
@@ -476,7 +549,10 @@ icnnm_tc_kernel(TcArgs a) {
     for (int e = tid; e < 4 * (nobp + 32); e += blockDim.x) ob[e] = 0.f;
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // the peer's barriers are initialised before any remote arrive / commit
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
@@ -488,6 +564,20 @@ icnnm_tc_kernel(TcArgs a) {
   int skew = a.skew < nkc / 2 ? a.skew : nkc / 2;
   skew = skew < san ? skew : san;
   skew = skew < 0 ? 0 : skew;
+  // Bricks by cluster slot: CTA `crank` of a cs-CTA cluster takes brick
+  // cs*s + crank of slot s, so both CTAs of a pair walk the same number of
+  // slots (they consume one multicast B stream in lockstep); a pair's odd
+  // tail brick is a dummy (brick nbr-1 re-read, nothing written).
+  const int ncta = PAIR ? 2 : 1;
+  const int crank = ncta > 1 ? static_cast<int>(blockIdx.x & 1u) : 0;
+  const int sfirst = static_cast<int>(blockIdx.x) / ncta;
+  const int sstep = static_cast<int>(gridDim.x) / ncta;
+  const int nslot = (nbr + ncta - 1) / ncta;
+  auto brick_of = [&](int sl) {
+    const int bb = sl * ncta + crank;
+    return bb < nbr ? bb : nbr - 1;
+  };
+  auto real_slot = [&](int sl) { return sl * ncta + crank < nbr; };
 
   if (warp < NB && !(a.skip & 8)) {
     // ===================== builders =====================
@@ -513,22 +603,22 @@ icnnm_tc_kernel(TcArgs a) {
       cp_async_commit();
     };
     if (FWD) {
-      if (blockIdx.x < nbr) issue_halo(halo, blockIdx.x);
+      if (sfirst < nslot) issue_halo(halo, brick_of(sfirst));
     }
     // F16x3 operand scale: forward per brick (the halo is prescaled in place);
     // adjoint: folded into cs
     // (the held chunk c and the next owned chunk c+2 must use different A and
     // W stages: sa >= 3 always; the adjoint's W ring needs 4)
-    const bool pair = (F16 || !a.bsplit) && a.bpair && san >= 3 && (FWD || wsn >= 4);
+    const bool pair = !PAIR && (F16 || !a.bsplit) && a.bpair && san >= 3 && (FWD || wsn >= 4);
+    const uint32_t lead_afull = PAIR ? mapa_u32(smem_u32(A_full), 0) : 0u;
     int pend_sa = -1, pend_wsi = 0;
     int iter = 0;
-    for (int b = blockIdx.x; b < nbr; b += gridDim.x, ++iter) {
+    for (int sl = sfirst; sl < nslot; sl += sstep, ++iter) {
       float* hcur = halo + (iter & 1) * nobp;
       if (FWD) {
         cp_async_wait_all();
         named_sync(1, NB * 32);  // this brick's halo landed; previous brick fully built
-        if (b + static_cast<int>(gridDim.x) < nbr)
-          issue_halo(halo + ((iter + 1) & 1) * nobp, b + gridDim.x);
+        if (sl + sstep < nslot) issue_halo(halo + ((iter + 1) & 1) * nobp, brick_of(sl + sstep));
         if (F16) {
           float mx = 0.f;
           for (int e = bt_tid; e < nob; e += NB * 32) mx = fmaxf(mx, fabsf(hcur[e]));
@@ -567,7 +657,10 @@ icnnm_tc_kernel(TcArgs a) {
           const int wsi = cnt % wsn;
           const uint32_t wph = (cnt / wsn) & 1;
           long long t0c = dbg.p ? clk() : 0;
-          mbar_wait(A_empty + sa, ph ^ 1);
+          if (PAIR)
+            mbar_wait_cluster(A_empty + sa, ph ^ 1);  // released by the leader's MMAs
+          else
+            mbar_wait(A_empty + sa, ph ^ 1);
           if (!FWD) mbar_wait(W_full + wsi, wph);
           tc_fence_after();
           long long t1c = dbg.p ? clk() : 0;
@@ -663,6 +756,12 @@ icnnm_tc_kernel(TcArgs a) {
               pend_sa = sa;
               pend_wsi = wsi;
             }
+          } else if (PAIR) {
+            // one arrival per warp on the leader's A_full (after the warp's wait::st)
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(lead_afull + 8u * static_cast<uint32_t>(sa));
+            if (!FWD) mbar_arrive(W_empty + wsi);
           } else {
             tc_fence_before();
             mbar_arrive(A_full + sa);
@@ -704,10 +803,13 @@ icnnm_tc_kernel(TcArgs a) {
     if (F16 && !FWD)
       us_adj = a.bunscale / f16_scale(a.mode >= 1 ? static_cast<float>(a.st->adj_amax) : a.amax);
     uint32_t biter = 0;
-    for (int b = blockIdx.x; b < nbr; b += gridDim.x, ++biter) {
+    const uint32_t lead_accempty = PAIR ? mapa_u32(smem_u32(ACC_empty), 0) : 0u;
+    for (int sl = sfirst; sl < nslot; sl += sstep, ++biter) {
+      const int b = brick_of(sl);
+      const bool breal = real_slot(sl);  // false: the pair's dummy tail brick, nothing written
       int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
       const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
-      const bool valid = (h0 + vh < g.H) && (w0 + vw < g.W) && (t0 + vt < g.T);
+      const bool valid = breal && (h0 + vh < g.H) && (w0 + vw < g.W) && (t0 + vt < g.T);
       const bool bfull = (h0 + g.bh <= g.H) && (w0 + g.bw <= g.W) && (t0 + g.bt <= g.T);
       float us = us_adj;
       if (F16 && FWD) {  // this brick's scale, published by the builders
@@ -786,9 +888,9 @@ icnnm_tc_kernel(TcArgs a) {
                   sq = fmaf(v.z, v.z, sq);
                   sq = fmaf(v.w, v.w, sq);
                 }
-                if (lane < ncol) atomicAdd(nrm + j0 + lane, static_cast<double>(sq));
+                if (breal && lane < ncol) atomicAdd(nrm + j0 + lane, static_cast<double>(sq));
                 const int t = quad * 32 + lane;
-                if (t == 0) {
+                if (t == 0 && breal) {
                   bulk_s2g(a.Wout + (static_cast<size_t>(b) * g.kp + j0) * 128, st,
                            static_cast<uint32_t>(ncol) * 512u);
                   bulk_wait_read();  // the stage may be refilled after this
@@ -842,7 +944,12 @@ icnnm_tc_kernel(TcArgs a) {
           }
         }
         tc_fence_before();
-        mbar_arrive(ACC_empty + acc);
+        if (PAIR) {  // one arrival per warp on the leader's ACC_empty
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(lead_accempty + 8u * static_cast<uint32_t>(acc));
+        } else {
+          mbar_arrive(ACC_empty + acc);
+        }
         if (dbg.p) {
           long long t2c = clk();
           dbg.acc[0] += t1c - t0c;
@@ -852,6 +959,10 @@ icnnm_tc_kernel(TcArgs a) {
       if (!FWD) {
         named_sync(2, NEPI * 32);
         for (int e = row; e < nob; e += 128) {
+          if (!breal) {  // dummy brick: clear the output bricks, write nothing
+            ob[e] = ob[obs + e] = ob[2 * obs + e] = ob[3 * obs + e] = 0.f;
+            continue;
+          }
           float s = ob[e] + ob[obs + e] + ob[2 * obs + e] + ob[3 * obs + e];
           ob[e] = 0.f;
           ob[obs + e] = 0.f;
@@ -883,7 +994,24 @@ icnnm_tc_kernel(TcArgs a) {
   } else if (warp < NB + NEPI) {
   } else if (warp == WMMA) {
     // ===================== MMA issuer (converged warp, elected lane issues) =====================
-    {
+    if (PAIR && crank != 0) {
+      // peer CTA of a pair: the leader issues the pair's MMAs; this warp relays
+      // "my half of B stage sb landed" to the leader's B_full
+      if (lane == 0 && !(a.skip & 16)) {
+        const uint32_t lead_bfull = mapa_u32(smem_u32(B_full), 0);
+        int sb = 0;
+        uint32_t bph = 0;
+        const int nfill = ((nslot - sfirst + sstep - 1) / sstep) * ntn * nkc;
+        for (int f = 0; f < nfill; ++f) {
+          mbar_wait(B_full + sb, bph);
+          mbar_arrive_cluster(lead_bfull + 8u * static_cast<uint32_t>(sb));
+          if (++sb == sbn) {
+            sb = 0;
+            bph ^= 1u;
+          }
+        }
+      }
+    } else {
       uint32_t cnt = 0, tcount = 0;
       int sb = 0;
       uint32_t bph = 0;
@@ -899,13 +1027,28 @@ icnnm_tc_kernel(TcArgs a) {
         if (kc == 0) {
           const uint32_t tci = tcount + static_cast<uint32_t>(t);
           long long q0 = a.dbg ? clk() : 0;
-          if (!(a.skip & 32)) mbar_wait(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
+          if (!(a.skip & 32)) {
+            if (PAIR)
+              mbar_wait_cluster(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
+            else
+              mbar_wait(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
+          }
           if (a.dbg) wacc += clk() - q0;
         }
         long long q1 = a.dbg ? clk() : 0;
-        if (first_use && !(a.skip & 8)) mbar_wait(A_full + sa, aph);
+        if (first_use && !(a.skip & 8)) {
+          if (PAIR)
+            mbar_wait_cluster(A_full + sa, aph);
+          else
+            mbar_wait(A_full + sa, aph);
+        }
         long long q2 = a.dbg ? clk() : 0;
-        if (!(a.skip & 16)) mbar_wait(B_full + sb, bph);
+        if (!(a.skip & 16)) {
+          if (PAIR)
+            mbar_wait_cluster(B_full + sb, bph);
+          else
+            mbar_wait(B_full + sb, bph);
+        }
         if (a.dbg) {
           long long q3 = clk();
           wa += q2 - q1;
@@ -917,7 +1060,13 @@ icnnm_tc_kernel(TcArgs a) {
         const uint32_t dcol = dcol_t[t], idesc = idesc_t[t];
         const int wn = wn_t[t];
         const bool acc_done = kc == nkc - 1 && !(a.skip & 32);
-        if (F16 && !(a.skip & 24)) {
+        if (PAIR) {
+          // this CTA's half of B: hi rows [0, wn/2) then lo rows (wn/2 x 32 B each)
+          tc_chunk_f16_pair(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + (wn / 2) * 32), idesc,
+                            kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
+                            bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
+                            (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
+        } else if (F16 && !(a.skip & 24)) {
           tc_chunk_f16(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + wn * 32), idesc,
                        kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
                        bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
@@ -966,13 +1115,13 @@ icnnm_tc_kernel(TcArgs a) {
           x.ph ^= 1u;
         }
       };
-      for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+      for (int sl = sfirst; sl < nslot; sl += sstep) {
         for (int gi = 0; gi < ngrp; ++gi) {
           const int nt0 = gi * grp;
           const int gsz = (ntn - nt0) < grp ? (ntn - nt0) : grp;
           for (int t = 0; t < gsz; ++t) {
             wn_t[t] = tile_width(a, nt0 + t);
-            idesc_t[t] = F16 ? idesc_f16(wn_t[t]) : idesc_tf32(wn_t[t]);
+            idesc_t[t] = PAIR ? idesc_f16_m256(wn_t[t]) : (F16 ? idesc_f16(wn_t[t]) : idesc_tf32(wn_t[t]));
             dcol_t[t] = tbase + ((tcount + t) & 1) * a.accw;
           }
           if (gsz == 1) {
@@ -1009,7 +1158,7 @@ icnnm_tc_kernel(TcArgs a) {
     if (lane == 0 && !(a.skip & 16)) {
       uint32_t bcnt = 0;
       long long wl = 0;
-      for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+      for (int sl = sfirst; sl < nslot; sl += sstep) {
         for (int gi = 0; gi < ngrp; ++gi) {
           const int nt0 = gi * grp;
           const int gsz = (ntn - nt0) < grp ? (ntn - nt0) : grp;
@@ -1021,18 +1170,37 @@ icnnm_tc_kernel(TcArgs a) {
             const uint32_t bytes = static_cast<uint32_t>(wn) * KC * (F16 ? 4 : 8);
             const int sb = bcnt % sbn;
             long long q0 = a.dbg ? clk() : 0;
-            mbar_wait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
+            if (PAIR)
+              mbar_wait_cluster(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
+            else
+              mbar_wait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
             if (a.dbg) wl += clk() - q0;
             if (a.skip & 4) {
               mbar_arrive(B_full + sb);  // timing experiment: no B traffic
               continue;
             }
-            mbar_arrive_expect_tx(B_full + sb, bytes);
             const float* src = a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4);
-            bulk_g2s(reinterpret_cast<uint8_t*>(Bst) + sb * BSTG, src, bytes, B_full + sb);
+            uint8_t* dst = reinterpret_cast<uint8_t*>(Bst) + sb * BSTG;
+            if (PAIR) {
+              // this CTA's half of the N rows, hi then lo (the canonical layout
+              // keeps each half of the rows contiguous: 8-row core-matrix groups)
+              const uint32_t hb = static_cast<uint32_t>(wn / 2) * 32u;
+              const uint8_t* sb8 = reinterpret_cast<const uint8_t*>(src);
+              mbar_arrive_expect_tx(B_full + sb, 2u * hb);
+              bulk_g2s(dst, sb8 + crank * hb, hb, B_full + sb);
+              bulk_g2s(dst + hb, sb8 + static_cast<uint32_t>(wn) * 32u + crank * hb, hb, B_full + sb);
+            } else {
+              mbar_arrive_expect_tx(B_full + sb, bytes);
+              bulk_g2s(dst, src, bytes, B_full + sb);
+            }
           }
         }
       }
+      // drain: every stage released by the leader's MMAs (their commits into
+      // this CTA have landed) before the final cluster sync
+      if (PAIR)
+        for (int q = 0; q < sbn; ++q, ++bcnt)
+          mbar_wait_cluster(B_empty + bcnt % sbn, ((bcnt / sbn) & 1) ^ 1);
       if (a.dbg) atomicAdd(a.dbg + DBG_LOAD_WAIT, static_cast<unsigned long long>(wl));
     }
     __syncwarp();
@@ -1043,7 +1211,8 @@ icnnm_tc_kernel(TcArgs a) {
       // has no W_old (the slot is only handed over).  Tiles are padded to an
       // even number of groups so that each stage serves one epilogue half.
       uint32_t gs = 0;
-      for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+      for (int sl = sfirst; sl < nslot; sl += sstep) {
+        const int b = brick_of(sl);
         for (int nt = 0; nt < ntn; ++nt) {
           const int wn = tile_width(a, nt);
           const int ng = (wn + 31) / 32, ngp = ng + (ng & 1);
@@ -1070,7 +1239,8 @@ icnnm_tc_kernel(TcArgs a) {
       // adjoint: stream W chunks (16 columns x 128 rows, 8 KB contiguous in the
       // [brick][j][row] layout) ahead of the builders
       uint32_t wcnt = 0;
-      for (int b = blockIdx.x; b < nbr; b += gridDim.x) {
+      for (int sl = sfirst; sl < nslot; sl += sstep) {
+        const int b = brick_of(sl);
         for (int gi = 0; gi < ngrp; ++gi) {
           for (int kc = 0; kc < nkc; ++kc, ++wcnt) {
             const int wsi = wcnt % wsn;
@@ -1087,25 +1257,35 @@ icnnm_tc_kernel(TcArgs a) {
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // no CTA leaves while its peer can still signal into it
+  else
+    __syncthreads();
   tc_fence_after();
   if (warp == WMMA) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
   }
 }
 
-template __global__ void icnnm_tc_kernel<true, false>(TcArgs);
-template __global__ void icnnm_tc_kernel<false, false>(TcArgs);
-template __global__ void icnnm_tc_kernel<true, true>(TcArgs);
-template __global__ void icnnm_tc_kernel<false, true>(TcArgs);
+template __global__ void icnnm_tc_kernel<true, false, false>(TcArgs);
+template __global__ void icnnm_tc_kernel<false, false, false>(TcArgs);
+template __global__ void icnnm_tc_kernel<true, true, false>(TcArgs);
+template __global__ void icnnm_tc_kernel<false, true, false>(TcArgs);
+template __global__ void icnnm_tc_kernel<true, true, true>(TcArgs);
+template __global__ void icnnm_tc_kernel<false, true, true>(TcArgs);
 
-void* fwd_kernel_ptr(bool f16) {
-  return f16 ? reinterpret_cast<void*>(&icnnm_tc_kernel<true, true>)
-             : reinterpret_cast<void*>(&icnnm_tc_kernel<true, false>);
+void* fwd_kernel_ptr(bool f16, bool pair) {
+  if (f16 && pair) return reinterpret_cast<void*>(&icnnm_tc_kernel<true, true, true>);
+  return f16 ? reinterpret_cast<void*>(&icnnm_tc_kernel<true, true, false>)
+             : reinterpret_cast<void*>(&icnnm_tc_kernel<true, false, false>);
 }
-void* adj_kernel_ptr(bool f16) {
-  return f16 ? reinterpret_cast<void*>(&icnnm_tc_kernel<false, true>)
-             : reinterpret_cast<void*>(&icnnm_tc_kernel<false, false>);
+void* adj_kernel_ptr(bool f16, bool pair) {
+  if (f16 && pair) return reinterpret_cast<void*>(&icnnm_tc_kernel<false, true, true>);
+  return f16 ? reinterpret_cast<void*>(&icnnm_tc_kernel<false, true, false>)
+             : reinterpret_cast<void*>(&icnnm_tc_kernel<false, false, false>);
 }
 
 }  // namespace tc

@@ -13,7 +13,7 @@ constexpr int KC = 16;                         // K per chunk (tf32: 2 MMA K-ste
 constexpr int SA = 6;                          // TMEM A stages (max; runtime a.sa); tf32: 2*KC
                                                // columns each, f16: KC columns (2 halves / column)
 constexpr int NSC = 8;                         // F16x3 forward: per-brick scale ring
-constexpr int SB = 6;                          // SMEM B stages (max; runtime a.sb)
+constexpr int SB = 12;                         // SMEM B stages (max; runtime a.sb)
 constexpr int WS = 8;                          // SMEM W stages (max; runtime a.ws, even)
 constexpr int W_STAGE_BYTES = 128 * KC * 4;    // adjoint: 8 KB W chunk, 16 columns x 128 rows
 constexpr int WO_STAGE_BYTES = 128 * 32 * 4;   // forward: 16 KB W group, 32 columns x 128 rows
@@ -22,7 +22,12 @@ constexpr int B_STAGE_BYTES = 256 * KC * 4 * 2;    // hi + lo, up to 256 rows = 
                                                    // also the packed-block stride in global)
 constexpr int B_STAGE_F16 = 256 * KC * 2 * 2;      // f16 hi + lo: 16 KB SMEM stage
 constexpr int BAR_BYTES = 640;                     // mbarriers + scale ring + builder maxima
-inline int b_stage_bytes(bool f16) { return f16 ? B_STAGE_F16 : B_STAGE_BYTES; }
+static_assert((2 * SA + 2 * SB + 4 + 2 * WS + NSC) * 8 + NSC * 4 + 16 * 4 <= BAR_BYTES,
+              "barrier block overflows BAR_BYTES");
+// CTA pairs hold half of every B tile (N split across the pair)
+inline int b_stage_bytes(bool f16, bool pair = false) {
+  return f16 ? (pair ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES;
+}
 
 struct TcArgs {
   Geo g;                 // kp = ktp = roundup(k, 32)
@@ -53,6 +58,7 @@ struct TcArgs {
   int bpair;                // builders hand over owned chunks in pairs (one wait::st)
   int grp;                  // N-tiles per tile group sharing each built A chunk (1 or 2)
   int skew;                 // tile-group schedule skew D (chunks), see tg_seq
+  int cs;                   // 2: CTA pairs (cta_group::2, M = 256, B split by N); 1: single CTAs
 };
 
 // dbg slots (cycles summed over CTAs)
@@ -62,15 +68,15 @@ enum { DBG_BUILD_WAIT = 0, DBG_BUILD_WORK, DBG_MMA_WAIT_A, DBG_MMA_WAIT_B, DBG_M
 template <bool FWD, bool F16>
 __global__ void icnnm_tc_kernel(TcArgs a);
 
-void* fwd_kernel_ptr(bool f16);
-void* adj_kernel_ptr(bool f16);
+void* fwd_kernel_ptr(bool f16, bool pair = false);
+void* adj_kernel_ptr(bool f16, bool pair = false);
 
 inline int threads(bool fwd) { return fwd ? 608 : 480; }
 
-inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16) {
+inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16, bool pair = false) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
   const size_t nobp = ((nob + 3) / 4) * 4;
-  size_t b = static_cast<size_t>(sb) * b_stage_bytes(f16) +
+  size_t b = static_cast<size_t>(sb) * b_stage_bytes(f16, pair) +
              static_cast<size_t>(ws) * (fwd ? WO_STAGE_BYTES : W_STAGE_BYTES) + BAR_BYTES + 16;
   b += ((g.ktp * 4 + 15) / 16) * 16;
   b += ((g.kp * 4 + 15) / 16) * 16;
