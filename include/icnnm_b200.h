@@ -94,6 +94,10 @@ const char* icnnm_last_error(void);
 /* Library / device information. */
 const char* icnnm_version(void);
 int icnnm_device_count(void);
+/* Device blocks freed by finished calls are cached per device and reused by
+ * later calls (no cudaMalloc/cudaFree per solve); this hands them back to the
+ * driver.  ICNNM_DEVCACHE=0 disables the cache.  (No reference counterpart.) */
+int icnnm_empty_cache(void);
 
 /* ------------------------------------------------------------------------
  * Solver.  Replaces

@@ -101,6 +101,7 @@ SIGNATURES = {
     "icnnm_last_error": (C.c_char_p, []),
     "icnnm_version": (C.c_char_p, []),
     "icnnm_device_count": (C.c_int, []),
+    "icnnm_empty_cache": (C.c_int, []),
     "icnnm_cuda_solve": (C.c_int, [C.c_int, _lp, _dp, _dp, _lp, _dp, _dp,
                                    C.POINTER(SolverConfigC), C.c_int, _dp,
                                    C.POINTER(SolveReportC)]),
@@ -187,6 +188,8 @@ def lib():
                     " or `make -C paper_2604_17001_b200/csrc`")
             handle = C.CDLL(LIB_PATH)
             for name, (res, args) in SIGNATURES.items():
+                if os.environ.get("ICNNM_LIB_AB") and not hasattr(handle, name):
+                    continue  # A/B run against an older build
                 fn = getattr(handle, name)
                 fn.restype = res
                 fn.argtypes = args

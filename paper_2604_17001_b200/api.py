@@ -438,6 +438,11 @@ def device_count() -> int:
     return int(lib().icnnm_device_count())
 
 
+def empty_cache() -> None:
+    """Return the library's cached device blocks to the driver."""
+    check(lib().icnnm_empty_cache())
+
+
 def probe_ffma_tflops(device: int = 0) -> float:
     out = C.c_double()
     check(lib().icnnm_probe_ffma_tflops(device, C.byref(out)))

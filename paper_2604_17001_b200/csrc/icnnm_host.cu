@@ -20,6 +20,7 @@
 #include <array>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/icnnm_b200.h"
@@ -35,6 +36,119 @@ using icnnm_dev::IterStats;
 namespace icnnm_host {
 
 thread_local std::string g_last_error;
+
+// ICNNM_TIMING=1: host-side phase times of the C-ABI calls on stderr (where an
+// end-to-end call spends its time outside the device-resident loop).
+struct PhaseTimer {
+  bool on = std::getenv("ICNNM_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void reset() { t = std::chrono::steady_clock::now(); }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[icnnm timing] %-24s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+thread_local PhaseTimer g_timer;
+
+// ---------------------------------------------------------------------------
+// Device memory cache (declared in icnnm_host_common.h)
+// ---------------------------------------------------------------------------
+namespace {
+struct CachedBlock {
+  void* p;
+  size_t bytes;
+  int dev;
+};
+std::mutex g_cache_mu;
+std::vector<CachedBlock> g_cache;
+bool cache_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ICNNM_DEVCACHE");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+void cache_flush_device(int dev) {  // caller holds g_cache_mu
+  size_t w = 0;
+  for (size_t i = 0; i < g_cache.size(); ++i) {
+    if (g_cache[i].dev == dev)
+      cudaFree(g_cache[i].p);
+    else
+      g_cache[w++] = g_cache[i];
+  }
+  g_cache.resize(w);
+}
+}  // namespace
+
+void* devcache_alloc(size_t bytes) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (cache_enabled()) {
+    // smallest cached block of this device that fits without wasting > 1/8
+    size_t best = g_cache.size();
+    for (size_t i = 0; i < g_cache.size(); ++i) {
+      const CachedBlock& c = g_cache[i];
+      if (c.dev == dev && c.bytes >= bytes && c.bytes - bytes <= c.bytes / 8 &&
+          (best == g_cache.size() || c.bytes < g_cache[best].bytes))
+        best = i;
+    }
+    if (best < g_cache.size()) {
+      void* p = g_cache[best].p;
+      g_cache.erase(g_cache.begin() + static_cast<std::ptrdiff_t>(best));
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();  // clear, hand the cached blocks back, retry once
+    cache_flush_device(dev);
+    e = cudaMalloc(&p, bytes);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(ICNNM_CUDA_ERROR,
+         "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
+  }
+  return p;
+}
+
+void devcache_free(void* p, size_t bytes) {
+  if (!p) return;
+  if (!cache_enabled()) {
+    cudaFree(p);
+    return;
+  }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaFree(p);
+    return;
+  }
+  // unwinding from an error: work on the block may still be in flight
+  if (std::uncaught_exceptions() > 0) cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache.push_back({p, bytes, dev});
+}
+
+void devcache_empty() {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (int d = 0; d < n; ++d) {
+    bool any = false;
+    for (auto& c : g_cache) any = any || c.dev == d;
+    if (!any) continue;
+    cudaSetDevice(d);
+    cache_flush_device(d);
+  }
+  cudaSetDevice(prev);
+}
 
 // DenseTensor / KernelShape::validate_for (tensor.hpp:81-107).
 Problem make_problem(int order, const int64_t* dims, const int64_t* kdims) {
@@ -294,6 +408,65 @@ std::vector<float> pack_b_tiles_f16(const Problem& p, TcPlan& t, const double* K
   return out;
 }
 
+// The same F16x3 tiles packed on the device from an f64 copy of K (one thread
+// per tile element; bit-identical to pack_b_tiles_f16: x * 2^eB is exact in
+// f64, then one rounding to f32 and the two RN conversions to f16).
+__global__ void icnnm_pack_b_f16(int k, int kp, int wbase, int nkc, int kh, int kw, int kt,
+                                 int fwd, double sc, const double* __restrict__ K,
+                                 __half* __restrict__ out, int64_t total) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int k16 = static_cast<int>(i % icnnm_dev::tc::KC);
+  int64_t q = i / icnnm_dev::tc::KC;
+  const int n = static_cast<int>(q % wbase);
+  q /= wbase;
+  const int kc = static_cast<int>(q % nkc);
+  const int nt = static_cast<int>(q / nkc);
+  const int wn = min(wbase, kp - nt * wbase);
+  if (n >= wn) return;
+  const int nn = nt * wbase + n;
+  const int kk = kc * icnnm_dev::tc::KC + k16;
+  double x = 0.0;
+  if (nn < k && kk < k) {
+    if (fwd) {
+      x = K[static_cast<size_t>(nn) * k + kk];
+    } else {
+      const int sh = nn % kh, r = nn / kh, st = r % kt, sw = r / kt;
+      x = K[static_cast<size_t>(kk) * k + (sh * kw + sw) * kt + st];
+    }
+  }
+  const float xs = static_cast<float>(x * sc);
+  const __half hi = __float2half_rn(xs);
+  const __half lo = __float2half_rn(xs - __half2float(hi));
+  __half* base = out + (static_cast<size_t>(nt) * nkc + kc) * (icnnm_dev::tc::B_STAGE_BYTES / 2);
+  const size_t off = (n / 8) * 128 + (k16 / 8) * 64 + (n % 8) * 8 + (k16 % 8);
+  base[off] = hi;
+  base[static_cast<size_t>(wn) * 16 + off] = lo;
+}
+
+void pack_b_tiles_f16_device(const Problem& p, TcPlan& t, const double* dK, bool fwd,
+                             DBuf<float>& out, cudaStream_t stream) {
+  const int blk = icnnm_dev::tc::B_STAGE_BYTES / 4;
+  out.alloc(static_cast<size_t>(t.ntn) * t.nkc * blk);
+  CK(cudaMemsetAsync(out.p, 0, out.bytes(), stream));
+  const int eb = static_cast<int>(std::lround(-std::log2(static_cast<double>(t.bunscale))));
+  const int64_t total = static_cast<int64_t>(t.ntn) * t.nkc * t.wbase * icnnm_dev::tc::KC;
+  icnnm_pack_b_f16<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(
+      p.k, t.kp, t.wbase, t.nkc, static_cast<int>(p.kd[0]), static_cast<int>(p.kd[1]),
+      static_cast<int>(p.kd[2]), fwd ? 1 : 0, std::ldexp(1.0, eb), dK,
+      reinterpret_cast<__half*>(out.p), total);
+  CKL();
+}
+
+// B's power-of-2 scale for F16x3 (max|K| below 2^14): sets t.bunscale = 2^-eB.
+void f16_basis_scale(const Problem& p, TcPlan& t, const double* Kcm) {
+  double amax = 0.0;
+  for (size_t i = 0; i < static_cast<size_t>(p.k) * p.k; ++i) amax = std::max(amax, std::fabs(Kcm[i]));
+  int ex = 0;
+  if (amax > 0) std::frexp(amax, &ex);
+  t.bunscale = static_cast<float>(std::ldexp(1.0, -(14 - ex)));
+}
+
 std::vector<float> pack_b_tiles(const Problem& p, TcPlan& t, const double* Kcm, bool fwd) {
   if (t.f16) return pack_b_tiles_f16(p, t, Kcm, fwd);
   const int k = p.k;
@@ -422,22 +595,34 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
     const char* e = std::getenv("ICNNM_TC_WS");  // A/B experiments
     return e ? std::atoi(e) : icnnm_dev::tc::WS;
   }();
+  // Adjoint epilogue: a second 4-warp half (alternate 32-column blocks, its
+  // own 4 output bricks) when those bricks fit next to a B ring of >= 4
+  // stages; otherwise one half.  ICNNM_TC_EHALF=1|2 overrides (A/B).
+  static const int eh_env = [] {
+    const char* e = std::getenv("ICNNM_TC_EHALF");
+    return e ? std::atoi(e) : -1;
+  }();
   a.sb = 2;
   a.ws = 2;
+  a.ehalf = 1;
   bool found = false;
-  for (int sbv = std::min(sb_cap, icnnm_dev::tc::SB); sbv >= 2 && !found; --sbv)
-    for (int wsv = std::min(ws_cap, icnnm_dev::tc::WS) & ~1; wsv >= 2 && !found; wsv -= 2)
-      if (icnnm_dev::tc::smem_bytes(gtc, fwd, sbv, wsv, t.f16, pairs) <= 227 * 1024) {
-        a.sb = sbv;
-        a.ws = wsv;
-        found = true;
-      }
+  for (int eh = fwd ? 1 : (eh_env > 0 ? eh_env : 2); eh >= 1 && !found; --eh) {
+    const int sb_min = (eh == 2 && eh_env <= 0) ? std::min(4, sb_cap) : 2;
+    for (int sbv = std::min(sb_cap, icnnm_dev::tc::SB); sbv >= sb_min && !found; --sbv)
+      for (int wsv = std::min(ws_cap, icnnm_dev::tc::WS) & ~1; wsv >= 2 && !found; wsv -= 2)
+        if (icnnm_dev::tc::smem_bytes(gtc, fwd, sbv, wsv, t.f16, pairs, eh) <= 227 * 1024) {
+          a.sb = sbv;
+          a.ws = wsv;
+          a.ehalf = eh;
+          found = true;
+        }
+  }
   a.nbricks = n_bricks(gtc);
   int dev = 0, nsm = 148;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   void* args[] = {&a};
-  const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16, pairs);
+  const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16, pairs, a.ehalf);
   if (smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
   const dim3 block(icnnm_dev::tc::threads(fwd));
   void* fn = fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16, a.cs > 1)
@@ -489,18 +674,39 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
 // EigenBasis::validate (spectral.cpp:25-41).
 void validate_basis(int k, const double* K, const double* evals) {
   if (!K) invalid("EigenBasis: K must be k x k");
-  double worst = 0.0;
-  std::vector<double> col(k);
-  for (int i = 0; i < k; ++i) {
-    const double* ci = K + static_cast<size_t>(i) * k;
-    for (int j = 0; j <= i; ++j) {
-      const double* cj = K + static_cast<size_t>(j) * k;
-      double d = 0.0;
-      for (int r = 0; r < k; ++r) d += ci[r] * cj[r];
-      if (i == j) d -= 1.0;
-      worst = std::max(worst, std::fabs(d));
+  // max |K^T K - I| over the lower triangle, four independent partial sums per
+  // dot product (the check is a 1e-10 tolerance, so summation order is free);
+  // rows interleaved over up to 8 host threads for large k
+  auto rows = [&](int t0, int step) {
+    double worst = 0.0;
+    for (int i = t0; i < k; i += step) {
+      const double* ci = K + static_cast<size_t>(i) * k;
+      for (int j = 0; j <= i; ++j) {
+        const double* cj = K + static_cast<size_t>(j) * k;
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+        int r = 0;
+        for (; r + 4 <= k; r += 4) {
+          d0 += ci[r] * cj[r];
+          d1 += ci[r + 1] * cj[r + 1];
+          d2 += ci[r + 2] * cj[r + 2];
+          d3 += ci[r + 3] * cj[r + 3];
+        }
+        for (; r < k; ++r) d0 += ci[r] * cj[r];
+        double d = (d0 + d1) + (d2 + d3);
+        if (i == j) d -= 1.0;
+        if (!(std::fabs(d) <= worst)) worst = std::isnan(d) ? HUGE_VAL : std::fabs(d);
+      }
     }
-  }
+    return worst;
+  };
+  const int nth = k >= 128 ? static_cast<int>(std::max(1u, std::min(8u, std::thread::hardware_concurrency()))) : 1;
+  std::vector<double> part(nth, 0.0);
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nth; ++t) pool.emplace_back([&, t] { part[t] = rows(t, nth); });
+  part[0] = rows(0, nth);
+  for (auto& th : pool) th.join();
+  double worst = 0.0;
+  for (double w : part) worst = std::max(worst, w);
   if (!(worst <= 1e-10)) invalid("EigenBasis: K is not orthogonal");
   if (evals) {
     for (int i = 0; i < k; ++i) {
@@ -580,6 +786,8 @@ struct Solver {
   DBuf<unsigned long long> dbg;  // 2 x DBG_SLOTS tcgen05 pipeline counters
 
   ~Solver() {
+    // the buffers go back to the device cache: nothing may still use them
+    if (stream) cudaStreamSynchronize(stream);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (evs) cudaEventDestroy(evs);
@@ -596,6 +804,7 @@ void solver_alloc(Solver& S) {
   CK(cudaEventCreate(&S.ev1));
   CK(cudaEventCreate(&S.evs));
   set_smem_attrs();
+  g_timer.mark("stream/events/attrs");
   S.tp = tc_plan(p);
   S.tp16 = tc_plan(p, true);
   const int64_t WT = p.dims[1] * p.dims[2];
@@ -617,27 +826,7 @@ void solver_alloc(Solver& S) {
     s.W.alloc(std::max<int64_t>(n_bricks(s.g) * BM * p.kp, tc_w_elems(s.gtc, S.tp)));
     CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
   }
-  std::vector<float> Krm, KT;
-  pack_basis(p, S.K.data(), Krm, KT);
-  S.Krm.alloc(Krm.size());
-  S.KT.alloc(KT.size());
-  CK(cudaMemcpyAsync(S.Krm.p, Krm.data(), S.Krm.bytes(), cudaMemcpyHostToDevice, S.stream));
-  CK(cudaMemcpyAsync(S.KT.p, KT.data(), S.KT.bytes(), cudaMemcpyHostToDevice, S.stream));
-  {
-    auto bf = pack_b_tiles(p, S.tp, S.K.data(), true);
-    auto ba = pack_b_tiles(p, S.tp, S.K.data(), false);
-    auto hf = pack_b_tiles(p, S.tp16, S.K.data(), true);
-    auto ha = pack_b_tiles(p, S.tp16, S.K.data(), false);
-    S.BpkF.alloc(bf.size());
-    S.BpkA.alloc(ba.size());
-    S.BpkF16.alloc(hf.size());
-    S.BpkA16.alloc(ha.size());
-    CK(cudaMemcpyAsync(S.BpkF.p, bf.data(), S.BpkF.bytes(), cudaMemcpyHostToDevice, S.stream));
-    CK(cudaMemcpyAsync(S.BpkA.p, ba.data(), S.BpkA.bytes(), cudaMemcpyHostToDevice, S.stream));
-    CK(cudaMemcpyAsync(S.BpkF16.p, hf.data(), S.BpkF16.bytes(), cudaMemcpyHostToDevice, S.stream));
-    CK(cudaMemcpyAsync(S.BpkA16.p, ha.data(), S.BpkA16.bytes(), cudaMemcpyHostToDevice, S.stream));
-    CK(cudaStreamSynchronize(S.stream));
-  }
+  g_timer.mark("device buffers");
   const int kpmax = std::max(p.kp, S.tp.kp);
   S.cvec.alloc(kpmax);
   S.red.alloc(kpmax + 8);
@@ -749,6 +938,38 @@ inline int f16_debug_mask() {
   return m;
 }
 
+// The basis in the layout of one engine, packed and uploaded on the first run
+// that uses the engine (an end-to-end call packs only what it runs).
+void ensure_engine_basis(Solver& S, int engine) {
+  const Problem& p = S.p;
+  auto up = [&](DBuf<float>& d, const std::vector<float>& h) {
+    d.alloc(h.size());
+    CK(cudaMemcpyAsync(d.p, h.data(), d.bytes(), cudaMemcpyHostToDevice, S.stream));
+  };
+  if (engine == ICNNM_ENGINE_FFMA && !S.Krm.p) {
+    std::vector<float> Krm, KT;
+    pack_basis(p, S.K.data(), Krm, KT);
+    up(S.Krm, Krm);
+    up(S.KT, KT);
+    CK(cudaStreamSynchronize(S.stream));
+  }
+  const bool f16 = engine == ICNNM_ENGINE_F16X3;
+  if ((engine == ICNNM_ENGINE_TF32X3 || (f16 && f16_debug_mask())) && !S.BpkF.p) {
+    up(S.BpkF, pack_b_tiles(p, S.tp, S.K.data(), true));
+    up(S.BpkA, pack_b_tiles(p, S.tp, S.K.data(), false));
+    CK(cudaStreamSynchronize(S.stream));
+  }
+  if (f16 && !S.BpkF16.p) {
+    // packed on the device (host packing cost ~9 ms per call at k = 405)
+    f16_basis_scale(p, S.tp16, S.K.data());
+    DBuf<double> dK(static_cast<size_t>(p.k) * p.k);
+    CK(cudaMemcpyAsync(dK.p, S.K.data(), dK.bytes(), cudaMemcpyHostToDevice, S.stream));
+    pack_b_tiles_f16_device(p, S.tp16, dK.p, true, S.BpkF16, S.stream);
+    pack_b_tiles_f16_device(p, S.tp16, dK.p, false, S.BpkA16, S.stream);
+    CK(cudaStreamSynchronize(S.stream));
+  }
+}
+
 void launch_fwd(Solver& S, Slab& s, int mode) {
   // mode 2 (exact residual): forward on L_{t+1}, epilogue sums the gap into slot[5]
   const float* src = mode == 2 ? s.Lr.p : s.Lt.p;
@@ -801,6 +1022,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   if (!S.uploaded) invalid("solve: no problem uploaded");
   const Problem& p = S.p;
   S.engine = cfg.engine;
+  ensure_engine_basis(S, S.engine);
   S.exact_res = cfg.exact_residual != 0;
   const int kpe = engine_kp(S);
   if (S.exact_res)
@@ -985,7 +1207,9 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     };
     // launch accounting: capture counts the TC/FFMA launches of one iteration
     const int64_t l0 = S.launches;
+    g_timer.mark("run: schedule/staging");
     cudaGraphExec_t gx = capture(true, U, one);
+    g_timer.mark("run: capture+instantiate");
     const int64_t captured = S.launches - l0;
     S.launches = l0;
     // per iteration: coef + update per slab + the counted engine launches
@@ -994,6 +1218,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
                              static_cast<int64_t>(S.slabs.size());
     cudaGraphExec_t gr = one ? nullptr : capture(false, U, false);
     CK(cudaStreamSynchronize(S.stream));  // uploads done; nothing of this solve has run
+    g_timer.mark("run: graph upload");
     CK(cudaGraphLaunch(gx, S.stream));
     S.launches += setup_l + per_iter * U;
     for (int it = U; it < iters; it += U) {
@@ -1016,6 +1241,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
                      S.stream));
   CK(cudaMemcpyAsync(&R.st, S.st.p, sizeof(IterState), cudaMemcpyDeviceToHost, S.stream));
   CK(cudaStreamSynchronize(S.stream));
+  g_timer.mark("run: device solve");
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, S.ev0, S.ev1));
   R.loop_ms = ms;
@@ -1106,6 +1332,10 @@ int icnnm_validate_config(const icnnm_solver_config* cfg) {
 
 const char* icnnm_last_error(void) { return g_last_error.c_str(); }
 
+int icnnm_empty_cache(void) {
+  return guard([&] { devcache_empty(); });
+}
+
 const char* icnnm_version(void) { return "icnnm_b200 0.1 (sm_100a)"; }
 
 int icnnm_device_count(void) {
@@ -1150,6 +1380,7 @@ int icnnm_solver_run(icnnm_solver_t h, const icnnm_solver_config* cfg,
     if (!h) invalid("null handle");
     validate_cfg(cfg);
     DeviceScope ds(h->S.device);
+    g_timer.reset();
     auto t0 = std::chrono::steady_clock::now();
     RunResult R = solver_run(h->S, *cfg);
     double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1221,23 +1452,30 @@ int icnnm_cuda_solve(int order, const int64_t* dims, const double* M_obs, const 
                      icnnm_solve_report* report) {
   return guard([&] {
     auto t0 = std::chrono::steady_clock::now();
+    g_timer.reset();
     validate_cfg(cfg);
     Problem p = make_problem(order, dims, kdims);
     if (!L_out) invalid("null output");
     validate_basis(p.k, K_colmajor, eigenvalues);
+    g_timer.mark("validate basis");
     DeviceScope ds(device);
-    Solver S;
-    S.p = p;
-    S.device = device;
-    S.K.assign(K_colmajor, K_colmajor + static_cast<size_t>(p.k) * p.k);
-    S.slabs.resize(1);
-    S.slabs[0].rows = p.dims[0];
-    solver_alloc(S);
-    solver_upload(S, M_obs, mask);
-    RunResult R = solver_run(S, *cfg);
-    solver_download(S, L_out);
-    double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    fill_report(S, *cfg, R, report, wall);
+    {
+      Solver S;
+      S.p = p;
+      S.device = device;
+      S.K.assign(K_colmajor, K_colmajor + static_cast<size_t>(p.k) * p.k);
+      S.slabs.resize(1);
+      S.slabs[0].rows = p.dims[0];
+      solver_alloc(S);
+      solver_upload(S, M_obs, mask);
+      g_timer.mark("upload (validate+H2D)");
+      RunResult R = solver_run(S, *cfg);
+      solver_download(S, L_out);
+      g_timer.mark("download");
+      double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      fill_report(S, *cfg, R, report, wall);
+    }
+    g_timer.mark("release");
   });
 }
 

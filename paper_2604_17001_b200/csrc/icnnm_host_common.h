@@ -62,34 +62,47 @@ int guard(F&& f) {
 // ---------------------------------------------------------------------------
 // Device buffers
 // ---------------------------------------------------------------------------
+// Device memory cache (icnnm_host.cu).  Freed blocks stay with the process,
+// per device, and serve later allocations of the same size class: a
+// one-shot C-ABI solve allocates ~1 GB of state at config 2, and handing it
+// back to the driver (cudaFree unmaps and synchronises) cost 0.2-0.3 s per
+// call on B200.  An allocation that fails first returns the device's cached
+// blocks to the driver and retries.  Callers free only after the work using
+// a block has completed (every C-ABI call synchronises its stream first).
+void* devcache_alloc(size_t bytes);
+void devcache_free(void* p, size_t bytes);
+void devcache_empty();
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  size_t cap = 0;  // bytes of the block behind p
   DBuf() = default;
   explicit DBuf(size_t count) { alloc(count); }
   void alloc(size_t count) {
     release();
-    n = count;
     if (count) {
-      cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-      if (e != cudaSuccess) {
-        p = nullptr;
-        fail(ICNNM_CUDA_ERROR, "cudaMalloc(" + std::to_string(count * sizeof(T)) +
-                                   " bytes): " + cudaGetErrorString(e));
-      }
+      p = static_cast<T*>(devcache_alloc(count * sizeof(T)));
+      cap = count * sizeof(T);
     }
+    n = count;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) devcache_free(p, cap);
     p = nullptr;
     n = 0;
+    cap = 0;
   }
   size_t bytes() const { return n * sizeof(T); }
   ~DBuf() { release(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), cap(o.cap) {
+    o.p = nullptr;
+    o.n = 0;
+    o.cap = 0;
+  }
 };
 
 struct DeviceScope {

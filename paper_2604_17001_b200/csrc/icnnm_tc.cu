@@ -419,12 +419,12 @@ __device__ __forceinline__ void tg_seq(int i, int gsz, int nkc, int D, int& t, i
 //   warp  9 + NEPI          B loader
 // ---------------------------------------------------------------------------
 template <bool FWD, bool F16, bool PAIR>
-__global__ void __launch_bounds__(FWD ? 608 : 480, 1)
+__global__ void __launch_bounds__(608, 1)
 icnnm_tc_kernel(TcArgs a) {
   constexpr int ASC = F16 ? KC : 2 * KC;  // TMEM columns per A stage
   constexpr int ALO = ASC / 2;            // column offset of the lo half
   constexpr int NB = 8;                  // builder warps
-  constexpr int NEPI = FWD ? 8 : 4;      // epilogue warps
+  constexpr int NEPI = 8;                // epilogue warps (adjoint: 4 * a.ehalf active)
   constexpr int WMMA = NB + NEPI;        // MMA warp
   constexpr int WLOAD = NB + NEPI + 1;   // B loader warp; W loader warp after it
   constexpr int BSTG = F16 ? (PAIR ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES;  // B stage stride
@@ -466,12 +466,16 @@ icnnm_tc_kernel(TcArgs a) {
   const int nob = g.HH * g.HW * g.HT;
   const int nobp = ((nob + 3) / 4) * 4;
   // FWD: halo[2] (2 x nobp) | nrm (kp doubles)
-  // ADJ: 4 output bricks (4 x nobp)
+  // ADJ: 4 * ehalf output bricks (nobp + 32 each)
   float* halo = reinterpret_cast<float*>(p);
   double* nrm = reinterpret_cast<double*>(halo + 2 * nobp);
   float* ob = reinterpret_cast<float*>(p);
 
   const int tid = threadIdx.x;
+  // adjoint epilogue: active 4-warp halves, each with its own 4 output bricks
+  // (two halves take alternate 32-column blocks of every accumulator)
+  const int ehalf = FWD ? 2 : (a.ehalf > 1 ? 2 : 1);
+  const int nepi_act = 4 * ehalf;
   // warp index through a shuffle: provably warp-uniform, so role branches are
   // uniform and the MMA issuer's counters can live in uniform registers
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
@@ -501,7 +505,7 @@ icnnm_tc_kernel(TcArgs a) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(ACC_full + i, 1);
-      mbar_init(ACC_empty + i, PAIR ? 2 * NEPI : NEPI * 32);
+      mbar_init(ACC_empty + i, PAIR ? 2 * nepi_act : nepi_act * 32);
     }
     for (int i = 0; i < WS; ++i) {
       mbar_init(W_full + i, 1);
@@ -546,7 +550,7 @@ icnnm_tc_kernel(TcArgs a) {
   if (FWD) {
     for (int j = tid; j < g.kp; j += blockDim.x) nrm[j] = 0.0;
   } else {
-    for (int e = tid; e < 4 * (nobp + 32); e += blockDim.x) ob[e] = 0.f;
+    for (int e = tid; e < nepi_act * (nobp + 32); e += blockDim.x) ob[e] = 0.f;
   }
   tc_fence_before();
   if (PAIR)
@@ -784,7 +788,7 @@ icnnm_tc_kernel(TcArgs a) {
     }
     dbg.flush(DBG_BUILD_WAIT, DBG_BUILD_WORK);
   } else if (warp < NB) {
-  } else if (warp < NB + NEPI && !(a.skip & 32)) {
+  } else if (warp < NB + nepi_act && !(a.skip & 32)) {
     // ===================== epilogue =====================
     const int ew = warp - NB;
     const int quad = ew & 3, half = ew >> 2;     // half in {0} (adjoint) or {0,1} (forward)
@@ -793,8 +797,8 @@ icnnm_tc_kernel(TcArgs a) {
     const int vt = row % g.bt, vw = (row / g.bt) % g.bw, vh = row / (g.bt * g.bw);
     const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
     const int obs = nobp + 32;             // output-brick stride (+32 scratch)
-    float* myob = ob + quad * obs;
-    constexpr int NHALF = NEPI / 4;
+    float* myob = ob + (FWD ? quad : ew) * obs;  // adjoint: one output brick per warp
+    const int NHALF = ehalf;
     uint32_t gbase = 0;  // forward: W-group ring slot of the current tile's first group
     float gacc = 0.f;  // mode 2: this thread's share of ||(1-c)W - A(L)K||^2
     uint32_t tcount = 0;
@@ -875,10 +879,14 @@ icnnm_tc_kernel(TcArgs a) {
                 }
                 fence_proxy_async_smem();   // the bulk store reads these writes
                 named_sync(3 + half, 128);
-                // column norms: lane l sums column l over this warp's 32 rows
-                // (float4 index rotated by lane: conflict-free, 4 wavefronts per
-                // load); the 4 warps of the half add their partials
-                const float* colp = st + lane * 128 + quad * 32;
+                // column norms: warp `quad` owns columns 8 quad .. 8 quad + 7, four
+                // lanes per column, each over 32 of the 128 rows (float4 index
+                // rotated by lane & 7: conflict-free within every quarter-warp),
+                // combined with two shuffles; one thread per column of the CTA
+                // then adds into nrm without an atomic (the columns of a group
+                // belong to one half, and a half's warps own disjoint columns)
+                const int cl = 8 * quad + (lane >> 2);
+                const float* colp = st + cl * 128 + (lane & 3) * 32;
                 float sq = 0.f;
 #pragma unroll
                 for (int k4 = 0; k4 < 8; ++k4) {
@@ -888,7 +896,9 @@ icnnm_tc_kernel(TcArgs a) {
                   sq = fmaf(v.z, v.z, sq);
                   sq = fmaf(v.w, v.w, sq);
                 }
-                if (breal && lane < ncol) atomicAdd(nrm + j0 + lane, static_cast<double>(sq));
+                sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+                sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+                if (breal && (lane & 3) == 0 && cl < ncol) nrm[j0 + cl] += static_cast<double>(sq);
                 const int t = quad * 32 + lane;
                 if (t == 0 && breal) {
                   bulk_s2g(a.Wout + (static_cast<size_t>(b) * g.kp + j0) * 128, st,
@@ -957,17 +967,14 @@ icnnm_tc_kernel(TcArgs a) {
         }
       }
       if (!FWD) {
-        named_sync(2, NEPI * 32);
-        for (int e = row; e < nob; e += 128) {
-          if (!breal) {  // dummy brick: clear the output bricks, write nothing
-            ob[e] = ob[obs + e] = ob[2 * obs + e] = ob[3 * obs + e] = 0.f;
-            continue;
+        named_sync(2, nepi_act * 32);
+        for (int e = ew * 32 + lane; e < nob; e += nepi_act * 32) {
+          float s = 0.f;
+          for (int q = 0; q < nepi_act; ++q) {
+            s += ob[q * obs + e];
+            ob[q * obs + e] = 0.f;
           }
-          float s = ob[e] + ob[obs + e] + ob[2 * obs + e] + ob[3 * obs + e];
-          ob[e] = 0.f;
-          ob[obs + e] = 0.f;
-          ob[2 * obs + e] = 0.f;
-          ob[3 * obs + e] = 0.f;
+          if (!breal) continue;  // dummy brick: output bricks cleared, nothing written
           if (s == 0.f) continue;
           int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
           int hs = h0 - (g.kh - 1) + aa + g.hoff;
@@ -977,7 +984,7 @@ icnnm_tc_kernel(TcArgs a) {
           int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
           atomicAdd(a.adj + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts, s);
         }
-        named_sync(2, NEPI * 32);
+        named_sync(2, nepi_act * 32);
       }
     }
     dbg.flush(DBG_EPI_WAIT, DBG_EPI_WORK);

@@ -59,6 +59,8 @@ struct TcArgs {
   int grp;                  // N-tiles per tile group sharing each built A chunk (1 or 2)
   int skew;                 // tile-group schedule skew D (chunks), see tg_seq
   int cs;                   // 2: CTA pairs (cta_group::2, M = 256, B split by N); 1: single CTAs
+  int ehalf;                // adjoint: epilogue halves in use (1 or 2; 4 warps and 4 output
+                            // bricks each -- 2 when the extra output bricks fit in SMEM)
 };
 
 // dbg slots (cycles summed over CTAs)
@@ -71,9 +73,11 @@ __global__ void icnnm_tc_kernel(TcArgs a);
 void* fwd_kernel_ptr(bool f16, bool pair = false);
 void* adj_kernel_ptr(bool f16, bool pair = false);
 
-inline int threads(bool fwd) { return fwd ? 608 : 480; }
+// 8 builder + 8 epilogue + MMA + B loader + W loader warps (both kernels)
+inline int threads(bool) { return 608; }
 
-inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16, bool pair = false) {
+inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16, bool pair = false,
+                         int ehalf = 1) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
   const size_t nobp = ((nob + 3) / 4) * 4;
   size_t b = static_cast<size_t>(sb) * b_stage_bytes(f16, pair) +
@@ -83,7 +87,7 @@ inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16, bool 
   if (fwd)
     b += 2 * nobp * 4 + static_cast<size_t>(g.kp) * 8;
   else
-    b += 4 * (nobp + 32) * 4;
+    b += static_cast<size_t>(4 * ehalf) * (nobp + 32) * 4;
   return b;
 }
 
