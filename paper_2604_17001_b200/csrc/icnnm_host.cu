@@ -590,7 +590,9 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
     const char* e = std::getenv("ICNNM_TC_SB");
     return e ? std::atoi(e) : -1;
   }();
-  const int sb_cap = sb_env > 0 ? sb_env : (pairs ? 8 : 4);
+  // F16x3 single CTAs: 8 stages (+1.8% / +1.3% over 4 / 6 on config 2,
+  // profiles/ab_r1/tune/, profiles/ab_r1/sb8/)
+  const int sb_cap = sb_env > 0 ? sb_env : (pairs ? 8 : (t.f16 ? 8 : 4));
   static const int ws_cap = [] {
     const char* e = std::getenv("ICNNM_TC_WS");  // A/B experiments
     return e ? std::atoi(e) : icnnm_dev::tc::WS;
@@ -938,6 +940,20 @@ inline int f16_debug_mask() {
   return m;
 }
 
+// icnnm_update grid: one resident wave (SMs x resident blocks of 256), capped
+// by the work (UPD_U elements per thread).
+int update_grid(int64_t m) {
+  static const int wave = [] {
+    int dev = 0, nsm = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, icnnm_dev::icnnm_update, 256, 0);
+    return nsm * std::max(1, per);
+  }();
+  const int64_t need = (m + 256 * icnnm_dev::UPD_U - 1) / (256 * icnnm_dev::UPD_U);
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(need, wave)));
+}
+
 // The basis in the layout of one engine, packed and uploaded on the first run
 // that uses the engine (an end-to-end call packs only what it runs).
 void ensure_engine_basis(Solver& S, int engine) {
@@ -1054,7 +1070,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     for (auto& s : S.slabs) launch_adj(S, s);
     exchange_adj(S);
     for (auto& s : S.slabs) {
-      icnnm_dev::icnnm_update<<<grid_for(s.m_own, 256, 148 * 8), 256, 0, S.stream>>>(
+      icnnm_dev::icnnm_update<<<update_grid(s.m_own), 256, 0, S.stream>>>(
           s.m_own, S.st.p, cfg.lambda, kd, s.adj.p + s.halo_elems, s.L.p, s.V.p, s.pm.p,
           s.mask.p, s.Lt.p + s.halo_elems, S.red.p + kpe,
           S.exact_res ? s.Lr.p + s.halo_elems : nullptr);
@@ -1150,7 +1166,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
       exchange_adj(S);
       CK(cudaEventRecord(e[2], S.stream));
       for (auto& s : S.slabs) {
-        icnnm_dev::icnnm_update<<<grid_for(s.m_own, 256, 148 * 8), 256, 0, S.stream>>>(
+        icnnm_dev::icnnm_update<<<update_grid(s.m_own), 256, 0, S.stream>>>(
             s.m_own, S.st.p, cfg.lambda, kd, s.adj.p + s.halo_elems, s.L.p, s.V.p, s.pm.p,
             s.mask.p, s.Lt.p + s.halo_elems, S.red.p + kpe,
             S.exact_res ? s.Lr.p + s.halo_elems : nullptr);

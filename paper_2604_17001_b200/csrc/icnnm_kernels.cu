@@ -492,6 +492,11 @@ __global__ void icnnm_coef(IterState* st, const double* __restrict__ theta,
 //   V <- r (k L_old - adj - k L_new)           (V = A*(Y/theta K^T))
 // plus the fp64 partial sums of the report (fit, ||D||, ||L||, residual).
 // ---------------------------------------------------------------------------
+// One resident wave (grid = SMs x resident blocks, host); each thread loads
+// UPD_U elements (stride = grid size) before computing, so every thread keeps
+// 5 x UPD_U independent loads in flight (the one-element-per-thread form was
+// latency-bound at 34 us for 27 MB at config 2: long-scoreboard stalls, 5% of
+// HBM bandwidth).
 __global__ void __launch_bounds__(256)
 icnnm_update(int64_t m, const IterState* __restrict__ st, double lambda, double kd,
              float* __restrict__ adj, double* __restrict__ L, double* __restrict__ V,
@@ -502,26 +507,45 @@ icnnm_update(int64_t m, const IterState* __restrict__ st, double lambda, double 
   const double r = st->r;
   const double ck = th / kd;
   double acc[5] = {0, 0, 0, 0, 0};  // dl2, l2o, fit, ip, ln2
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double a = adj[i];
-    const double lo = L[i];
-    const double mk = mask[i];
-    const double p = pm[i];
-    const double d = (lambda * (p - mk * lo) - ck * a) / (lambda * mk + th);
-    const double ln = lo + d;
-    const double v = V[i];
-    L[i] = ln;
-    Lt[i] = static_cast<float>(ln + r * d);
-    if (Lr != nullptr) Lr[i] = static_cast<float>(ln);
-    adj[i] = 0.f;
-    V[i] = r * (kd * lo - a - kd * ln);
-    const double f = mk * (ln - p);
-    acc[0] += d * d;
-    acc[1] += lo * lo;
-    acc[2] += f * f;
-    acc[3] += (kd * lo - v - a) * ln;
-    acc[4] += ln * ln;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < m;
+       i0 += UPD_U * stride) {
+    float a_[UPD_U], mk_[UPD_U], p_[UPD_U];
+    double lo_[UPD_U], v_[UPD_U];
+#pragma unroll
+    for (int u = 0; u < UPD_U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < m) {
+        a_[u] = adj[i];
+        lo_[u] = L[i];
+        mk_[u] = mask[i];
+        p_[u] = pm[i];
+        v_[u] = V[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UPD_U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= m) break;
+      const double a = a_[u];
+      const double lo = lo_[u];
+      const double mk = mk_[u];
+      const double p = p_[u];
+      const double d = (lambda * (p - mk * lo) - ck * a) / (lambda * mk + th);
+      const double ln = lo + d;
+      const double v = v_[u];
+      L[i] = ln;
+      Lt[i] = static_cast<float>(ln + r * d);
+      if (Lr != nullptr) Lr[i] = static_cast<float>(ln);
+      adj[i] = 0.f;
+      V[i] = r * (kd * lo - a - kd * ln);
+      const double f = mk * (ln - p);
+      acc[0] += d * d;
+      acc[1] += lo * lo;
+      acc[2] += f * f;
+      acc[3] += (kd * lo - v - a) * ln;
+      acc[4] += ln * ln;
+    }
   }
   block_reduce_add<5>(acc, slot);
 }

@@ -72,6 +72,7 @@ __global__ void icnnm_adj_ffma(Geo g, const float* Wm, const float* KT, const fl
 __global__ void icnnm_coef(IterState* st, const double* theta, double* red, float* cvec,
                            IterStats* stats, int k, int kp, double kd, double res_scale,
                            double tol_p, double tol_c, double floor_rel, int exact);
+constexpr int UPD_U = 4;  // elements in flight per thread (icnnm_update)
 __global__ void icnnm_update(int64_t m, const IterState* st, double lambda, double kd,
                              float* adj, double* L, double* V, const float* pm,
                              const float* mask, float* Lt, double* slot, float* Lr);

@@ -476,6 +476,15 @@ icnnm_tc_kernel(TcArgs a) {
   // (two halves take alternate 32-column blocks of every accumulator)
   const int ehalf = FWD ? 2 : (a.ehalf > 1 ? 2 : 1);
   const int nepi_act = 4 * ehalf;
+  // CTA pairs: barriers completed by the peer (remote arrives, multicast
+  // commits) are waited on with cluster-scope acquire; skip bit 64 (A/B
+  // experiment) uses the default CTA-scope wait, as CUTLASS's 2-SM pipelines do
+  auto pwait = [&](uint64_t* b, uint32_t ph) {
+    if (a.skip & 64)
+      mbar_wait(b, ph);
+    else
+      mbar_wait_cluster(b, ph);
+  };
   // warp index through a shuffle: provably warp-uniform, so role branches are
   // uniform and the MMA issuer's counters can live in uniform registers
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
@@ -662,7 +671,7 @@ icnnm_tc_kernel(TcArgs a) {
           const uint32_t wph = (cnt / wsn) & 1;
           long long t0c = dbg.p ? clk() : 0;
           if (PAIR)
-            mbar_wait_cluster(A_empty + sa, ph ^ 1);  // released by the leader's MMAs
+            pwait(A_empty + sa, ph ^ 1);  // released by the leader's MMAs
           else
             mbar_wait(A_empty + sa, ph ^ 1);
           if (!FWD) mbar_wait(W_full + wsi, wph);
@@ -1036,7 +1045,7 @@ icnnm_tc_kernel(TcArgs a) {
           long long q0 = a.dbg ? clk() : 0;
           if (!(a.skip & 32)) {
             if (PAIR)
-              mbar_wait_cluster(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
+              pwait(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
             else
               mbar_wait(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
           }
@@ -1045,14 +1054,14 @@ icnnm_tc_kernel(TcArgs a) {
         long long q1 = a.dbg ? clk() : 0;
         if (first_use && !(a.skip & 8)) {
           if (PAIR)
-            mbar_wait_cluster(A_full + sa, aph);
+            pwait(A_full + sa, aph);
           else
             mbar_wait(A_full + sa, aph);
         }
         long long q2 = a.dbg ? clk() : 0;
         if (!(a.skip & 16)) {
           if (PAIR)
-            mbar_wait_cluster(B_full + sb, bph);
+            pwait(B_full + sb, bph);
           else
             mbar_wait(B_full + sb, bph);
         }
@@ -1178,7 +1187,7 @@ icnnm_tc_kernel(TcArgs a) {
             const int sb = bcnt % sbn;
             long long q0 = a.dbg ? clk() : 0;
             if (PAIR)
-              mbar_wait_cluster(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
+              pwait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
             else
               mbar_wait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
             if (a.dbg) wl += clk() - q0;
@@ -1207,7 +1216,7 @@ icnnm_tc_kernel(TcArgs a) {
       // this CTA have landed) before the final cluster sync
       if (PAIR)
         for (int q = 0; q < sbn; ++q, ++bcnt)
-          mbar_wait_cluster(B_empty + bcnt % sbn, ((bcnt / sbn) & 1) ^ 1);
+          pwait(B_empty + bcnt % sbn, ((bcnt / sbn) & 1) ^ 1);
       if (a.dbg) atomicAdd(a.dbg + DBG_LOAD_WAIT, static_cast<unsigned long long>(wl));
     }
     __syncwarp();
