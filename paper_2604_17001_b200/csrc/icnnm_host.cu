@@ -579,6 +579,13 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   a.cs = cs_env >= 0 ? cs_env : 1;  // pairs: opt-in until they beat single CTAs
   if (!t.f16 || n_bricks(gtc) < 2) a.cs = 1;
   const bool pairs = a.cs > 1;
+  // B multicast (F16x3 single CTAs in 2-CTA clusters sharing one B stream, each
+  // CTA loading half of every stage): ICNNM_TC_MCB=1 (A/B experiment)
+  static const int mcb_env = [] {
+    const char* e = std::getenv("ICNNM_TC_MCB");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.mcb = (mcb_env > 0 && t.f16 && !pairs && n_bricks(gtc) >= 2) ? 1 : 0;
   // F16x3 B stages are 16 KB (half the TF32 stage), which leaves room for
   // an 8-deep forward W-group ring: a 208-column tile has 8 W groups, so the
   // whole tile's W_old is in flight before its epilogue starts.  Deepest B
@@ -629,8 +636,8 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   const dim3 block(icnnm_dev::tc::threads(fwd));
   void* fn = fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16, a.cs > 1)
                  : icnnm_dev::tc::adj_kernel_ptr(t.f16, a.cs > 1);
-  if (a.cs > 1) {
-    // persistent grid: as many pairs as can be co-resident (pairs live in one GPC)
+  if (a.cs > 1 || a.mcb) {
+    // persistent grid: as many 2-CTA clusters as can be co-resident (one GPC each)
     static std::map<std::pair<void*, size_t>, int> max_pairs;
     static std::mutex mp_mu;
     std::lock_guard<std::mutex> lk(mp_mu);

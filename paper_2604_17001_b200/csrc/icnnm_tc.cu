@@ -79,6 +79,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Multicast bulk copy: the bytes land at the same shared-memory offset in every
+// CTA of ctaMask, each of whose mbarrier at the same offset gets complete_tx.
+__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
                    : "memory");
@@ -246,6 +256,39 @@ __device__ __forceinline__ void tc_chunk_f16(uint32_t d, uint32_t a, uint32_t al
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, t;\n"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, t;\n"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n"
+      "@qa tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n"
+      "@qc tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n"
+      "}\n" ::"r"(d),
+      "r"(a), "r"(alo), "l"(dh), "l"(dl), "r"(idesc), "r"(accum), "r"(bar_b), "r"(bar_a),
+      "r"(bar_acc), "r"(flags)
+      : "memory");
+}
+// tc_chunk_f16 for B-multicast clusters: the B-stage release is committed to
+// the barrier at the same offset in both CTAs of the 2-CTA cluster (the stage
+// is refilled, for both, only after both CTAs' MMAs have read it).
+__device__ __forceinline__ void tc_chunk_f16_mcb(uint32_t d, uint32_t a, uint32_t alo, uint64_t dh,
+                                                 uint64_t dl, uint32_t idesc, uint32_t accum,
+                                                 uint32_t bar_b, uint32_t bar_a, uint32_t bar_acc,
+                                                 uint32_t flags) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t, qa, qc;\n"
+      ".reg .b32 f;\n"
+      ".reg .b16 m;\n"
+      "mov.b16 m, 3;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "setp.eq.b32 t, %6, %6;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "and.b32 f, %10, 1;\n"
+      "setp.ne.b32 qa, f, 0;\n"
+      "and.b32 f, %10, 2;\n"
+      "setp.ne.b32 qc, f, 0;\n"
+      "and.pred qa, qa, e;\n"
+      "and.pred qc, qc, e;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, t;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], m;\n"
       "@qa tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n"
       "@qc tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n"
       "}\n" ::"r"(d),
@@ -475,6 +518,11 @@ icnnm_tc_kernel(TcArgs a) {
   // adjoint epilogue: active 4-warp halves, each with its own 4 output bricks
   // (two halves take alternate 32-column blocks of every accumulator)
   const int ehalf = FWD ? 2 : (a.ehalf > 1 ? 2 : 1);
+  // B multicast: a 2-CTA cluster of independent CTAs (own bricks, own M = 128
+  // MMAs) consuming one B stream; each CTA loads half of every B stage and
+  // multicasts it to both, so the L2 -> SM traffic of the basis halves
+  const bool MCB = !PAIR && F16 && a.mcb != 0;
+  const bool CL2 = PAIR || MCB;  // launched as 2-CTA clusters
   const int nepi_act = 4 * ehalf;
   // CTA pairs: barriers completed by the peer (remote arrives, multicast
   // commits) are waited on with cluster-scope acquire; skip bit 64 (A/B
@@ -510,7 +558,7 @@ icnnm_tc_kernel(TcArgs a) {
     }
     for (int i = 0; i < SB; ++i) {
       mbar_init(B_full + i, (PAIR && (blockIdx.x & 1u) == 0) ? 2 : 1);
-      mbar_init(B_empty + i, 1);
+      mbar_init(B_empty + i, MCB ? 2 : 1);  // MCB: released by both CTAs' MMAs
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(ACC_full + i, 1);
@@ -562,7 +610,7 @@ icnnm_tc_kernel(TcArgs a) {
     for (int e = tid; e < nepi_act * (nobp + 32); e += blockDim.x) ob[e] = 0.f;
   }
   tc_fence_before();
-  if (PAIR)
+  if (CL2)
     cluster_sync_all();  // the peer's barriers are initialised before any remote arrive / commit
   else
     __syncthreads();
@@ -581,7 +629,7 @@ icnnm_tc_kernel(TcArgs a) {
   // cs*s + crank of slot s, so both CTAs of a pair walk the same number of
   // slots (they consume one multicast B stream in lockstep); a pair's odd
   // tail brick is a dummy (brick nbr-1 re-read, nothing written).
-  const int ncta = PAIR ? 2 : 1;
+  const int ncta = CL2 ? 2 : 1;
   const int crank = ncta > 1 ? static_cast<int>(blockIdx.x & 1u) : 0;
   const int sfirst = static_cast<int>(blockIdx.x) / ncta;
   const int sstep = static_cast<int>(gridDim.x) / ncta;
@@ -1082,6 +1130,11 @@ icnnm_tc_kernel(TcArgs a) {
                             kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
                             bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
                             (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
+        } else if (MCB && !(a.skip & 24)) {
+          tc_chunk_f16_mcb(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + wn * 32), idesc,
+                           kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
+                           bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
+                           (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
         } else if (F16 && !(a.skip & 24)) {
           tc_chunk_f16(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + wn * 32), idesc,
                        kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
@@ -1186,7 +1239,7 @@ icnnm_tc_kernel(TcArgs a) {
             const uint32_t bytes = static_cast<uint32_t>(wn) * KC * (F16 ? 4 : 8);
             const int sb = bcnt % sbn;
             long long q0 = a.dbg ? clk() : 0;
-            if (PAIR)
+            if (CL2)
               pwait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
             else
               mbar_wait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
@@ -1205,6 +1258,15 @@ icnnm_tc_kernel(TcArgs a) {
               mbar_arrive_expect_tx(B_full + sb, 2u * hb);
               bulk_g2s(dst, sb8 + crank * hb, hb, B_full + sb);
               bulk_g2s(dst + hb, sb8 + static_cast<uint32_t>(wn) * 32u + crank * hb, hb, B_full + sb);
+            } else if (MCB) {
+              // this CTA's half of the stage, multicast to both CTAs; the
+              // local B_full expects the whole stage (both halves)
+              const uint32_t h0 = ((bytes / 2) + 15u) & ~15u;
+              const uint32_t mine = crank == 0 ? h0 : bytes - h0;
+              const uint32_t off = crank == 0 ? 0u : h0;
+              mbar_arrive_expect_tx(B_full + sb, bytes);
+              bulk_g2s_mc(dst + off, reinterpret_cast<const uint8_t*>(src) + off, mine, B_full + sb,
+                          static_cast<uint16_t>(3));
             } else {
               mbar_arrive_expect_tx(B_full + sb, bytes);
               bulk_g2s(dst, src, bytes, B_full + sb);
@@ -1212,9 +1274,9 @@ icnnm_tc_kernel(TcArgs a) {
           }
         }
       }
-      // drain: every stage released by the leader's MMAs (their commits into
-      // this CTA have landed) before the final cluster sync
-      if (PAIR)
+      // drain: every stage released by the MMAs that signal into this CTA
+      // (the leader's, or both CTAs' under MCB) before the final cluster sync
+      if (CL2)
         for (int q = 0; q < sbn; ++q, ++bcnt)
           pwait(B_empty + bcnt % sbn, ((bcnt / sbn) & 1) ^ 1);
       if (a.dbg) atomicAdd(a.dbg + DBG_LOAD_WAIT, static_cast<unsigned long long>(wl));
@@ -1273,7 +1335,7 @@ icnnm_tc_kernel(TcArgs a) {
   }
 
   tc_fence_before();
-  if (PAIR)
+  if (CL2)
     cluster_sync_all();  // no CTA leaves while its peer can still signal into it
   else
     __syncthreads();

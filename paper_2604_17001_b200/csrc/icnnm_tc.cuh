@@ -59,6 +59,7 @@ struct TcArgs {
   int grp;                  // N-tiles per tile group sharing each built A chunk (1 or 2)
   int skew;                 // tile-group schedule skew D (chunks), see tg_seq
   int cs;                   // 2: CTA pairs (cta_group::2, M = 256, B split by N); 1: single CTAs
+  int mcb;                  // F16x3 single CTAs in 2-CTA clusters sharing one multicast B stream
   int ehalf;                // adjoint: epilogue halves in use (1 or 2; 4 warps and 4 output
                             // bricks each -- 2 when the extra output bricks fit in SMEM)
 };

@@ -609,3 +609,47 @@ def test_solve_edge_cases(gpu, dims, ks, iters, engine):
     Lg, _ = gpu.icnnm_solve(X * mask, mask, B, gpu.SolverConfig(max_iters=iters, engine=engine, **FIXED))
     Lo, _ = O.icnnm_solve(X * mask, mask, _oracle_basis(B), O.SolverConfig(max_iters=iters, **FIXED))
     assert _rel(Lg, Lo) <= 1e-4
+
+
+# --------------------------------------------------------------------------
+# opt-in 2-CTA cluster modes of the F16x3 engine (read from the environment
+# once per process, so each runs in a subprocess): CTA pairs (cta_group::2,
+# ICNNM_TC_CS=2) and B multicast (ICNNM_TC_MCB=1)
+# --------------------------------------------------------------------------
+_CLUSTER_CHECK = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2604_17001_b200 as P
+from oracle import icnnm_oracle as O
+out = []
+for dims, ks in [((16, 16, 32), (9, 9, 5)), ((7, 5, 9), (3, 2, 4)), ((12, 11, 10), (4, 4, 8))]:
+    k = int(np.prod(ks))
+    L = np.random.default_rng(1).integers(-8, 9, size=dims).astype(np.float64)
+    f = P.BasisConvolver(dims, ks, np.eye(k), engine="f16x3").apply(L)
+    assert np.array_equal(f, O.conv_matrix(L, ks)), ("fwd", dims)
+    W = np.random.default_rng(4).integers(-4, 5, size=(L.size, k)).astype(np.float64)
+    a = P.conv_adjoint(W, ks, dims, engine="f16x3")
+    assert np.array_equal(a, O.conv_adjoint(W, ks, dims)), ("adj", dims)
+from paper_2604_17001_b200 import synth
+w = synth.scaled(synth.WORKLOADS[2], (16, 16, 32), iters=30)
+X, mask = w.target(), w.mask()
+B = P.learn_ensemble_basis(w.training(), w.kernel)
+cfg = P.SolverConfig(max_iters=30, tol_primal=1e-300, tol_change=1e-300)
+Lg, _ = P.icnnm_solve(X * mask, mask, B, cfg)
+Lo, _ = O.icnnm_solve(X * mask, mask, O.EigenBasis(B.kernel_shape, B.K, B.eigenvalues),
+                      O.SolverConfig(max_iters=30, tol_primal=1e-300, tol_change=1e-300))
+rel = float(np.linalg.norm(Lg - Lo) / np.linalg.norm(Lo))
+assert rel <= 1e-4, rel
+print("ok", rel)
+"""
+
+
+@pytest.mark.parametrize("env", [{"ICNNM_TC_CS": "2"}, {"ICNNM_TC_MCB": "1"}])
+def test_cluster_modes_exact_and_solve_parity(gpu, env):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _CLUSTER_CHECK, root], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
