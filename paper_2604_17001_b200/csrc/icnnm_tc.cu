@@ -163,10 +163,14 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
-// Arrive on a (possibly remote) mbarrier with cluster-scope release.
+// Arrive on a (possibly remote) mbarrier.  Default (CTA-scope) semantics, as
+// CUTLASS's ClusterBarrier::arrive(cta_id): what these arrivals publish is TMEM
+// state ordered by tcgen05.wait::{st,ld} + tcgen05.fence::before_thread_sync,
+// or a TMA completion already observed through the local barrier.  The
+// .release.cluster form compiled to MEMBAR.ALL.GPU + ERRBAR per arrive (22% of
+// the pair forward's stall samples, profiles/ab_r1/pairs_skip/).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
 // Wait whose acquire covers arrivals released by the peer CTA.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
@@ -524,14 +528,16 @@ icnnm_tc_kernel(TcArgs a) {
   const bool MCB = !PAIR && F16 && a.mcb != 0;
   const bool CL2 = PAIR || MCB;  // launched as 2-CTA clusters
   const int nepi_act = 4 * ehalf;
-  // CTA pairs: barriers completed by the peer (remote arrives, multicast
-  // commits) are waited on with cluster-scope acquire; skip bit 64 (A/B
-  // experiment) uses the default CTA-scope wait, as CUTLASS's 2-SM pipelines do
+  // CTA pairs / B multicast: barriers completed by the peer (remote arrives,
+  // multicast commits) are waited on with the default CTA-scope wait, as
+  // CUTLASS's 2-SM pipelines do (the .acquire.cluster form adds a CCTL.IVALL --
+  // an L1 invalidation -- after every wait: 25% of the pair adjoint's stall
+  // samples); skip bit 64 restores it (A/B)
   auto pwait = [&](uint64_t* b, uint32_t ph) {
     if (a.skip & 64)
-      mbar_wait(b, ph);
-    else
       mbar_wait_cluster(b, ph);
+    else
+      mbar_wait(b, ph);
   };
   // warp index through a shuffle: provably warp-uniform, so role branches are
   // uniform and the MMA issuer's counters can live in uniform registers
