@@ -366,6 +366,32 @@ def test_handle_api_equals_one_shot(gpu):
     assert r2.iterations == r3.iterations == 50
 
 
+def test_device_cache_reuse_across_sizes_and_empty(gpu):
+    """Device blocks freed by one call are reused by the next (icnnm_host.cu
+    devcache): interleaved solves of two sizes and engines, a cache flush in
+    between, and every result still equals the first solve of its problem."""
+    from paper_2604_17001_b200 import synth
+    probs = []
+    for dims, rate, seed in [((32, 32, 8), 0.5, 3), ((24, 20, 16), 0.4, 4)]:
+        w = synth.scaled(synth.WORKLOADS[1], dims, iters=30)
+        X = w.target()
+        mask = (np.random.default_rng(seed).random(dims) < rate).astype(np.float64)
+        B = gpu.learn_ensemble_basis(w.training(), w.kernel)
+        probs.append((X * mask, mask, B))
+    ref = {}
+    for rnd in range(3):
+        for i, (M, mask, B) in enumerate(probs):
+            for eng in ("f16x3", "ffma"):
+                L, r = gpu.icnnm_solve(M, mask, B, gpu.SolverConfig(max_iters=30, engine=eng, **FIXED))
+                assert r.iterations == 30 and np.all(np.isfinite(L))
+                if (i, eng) not in ref:
+                    ref[(i, eng)] = L
+                else:
+                    assert _rel(L, ref[(i, eng)]) < 1e-6
+        if rnd == 1:
+            gpu.empty_cache()
+
+
 @pytest.mark.parametrize("engine", ENGINES)
 def test_sharded_virtual_slabs_match_unsharded(gpu, engine):
     """H-sharded iteration (halo exchange + norm all-reduce) with G virtual
