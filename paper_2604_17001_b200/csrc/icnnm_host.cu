@@ -5,6 +5,7 @@
 // validation rules and error classes follow solver.cpp:26-40,66-72,
 // tensor.hpp:100-107,115-121 and spectral.cpp:25-41; the ADMM loop is the
 // restated form of solver.cpp:62-146 documented in DESIGN.md §2.
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -21,6 +22,7 @@
 #include <map>
 #include <mutex>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "../../include/icnnm_b200.h"
@@ -502,6 +504,45 @@ inline int64_t tc_w_elems(const Geo& g, const TcPlan& t) {
   return n_bricks(g) * static_cast<int64_t>(t.kp) * 128;
 }
 
+// 2-D tensor map (rows of 32 B = 16 halves) over a packed F16x3 B buffer with a
+// box of `rows` rows, for the CTA pairs' .cta_group::2 tensor copies.  Encoded
+// through the runtime's driver entry point (no libcuda link); cached per
+// (buffer, box).
+CUtensorMap pair_b_map(const float* Bpk, const TcPlan& t, int rows) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      fail(ICNNM_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<Encode>(fn);
+  }();
+  static std::map<std::tuple<const float*, int, int>, CUtensorMap> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  const int64_t total_rows =
+      static_cast<int64_t>(t.ntn) * t.nkc * (icnnm_dev::tc::B_STAGE_BYTES / 32);
+  auto key = std::make_tuple(Bpk, rows, static_cast<int>(total_rows));
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  CUtensorMap m{};
+  const cuuint64_t dims[2] = {16, static_cast<cuuint64_t>(total_rows)};
+  const cuuint64_t strides[1] = {32};
+  const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<float*>(Bpk), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(ICNNM_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  cache.emplace(key, m);
+  return m;
+}
+
 void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const float* src,
                       float* W, const float* Bpk, const float* cvec, float* adj, double* norm2,
                       const IterState* st, cudaStream_t stream,
@@ -579,6 +620,18 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   a.cs = cs_env >= 0 ? cs_env : 1;  // pairs: opt-in until they beat single CTAs
   if (!t.f16 || n_bricks(gtc) < 2) a.cs = 1;
   const bool pairs = a.cs > 1;
+  // pairs: the peer's half of every B stage signals the leader's barrier
+  // directly through 2-SM tensor copies (ICNNM_TC_TMAPAIR=0: bulk copies and a
+  // relay thread, the first pair design)
+  static const int tmapair_env = [] {
+    const char* e = std::getenv("ICNNM_TC_TMAPAIR");
+    return e ? std::atoi(e) : 1;
+  }();
+  a.tma_pair = (pairs && tmapair_env != 0 && Bpk != nullptr) ? 1 : 0;
+  if (a.tma_pair) {
+    a.tmB[0] = pair_b_map(Bpk, t, t.wbase / 2);
+    a.tmB[1] = pair_b_map(Bpk, t, std::max(8, t.nlast / 2));
+  }
   // B multicast (F16x3 single CTAs in 2-CTA clusters sharing one B stream, each
   // CTA loading half of every stage): ICNNM_TC_MCB=1 (A/B experiment)
   static const int mcb_env = [] {

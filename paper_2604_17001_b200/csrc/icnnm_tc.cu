@@ -89,6 +89,17 @@ __device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
+// 2-SM tensor copy: box at (0, row) of a 2-D tensor map into this CTA's
+// shared memory, complete_tx signalled on `bar_cluster` -- with .cta_group::2
+// the barrier may live in the peer CTA of the pair (the leader's B_full).
+__device__ __forceinline__ void tma2d_pair(void* dst, const CUtensorMap* map, int row,
+                                           uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.cta_group::2 "
+      "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(bar_cluster)
+      : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
                    : "memory");
@@ -467,7 +478,7 @@ __device__ __forceinline__ void tg_seq(int i, int gsz, int nkc, int D, int& t, i
 // ---------------------------------------------------------------------------
 template <bool FWD, bool F16, bool PAIR>
 __global__ void __launch_bounds__(608, 1)
-icnnm_tc_kernel(TcArgs a) {
+icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   constexpr int ASC = F16 ? KC : 2 * KC;  // TMEM columns per A stage
   constexpr int ALO = ASC / 2;            // column offset of the lo half
   constexpr int NB = 8;                  // builder warps
@@ -563,7 +574,7 @@ icnnm_tc_kernel(TcArgs a) {
       mbar_init(A_empty + i, 1);
     }
     for (int i = 0; i < SB; ++i) {
-      mbar_init(B_full + i, (PAIR && (blockIdx.x & 1u) == 0) ? 2 : 1);
+      mbar_init(B_full + i, (PAIR && !a.tma_pair && (blockIdx.x & 1u) == 0) ? 2 : 1);
       mbar_init(B_empty + i, MCB ? 2 : 1);  // MCB: released by both CTAs' MMAs
     }
     for (int i = 0; i < 2; ++i) {
@@ -1065,9 +1076,9 @@ icnnm_tc_kernel(TcArgs a) {
   } else if (warp == WMMA) {
     // ===================== MMA issuer (converged warp, elected lane issues) =====================
     if (PAIR && crank != 0) {
-      // peer CTA of a pair: the leader issues the pair's MMAs; this warp relays
-      // "my half of B stage sb landed" to the leader's B_full
-      if (lane == 0 && !(a.skip & 16)) {
+      // peer CTA of a pair: the leader issues the pair's MMAs; without tma_pair
+      // this warp relays "my half of B stage sb landed" to the leader's B_full
+      if (lane == 0 && !(a.skip & 16) && !a.tma_pair) {
         const uint32_t lead_bfull = mapa_u32(smem_u32(B_full), 0);
         int sb = 0;
         uint32_t bph = 0;
@@ -1256,7 +1267,18 @@ icnnm_tc_kernel(TcArgs a) {
             }
             const float* src = a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4);
             uint8_t* dst = reinterpret_cast<uint8_t*>(Bst) + sb * BSTG;
-            if (PAIR) {
+            if (PAIR && a.tma_pair) {
+              // this CTA's half of the N rows (hi, then lo) as two 2-SM tensor
+              // copies that complete_tx on the leader's B_full, which expects
+              // the whole stage (both CTAs' halves)
+              const uint32_t hb = static_cast<uint32_t>(wn / 2) * 32u;
+              const CUtensorMap* map = &a.tmB[wn == a.wbase ? 0 : 1];
+              const int row0 = (nt * nkc + kc) * (B_STAGE_BYTES / 32);
+              const uint32_t lead_bar = mapa_u32(smem_u32(B_full + sb), 0);
+              if (crank == 0) mbar_arrive_expect_tx(B_full + sb, 4u * hb);
+              tma2d_pair(dst, map, row0 + crank * (wn / 2), lead_bar);
+              tma2d_pair(dst + hb, map, row0 + wn + crank * (wn / 2), lead_bar);
+            } else if (PAIR) {
               // this CTA's half of the N rows, hi then lo (the canonical layout
               // keeps each half of the rows contiguous: 8-row core-matrix groups)
               const uint32_t hb = static_cast<uint32_t>(wn / 2) * 32u;
@@ -1354,12 +1376,12 @@ icnnm_tc_kernel(TcArgs a) {
   }
 }
 
-template __global__ void icnnm_tc_kernel<true, false, false>(TcArgs);
-template __global__ void icnnm_tc_kernel<false, false, false>(TcArgs);
-template __global__ void icnnm_tc_kernel<true, true, false>(TcArgs);
-template __global__ void icnnm_tc_kernel<false, true, false>(TcArgs);
-template __global__ void icnnm_tc_kernel<true, true, true>(TcArgs);
-template __global__ void icnnm_tc_kernel<false, true, true>(TcArgs);
+template __global__ void icnnm_tc_kernel<true, false, false>(const __grid_constant__ TcArgs);
+template __global__ void icnnm_tc_kernel<false, false, false>(const __grid_constant__ TcArgs);
+template __global__ void icnnm_tc_kernel<true, true, false>(const __grid_constant__ TcArgs);
+template __global__ void icnnm_tc_kernel<false, true, false>(const __grid_constant__ TcArgs);
+template __global__ void icnnm_tc_kernel<true, true, true>(const __grid_constant__ TcArgs);
+template __global__ void icnnm_tc_kernel<false, true, true>(const __grid_constant__ TcArgs);
 
 void* fwd_kernel_ptr(bool f16, bool pair) {
   if (f16 && pair) return reinterpret_cast<void*>(&icnnm_tc_kernel<true, true, true>);

@@ -1,6 +1,8 @@
 // tcgen05 engines (TF32x3, F16x3) of the two ICNNM contractions: shared
 // host/device declarations.  See icnnm_tc.cu for the kernel design.
 #pragma once
+#include <cuda.h>  // CUtensorMap (types only; encoded through the runtime's driver entry point)
+
 #include <cstddef>
 #include <cstdint>
 
@@ -29,7 +31,12 @@ inline int b_stage_bytes(bool f16, bool pair = false) {
   return f16 ? (pair ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES;
 }
 
-struct TcArgs {
+struct alignas(64) TcArgs {
+  // CTA pairs (F16x3): 2-D views (rows of 32 B) of the packed B tiles for
+  // cp.async.bulk.tensor .cta_group::2 -- each CTA's half-tile copy signals
+  // the leader's B_full directly; [0]: box of wbase/2 rows, [1]: nlast/2 rows
+  CUtensorMap tmB[2];
+  int tma_pair;          // 1: pair B halves via tmB (no relay); 0: bulk copies + relay
   Geo g;                 // kp = ktp = roundup(k, 32)
   const float* src;      // forward: L~ (natural [H,W,T] layout, slab halo rows first)
   const float* Win;      // adjoint: W in this engine's layout
