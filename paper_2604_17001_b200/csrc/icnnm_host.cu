@@ -832,9 +832,8 @@ struct Solver {
   DBuf<float> xfer_send, xfer_recv;  // cross-process halo buffers
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
-  double* h_theta = nullptr;  // pinned staging of the theta schedule
-  size_t h_theta_n = 0;
-  IterState* h_st = nullptr;  // pinned: [0] initial state, [1] state readback
+  double* h_theta = nullptr;  // pinned staging of the theta schedule (thread's pool)
+  IterState* h_st = nullptr;  // pinned: [0] initial state, [1] state readback (pool)
   // host copies of the basis (validation happens once at create)
   std::vector<double> K;
   // per-problem scalars (from upload)
@@ -853,8 +852,6 @@ struct Solver {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (evs) cudaEventDestroy(evs);
-    if (h_theta) cudaFreeHost(h_theta);
-    if (h_st) cudaFreeHost(h_st);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -1149,12 +1146,28 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   if (S.tc_counters && !S.dbg.p) S.dbg.alloc(2 * icnnm_dev::tc::DBG_SLOTS);  // captured pointer
   // pinned staging of the per-run host inputs (theta schedule, initial state),
   // so that their uploads are capturable stream operations
-  if (S.h_theta_n < th.size()) {
-    if (S.h_theta) cudaFreeHost(S.h_theta);
-    CK(cudaMallocHost(&S.h_theta, th.size() * sizeof(double)));
-    S.h_theta_n = th.size();
+  // pinned staging from a grow-only per-thread pool (cudaMallocHost per call
+  // occasionally cost tens of ms in the end-to-end path); run() completes the
+  // solve before returning, so solvers on one thread never share it in flight
+  struct PinnedPool {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~PinnedPool() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  static thread_local PinnedPool pool;
+  const size_t need = 2 * sizeof(IterState) + th.size() * sizeof(double);
+  if (pool.bytes < need) {
+    if (pool.p) cudaFreeHost(pool.p);
+    pool.p = nullptr;
+    pool.bytes = 0;
+    const size_t want = std::max<size_t>(need, 64 * 1024);
+    CK(cudaMallocHost(&pool.p, want));
+    pool.bytes = want;
   }
-  if (!S.h_st) CK(cudaMallocHost(&S.h_st, 2 * sizeof(IterState)));
+  S.h_st = static_cast<IterState*>(pool.p);
+  S.h_theta = reinterpret_cast<double*>(static_cast<char*>(pool.p) + 2 * sizeof(IterState));
   std::copy(th.begin(), th.end(), S.h_theta);
   IterState st0{};
   st0.active = 1;
