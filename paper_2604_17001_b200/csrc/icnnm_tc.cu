@@ -691,6 +691,18 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     const uint32_t lead_afull = PAIR ? mapa_u32(smem_u32(A_full), 0) : 0u;
     int pend_sa = -1, pend_wsi = 0;
     int iter = 0;
+    int st_sa = 0, st_ws = 0;
+    uint32_t st_ph = 0, st_wph = 0;
+    auto adv_stage = [&]() {
+      if (++st_sa == san) {
+        st_sa = 0;
+        st_ph ^= 1u;
+      }
+      if (++st_ws == wsn) {
+        st_ws = 0;
+        st_wph ^= 1u;
+      }
+    };
     for (int sl = sfirst; sl < nslot; sl += sstep, ++iter) {
       float* hcur = halo + (iter & 1) * nobp;
       if (FWD) {
@@ -725,15 +737,17 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         }
       }
       for (int gi = 0; gi < ngrp; ++gi) {
-        for (int kc = 0; kc < nkc; ++kc, ++cnt) {
+        for (int kc = 0; kc < nkc; ++kc, ++cnt, adv_stage()) {
           // bsplit = 0: group `half` owns the chunks with cnt % 2 == half and
           // builds all KC columns, so each warp has two chunk periods of MMA
           // time to cover its TMEM-store round trip.
           if ((F16 || !a.bsplit) && static_cast<int>(cnt & 1u) != half) continue;
-          const int sa = cnt % san;
-          const uint32_t ph = (cnt / san) & 1;
-          const int wsi = cnt % wsn;
-          const uint32_t wph = (cnt / wsn) & 1;
+          // A / W stage (index, parity) of chunk cnt, advanced incrementally
+          // (cnt % san and cnt / san were a 32-bit division per chunk)
+          const int sa = st_sa;
+          const uint32_t ph = st_ph;
+          const int wsi = st_ws;
+          const uint32_t wph = st_wph;
           long long t0c = dbg.p ? clk() : 0;
           if (PAIR)
             pwait(A_empty + sa, ph ^ 1);  // released by the leader's MMAs
