@@ -259,7 +259,8 @@ void set_smem_attrs() {
 // Brick-ordered row of voxel (h, w, t) in a launch geometry.
 inline int64_t brick_row(const Geo& g, int64_t h, int64_t w, int64_t t) {
   int64_t b = (h / g.bh * g.nbw + w / g.bw) * g.nbt + t / g.bt;
-  int64_t v = ((h % g.bh) * g.bw + (w % g.bw)) * g.bt + (t % g.bt);
+  int64_t v = g.vmap ? ((w % g.bw) * g.bh + (h % g.bh)) * g.bt + (t % g.bt)
+                     : ((h % g.bh) * g.bw + (w % g.bw)) * g.bt + (t % g.bt);
   return b * BM + v;
 }
 
@@ -284,6 +285,7 @@ struct TcPlan {
   int kp = 0, ntn = 0, nkc = 0, nlast = 0, wbase = 0, sa = 0;
   bool f16 = false;        // F16x3 engine (kind::f16) instead of TF32x3
   float bunscale = 1.f;    // F16x3: inverse of B's power-of-2 scale
+  int vmap = 0;            // voxel order of the brick geometry (Geo::vmap; adjoint N order)
   int width(int nt) const { return std::min(wbase, kp - nt * wbase); }
 };
 
@@ -349,6 +351,22 @@ Geo tc_geo(const Geo& g, const TcPlan& t) {
     q.HW = q.bw + q.kw - 1;
     q.HT = q.bt + q.kt - 1;
   }
+  // Voxel order within a brick.  A warp's 32 TMEM lanes are two runs of 16
+  // consecutive t (bt = 16) one brick row apart: D = HT words (vmap 0, rows
+  // differ in w) or HW*HT words (vmap 1, rows differ in h).  The halo gathers
+  // and the adjoint's col2im scatter hit |16 - D mod 32| lanes in 2-way bank
+  // conflicts; config 2 (HT = 20, HW*HT = 240): 4 vs 0.  vmap 1 needs bh*bt = 32
+  // (a warp then shares vw; the adjoint's N order becomes sw-fastest).
+  q.vmap = 0;
+  static const int vmap_env = [] {
+    const char* e = std::getenv("ICNNM_TC_VMAP");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (q.bt == 16 && q.bh * q.bt == 32 && q.kw >= 1) {
+    auto conf = [](int d) { return std::abs(16 - (d % 32)); };
+    const bool better = conf(q.HW * q.HT) < conf(q.HT);
+    q.vmap = vmap_env >= 0 ? (vmap_env != 0 ? 1 : 0) : (better ? 1 : 0);
+  }
   return q;
 }
 
@@ -365,10 +383,14 @@ inline float tf32_rna(float x) {
 // lo TF32 parts: [nt][kc] blocks of 32 KB = [hl][q][n/8][k/4][n%8][k%4].
 // forward: B(n=j, k=s) = K[s][j];  adjoint: B(n=s, k=j) = K[s][j].
 // Adjoint N order (icnnm_tc.cu tapoff): n = (sw*kt + st)*kh + sh -> tap s.
-inline int adj_tap(const Problem& p, int n) {
+// vmap 1 (warps share vw): n = (sh*kt + st)*kw + sw, sw fastest.
+inline int adj_tap(const Problem& p, int n, int vmap) {
   const int kh = static_cast<int>(p.kd[0]), kw = static_cast<int>(p.kd[1]),
             kt = static_cast<int>(p.kd[2]);
-  (void)kw;
+  if (vmap) {
+    const int sw = n % kw, q = n / kw, st = q % kt, sh = q / kt;
+    return (sh * kw + sw) * kt + st;
+  }
   const int sh = n % kh, q = n / kh, st = q % kt, sw = q / kt;
   return (sh * kw + sw) * kt + st;
 }
@@ -397,7 +419,7 @@ std::vector<float> pack_b_tiles_f16(const Problem& p, TcPlan& t, const double* K
           double x = 0.0;
           if (nn < k && kk < k)
             x = fwd ? Kcm[static_cast<size_t>(nn) * k + kk]
-                    : Kcm[static_cast<size_t>(kk) * k + adj_tap(p, nn)];
+                    : Kcm[static_cast<size_t>(kk) * k + adj_tap(p, nn, t.vmap)];
           const float xs = static_cast<float>(std::ldexp(x, eb));
           const __half hi = __float2half_rn(xs);
           const __half lo = __float2half_rn(xs - __half2float(hi));
@@ -414,7 +436,7 @@ std::vector<float> pack_b_tiles_f16(const Problem& p, TcPlan& t, const double* K
 // per tile element; bit-identical to pack_b_tiles_f16: x * 2^eB is exact in
 // f64, then one rounding to f32 and the two RN conversions to f16).
 __global__ void icnnm_pack_b_f16(int k, int kp, int wbase, int nkc, int kh, int kw, int kt,
-                                 int fwd, double sc, const double* __restrict__ K,
+                                 int fwd, int vmap, double sc, const double* __restrict__ K,
                                  __half* __restrict__ out, int64_t total) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= total) return;
@@ -433,7 +455,18 @@ __global__ void icnnm_pack_b_f16(int k, int kp, int wbase, int nkc, int kh, int 
     if (fwd) {
       x = K[static_cast<size_t>(nn) * k + kk];
     } else {
-      const int sh = nn % kh, r = nn / kh, st = r % kt, sw = r / kt;
+      int sh, sw, st;
+      if (vmap) {
+        sw = nn % kw;
+        const int r = nn / kw;
+        st = r % kt;
+        sh = r / kt;
+      } else {
+        sh = nn % kh;
+        const int r = nn / kh;
+        st = r % kt;
+        sw = r / kt;
+      }
       x = K[static_cast<size_t>(kk) * k + (sh * kw + sw) * kt + st];
     }
   }
@@ -455,7 +488,7 @@ void pack_b_tiles_f16_device(const Problem& p, TcPlan& t, const double* dK, bool
   const int64_t total = static_cast<int64_t>(t.ntn) * t.nkc * t.wbase * icnnm_dev::tc::KC;
   icnnm_pack_b_f16<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(
       p.k, t.kp, t.wbase, t.nkc, static_cast<int>(p.kd[0]), static_cast<int>(p.kd[1]),
-      static_cast<int>(p.kd[2]), fwd ? 1 : 0, std::ldexp(1.0, eb), dK,
+      static_cast<int>(p.kd[2]), fwd ? 1 : 0, t.vmap, std::ldexp(1.0, eb), dK,
       reinterpret_cast<__half*>(out.p), total);
   CKL();
 }
@@ -486,7 +519,7 @@ std::vector<float> pack_b_tiles(const Problem& p, TcPlan& t, const double* Kcm, 
             double x = 0.0;
             if (nn < k && kk < k)
               x = fwd ? Kcm[static_cast<size_t>(nn) * k + kk]
-                      : Kcm[static_cast<size_t>(kk) * k + adj_tap(p, nn)];
+                      : Kcm[static_cast<size_t>(kk) * k + adj_tap(p, nn, t.vmap)];
             const float xf = static_cast<float>(x);
             const float hi = tf32_rna(xf);
             const float lo = xf - hi;
@@ -880,6 +913,7 @@ void solver_alloc(Solver& S) {
     s.L.alloc(s.m_own);
     s.V.alloc(s.m_own);
     s.gtc = tc_geo(s.g, S.tp);
+    S.tp.vmap = S.tp16.vmap = s.gtc.vmap;  // same brick shape in every slab
     check_smem(icnnm_dev::tc::smem_bytes(s.gtc, true, 2, 2, false));
     check_smem(icnnm_dev::tc::smem_bytes(s.gtc, false, 2, 2, false));
     s.W.alloc(std::max<int64_t>(n_bricks(s.g) * BM * p.kp, tc_w_elems(s.gtc, S.tp)));
@@ -1588,6 +1622,7 @@ int icnnm_cuda_conv_forward_ex(int order, const int64_t* dims, const double* L,
     if (is_tc(engine)) {
       TcPlan t = tc_plan(p, engine == ICNNM_ENGINE_F16X3);
       Geo gt = tc_geo(g, t);
+      t.vmap = gt.vmap;
       check_smem(icnnm_dev::tc::smem_bytes(gt, true, 2, 2, t.f16));
       auto bf = pack_b_tiles(p, t, K_colmajor, true);
       DBuf<float> dB(bf.size()), dW(tc_w_elems(gt, t));
@@ -1653,6 +1688,7 @@ int icnnm_cuda_conv_adjoint_ex(int order, const int64_t* dims, const int64_t* kd
     if (is_tc(engine)) {
       TcPlan t = tc_plan(p, engine == ICNNM_ENGINE_F16X3);
       Geo gt = tc_geo(g, t);
+      t.vmap = gt.vmap;
       check_smem(icnnm_dev::tc::smem_bytes(gt, false, 2, 2, t.f16));
       std::vector<double> I(static_cast<size_t>(p.k) * p.k, 0.0);
       for (int j = 0; j < p.k; ++j) I[static_cast<size_t>(j) * p.k + j] = 1.0;

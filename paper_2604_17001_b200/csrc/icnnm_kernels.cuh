@@ -31,6 +31,8 @@ struct Geo {
   int Hsrc;             // rows of the source (L~) / target (adj) buffer
   int hoff;             // buffer row = h + hoff   (h may be negative)
   int wrapH;            // 1: periodic in H over Hsrc rows; 0: slab buffer
+  int vmap;             // tcgen05 engines: voxel order within a brick (TMEM lane / W row)
+                        // 0: v = (vh*bw + vw)*bt + vt;  1: v = (vw*bh + vh)*bt + vt
 };
 
 // Per-iteration scalars, written by the coefficient kernel and read by the

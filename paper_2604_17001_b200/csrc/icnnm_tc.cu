@@ -598,13 +598,21 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         sw = q % g.kw;
         sh = q / g.kw;
       } else {
-        // adjoint N order: sh fastest (see tap_perm in the host): within a
-        // warp the 32 rows share vh, so taps with different sh never hit the
-        // same output cell -> the col2im scatter can batch them hazard-free
-        sh = s % g.kh;
-        const int q = s / g.kh;
-        st = q % g.kt;
-        sw = q / g.kt;
+        // adjoint N order (host adj_tap): vmap 0 -- sh fastest: within a warp
+        // the 32 rows share vh, so taps with different sh never hit the same
+        // output cell and the col2im scatter can batch them hazard-free;
+        // vmap 1 -- the rows share vw, sw fastest
+        if (g.vmap) {
+          sw = s % g.kw;
+          const int q = s / g.kw;
+          st = q % g.kt;
+          sh = q / g.kt;
+        } else {
+          sh = s % g.kh;
+          const int q = s / g.kh;
+          st = q % g.kt;
+          sw = q / g.kt;
+        }
       }
       off = (sh * g.HW + sw) * g.HT + st;
     }
@@ -662,7 +670,9 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     const int quad = warp & 3, half = warp >> 2;
     const int row = 32 * quad + lane;
     const int bt_tid = tid;                       // 0..255
-    const int vt = row % g.bt, vw = (row / g.bt) % g.bw, vh = row / (g.bt * g.bw);
+    const int vt = row % g.bt;
+    const int vw = g.vmap ? row / (g.bt * g.bh) : (row / g.bt) % g.bw;
+    const int vh = g.vmap ? (row / g.bt) % g.bh : row / (g.bt * g.bw);
     const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
     const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
     uint32_t cnt = 0;
@@ -882,7 +892,9 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     const int quad = ew & 3, half = ew >> 2;     // half in {0} (adjoint) or {0,1} (forward)
     const int row = 32 * quad + lane;
     const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
-    const int vt = row % g.bt, vw = (row / g.bt) % g.bw, vh = row / (g.bt * g.bw);
+    const int vt = row % g.bt;
+    const int vw = g.vmap ? row / (g.bt * g.bh) : (row / g.bt) % g.bw;
+    const int vh = g.vmap ? (row / g.bt) % g.bh : row / (g.bt * g.bw);
     const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
     const int obs = nobp + 32;             // output-brick stride (+32 scratch)
     float* myob = ob + (FWD ? quad : ew) * obs;  // adjoint: one output brick per warp
@@ -1008,8 +1020,9 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
               return F16 ? __uint_as_float(u[i]) * us : __uint_as_float(u[i]);
             };
             const int s0 = nt * a.wbase + c0;
-            if (g.kh >= 4) {
-              // batches of 4 consecutive N columns = 4 distinct sh: no hazards
+            if ((g.vmap ? g.kw : g.kh) >= 4) {
+              // batches of 4 consecutive N columns = 4 distinct sh (vmap 0) or
+              // sw (vmap 1), the coordinate the warp's rows share: no hazards
 #pragma unroll
               for (int i = 0; i < 32; i += 4) {
                 float* o[4];
