@@ -35,4 +35,8 @@ if os.environ.get("ICNNM_TC_COUNTERS"):
         print(k, "MMA-thread cycles per CTA per launch: %.0f" % (tot / nsm / a.iters),
               "cycles per MMA issued: %.1f" % (tot / (mmas * a.iters)),
               "kernel time per launch (ms):", S.kernel_times_ms() if False else "")
-        print(k, {n: round(v / tot, 3) for n, v in d.items()}, "(fractions of MMA-thread cycles; builder/epi sums over 4 warps' lane 0)")
+        print(k, {n: round(v / tot, 3) for n, v in d.items()}, "(fractions of MMA-thread cycles; builder/epi: sums over the role's warps (lane 0))")
+        bt = max(d["build_total"], 1)
+        print(k, "builder warp time split: chunk waits %.3f, chunk work %.3f, per-brick prep %.3f, other %.3f"
+              % (d["build_wait"] / bt, d["build_work"] / bt, d["build_prep"] / bt,
+                 1 - (d["build_wait"] + d["build_work"] + d["build_prep"]) / bt))
