@@ -300,7 +300,10 @@ int icnnm_dist_unique_id(char* out128);
  * (G = local_slabs * world slabs).  Each process passes the FULL tensor
  * (M_obs, mask: m doubles) and receives its own slabs' rows of L in
  * L_out (rows [row0, row0 + nrows) of the H axis, written to
- * L_out[0 .. nrows*W*T)).  world == 1 needs no NCCL id (pass NULL).
+ * L_out[0 .. nrows*W*T)).  world == 1 needs no NCCL id (pass NULL: the
+ * exchange is device copies); world == 1 WITH an id (icnnm_dist_unique_id)
+ * runs the exchange through a one-rank NCCL communicator (self send/recv,
+ * all-reduce) -- the multi-process transport, exercised on one GPU.
  * row0/nrows may be NULL. */
 int icnnm_sharded_solve(int order, const int64_t* dims, const double* M_obs,
                         const double* mask, const int64_t* kdims,

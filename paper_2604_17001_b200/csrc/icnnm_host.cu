@@ -876,6 +876,11 @@ struct Solver {
   int64_t launches = 0;
   bool profile = false;
   bool tc_counters = false;
+  // head graph launched while the rest of the solve is captured (ICNNM_GRAPH_SPLIT=0: one graph)
+  bool graph_split = [] {
+    const char* e = std::getenv("ICNNM_GRAPH_SPLIT");
+    return !(e && std::atoi(e) == 0);
+  }();
   double prof_ms[4] = {0, 0, 0, 0};
   DBuf<unsigned long long> dbg;  // 2 x DBG_SLOTS tcgen05 pipeline counters
 
@@ -927,7 +932,7 @@ void solver_alloc(Solver& S) {
   int64_t mtot = p.m;
   S.Mstage.alloc(mtot);
   S.maskstage.alloc(mtot);
-  if (S.world > 1) {
+  if (S.comm) {
     S.xfer_send.alloc((p.kd[0] - 1) * WT + 1);
     S.xfer_recv.alloc((p.kd[0] - 1) * WT + 1);
   }
@@ -970,7 +975,7 @@ void exchange_lt(Solver& S, DBuf<float> Slab::*buf = &Slab::Lt) {
   const size_t he = S.slabs[0].halo_elems;
   if (he == 0) return;
   const int nl = static_cast<int>(S.slabs.size());
-  if (S.world == 1) {
+  if (!S.comm) {
     for (int i = 0; i < nl; ++i) {
       const Slab& src = S.slabs[i];
       Slab& dst = S.slabs[(i + 1) % nl];
@@ -998,7 +1003,7 @@ void exchange_adj(Solver& S) {
     CKL();
     ++S.launches;
   };
-  if (S.world == 1) {
+  if (!S.comm) {
     for (int i = 0; i < nl; ++i) {
       Slab& src = S.slabs[i];
       Slab& dst = S.slabs[(i + nl - 1) % nl];
@@ -1114,7 +1119,7 @@ int engine_kp(const Solver& S) {
 }
 
 void allreduce_red(Solver& S) {
-  if (S.world > 1) S.comm->allreduce_sum(S.red.p, engine_kp(S) + 8, S.stream);
+  if (S.comm) S.comm->allreduce_sum(S.red.p, engine_kp(S) + 8, S.stream);
 }
 
 struct RunResult {
@@ -1301,17 +1306,30 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     for (auto& x : e) cudaEventDestroy(x);
     finish();
   } else {
-    // The whole solve -- setup, its events, every iteration, the final coef --
-    // is one CUDA graph (up to GMAX iterations), captured and instantiated
-    // before anything runs: the device time of a solve is one graph launch and
-    // host-side delays (driver locks, scheduling) can never stretch it.
-    // Longer solves replay GMAX-iteration graphs between a head and a tail;
-    // replays past max_iters are no-ops (the coef kernel deactivates), and with
-    // tolerances the host checks the state between replays.
+    // The solve -- setup, its events, every iteration, the final coef -- runs as
+    // CUDA graphs captured and instantiated before they are launched, so the
+    // device time of a solve can never be stretched by host-side delays
+    // inside a graph.  A long solve is split: a head graph (setup + H
+    // iterations) is launched first, and the rest is captured and
+    // instantiated while the head runs on the device (capture+instantiate
+    // costs ~30 us per iteration on the host: 8-9 ms of every end-to-end call
+    // at config 2 otherwise).  H is sized from the contraction's flops so the
+    // head outlasts that capture 3x over; short or small solves stay one graph.
+    // Solves longer than GMAX replay a GMAX-iteration body graph; replays past
+    // max_iters are no-ops (the coef kernel deactivates), and with tolerances
+    // the host checks the state between replays.
     constexpr int GMAX = 512;
-    const bool one = iters <= GMAX;
-    const int U = one ? iters : GMAX;
     const bool may_stop = !(cfg.tol_primal <= 1e-200 && cfg.tol_change <= 1e-200);
+    const double t_it = 4.0 * static_cast<double>(p.m) * kd * kd / 2.0e14 + 25e-6;  // s, est.
+    const double cap_it = 30e-6;                                                      // s, host
+    int H = iters;
+    if (S.graph_split && iters > 1) {
+      const double need = 3.0 * (cap_it * std::min(iters, GMAX) + 2e-3);
+      const int h = static_cast<int>(std::ceil(need / t_it));
+      if (2 * h <= iters) H = std::max(h, 1);
+    }
+    if (H > GMAX) H = GMAX;
+    const bool one = H == iters;  // head graph holds the whole solve, final coef included
     auto capture = [&](bool head, int n, bool tail) {
       cudaGraph_t g = nullptr;
       cudaGraphExec_t e = nullptr;
@@ -1331,30 +1349,44 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     // launch accounting: capture counts the TC/FFMA launches of one iteration
     const int64_t l0 = S.launches;
     g_timer.mark("run: schedule/staging");
-    cudaGraphExec_t gx = capture(true, U, one);
-    g_timer.mark("run: capture+instantiate");
+    cudaGraphExec_t gx = capture(true, H, one);
+    g_timer.mark("run: capture+instantiate (head)");
     const int64_t captured = S.launches - l0;
     S.launches = l0;
     // per iteration: coef + update per slab + the counted engine launches
     const int64_t setup_l = static_cast<int64_t>(S.slabs.size()) * 2 + (one ? 1 : 0);
-    const int64_t per_iter = (captured - setup_l) / std::max(1, U) + 1 +
+    const int64_t per_iter = (captured - setup_l) / std::max(1, H) + 1 +
                              static_cast<int64_t>(S.slabs.size());
-    cudaGraphExec_t gr = one ? nullptr : capture(false, U, false);
     CK(cudaStreamSynchronize(S.stream));  // uploads done; nothing of this solve has run
     g_timer.mark("run: graph upload");
     CK(cudaGraphLaunch(gx, S.stream));
-    S.launches += setup_l + per_iter * U;
-    for (int it = U; it < iters; it += U) {
-      if (may_stop) {
-        CK(cudaMemcpyAsync(S.h_st + 1, S.st.p, sizeof(IterState), cudaMemcpyDeviceToHost,
-                           S.stream));
-        CK(cudaStreamSynchronize(S.stream));
-        if (!S.h_st[1].active) break;
+    S.launches += setup_l + per_iter * H;
+    cudaGraphExec_t gr = nullptr;
+    bool finished = one;
+    if (!one) {
+      const int R = iters - H;
+      const int U = std::min(R, GMAX);
+      const bool tail_in = R <= GMAX && !may_stop;  // launched exactly once
+      const int64_t l1 = S.launches;
+      gr = capture(false, U, tail_in);  // overlaps the head on the device
+      S.launches = l1;
+      g_timer.mark("run: capture+instantiate (body, overlapped)");
+      for (int it = H; it < iters; it += U) {
+        if (may_stop) {
+          CK(cudaMemcpyAsync(S.h_st + 1, S.st.p, sizeof(IterState), cudaMemcpyDeviceToHost,
+                             S.stream));
+          CK(cudaStreamSynchronize(S.stream));
+          if (!S.h_st[1].active) break;
+        }
+        CK(cudaGraphLaunch(gr, S.stream));
+        S.launches += per_iter * std::min(U, iters - it);
+        if (tail_in) {
+          finished = true;
+          S.launches += 1;
+        }
       }
-      CK(cudaGraphLaunch(gr, S.stream));
-      S.launches += per_iter * std::min(U, iters - it);
     }
-    if (!one) finish();
+    if (!finished) finish();
     gexec[0] = gx;
     gexec[1] = gr;
   }
@@ -1985,7 +2017,9 @@ int icnnm_sharded_solve(int order, const int64_t* dims, const double* M_obs, con
       S.slabs[i].row0 = s;
       S.slabs[i].rows = c;
     }
-    if (world > 1) {
+    // world == 1 with an id: a one-rank communicator carries the exchange
+    // (self send/recv + all-reduce), so the NCCL transport runs on one GPU
+    if (world > 1 || nccl_id128) {
       if (!nccl_id128) invalid("sharded solve: NCCL unique id required for world > 1");
       S.comm = comm_create(nccl_id128, world, rank);
     }

@@ -679,3 +679,50 @@ def test_cluster_modes_exact_and_solve_parity(gpu, env):
     r = subprocess.run([sys.executable, "-c", _CLUSTER_CHECK, root], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+# --------------------------------------------------------------------------
+# The NCCL transport of the sharded solve on one GPU: world == 1 with a NCCL
+# id routes the halo shifts through self send/recv and the norm vector through
+# ncclAllReduce (captured in the solve graph), the same calls a multi-process
+# run makes.  In a subprocess with a timeout so a transport hang cannot stall
+# the suite.
+# --------------------------------------------------------------------------
+_NCCL_ONE_RANK = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2604_17001_b200 as P
+from oracle import icnnm_oracle as O
+from paper_2604_17001_b200 import synth
+engine = sys.argv[2]
+X = synth.synth_video(48, 16, 16, 8, 2, 21)
+mask = synth.synth_mask(48, 16, 16, synth.MASK_IID, 0.3, 22)
+mask[20:30, 3:9, 4:12] = 0.0
+B = P.learn_ensemble_basis([synth.synth_video(48, 16, 16, 8, 2, 23)], (5, 3, 3))
+F = dict(tol_primal=1e-300, tol_change=1e-300)
+cfg = P.SolverConfig(max_iters=40, engine=engine, **F)
+L1, r1 = P.icnnm_solve(X * mask, mask, B, cfg)
+Lo, _ = O.icnnm_solve(X * mask, mask, O.EigenBasis(B.kernel_shape, B.K, B.eigenvalues),
+                      O.SolverConfig(max_iters=40, **F))
+for G in (1, 3):
+    row0, rows, rep = P.sharded_solve(X * mask, mask, B, cfg, local_slabs=G, world=1, rank=0,
+                                      nccl_id=P.dist_unique_id())
+    assert row0 == 0 and rows.shape == X.shape
+    rel = float(np.linalg.norm(rows - L1) / np.linalg.norm(L1))
+    relo = float(np.linalg.norm(rows - Lo) / np.linalg.norm(Lo))
+    assert rel <= 1e-5 and relo <= 1e-4, (G, rel, relo)
+    np.testing.assert_allclose(rep.objective, r1.objective, rtol=1e-5)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("engine", ["f16x3", "ffma"])
+def test_sharded_nccl_one_rank_transport(gpu, engine):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _NCCL_ONE_RANK, root, engine],
+                       env={**os.environ, "NCCL_DEBUG": "WARN"},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
