@@ -579,7 +579,7 @@ CUtensorMap pair_b_map(const float* Bpk, const TcPlan& t, int rows) {
 void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const float* src,
                       float* W, const float* Bpk, const float* cvec, float* adj, double* norm2,
                       const IterState* st, cudaStream_t stream,
-                      unsigned long long* dbg = nullptr, float amax = 0.f) {
+                      unsigned long long* dbg = nullptr, float amax = 0.f, bool pdl = false) {
   icnnm_dev::tc::TcArgs a{};
   a.bunscale = t.bunscale;
   a.amax = amax;
@@ -762,7 +762,17 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
     CK(cudaLaunchKernelExC(&lc, fn, args));
   } else {
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.nbricks, nsm));
-    CK(cudaLaunchKernel(fn, dim3(grid), block, args, smem, stream));
+    cudaLaunchConfig_t lc{};
+    cudaLaunchAttribute at{};
+    at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at.val.programmaticStreamSerializationAllowed = 1;
+    lc.gridDim = dim3(grid);
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = stream;
+    lc.attrs = &at;
+    lc.numAttrs = pdl ? 1 : 0;
+    CK(cudaLaunchKernelExC(&lc, fn, args));
   }
 }
 
@@ -1082,6 +1092,19 @@ void ensure_engine_basis(Solver& S, int engine) {
   }
 }
 
+// Programmatic dependent launch for the kernel-to-kernel edges of the
+// iteration graph (adjoint <- coef, update <- adjoint, forward <- update):
+// the successor's prologue overlaps its predecessor's tail.  Off for the
+// sharded solve (copies / NCCL between the kernels), the per-family profile
+// and ICNNM_PDL=0.
+bool use_pdl(const Solver& S) {
+  static const bool on = [] {
+    const char* e = std::getenv("ICNNM_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on && !S.sharded && !S.profile;
+}
+
 void launch_fwd(Solver& S, Slab& s, int mode) {
   // mode 2 (exact residual): forward on L_{t+1}, epilogue sums the gap into slot[5]
   const float* src = mode == 2 ? s.Lr.p : s.Lt.p;
@@ -1090,7 +1113,7 @@ void launch_fwd(Solver& S, Slab& s, int mode) {
     const bool f16 = S.engine == ICNNM_ENGINE_F16X3 && !(f16_debug_mask() & 2);
     launch_tc_kernel(s.gtc, f16 ? S.tp16 : S.tp, true, mode, src, s.W.p,
                      f16 ? S.BpkF16.p : S.BpkF.p, S.cvec.p, s.adj.p, acc, S.st.p, S.stream,
-                     S.tc_counters ? S.dbg.p : nullptr);
+                     S.tc_counters ? S.dbg.p : nullptr, 0.f, mode != 0 && use_pdl(S));
     ++S.launches;
     return;
   }
@@ -1104,7 +1127,8 @@ void launch_adj(Solver& S, Slab& s) {
     const bool f16 = S.engine == ICNNM_ENGINE_F16X3 && !(f16_debug_mask() & 1);
     launch_tc_kernel(s.gtc, f16 ? S.tp16 : S.tp, false, 1, s.Lt.p, s.W.p,
                      f16 ? S.BpkA16.p : S.BpkA.p, S.cvec.p, s.adj.p, S.red.p, S.st.p, S.stream,
-                     S.tc_counters ? S.dbg.p + icnnm_dev::tc::DBG_SLOTS : nullptr);
+                     S.tc_counters ? S.dbg.p + icnnm_dev::tc::DBG_SLOTS : nullptr, 0.f,
+                     use_pdl(S));
     ++S.launches;
     return;
   }
@@ -1166,11 +1190,21 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     for (auto& s : S.slabs) launch_adj(S, s);
     exchange_adj(S);
     for (auto& s : S.slabs) {
-      icnnm_dev::icnnm_update<<<update_grid(s.m_own), 256, 0, S.stream>>>(
-          s.m_own, S.st.p, cfg.lambda, kd, s.adj.p + s.halo_elems, s.L.p, s.V.p, s.pm.p,
-          s.mask.p, s.Lt.p + s.halo_elems, S.red.p + kpe,
-          S.exact_res ? s.Lr.p + s.halo_elems : nullptr);
-      CKL();
+      cudaLaunchConfig_t lc{};
+      cudaLaunchAttribute at{};
+      at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at.val.programmaticStreamSerializationAllowed = 1;
+      lc.gridDim = dim3(update_grid(s.m_own));
+      lc.blockDim = dim3(256);
+      lc.stream = S.stream;
+      lc.attrs = &at;
+      lc.numAttrs = use_pdl(S) ? 1 : 0;
+      CK(cudaLaunchKernelEx(&lc, icnnm_dev::icnnm_update, s.m_own,
+                            static_cast<const icnnm_dev::IterState*>(S.st.p), cfg.lambda, kd,
+                            s.adj.p + s.halo_elems, s.L.p, s.V.p,
+                            static_cast<const float*>(s.pm.p), static_cast<const float*>(s.mask.p),
+                            s.Lt.p + s.halo_elems, S.red.p + kpe,
+                            S.exact_res ? s.Lr.p + s.halo_elems : static_cast<float*>(nullptr)));
     }
     exchange_lt(S);
     if (S.exact_res) {

@@ -417,6 +417,8 @@ __global__ void icnnm_coef(IterState* st, const double* __restrict__ theta,
                            IterStats* __restrict__ stats, int k, int kp, double kd,
                            double res_scale, double tol_p, double tol_c, double floor_rel,
                            int exact) {
+  pdl_wait();
+  pdl_trigger();
   // red = [norm2 (kp) | update slot (dl2, l2o, fit, ip, ln2) | pad]
   __shared__ int go;
   __shared__ int cur;
@@ -502,6 +504,8 @@ icnnm_update(int64_t m, const IterState* __restrict__ st, double lambda, double 
              float* __restrict__ adj, double* __restrict__ L, double* __restrict__ V,
              const float* __restrict__ pm, const float* __restrict__ mask,
              float* __restrict__ Lt, double* __restrict__ slot, float* __restrict__ Lr) {
+  pdl_wait();
+  pdl_trigger();
   if (!st->active) return;
   const double th = st->theta;
   const double r = st->r;

@@ -11,6 +11,20 @@
 
 namespace icnnm_dev {
 
+// Programmatic dependent launch (PDL).  The hot-loop kernels launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start (prologue:
+// TMEM alloc, barrier init, tap tables) while their predecessor finishes;
+// pdl_wait() blocks until the predecessor grid has completed and its writes
+// are visible, and every kernel of the chain executes it before its first
+// dependent global access, so completion stays transitive.  Without the
+// attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 constexpr int BM = 128;   // voxels per tile (one brick)
 constexpr int BN = 64;    // output columns per N-tile
 constexpr int BK = 32;    // reduction chunk

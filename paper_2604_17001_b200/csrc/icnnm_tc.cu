@@ -487,13 +487,6 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   constexpr int WLOAD = NB + NEPI + 1;   // B loader warp; W loader warp after it
   constexpr int BSTG = F16 ? (PAIR ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES;  // B stage stride
   const Geo& g = a.g;
-  float rr = 0.f;
-  if (a.mode == 1) {
-    if (!a.st->active) return;
-    if (FWD && a.st->it >= a.st->max_iters - 1) return;
-    rr = static_cast<float>(a.st->r);
-  }
-  if (a.mode == 2 && !a.st->active) return;  // forward on L_{t+1}: exact residual only
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* p = smem;
   const int sbn = a.sb, wsn = a.ws, san = a.sa;
@@ -617,6 +610,39 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       off = (sh * g.HW + sw) * g.HT + st;
     }
     tapoff[s] = off;
+  }
+  // everything above reads only the launch parameters: with PDL it overlaps
+  // the predecessor kernel; from here on the predecessor's writes are read
+  pdl_wait();
+  pdl_trigger();
+  // iteration state: a finished solve's replays are no-ops (uniform over the grid)
+  float rr = 0.f;
+  {
+    bool quit = false;
+    if (a.mode == 1) {
+      if (!a.st->active)
+        quit = true;
+      else if (FWD && a.st->it >= a.st->max_iters - 1)
+        quit = true;
+      else
+        rr = static_cast<float>(a.st->r);
+    }
+    if (a.mode == 2 && !a.st->active) quit = true;  // forward on L_{t+1}: exact residual only
+    if (quit) {
+      tc_fence_before();
+      if (CL2)
+        cluster_sync_all();
+      else
+        __syncthreads();
+      tc_fence_after();
+      if (warp == WMMA) {
+        if (PAIR)
+          asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(*tmem_slot));
+        else
+          asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(*tmem_slot));
+      }
+      return;
+    }
   }
   // cs[j]: forward mode 1: r c_j (the W_old weight); mode 2: c_j; adjoint:
   // c_j (mode 1) or 1, times the F16x3 operand scale
