@@ -726,3 +726,45 @@ def test_sharded_nccl_one_rank_transport(gpu, engine):
                        env={**os.environ, "NCCL_DEBUG": "WARN"},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+# --------------------------------------------------------------------------
+# Launch-structure options must not change results: PDL edges (ICNNM_PDL) and
+# the head/body graph split (ICNNM_GRAPH_SPLIT), both read once per process.
+# 64x64x32 with kernel 9x9x5 and 100 iterations is long enough to split.
+# --------------------------------------------------------------------------
+_LAUNCH_MODES = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2604_17001_b200 as P
+from paper_2604_17001_b200 import synth
+w = synth.scaled(synth.WORKLOADS[2], (64, 64, 32), iters=100, n_train=2)
+X, mask = w.target(), w.mask()
+B = P.learn_ensemble_basis(w.training(), w.kernel)
+for eng in ("f16x3", "ffma"):
+    L, r = P.icnnm_solve(X * mask, mask, B, P.SolverConfig(max_iters=100, engine=eng,
+                                                           tol_primal=1e-300, tol_change=1e-300))
+    assert r.iterations == 100
+    np.save(sys.argv[2] + "_" + eng + ".npy", L)
+    np.save(sys.argv[2] + "_" + eng + "_obj.npy", np.asarray(r.objective))
+print("ok")
+"""
+
+
+def test_launch_modes_do_not_change_results(gpu, tmp_path):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for tag, env in [("base", {}), ("nopdl", {"ICNNM_PDL": "0"}),
+                     ("nosplit", {"ICNNM_GRAPH_SPLIT": "0"})]:
+        r = subprocess.run([sys.executable, "-c", _LAUNCH_MODES, root, str(tmp_path / tag)],
+                           env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+    for eng in ("f16x3", "ffma"):
+        ref = np.load(tmp_path / f"base_{eng}.npy")
+        obj = np.load(tmp_path / f"base_{eng}_obj.npy")
+        for tag in ("nopdl", "nosplit"):
+            assert _rel(np.load(tmp_path / f"{tag}_{eng}.npy"), ref) < 1e-6, (tag, eng)
+            np.testing.assert_allclose(np.load(tmp_path / f"{tag}_{eng}_obj.npy"), obj, rtol=1e-6)
