@@ -380,9 +380,11 @@ def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
                                   "unavailable": "config 5 W state (%.0f GB) exceeds one B200; "
                                                  "run with --gpus >= 2 or --dims" % (need / 1e9)}))
             return 0
-    nid = None
+    # the NCCL transport is in the loop at every N: at N = 1 a one-rank
+    # communicator carries the halo shifts (self send/recv) and the all-reduce
+    nid = P.dist_unique_id()
     if world > 1:
-        obj = [P.dist_unique_id() if rank == 0 else None]
+        obj = [nid if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     X = w.target()
@@ -399,6 +401,17 @@ def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
                 times.append(rep.device_seconds)
     t_max = max_over_ranks(dist, dev, float(sum(times)))
     value = w.m * iters * args.steps / t_max
+    # solve-level roofline: both contractions' algorithmic flops (4 m k^2 per
+    # iteration, all ranks) over the whole device time of the solve -- the
+    # elementwise kernels, halo exchange and all-reduce count against it
+    peaks = load_peaks()
+    f16 = peaks.get("bf16_tflops") or 1650.0
+    achieved = 4.0 * w.m * w.k * w.k * iters * args.steps / t_max / 1e12
+    roof = {"bound": "tensor", "kernel": "whole iteration (solve-level)",
+            "achieved": achieved / world, "peak": f16 / 3.0, "unit": "TFLOP/s",
+            "frac": achieved / world / (f16 / 3.0),
+            "peak_source": "MEASURED_PEAKS.json dense bf16 / 3 kind::f16 MMAs per fp32 product; "
+                           "per GPU", "traffic": None}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
@@ -410,6 +423,9 @@ def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
                                                           "x".join(map(str, w.kernel)), iters, world),
                            "engine": args.engine, "parallelism": f"H-shard x{world}"},
                 "psnr_db_own_rows": synth.psnr(X[row0:row0 + rows.shape[0]], rows),
+                "roofline": roof,
+                "transport": "NCCL (ncclSend/ncclRecv halo shifts + ncclAllReduce of the "
+                             "k+8 reduction vector, captured in the solve graph)",
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if dist:
