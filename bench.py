@@ -381,12 +381,16 @@ def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
                                                  "run with --gpus >= 2 or --dims" % (need / 1e9)}))
             return 0
     # the NCCL transport is in the loop at every N: at N = 1 a one-rank
-    # communicator carries the halo shifts (self send/recv) and the all-reduce
-    nid = P.dist_unique_id()
-    if world > 1:
-        obj = [nid if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
+    # communicator carries the halo shifts (self send/recv) and the all-reduce.
+    # Every solve builds its own communicator, so every solve needs a fresh
+    # unique id (an id bootstraps exactly one ncclCommInitRank).
+    def fresh_id():
+        nid = P.dist_unique_id() if rank == 0 else None
+        if world > 1:
+            obj = [nid]
+            dist.broadcast_object_list(obj, src=0)
+            nid = obj[0]
+        return nid
     X = w.target()
     mask = w.mask()
     M = X * mask
@@ -395,6 +399,7 @@ def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
         for it in range(args.warmup + args.steps):
             if dist:
                 dist.barrier()
+            nid = fresh_id()
             row0, rows, rep = P.sharded_solve(M, mask, B, cfg, local_slabs=local_slabs,
                                               world=world, rank=rank, nccl_id=nid, device=dev)
             if it >= args.warmup:

@@ -304,6 +304,8 @@ int icnnm_dist_unique_id(char* out128);
  * exchange is device copies); world == 1 WITH an id (icnnm_dist_unique_id)
  * runs the exchange through a one-rank NCCL communicator (self send/recv,
  * all-reduce) -- the multi-process transport, exercised on one GPU.
+ * Each call builds (and destroys) its communicator, so each call needs a fresh
+ * id from icnnm_dist_unique_id (an id bootstraps exactly one communicator).
  * row0/nrows may be NULL. */
 int icnnm_sharded_solve(int order, const int64_t* dims, const double* M_obs,
                         const double* mask, const int64_t* kdims,
