@@ -5,7 +5,7 @@ import numpy as np
 import paper_2604_17001_b200 as P
 from paper_2604_17001_b200 import synth
 
-for engine in ("tf32x3", "ffma"):
+for engine in ("f16x3", "tf32x3", "ffma"):
     X = synth.synth_video(16, 12, 16, 6, 1, 5)
     mask = synth.reference_bernoulli_mask(X.shape, 0.4, 2)
     B = P.learn_ensemble_basis([synth.synth_video(16, 12, 16, 6, 1, 6)], (3, 3, 3))
