@@ -478,6 +478,10 @@ def report_line(args, P, w, B, cfg, iters, dev, world, value, t_max, kt, psnr, l
     e2e = None
     if not args.no_e2e:
         e2e_t = []
+        # one untimed call first: like the device-timed steps, e2e is measured
+        # warm (its first call allocates the 1 GB solver state next to the
+        # still-open handle solver; later calls reuse the device block cache)
+        P.icnnm_solve(np.ascontiguousarray(M), mask, B, cfg, device=dev)
         for _ in range(max(1, min(args.steps, 3))):
             Mh = np.ascontiguousarray(M)
             t0 = time.perf_counter()
