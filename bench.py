@@ -1,22 +1,31 @@
 #!/usr/bin/env python
 """ICNNM hot-path benchmark (BASELINE.json metric: voxel-iterations/s).
 
-Default workload: BASELINE config 2 (128x128x32 video completion, kernel
-9x9x5 -> k = 405, 20% observed, 300 iterations), one complete ICNNM solve per
-step on inputs already resident in HBM.  N > 1 (torchrun): every rank solves
-its own independently seeded config-2 tensor (batch split, no data-path
-collective) -> weak scaling; value = total voxel-iterations / max-over-ranks
-device time.
+Default workload: BASELINE config 4 -- frame interpolation, a batch of 64
+independent 128x128x32 tensors (even frames observed), kernel 7x7x5 (k = 245),
+200 iterations each, one shared eigenvector set.  One *step* is the rank's
+share of the 64-tensor batch (contiguous block; N = 1: all 64), each tensor a
+complete ICNNM solve; the batch is split over the ranks with no inter-GPU
+communication (BASELINE: "split across 1/2/4/8 GPUs"), so total work is
+fixed as N grows: scaling "strong".  value = 64 * m * iterations * steps /
+(max over ranks of the summed per-solve device time, CUDA events on the
+solver stream; the inputs of each solve are resident in HBM before its
+timed region starts).  e2e = the same metric through the public batch call
+(icnnm_cuda_solve_batch: host f64 inputs, validation, H2D, solves, D2H).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C]
-  python bench.py --impl reference ...   # reference CPU path (oracle port)
+  python bench.py --impl reference ...   # the reference's CPU path (oracle port)
 
-Synthetic data (BASELINE.json's generator; no datasets exist here).  Every
-step's W state (0.85 GB) exceeds L2 (126 MB), so no explicit L2 flush.
+Configs 1-3 run one tensor per rank (replicas, weak scaling); config 5 is the
+H-sharded single tensor (halo exchange + all-reduce; strong scaling).
+Synthetic data (BASELINE.json's generator, seeded; no datasets exist here).
+Every solve's W state (config 4: 0.54 GB) exceeds L2 (126 MB): no explicit
+L2 flush is needed between timed iterations.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -32,17 +41,19 @@ import numpy as np  # noqa: E402
 
 METRIC = "ICNNM voxel-iterations/sec"
 UNIT = "voxel-iter/s"
+DEFAULT_CONFIG = 4
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
     ap.add_argument("--engine", default="f16x3", choices=["f16x3", "tf32x3", "ffma"])
     ap.add_argument("--iters", type=int, default=0, help="override iterations per solve")
+    ap.add_argument("--batch", type=int, default=0, help="override the config-4 batch size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dims", type=int, nargs=3, default=None,
@@ -117,67 +128,6 @@ class ClockSampler:
                 "power_w_max": max(pw) if pw else None}
 
 
-def measure_tf32_peak(dev: int) -> float:
-    """Dense TF32 tensor throughput (cuBLAS 8192^3, best of 5) on this GPU --
-    the denominator of the TF32x3 engine's roofline (MEASURED_PEAKS.json has
-    only bf16)."""
-    import torch
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True
-    try:
-        n = 8192
-        a = torch.randn(n, n, device=f"cuda:{dev}")
-        b = torch.randn(n, n, device=f"cuda:{dev}")
-        for _ in range(2):
-            a @ b
-        best = 0.0
-        for _ in range(5):
-            s0 = torch.cuda.Event(enable_timing=True)
-            s1 = torch.cuda.Event(enable_timing=True)
-            s0.record()
-            a @ b
-            s1.record()
-            s1.synchronize()
-            best = max(best, 2 * n ** 3 / (s0.elapsed_time(s1) * 1e-3) / 1e12)
-        del a, b
-        return best
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-
-
-def measure_f16_peak(dev: int) -> float:
-    """Dense fp16 tensor throughput (cuBLAS 8192^3, best of 5): fallback
-    denominator of the F16x3 engine when MEASURED_PEAKS.json is absent."""
-    import torch
-    n = 8192
-    a = torch.randn(n, n, device=f"cuda:{dev}", dtype=torch.float16)
-    b = torch.randn(n, n, device=f"cuda:{dev}", dtype=torch.float16)
-    for _ in range(2):
-        a @ b
-    best = 0.0
-    for _ in range(5):
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
-        s0.record()
-        a @ b
-        s1.record()
-        s1.synchronize()
-        best = max(best, 2 * n ** 3 / (s0.elapsed_time(s1) * 1e-3) / 1e12)
-    del a, b
-    return best
-
-
-def load_ncu_traffic(engine: str):
-    """dram bytes per launch of the dominant kernels from the committed ncu
-    --set full capture (profiles/ncu_summary_*.json), if present."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary_latest.json")) as f:
-            d = json.load(f)
-        return d.get(engine)
-    except Exception:
-        return None
-
-
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -186,9 +136,57 @@ def load_peaks():
         return {}
 
 
+def lib_sha16() -> str:
+    """Identity of the product library build (pairs ncu traffic with a build)."""
+    path = os.path.join(ROOT, "paper_2604_17001_b200", "libicnnm_b200.so")
+    try:
+        with open(path, "rb") as f:
+            return hashlib.sha256(f.read()).hexdigest()[:16]
+    except OSError:
+        return "missing"
+
+
+def load_ncu_traffic(config: int, engine: str):
+    """DRAM bytes (read + write) per launch of the forward / adjoint kernels
+    from the committed `ncu --set full` capture of this build and config
+    (profiles/ncu_traffic_r2.json, written by tools/ncu_traffic.py); None when
+    the capture is of another build (then the traffic is unmeasured)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r2.json")) as f:
+            d = json.load(f)
+    except Exception:
+        return None, "no capture"
+    e = d.get(f"config{config}", {}).get(engine)
+    if not e:
+        return None, "no capture of this config/engine"
+    if e.get("lib_sha16") != lib_sha16():
+        return None, "capture is of build %s, this is %s" % (e.get("lib_sha16"), lib_sha16())
+    return e, "ncu --set full, this build (%s)" % e.get("lib_sha16")
+
+
+def workload(args, synth):
+    w = synth.WORKLOADS[args.config]
+    if args.dims:
+        w = synth.scaled(w, tuple(args.dims))
+    if args.iters:
+        w = synth.scaled(w, w.dims, iters=args.iters)
+    if args.batch and args.config == 4:
+        import dataclasses
+        w = dataclasses.replace(w, batch=args.batch)
+    return w
+
+
+def rank_share(nb: int, rank: int, world: int):
+    """Contiguous block of the batch for this rank (as icnnm_cuda_solve_batch
+    splits over devices)."""
+    return list(range(nb * rank // world, nb * (rank + 1) // world))
+
+
 # --------------------------------------------------------------------------
-# reference arm: the reference's CPU path (oracle port; the C++ reference
-# needs Eigen3 + FFTW3, absent in this image) on all host cores
+# reference arm: the reference's CPU path.  The C++ reference needs Eigen3 +
+# FFTW3 (absent in this image), so this is the fp64 oracle port of its
+# solver (oracle/icnnm_oracle.py) on all host cores.  Inputs come from
+# synthgen; neither module loads the product library.
 # --------------------------------------------------------------------------
 def run_reference(args):
     rank, world, local = dist_env()
@@ -197,10 +195,10 @@ def run_reference(args):
     ncores = os.cpu_count() or 1
     os.environ["ICNNM_ORACLE_THREADS"] = str(ncores)
     from threadpoolctl import threadpool_limits
-    from paper_2604_17001_b200 import synth
+    import synthgen as synth
     from oracle import icnnm_oracle as O
     O.WORKERS = ncores
-    w = synth.WORKLOADS[args.config]
+    w = workload(args, synth)
     X = w.target()
     mask = w.mask()
     with threadpool_limits(limits=ncores):
@@ -218,15 +216,17 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if args.config == 4 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (BASELINE.json generator, seeded)",
         "config": {"workload": f"BASELINE config {args.config}", "dims": list(w.dims),
-                   "kernel": list(w.kernel), "k": w.k,
+                   "kernel": list(w.kernel), "k": w.k, "iterations": w.iters,
+                   "batch": w.batch,
                    "step": "one ADMM iteration of the literal fp64 reference loop "
-                           "(solver.cpp:107-139) -- bounded sample of the "
-                           f"{w.iters}-iteration solve"},
+                           "(solver.cpp:107-139) on tensor 0 of the batch -- a bounded "
+                           f"sample of the {w.batch} x {w.iters}-iteration workload"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncores, "kind": "port",
                          "sample": f"{args.steps} ADMM iterations of config {args.config} "
-                                   f"after {args.warmup} warm-up iterations"},
+                                   f"tensor 0 after {args.warmup} warm-up iterations"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -255,7 +255,7 @@ def cpu_baseline_sample(w, M, mask, B, budget_s=20.0):
         dt = time.perf_counter() - t0
     return {"value": w.m * n / dt, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"{n} ADMM iterations of the literal fp64 oracle on config {w.cfg} "
-                      f"(1 thread, {dt:.1f} s)"}
+                      f"tensor 0 (1 thread, {dt:.1f} s)"}
 
 
 def setup_dist(world, local):
@@ -286,12 +286,10 @@ def main():
     import torch
     dist = setup_dist(world, local)
     import paper_2604_17001_b200 as P
-    from paper_2604_17001_b200 import synth
+    import synthgen as synth
 
-    w = synth.WORKLOADS[args.config]
-    if args.dims:
-        w = synth.scaled(w, tuple(args.dims))
-    iters = args.iters or w.iters
+    w = workload(args, synth)
+    iters = w.iters
     dev = local
     cfg = P.SolverConfig(max_iters=iters, tol_primal=1e-300, tol_change=1e-300,
                          engine=args.engine)
@@ -300,30 +298,26 @@ def main():
     if args.config == 5:
         return bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist)
 
-    # batch of tensors for this rank: cfg 4 splits the 64-tensor batch over
-    # the ranks (strong scaling); cfgs 1-3 give every rank its own tensor
-    # (independent replicas, weak scaling)
+    # config 4: the batch is split over the ranks (fixed total work, strong
+    # scaling); configs 1-3: every rank solves its own tensor (replicas)
     if args.config == 4:
-        nb = w.batch
-        mine = list(range(rank, nb, world))
-        scaling, units_total = "strong", nb
+        mine = rank_share(w.batch, rank, world)
+        scaling, units_total = "strong", w.batch
     else:
         mine = [rank]
         scaling, units_total = "weak", world
     mask = w.mask()
     targets = {b: w.target(b=b) for b in mine}
+    obs = {b: targets[b] * mask for b in mine}
     S = P.Solver(w.dims, B, device=dev)
-
-    loops = []
 
     def step():
         t = 0.0
         n = 0
         for b in mine:
-            S.upload(targets[b] * mask, mask)
-            rep = S.run(cfg)
+            S.upload(obs[b], mask)          # H2D before the solve's timed region
+            rep = S.run(cfg)                # device-resident solve, CUDA events
             t += rep.device_seconds
-            loops.append(rep.loop_seconds)
             n += S.last_launches
         return t, n
 
@@ -347,18 +341,43 @@ def main():
     L = S.download()
     psnr = synth.psnr(targets[mine[-1]], L)
 
-    # per-kernel times (live, CUDA events on the solver stream) for roofline
+    # per-kernel times (live, CUDA events on the solver stream) for the roofline
+    S.upload(obs[mine[0]], mask)
     S.set_profile(True)
     S.run(cfg)
     kt = S.kernel_times_ms()
     S.set_profile(False)
+    S.close()
+
+    # end to end through the public batch call, host buffers (every rank, its share)
+    e2e = None
+    if not args.no_e2e:
+        Ms = [obs[b] for b in mine]
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        Ls, reps = P.icnnm_solve_batch(Ms, mask, B, cfg, devices=[dev])
+        te = time.perf_counter() - t0
+        te = max_over_ranks(dist, dev, te)
+        n_mine = len(mine)
+        e2e = {"value": w.m * iters * units_total / te, "unit": UNIT,
+               "h2d_bytes_per_step": int(n_mine * (obs[mine[0]].nbytes + mask.nbytes)
+                                         + B.K.nbytes),
+               "d2h_bytes_per_step": int(n_mine * (Ls[0].nbytes + 3 * 8 * iters)),
+               "seconds": te,
+               "path": "icnnm_cuda_solve_batch C ABI on host f64 buffers: basis validation, "
+                       "per-tensor input validation, allocation, H2D, %d solves, D2H of L and "
+                       "the per-iteration reports, all inside the timed region (wall clock, "
+                       "max over ranks)" % n_mine,
+               "psnr_db_last": synth.psnr(targets[mine[-1]], Ls[-1])}
 
     if rank == 0:
-        report_line(args, P, w, B, cfg, iters, dev, world, value, t_max, kt, psnr, launches,
-                    clk, scaling, mask, targets[mine[0]] * mask,
-                    extra={"step_device_s": [round(x, 5) for x in dev_s],
-                           "loop_s": [round(x, 5) for x in loops[-args.steps:]]})
-    S.close()
+        cpu = None
+        if not args.no_cpu_baseline and w.m * w.k <= 3e8:
+            cpu = cpu_baseline_sample(w, obs[mine[0]], mask, B)
+        report_line(args, P, w, iters, world, value, t_max, kt, psnr, launches, clk, scaling,
+                    e2e, cpu, n_per_rank=len(mine),
+                    extra={"step_device_s": [round(x, 5) for x in dev_s]})
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -368,9 +387,8 @@ def main():
 def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
     """BASELINE config 5: one tensor H-sharded over the ranks (halo exchange +
     one NCCL all-reduce per iteration), strong scaling."""
-    import torch
     import paper_2604_17001_b200 as P
-    from paper_2604_17001_b200 import synth
+    import synthgen as synth
     local_slabs = 1
     if world == 1:
         need = w.m * ((w.k + 127) // 128 * 128) * 4
@@ -380,10 +398,9 @@ def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
                                   "unavailable": "config 5 W state (%.0f GB) exceeds one B200; "
                                                  "run with --gpus >= 2 or --dims" % (need / 1e9)}))
             return 0
-    # the NCCL transport is in the loop at every N: at N = 1 a one-rank
-    # communicator carries the halo shifts (self send/recv) and the all-reduce.
-    # Every solve builds its own communicator, so every solve needs a fresh
-    # unique id (an id bootstraps exactly one ncclCommInitRank).
+
+    # every solve builds its own communicator, so every solve needs a fresh
+    # unique id (an id bootstraps exactly one ncclCommInitRank)
     def fresh_id():
         nid = P.dist_unique_id() if rank == 0 else None
         if world > 1:
@@ -406,17 +423,14 @@ def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
                 times.append(rep.device_seconds)
     t_max = max_over_ranks(dist, dev, float(sum(times)))
     value = w.m * iters * args.steps / t_max
-    # solve-level roofline: both contractions' algorithmic flops (4 m k^2 per
-    # iteration, all ranks) over the whole device time of the solve -- the
-    # elementwise kernels, halo exchange and all-reduce count against it
     peaks = load_peaks()
-    f16 = peaks.get("bf16_tflops") or 1650.0
+    f16 = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops") or 1393.6
     achieved = 4.0 * w.m * w.k * w.k * iters * args.steps / t_max / 1e12
     roof = {"bound": "tensor", "kernel": "whole iteration (solve-level)",
             "achieved": achieved / world, "peak": f16 / 3.0, "unit": "TFLOP/s",
             "frac": achieved / world / (f16 / 3.0),
-            "peak_source": "MEASURED_PEAKS.json dense bf16 / 3 kind::f16 MMAs per fp32 product; "
-                           "per GPU", "traffic": None}
+            "peak_source": "MEASURED_PEAKS.json dense bf16 sustained / 3 kind::f16 MMAs per "
+                           "fp32 product; per GPU", "traffic": None}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
@@ -439,86 +453,87 @@ def bench_sharded(args, w, B, cfg, iters, rank, world, dev, dist):
     return 0
 
 
-def report_line(args, P, w, B, cfg, iters, dev, world, value, t_max, kt, psnr, launches, clk,
-                scaling, mask, M, extra=None):
-    import numpy as np
-    from paper_2604_17001_b200 import synth
-    peaks = load_peaks()
-    k = w.k
-    flops = 2.0 * w.m * k * k            # algorithmic, per launch (either contraction)
-    dom = "forward" if kt["forward"] >= kt["adjoint"] else "adjoint"
-    achieved = flops / (kt[dom] * 1e-3) / 1e12
-    if args.engine == "tf32x3":
-        tf32 = measure_tf32_peak(dev)
-        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": tf32 / 3.0,
-                "unit": "TFLOP/s", "frac": achieved / (tf32 / 3.0),
-                "peak_source": "measured dense TF32 (cuBLAS 8192^3 burst, %.0f TFLOP/s) / 3 "
-                               "tensor MMAs per fp32 product" % tf32,
-                "tensor_pipe_frac": 3.0 * achieved / tf32}
-    elif args.engine == "f16x3":
-        f16 = peaks.get("bf16_tflops")
-        src = "MEASURED_PEAKS.json dense bf16 (burst)"
-        if not f16:
-            f16, src = measure_f16_peak(dev), "measured dense fp16 (cuBLAS 8192^3 burst)"
-        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": f16 / 3.0,
-                "unit": "TFLOP/s", "frac": achieved / (f16 / 3.0),
-                "peak_source": "%s %.0f TFLOP/s / 3 kind::f16 MMAs per fp32 product "
-                               "(kind::f16 runs at the bf16 rate)" % (src, f16),
-                "tensor_pipe_frac": 3.0 * achieved / f16}
+def kernel_roofline(w, kt, peaks, engine, P, dev):
+    """Per-kernel rooflines: algorithmic flops 2 m k^2 per launch (either
+    contraction) on the pipe used (F16x3: 3 kind::f16 MMAs per fp32 product)
+    and algorithmic bytes (forward: W read + written, 8 m k, + L~ 4 m; adjoint:
+    W read 4 m k + adj written 4 m); each kernel's bound is the
+    slower of the two at the measured peaks (sustained bf16: the kernels run
+    inside a seconds-long solve)."""
+    k, m = w.k, w.m
+    flops = 2.0 * m * k * k
+    hbm = peaks.get("hbm_gbs") or 6550.1
+    if engine == "f16x3":
+        tpeak = (peaks.get("bf16_tflops_sustained") or 1393.6) / 3.0
+        src = "MEASURED_PEAKS.json bf16 sustained %.1f TFLOP/s / 3 kind::f16 MMAs per fp32 " \
+              "product; HBM %.1f GB/s" % (tpeak * 3, hbm)
+    elif engine == "tf32x3":
+        tpeak = (peaks.get("bf16_tflops_sustained") or 1393.6) / 2.0 / 3.0
+        src = "half the bf16 sustained rate (kind::tf32 K=8) / 3 MMAs per product"
     else:
-        ffma_peak = P.probe_ffma_tflops(dev)
-        roof = {"bound": "fp32", "kernel": dom, "achieved": achieved, "peak": ffma_peak,
-                "unit": "TFLOP/s", "frac": achieved / ffma_peak,
-                "peak_source": "measured FFMA probe (icnnm_probe_ffma_tflops)"}
-    traffic = load_ncu_traffic(args.engine) if args.config == 2 else None
-    roof["traffic"] = traffic.get(dom) if isinstance(traffic, dict) else None
-    roof["algorithmic_bytes"] = (8.0 if dom == "forward" else 4.0) * w.m * k
-    roof["per_launch_ms"] = kt
-    roof["flops_per_launch"] = flops
-    e2e = None
-    if not args.no_e2e:
-        e2e_t = []
-        # one untimed call first: like the device-timed steps, e2e is measured
-        # warm (its first call allocates the 1 GB solver state next to the
-        # still-open handle solver; later calls reuse the device block cache)
-        P.icnnm_solve(np.ascontiguousarray(M), mask, B, cfg, device=dev)
-        for _ in range(max(1, min(args.steps, 3))):
-            Mh = np.ascontiguousarray(M)
-            t0 = time.perf_counter()
-            Lh, r = P.icnnm_solve(Mh, mask, B, cfg, device=dev)
-            e2e_t.append(time.perf_counter() - t0)
-        te = float(np.mean(e2e_t))
-        e2e = {"value": w.m * iters / te * (world if args.config != 4 else 1), "unit": UNIT,
-               "h2d_bytes_per_step": int(M.nbytes + mask.nbytes + B.K.nbytes),
-               "d2h_bytes_per_step": int(Lh.nbytes + 3 * 8 * iters),
-               "path": "icnnm_cuda_solve C ABI on host f64 buffers (validation, allocation, "
-                       "H2D, solve, D2H inside the timed region); one tensor per rank"}
-    cpu = None
-    if not args.no_cpu_baseline and w.m * k <= 3e8:
-        cpu = cpu_baseline_sample(w, M, mask, B)
+        tpeak = P.probe_ffma_tflops(dev)
+        src = "measured FFMA probe"
+    out = {}
+    for name, nbytes in (("forward", 8.0 * m * k + 4.0 * m), ("adjoint", 4.0 * m * k + 4.0 * m)):
+        ms = kt[name]
+        t_tensor = flops / (tpeak * 1e12) * 1e3
+        t_hbm = nbytes / (hbm * 1e9) * 1e3
+        bound = "hbm" if t_hbm > t_tensor else "tensor"
+        if bound == "hbm":
+            achieved, peak, unit = nbytes / (ms * 1e-3) / 1e9, hbm, "GB/s"
+        else:
+            achieved, peak, unit = flops / (ms * 1e-3) / 1e12, tpeak, "TFLOP/s"
+        out[name] = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                     "frac": achieved / peak, "ms_per_launch": ms,
+                     "algorithmic_bytes": nbytes, "algorithmic_flops": flops,
+                     "roofline_ms": max(t_tensor, t_hbm)}
+    return out, src
+
+
+def report_line(args, P, w, iters, world, value, t_max, kt, psnr, launches, clk, scaling,
+                e2e, cpu, n_per_rank, extra=None):
+    peaks = load_peaks()
+    per, src = kernel_roofline(w, kt, peaks, args.engine, P, 0)
+    dom = "forward" if kt["forward"] >= kt["adjoint"] else "adjoint"
+    d = per[dom]
+    traffic, tsrc = load_ncu_traffic(args.config, args.engine)
+    roof = {"bound": d["bound"], "kernel": dom, "achieved": d["achieved"], "peak": d["peak"],
+            "unit": d["unit"], "frac": d["frac"],
+            "traffic": (traffic or {}).get(dom),
+            "traffic_source": tsrc,
+            "peak_source": src,
+            "per_kernel": per,
+            "per_launch_ms": kt,
+            # the whole iteration against its roofline (both contractions +
+            # the elementwise kernels, vs the sum of the two kernels' bounds)
+            "iteration_frac": (per["forward"]["roofline_ms"] + per["adjoint"]["roofline_ms"])
+            / (t_max * 1e3 / (args.steps * n_per_rank * iters))}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (BASELINE.json generator, seeded)",
-        "config": {"workload": f"BASELINE config {args.config}: {w.dims[0]}x{w.dims[1]}x"
-                               f"{w.dims[2]} kernel {w.kernel[0]}x{w.kernel[1]}x"
-                               f"{w.kernel[2]} (k={k}), {iters} iterations per solve",
+        "config": {"workload": f"BASELINE config {args.config}: "
+                               + (f"batch of {w.batch} x " if args.config == 4 else "")
+                               + f"{w.dims[0]}x{w.dims[1]}x{w.dims[2]} kernel "
+                               f"{w.kernel[0]}x{w.kernel[1]}x{w.kernel[2]} (k={w.k}), "
+                               f"{iters} iterations per solve",
                    "engine": args.engine,
-                   "step": "one full ICNNM solve from HBM" + (
-                       " per tensor of the rank's share of the 64-tensor batch"
-                       if args.config == 4 else ""),
-                   "l2": "inputs larger than L2 (W state %.2f GB)" % (
-                       w.m * ((k + 127) // 128 * 128) * 4 / 1e9),
-                   "parallelism": ("batch split x%d (no communication)" % world)},
+                   "step": ("the rank's share of the %d-tensor batch (%d tensors), one full "
+                            "ICNNM solve each from HBM" % (w.batch, n_per_rank))
+                   if args.config == 4 else "one full ICNNM solve from HBM",
+                   "l2": "inputs larger than L2 (W state %.2f GB per solve)" % (
+                       w.m * ((w.k + 15) // 16 * 16) * 4 / 1e9),
+                   "parallelism": ("batch split x%d (no communication)" % world)
+                   if args.config == 4 else "replicas x%d" % world},
         "psnr_db": psnr,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
-        "hbm_peak_gbs": peaks.get("hbm_gbs"),
+        "lib_sha16": lib_sha16(),
     }
     if extra:
         line["timing_detail"] = extra

@@ -113,6 +113,25 @@ int icnnm_cuda_solve(int order, const int64_t* dims, const double* M_obs,
                      const icnnm_solver_config* cfg, int device, double* L_out,
                      icnnm_solve_report* report);
 
+/* Batch of independent solves (BASELINE config 4: 64 tensors, one shared
+ * basis and config).  Each problem i is exactly icnnm_cuda_solve on
+ * (M_obs[i], masks[i]) -- its own theta0 (solver.cpp:88-91), res_scale
+ * (:97) and stopping test -- the reference's "concurrent independent solves"
+ * contract (solver.hpp:64-67) as one call.  Problems are split
+ * into contiguous blocks over the n_devices GPUs in `devices` (one host
+ * thread, stream and solver state per device, no inter-GPU communication);
+ * the basis is validated once for the whole batch.  reports may be NULL or
+ * an array of n reports (each with its own caller-allocated trace arrays).
+ * On failure the status of the first failing problem is returned and
+ * icnnm_last_error() names it. */
+int icnnm_cuda_solve_batch(int n, int order, const int64_t* dims,
+                           const double* const* M_obs,
+                           const double* const* masks, const int64_t* kdims,
+                           const double* K_colmajor, const double* eigenvalues,
+                           const icnnm_solver_config* cfg, const int* devices,
+                           int n_devices, double* const* L_out,
+                           icnnm_solve_report* reports);
+
 /* Handle API mirroring BasisConvolver's precompute-once pattern
  * (conv_op.hpp:61-81): create binds dims, kernel box and K to a device;
  * upload stages one problem in HBM; run solves it from HBM; download
@@ -320,49 +339,6 @@ int icnnm_sharded_solve(int order, const int64_t* dims, const double* M_obs,
  * thinner than kh-1 rows. */
 int icnnm_shard_plan(int64_t H, int G, int64_t kh, int g, int64_t* start,
                      int64_t* count);
-
-/* ------------------------------------------------------------------------
- * BASELINE synthetic generator (host, std::mt19937_64).
- * ---------------------------------------------------------------------- */
-
-/* Sum of n_sin 3-D sinusoids (amplitude U[0.5,1.5], integer frequencies
- * 0..4 per axis, phase U[0,2pi)) plus n_blob Gaussian blobs (sigma px,
- * amplitude U[0.5,1.5], moving 1 px/frame along a random direction,
- * periodic), min-max scaled to [0,1], then + N(0, noise_sigma^2).
- * dims = H, W, T; out has H*W*T doubles (row-major). */
-int icnnm_synth_video(int64_t H, int64_t W, int64_t T, int n_sin, int n_blob,
-                      double blob_sigma, double noise_sigma, uint64_t seed,
-                      double* out);
-
-/* Mask kinds. */
-#define ICNNM_MASK_IID 0          /* voxel kept iff U[0,1) < rate            */
-#define ICNNM_MASK_EXACT 1        /* exactly llround(rate*m) kept, shuffle   */
-                                  /* (reference bernoulli_mask, mask.cpp:49-59) */
-#define ICNNM_MASK_T_FRAMES 2     /* keep T-frames t with (t % 2 == 0)       */
-#define ICNNM_MASK_T_PREFIX 3     /* keep T-frames t < (int)rate             */
-#define ICNNM_MASK_IID_BOXES 4    /* iid(rate) minus n_boxes boxes            */
-
-int icnnm_synth_mask(int64_t H, int64_t W, int64_t T, int kind, double rate,
-                     int n_boxes, uint64_t seed, double* out);
-
-/* Reference-test data generators (proj/tests/test_util.hpp:27-49 and
- * mask.cpp:49-59), reproducing libstdc++'s std::mt19937_64 streams so that
- * the reference's own known-answer cases can be rebuilt bit-for-bit. */
-typedef struct icnnm_rng_s* icnnm_rng_t;
-icnnm_rng_t icnnm_rng_create(uint64_t seed);
-void icnnm_rng_destroy(icnnm_rng_t r);
-/* uniform_real_distribution<double>(lo, hi) draws */
-void icnnm_rng_uniform(icnnm_rng_t r, double lo, double hi, int64_t n,
-                       double* out);
-/* uniform_int_distribution<int64_t>(lo, hi) draws */
-void icnnm_rng_uniform_int(icnnm_rng_t r, int64_t lo, int64_t hi, int64_t n,
-                           int64_t* out);
-/* normal_distribution<double>(mean, stddev) draws */
-void icnnm_rng_normal(icnnm_rng_t r, double mean, double stddev, int64_t n,
-                      double* out);
-/* bernoulli_mask(dims, rate, seed) of mask.cpp:49-59 (flat, m entries). */
-int icnnm_reference_bernoulli_mask(int64_t m, double rate, uint64_t seed,
-                                   double* out);
 
 /* ------------------------------------------------------------------------
  * Reference file formats (tensor_io.cpp:86-128, report_io.cpp:39-68), used

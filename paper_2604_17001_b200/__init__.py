@@ -6,7 +6,7 @@ package is the Python mirror of the reference's solver/operator interface.
 """
 from ._lib import IcnnmError, InvalidArgument, CudaError, LIB_PATH, lib
 from .api import (SolverConfig, SolveReport, EigenBasis, Solver, BasisConvolver,
-                  icnnm_solve, cnnm_solve, learn_ensemble_basis, conv_adjoint, prox_l21, conv_gram,
+                  icnnm_solve, icnnm_solve_batch, cnnm_solve, learn_ensemble_basis, conv_adjoint, prox_l21, conv_gram,
                   objective_icnnm, symeig, sharded_solve, shard_plan, dist_unique_id,
                   device_count, empty_cache, probe_ffma_tflops)
 from . import synth, analysis
@@ -14,7 +14,7 @@ from . import synth, analysis
 __all__ = [
     "IcnnmError", "InvalidArgument", "CudaError", "LIB_PATH", "lib",
     "SolverConfig", "SolveReport", "EigenBasis", "Solver", "BasisConvolver",
-    "icnnm_solve", "cnnm_solve", "learn_ensemble_basis", "conv_adjoint", "prox_l21", "conv_gram",
+    "icnnm_solve", "icnnm_solve_batch", "cnnm_solve", "learn_ensemble_basis", "conv_adjoint", "prox_l21", "conv_gram",
     "objective_icnnm", "symeig", "sharded_solve", "shard_plan", "dist_unique_id",
     "device_count", "empty_cache", "probe_ffma_tflops", "synth", "analysis",
 ]

@@ -12,8 +12,6 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libicnnm_b200.so")
-# A/B kernel experiments only: load another build of the same C ABI
-LIB_PATH = os.environ.get("ICNNM_LIB_AB") or LIB_PATH
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "icnnm_b200.h")
 
 ICNNM_OK = 0
@@ -105,6 +103,10 @@ SIGNATURES = {
     "icnnm_cuda_solve": (C.c_int, [C.c_int, _lp, _dp, _dp, _lp, _dp, _dp,
                                    C.POINTER(SolverConfigC), C.c_int, _dp,
                                    C.POINTER(SolveReportC)]),
+    "icnnm_cuda_solve_batch": (C.c_int, [C.c_int, C.c_int, _lp, C.POINTER(_dp), C.POINTER(_dp),
+                                         _lp, _dp, _dp, C.POINTER(SolverConfigC),
+                                         C.POINTER(C.c_int), C.c_int, C.POINTER(_dp),
+                                         C.POINTER(SolveReportC)]),
     "icnnm_solver_create": (C.c_int, [C.c_int, _lp, _lp, _dp, _dp, C.c_int,
                                       C.POINTER(C.c_void_p)]),
     "icnnm_solver_upload": (C.c_int, [C.c_void_p, _dp, _dp]),
@@ -134,16 +136,6 @@ SIGNATURES = {
                                       C.c_int, C.c_char_p, C.c_int, _dp, _lp, _lp,
                                       C.POINTER(SolveReportC)]),
     "icnnm_shard_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int64, C.c_int, _lp, _lp]),
-    "icnnm_synth_video": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
-                                    C.c_double, C.c_double, C.c_uint64, _dp]),
-    "icnnm_synth_mask": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_double,
-                                   C.c_int, C.c_uint64, _dp]),
-    "icnnm_rng_create": (C.c_void_p, [C.c_uint64]),
-    "icnnm_rng_destroy": (None, [C.c_void_p]),
-    "icnnm_rng_uniform": (None, [C.c_void_p, C.c_double, C.c_double, C.c_int64, _dp]),
-    "icnnm_rng_uniform_int": (None, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, _lp]),
-    "icnnm_rng_normal": (None, [C.c_void_p, C.c_double, C.c_double, C.c_int64, _dp]),
-    "icnnm_reference_bernoulli_mask": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, _dp]),
     "icnnm_probe_ffma_tflops": (C.c_int, [C.c_int, _dp]),
     "icnnm_io_last_error": (C.c_char_p, []),
     "icnnm_write_tnsr": (C.c_int, [C.c_char_p, C.c_int, _lp, _dp]),
@@ -188,8 +180,6 @@ def lib():
                     " or `make -C paper_2604_17001_b200/csrc`")
             handle = C.CDLL(LIB_PATH)
             for name, (res, args) in SIGNATURES.items():
-                if os.environ.get("ICNNM_LIB_AB") and not hasattr(handle, name):
-                    continue  # A/B run against an older build
                 fn = getattr(handle, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -176,6 +176,50 @@ def icnnm_solve(M_obs, mask, basis: EigenBasis, cfg: Optional[SolverConfig] = No
     return L, _report_from_c(rep, obj, res, lc)
 
 
+def icnnm_solve_batch(M_obs: Sequence[np.ndarray], masks, basis: EigenBasis,
+                      cfg: Optional[SolverConfig] = None, devices: Sequence[int] = (0,)
+                      ) -> Tuple[List[np.ndarray], List[SolveReport]]:
+    """A batch of independent icnnm_solve calls sharing one basis and config
+    (BASELINE config 4), split in contiguous blocks over `devices` inside one
+    library call (icnnm_cuda_solve_batch).  `masks` is one mask per tensor or
+    a single mask shared by all.  Returns the recovered tensors and one
+    SolveReport per tensor."""
+    cfg = cfg or SolverConfig()
+    Ms = [_f64(x) for x in M_obs]
+    n = len(Ms)
+    if n == 0:
+        return [], []
+    if isinstance(masks, np.ndarray) and masks.shape == Ms[0].shape:
+        Ws = [_f64(masks)] * n
+    else:
+        Ws = [_f64(x) for x in masks]
+    if len(Ws) != n:
+        raise InvalidArgument("solve_batch: one mask per tensor (or one shared mask)")
+    shape = Ms[0].shape
+    for M, W in zip(Ms, Ws):
+        if M.shape != shape or W.shape != shape:
+            raise InvalidArgument("solve_batch: all tensors and masks must share dims")
+    _check_basis_shape(basis, shape)
+    c = cfg.to_c()
+    Ls = [np.empty_like(M) for M in Ms]
+    bufs = [_report_buffers(max(int(cfg.max_iters), 1)) for _ in range(n)]
+    reps = (SolveReportC * n)()
+    for i, (rep, _, _, _) in enumerate(bufs):
+        reps[i] = rep
+    Kc = _colmajor(basis.K)
+    ev = _f64(basis.eigenvalues) if basis.eigenvalues is not None else None
+    pM = (C.POINTER(C.c_double) * n)(*[dptr(x) for x in Ms])
+    pW = (C.POINTER(C.c_double) * n)(*[dptr(x) for x in Ws])
+    pL = (C.POINTER(C.c_double) * n)(*[dptr(x) for x in Ls])
+    devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+    check(lib().icnnm_cuda_solve_batch(n, len(shape), lptr(_dims(shape)), pM, pW,
+                                       lptr(_dims(basis.kernel_shape)), dptr(Kc),
+                                       dptr(ev) if ev is not None else None, C.byref(c),
+                                       devs, len(devices), pL, reps))
+    out = [_report_from_c(reps[i], b[1], b[2], b[3]) for i, b in enumerate(bufs)]
+    return Ls, out
+
+
 class Solver:
     """Handle API: basis bound once (BasisConvolver's precompute-once
     pattern, conv_op.hpp:61-81); problems are uploaded to HBM and solved
@@ -209,7 +253,15 @@ class Solver:
         return _report_from_c(rep, obj, res, lc)
 
     def download(self, out: Optional[np.ndarray] = None) -> np.ndarray:
-        L = out if out is not None else np.empty(self.dims)
+        if out is not None:
+            if (not isinstance(out, np.ndarray) or out.shape != tuple(self.dims)
+                    or out.dtype != np.float64 or not out.flags.c_contiguous
+                    or not out.flags.writeable):
+                raise InvalidArgument("download: out must be a writeable C-contiguous "
+                                      f"float64 array of shape {tuple(self.dims)}")
+            L = out
+        else:
+            L = np.empty(self.dims)
         check(lib().icnnm_solver_download(self._h, dptr(L)))
         return L
 

@@ -39,6 +39,13 @@ namespace icnnm_host {
 
 thread_local std::string g_last_error;
 
+#ifdef ICNNM_EXPERIMENTS
+int env_knob(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+#endif
+
 // ICNNM_TIMING=1: host-side phase times of the C-ABI calls on stderr (where an
 // end-to-end call spends its time outside the device-resident loop).
 struct PhaseTimer {
@@ -336,10 +343,7 @@ Geo tc_geo(const Geo& g, const TcPlan& t) {
   Geo q = g;
   q.kp = t.kp;
   q.ktp = t.kp;
-  static const bool bt32 = [] {
-    const char* e = std::getenv("ICNNM_TC_BT32");
-    return e && std::atoi(e) == 1;
-  }();
+  static const bool bt32 = env_knob("ICNNM_TC_BT32", 0) == 1;
   if (bt32 && g.T % 32 == 0 && g.W >= 2 && g.H >= 2) {
     q.bt = 32;
     q.bw = 2;
@@ -358,10 +362,7 @@ Geo tc_geo(const Geo& g, const TcPlan& t) {
   // conflicts; config 2 (HT = 20, HW*HT = 240): 4 vs 0.  vmap 1 needs bh*bt = 32
   // (a warp then shares vw; the adjoint's N order becomes sw-fastest).
   q.vmap = 0;
-  static const int vmap_env = [] {
-    const char* e = std::getenv("ICNNM_TC_VMAP");
-    return e ? std::atoi(e) : -1;
-  }();
+  static const int vmap_env = env_knob("ICNNM_TC_VMAP", -1);
   if (q.bt == 16 && q.bh * q.bt == 32 && q.kw >= 1) {
     auto conf = [](int d) { return std::abs(16 - (d % 32)); };
     const bool better = conf(q.HW * q.HT) < conf(q.HT);
@@ -584,20 +585,11 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   a.bunscale = t.bunscale;
   a.amax = amax;
   a.dbg = dbg;
-  static const int skip_env = [] {
-    const char* e = std::getenv("ICNNM_TC_SKIP");  // timing experiments only
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int skip_env = env_knob("ICNNM_TC_SKIP", 0);  // timing experiments only (results invalid)
   a.skip = skip_env;
-  static const int bsplit_env = [] {
-    const char* e = std::getenv("ICNNM_TC_BSPLIT");  // A/B experiments only
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int bsplit_env = env_knob("ICNNM_TC_BSPLIT", 0);
   a.bsplit = bsplit_env;
-  static const int bpair_env = [] {
-    const char* e = std::getenv("ICNNM_TC_BPAIR");  // A/B experiments
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int bpair_env = env_knob("ICNNM_TC_BPAIR", 0);
   a.bpair = bpair_env;
   a.g = gtc;
   a.src = src;
@@ -623,14 +615,8 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   // 0.73 ms), the forward loses (0.70 -> 0.77 ms: its heavier epilogue is no
   // longer hidden behind the other tile's MMAs), so only the adjoint pairs.
   // ICNNM_TC_GRP / ICNNM_TC_SKEW override both kernels for A/B experiments.
-  static const int grp_env = [] {
-    const char* e = std::getenv("ICNNM_TC_GRP");
-    return e ? std::atoi(e) : -1;
-  }();
-  static const int skew_env = [] {
-    const char* e = std::getenv("ICNNM_TC_SKEW");
-    return e ? std::atoi(e) : -1;
-  }();
+  static const int grp_env = env_knob("ICNNM_TC_GRP", -1);
+  static const int skew_env = env_knob("ICNNM_TC_SKEW", -1);
   const bool can_pair = t.ntn >= 2 && t.sa >= 4;
   a.grp = grp_env >= 0 ? grp_env : ((can_pair && !fwd) ? 2 : 1);
   a.skew = skew_env >= 0 ? skew_env : std::max(0, t.sa - 2);
@@ -646,20 +632,14 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   // B stream -- 13.3 KB per 312-cycle chunk and SM, the largest L2 and SMEM
   // consumer (and a quarter of the board power, profiles/ab_r1) -- halves.
   // ICNNM_TC_CS=2 enables (A/B experiments; first measurement: slower, see DESIGN).
-  static const int cs_env = [] {
-    const char* e = std::getenv("ICNNM_TC_CS");
-    return e ? std::atoi(e) : -1;
-  }();
+  static const int cs_env = env_knob("ICNNM_TC_CS", -1);
   a.cs = cs_env >= 0 ? cs_env : 1;  // pairs: opt-in until they beat single CTAs
   if (!t.f16 || n_bricks(gtc) < 2) a.cs = 1;
   const bool pairs = a.cs > 1;
   // pairs: the peer's half of every B stage signals the leader's barrier
   // directly through 2-SM tensor copies (ICNNM_TC_TMAPAIR=0: bulk copies and a
   // relay thread, the first pair design)
-  static const int tmapair_env = [] {
-    const char* e = std::getenv("ICNNM_TC_TMAPAIR");
-    return e ? std::atoi(e) : 1;
-  }();
+  static const int tmapair_env = env_knob("ICNNM_TC_TMAPAIR", 1);
   a.tma_pair = (pairs && tmapair_env != 0 && Bpk != nullptr) ? 1 : 0;
   if (a.tma_pair) {
     a.tmB[0] = pair_b_map(Bpk, t, t.wbase / 2);
@@ -667,36 +647,24 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   }
   // B multicast (F16x3 single CTAs in 2-CTA clusters sharing one B stream, each
   // CTA loading half of every stage): ICNNM_TC_MCB=1 (A/B experiment)
-  static const int mcb_env = [] {
-    const char* e = std::getenv("ICNNM_TC_MCB");
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int mcb_env = env_knob("ICNNM_TC_MCB", 0);
   a.mcb = (mcb_env > 0 && t.f16 && !pairs && n_bricks(gtc) >= 2) ? 1 : 0;
   // F16x3 B stages are 16 KB (half the TF32 stage), which leaves room for
   // an 8-deep forward W-group ring: a 208-column tile has 8 W groups, so the
   // whole tile's W_old is in flight before its epilogue starts.  Deepest B
   // ring up to the cap first, then the deepest even W ring that still fits.
-  static const int sb_env = [] {
-    // 4 B stages measured faster than 5-6 for TF32x3 (more SMEM leaves less L1):
-    // profiles/README_r1.md; CTA pairs hold half-size stages, so twice as many
-    // in the same space.  ICNNM_TC_SB overrides for A/B experiments
-    const char* e = std::getenv("ICNNM_TC_SB");
-    return e ? std::atoi(e) : -1;
-  }();
+  // 4 B stages measured faster than 5-6 for TF32x3 (more SMEM leaves less L1):
+  // profiles/README_r1.md; CTA pairs hold half-size stages, so twice as many
+  // in the same space
+  static const int sb_env = env_knob("ICNNM_TC_SB", -1);
   // F16x3 single CTAs: 8 stages (+1.8% / +1.3% over 4 / 6 on config 2,
   // profiles/ab_r1/tune/, profiles/ab_r1/sb8/)
   const int sb_cap = sb_env > 0 ? sb_env : (pairs ? 8 : (t.f16 ? 8 : 4));
-  static const int ws_cap = [] {
-    const char* e = std::getenv("ICNNM_TC_WS");  // A/B experiments
-    return e ? std::atoi(e) : icnnm_dev::tc::WS;
-  }();
+  static const int ws_cap = env_knob("ICNNM_TC_WS", icnnm_dev::tc::WS);
   // Adjoint epilogue: a second 4-warp half (alternate 32-column blocks, its
   // own 4 output bricks) when those bricks fit next to a B ring of >= 4
   // stages; otherwise one half.  ICNNM_TC_EHALF=1|2 overrides (A/B).
-  static const int eh_env = [] {
-    const char* e = std::getenv("ICNNM_TC_EHALF");
-    return e ? std::atoi(e) : -1;
-  }();
+  static const int eh_env = env_knob("ICNNM_TC_EHALF", -1);
   a.sb = 2;
   a.ws = 2;
   a.ehalf = 1;
@@ -776,49 +744,16 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   }
 }
 
-// EigenBasis::validate (spectral.cpp:25-41).
-// Bases that passed the orthogonality check, keyed by k and two independent
-// 64-bit hashes of their bytes: a repeated solve with the same basis (the
-// end-to-end path validates on every call, as the reference does) skips the
-// O(k^3) check -- the same bytes give the same verdict.  Hashing 1.3 MB costs
-// ~0.1 ms against ~1.5 ms for the check at k = 405.
+// EigenBasis::validate (spectral.cpp:25-41), run on every call that takes a
+// basis, as the reference runs it inside every icnnm_solve (solver.cpp:154);
+// the handle API validates once at create (BasisConvolver's precompute-once
+// pattern, conv_op.hpp:61-64).
 void validate_orthogonal(int k, const double* K);
 void validate_evals(int k, const double* evals);
 
-struct BasisKey {
-  int k;
-  uint64_t h1, h2;
-  bool operator==(const BasisKey& o) const { return k == o.k && h1 == o.h1 && h2 == o.h2; }
-};
-BasisKey basis_key(int k, const double* K) {
-  const size_t n = static_cast<size_t>(k) * k;
-  uint64_t h1 = 0xcbf29ce484222325ull ^ static_cast<uint64_t>(k), h2 = 0x9e3779b97f4a7c15ull;
-  for (size_t i = 0; i < n; ++i) {
-    uint64_t w;
-    std::memcpy(&w, K + i, sizeof(w));
-    h1 = (h1 ^ w) * 0x100000001b3ull;
-    h2 = (h2 + w * 0xff51afd7ed558ccdull);
-    h2 = ((h2 << 31) | (h2 >> 33)) * 0xc4ceb9fe1a85ec53ull;
-  }
-  return {k, h1, h2};
-}
-std::mutex g_basis_mu;
-std::vector<BasisKey> g_basis_ok;  // most recent last, at most 16
-
 void validate_basis(int k, const double* K, const double* evals) {
   if (!K) invalid("EigenBasis: K must be k x k");
-  const BasisKey key = basis_key(k, K);
-  bool known = false;
-  {
-    std::lock_guard<std::mutex> lk(g_basis_mu);
-    for (const auto& x : g_basis_ok) known = known || x == key;
-  }
-  if (!known) validate_orthogonal(k, K);
-  if (!known) {
-    std::lock_guard<std::mutex> lk(g_basis_mu);
-    if (g_basis_ok.size() >= 16) g_basis_ok.erase(g_basis_ok.begin());
-    g_basis_ok.push_back(key);
-  }
+  validate_orthogonal(k, K);
   validate_evals(k, evals);
 }
 
@@ -934,10 +869,7 @@ struct Solver {
   bool profile = false;
   bool tc_counters = false;
   // head graph launched while the rest of the solve is captured (ICNNM_GRAPH_SPLIT=0: one graph)
-  bool graph_split = [] {
-    const char* e = std::getenv("ICNNM_GRAPH_SPLIT");
-    return !(e && std::atoi(e) == 0);
-  }();
+  bool graph_split = env_knob("ICNNM_GRAPH_SPLIT", 1) != 0;
   double prof_ms[4] = {0, 0, 0, 0};
   DBuf<unsigned long long> dbg;  // 2 x DBG_SLOTS tcgen05 pipeline counters
 
@@ -1000,6 +932,11 @@ void solver_alloc(Solver& S) {
 void solver_upload(Solver& S, const double* M, const double* mask) {
   if (!M || !mask) invalid("solve: null input");
   const int64_t m = S.p.m;
+  // The staging buffers are overwritten below before the scan has finished:
+  // the handle holds no problem until this upload has validated (a rejected
+  // upload leaves "no problem uploaded", never the previous problem's scalars
+  // next to the rejected data).
+  S.uploaded = false;
   // The validation scan (sequential: pm's sums feed theta0 / res_scale in the
   // reference's order) runs on a helper thread while this thread pushes the
   // pageable H2D copies; an invalid input is reported after both finish.
@@ -1100,13 +1037,10 @@ void exchange_adj(Solver& S) {
 
 int engine_kp(const Solver& S);
 
-// Debugging only: ICNNM_F16_OFF=1 runs the F16x3 engine's adjoint in TF32x3,
+// Debugging only (experiments build): ICNNM_F16_OFF=1 runs the F16x3 engine's adjoint in TF32x3,
 // =2 its forward (isolates a kernel when bisecting a failure).
 inline int f16_debug_mask() {
-  static const int m = [] {
-    const char* e = std::getenv("ICNNM_F16_OFF");
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int m = env_knob("ICNNM_F16_OFF", 0);  // bisection only
   return m;
 }
 
@@ -1162,10 +1096,7 @@ void ensure_engine_basis(Solver& S, int engine) {
 // sharded solve (copies / NCCL between the kernels), the per-family profile
 // and ICNNM_PDL=0.
 bool use_pdl(const Solver& S) {
-  static const bool on = [] {
-    const char* e = std::getenv("ICNNM_PDL");
-    return !(e && std::atoi(e) == 0);
-  }();
+  static const bool on = env_knob("ICNNM_PDL", 1) != 0;
   return on && !S.sharded && !S.profile;
 }
 
@@ -1729,6 +1660,71 @@ int icnnm_cuda_solve(int order, const int64_t* dims, const double* M_obs, const 
       fill_report(S, *cfg, R, report, wall);
     }
     g_timer.mark("release");
+  });
+}
+
+int icnnm_cuda_solve_batch(int n, int order, const int64_t* dims, const double* const* M_obs,
+                           const double* const* masks, const int64_t* kdims,
+                           const double* K_colmajor, const double* eigenvalues,
+                           const icnnm_solver_config* cfg, const int* devices, int n_devices,
+                           double* const* L_out, icnnm_solve_report* reports) {
+  return guard([&] {
+    if (n < 0) invalid("solve_batch: negative batch size");
+    if (n == 0) return;
+    if (!M_obs || !masks || !L_out) invalid("solve_batch: null input/output array");
+    if (!devices || n_devices < 1) invalid("solve_batch: no devices");
+    validate_cfg(cfg);
+    Problem p = make_problem(order, dims, kdims);
+    for (int i = 0; i < n; ++i)
+      if (!M_obs[i] || !masks[i] || !L_out[i])
+        invalid("solve_batch: null tensor pointer at index " + std::to_string(i));
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    for (int d = 0; d < n_devices; ++d)
+      if (devices[d] < 0 || devices[d] >= ndev)
+        invalid("device index " + std::to_string(devices[d]) + " out of range (" +
+                std::to_string(ndev) + " devices)");
+    validate_basis(p.k, K_colmajor, eigenvalues);  // once: one shared basis
+    // contiguous blocks of problems per device; one worker thread per device
+    const int nw = std::min(n, n_devices);
+    struct Outcome {
+      int code = ICNNM_OK;
+      int index = -1;
+      std::string msg;
+    };
+    std::vector<Outcome> out(nw);
+    auto worker = [&](int w) {
+      const int i0 = static_cast<int>(static_cast<int64_t>(n) * w / nw);
+      const int i1 = static_cast<int>(static_cast<int64_t>(n) * (w + 1) / nw);
+      int cur = i0;
+      const int rc = guard([&] {
+        DeviceScope ds(devices[w]);
+        Solver S;
+        S.p = p;
+        S.device = devices[w];
+        S.K.assign(K_colmajor, K_colmajor + static_cast<size_t>(p.k) * p.k);
+        S.slabs.resize(1);
+        S.slabs[0].rows = p.dims[0];
+        solver_alloc(S);
+        for (cur = i0; cur < i1; ++cur) {
+          const auto t0 = std::chrono::steady_clock::now();
+          solver_upload(S, M_obs[cur], masks[cur]);
+          RunResult R = solver_run(S, *cfg);
+          solver_download(S, L_out[cur]);
+          const double wall =
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          if (reports) fill_report(S, *cfg, R, reports + cur, wall);
+        }
+      });
+      if (rc != ICNNM_OK) out[w] = {rc, cur, g_last_error};
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < nw; ++w) pool.emplace_back(worker, w);
+    worker(0);
+    for (auto& t : pool) t.join();
+    for (const Outcome& o : out)
+      if (o.code != ICNNM_OK)
+        fail(o.code, "solve_batch: problem " + std::to_string(o.index) + ": " + o.msg);
   });
 }
 

@@ -20,6 +20,22 @@ using icnnm_dev::Geo;
 namespace icnnm_host {
 
 // ---------------------------------------------------------------------------
+// A/B experiment knobs.  The shipped library is built without
+// ICNNM_EXPERIMENTS: every kernel-configuration knob then returns its default
+// and the environment is never read, so a stale variable from a profiling
+// session cannot change what a product call computes or how.  `make
+// EXPERIMENTS=1` builds the A/B library (environment overrides, plus the
+// work-skipping timing switches, whose results are invalid by design).
+// ---------------------------------------------------------------------------
+#ifdef ICNNM_EXPERIMENTS
+int env_knob(const char* name, int dflt);
+constexpr bool kExperiments = true;
+#else
+inline int env_knob(const char*, int dflt) { return dflt; }
+constexpr bool kExperiments = false;
+#endif
+
+// ---------------------------------------------------------------------------
 // Errors
 // ---------------------------------------------------------------------------
 struct Error {

@@ -43,6 +43,14 @@
 namespace icnnm_dev {
 namespace tc {
 
+// Work-skipping timing switches (TcArgs::skip) exist only in the experiments
+// build (make EXPERIMENTS=1); the shipped kernels compile them out.
+#ifdef ICNNM_EXPERIMENTS
+#define TC_SKIP(a) ((a).skip)
+#else
+#define TC_SKIP(a) 0
+#endif
+
 // ---------------------------------------------------------------------------
 // PTX wrappers
 // ---------------------------------------------------------------------------
@@ -538,7 +546,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   // an L1 invalidation -- after every wait: 25% of the pair adjoint's stall
   // samples); skip bit 64 restores it (A/B)
   auto pwait = [&](uint64_t* b, uint32_t ph) {
-    if (a.skip & 64)
+    if (TC_SKIP(a) & 64)
       mbar_wait_cluster(b, ph);
     else
       mbar_wait(b, ph);
@@ -691,7 +699,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   };
   auto real_slot = [&](int sl) { return sl * ncta + crank < nbr; };
 
-  if (warp < NB && !(a.skip & 8)) {
+  if (warp < NB && !(TC_SKIP(a) & 8)) {
     // ===================== builders =====================
     const int quad = warp & 3, half = warp >> 2;
     const int row = 32 * quad + lane;
@@ -792,7 +800,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           if (!FWD) mbar_wait(W_full + wsi, wph);
           tc_fence_after();
           long long t1c = dbg.p ? clk() : 0;
-          if (!(a.skip & 1)) {
+          if (!(TC_SKIP(a) & 1)) {
             const uint32_t col = a_col0 + sa * ASC;
             // the chunk's 16 tap offsets (forward) or c_j factors (adjoint), 4 vector loads
             int tq[KC];
@@ -873,7 +881,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             // one after a single wait::st (its store latency overlapped this
             // chunk's gathers); the last chunk of a brick is flushed below
             if (pend_sa >= 0) {
-              if (!(a.skip & 1)) tmem_wait_st();
+              if (!(TC_SKIP(a) & 1)) tmem_wait_st();
               tc_fence_before();
               mbar_arrive(A_full + pend_sa);
               if (!FWD) mbar_arrive(W_empty + pend_wsi);
@@ -903,7 +911,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         }
       }
       if (pair && pend_sa >= 0) {  // flush the brick's last owned chunk
-        if (!(a.skip & 1)) tmem_wait_st();
+        if (!(TC_SKIP(a) & 1)) tmem_wait_st();
         tc_fence_before();
         mbar_arrive(A_full + pend_sa);
         if (!FWD) mbar_arrive(W_empty + pend_wsi);
@@ -912,7 +920,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     }
     dbg.flush(DBG_BUILD_WAIT, DBG_BUILD_WORK);
   } else if (warp < NB) {
-  } else if (warp < NB + nepi_act && !(a.skip & 32)) {
+  } else if (warp < NB + nepi_act && !(TC_SKIP(a) & 32)) {
     // ===================== epilogue =====================
     const int ew = warp - NB;
     const int quad = ew & 3, half = ew >> 2;     // half in {0} (adjoint) or {0,1} (forward)
@@ -963,7 +971,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             const uint32_t gsl = gbase + gq;
             const int wsl = static_cast<int>(gsl % wsn);
             mbar_wait(W_full + wsl, (gsl / wsn) & 1);
-            if (gq < ng && !(a.skip & 2)) {
+            if (gq < ng && !(TC_SKIP(a) & 2)) {
               const int c0 = 32 * gq;
               const int ncol = (wn - c0) < 32 ? (wn - c0) : 32;
               const int j0 = nt * a.wbase + c0;
@@ -1037,7 +1045,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           }
           gbase += static_cast<uint32_t>(ngp);
         } else {
-          for (int c0 = 32 * half; c0 < wn && !(a.skip & 2); c0 += 32 * NHALF) {
+          for (int c0 = 32 * half; c0 < wn && !(TC_SKIP(a) & 2); c0 += 32 * NHALF) {
             uint32_t u[32];
             tmem_ld32(tbase + lane_base + acc * a.accw + c0, u);
             tmem_wait_ld();
@@ -1131,7 +1139,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     if (PAIR && crank != 0) {
       // peer CTA of a pair: the leader issues the pair's MMAs; without tma_pair
       // this warp relays "my half of B stage sb landed" to the leader's B_full
-      if (lane == 0 && !(a.skip & 16) && !a.tma_pair) {
+      if (lane == 0 && !(TC_SKIP(a) & 16) && !a.tma_pair) {
         const uint32_t lead_bfull = mapa_u32(smem_u32(B_full), 0);
         int sb = 0;
         uint32_t bph = 0;
@@ -1161,7 +1169,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         if (kc == 0) {
           const uint32_t tci = tcount + static_cast<uint32_t>(t);
           long long q0 = a.dbg ? clk() : 0;
-          if (!(a.skip & 32)) {
+          if (!(TC_SKIP(a) & 32)) {
             if (PAIR)
               pwait(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
             else
@@ -1170,14 +1178,14 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           if (a.dbg) wacc += clk() - q0;
         }
         long long q1 = a.dbg ? clk() : 0;
-        if (first_use && !(a.skip & 8)) {
+        if (first_use && !(TC_SKIP(a) & 8)) {
           if (PAIR)
             pwait(A_full + sa, aph);
           else
             mbar_wait(A_full + sa, aph);
         }
         long long q2 = a.dbg ? clk() : 0;
-        if (!(a.skip & 16)) {
+        if (!(TC_SKIP(a) & 16)) {
           if (PAIR)
             pwait(B_full + sb, bph);
           else
@@ -1193,19 +1201,19 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         const uint32_t bhi = bs0 + sb * BSTG;
         const uint32_t dcol = dcol_t[t], idesc = idesc_t[t];
         const int wn = wn_t[t];
-        const bool acc_done = kc == nkc - 1 && !(a.skip & 32);
+        const bool acc_done = kc == nkc - 1 && !(TC_SKIP(a) & 32);
         if (PAIR) {
           // this CTA's half of B: hi rows [0, wn/2) then lo rows (wn/2 x 32 B each)
           tc_chunk_f16_pair(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + (wn / 2) * 32), idesc,
                             kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
                             bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
                             (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
-        } else if (MCB && !(a.skip & 24)) {
+        } else if (MCB && !(TC_SKIP(a) & 24)) {
           tc_chunk_f16_mcb(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + wn * 32), idesc,
                            kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
                            bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
                            (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
-        } else if (F16 && !(a.skip & 24)) {
+        } else if (F16 && !(TC_SKIP(a) & 24)) {
           tc_chunk_f16(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + wn * 32), idesc,
                        kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
                        bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
@@ -1229,8 +1237,8 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
               tc_mma_ts_elect(dcol, acol + q * 8, dl, idesc, 1u);
             }
           }
-          if (last_use && !(a.skip & 8)) tc_commit_elect(A_empty + sa);
-          if (!(a.skip & 16)) tc_commit_elect(B_empty + sb);
+          if (last_use && !(TC_SKIP(a) & 8)) tc_commit_elect(A_empty + sa);
+          if (!(TC_SKIP(a) & 16)) tc_commit_elect(B_empty + sb);
           if (acc_done) tc_commit_elect(ACC_full + ((tcount + static_cast<uint32_t>(t)) & 1));
         }
         if (++sb == sbn) {
@@ -1294,7 +1302,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     __syncwarp();
   } else if (warp == WLOAD) {
     // ===================== B loader =====================
-    if (lane == 0 && !(a.skip & 16)) {
+    if (lane == 0 && !(TC_SKIP(a) & 16)) {
       uint32_t bcnt = 0;
       long long wl = 0;
       for (int sl = sfirst; sl < nslot; sl += sstep) {
@@ -1314,7 +1322,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             else
               mbar_wait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
             if (a.dbg) wl += clk() - q0;
-            if (a.skip & 4) {
+            if (TC_SKIP(a) & 4) {
               mbar_arrive(B_full + sb);  // timing experiment: no B traffic
               continue;
             }
@@ -1378,7 +1386,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           for (int gq = 0; gq < ngp; ++gq, ++gs) {
             const int wsl = static_cast<int>(gs % wsn);
             mbar_wait(W_empty + wsl, ((gs / wsn) & 1) ^ 1);
-            if (gq < ng && a.mode >= 1 && !(a.skip & 2)) {
+            if (gq < ng && a.mode >= 1 && !(TC_SKIP(a) & 2)) {
               const int ncol = (wn - 32 * gq) < 32 ? (wn - 32 * gq) : 32;
               const uint32_t bytes = static_cast<uint32_t>(ncol) * 512u;
               mbar_arrive_expect_tx(W_full + wsl, bytes);

@@ -11,7 +11,7 @@
 #include <random>
 #include <vector>
 
-#include "../../include/icnnm_b200.h"
+#include "../include/icnnm_synth.h"
 
 namespace {
 constexpr double kTwoPi = 6.283185307179586476925286766559;
@@ -26,7 +26,7 @@ extern "C" {
 
 int icnnm_synth_video(int64_t H, int64_t W, int64_t T, int n_sin, int n_blob, double blob_sigma,
                       double noise_sigma, uint64_t seed, double* out) {
-  if (H < 1 || W < 1 || T < 1 || n_sin < 0 || n_blob < 0 || !out) return ICNNM_INVALID_ARGUMENT;
+  if (H < 1 || W < 1 || T < 1 || n_sin < 0 || n_blob < 0 || !out) return ICNNM_SYNTH_INVALID;
   std::mt19937_64 rng(seed);
   std::uniform_real_distribution<double> amp(0.5, 1.5);
   std::uniform_real_distribution<double> phase(0.0, kTwoPi);
@@ -76,18 +76,18 @@ int icnnm_synth_video(int64_t H, int64_t W, int64_t T, int n_sin, int n_blob, do
     std::normal_distribution<double> g(0.0, noise_sigma);
     for (int64_t i = 0; i < m; ++i) out[i] += g(rng);
   }
-  return ICNNM_OK;
+  return ICNNM_SYNTH_OK;
 }
 
 int icnnm_synth_mask(int64_t H, int64_t W, int64_t T, int kind, double rate, int n_boxes,
                      uint64_t seed, double* out) {
-  if (H < 1 || W < 1 || T < 1 || !out) return ICNNM_INVALID_ARGUMENT;
+  if (H < 1 || W < 1 || T < 1 || !out) return ICNNM_SYNTH_INVALID;
   const int64_t m = H * W * T;
   std::mt19937_64 rng(seed);
   switch (kind) {
     case ICNNM_MASK_IID:
     case ICNNM_MASK_IID_BOXES: {
-      if (rate < 0 || rate > 1) return ICNNM_INVALID_ARGUMENT;
+      if (rate < 0 || rate > 1) return ICNNM_SYNTH_INVALID;
       std::uniform_real_distribution<double> u(0.0, 1.0);
       for (int64_t i = 0; i < m; ++i) out[i] = u(rng) < rate ? 1.0 : 0.0;
       if (kind == ICNNM_MASK_IID_BOXES) {
@@ -102,25 +102,25 @@ int icnnm_synth_mask(int64_t H, int64_t W, int64_t T, int kind, double rate, int
                 out[(((h0 + a) % H) * W + (w0 + c) % W) * T + (t0 + d) % T] = 0.0;
         }
       }
-      return ICNNM_OK;
+      return ICNNM_SYNTH_OK;
     }
     case ICNNM_MASK_EXACT:
       return icnnm_reference_bernoulli_mask(m, rate, seed, out);
     case ICNNM_MASK_T_FRAMES:
       for (int64_t i = 0; i < m; ++i) out[i] = ((i % T) % 2 == 0) ? 1.0 : 0.0;
-      return ICNNM_OK;
+      return ICNNM_SYNTH_OK;
     case ICNNM_MASK_T_PREFIX:
       for (int64_t i = 0; i < m; ++i) out[i] = (static_cast<double>(i % T) < rate) ? 1.0 : 0.0;
-      return ICNNM_OK;
+      return ICNNM_SYNTH_OK;
     default:
-      return ICNNM_INVALID_ARGUMENT;
+      return ICNNM_SYNTH_INVALID;
   }
 }
 
 // bernoulli_mask (mask.cpp:49-59): exactly llround(rate*m) entries observed,
 // chosen by std::shuffle of 0..m-1 with mt19937_64(seed).
 int icnnm_reference_bernoulli_mask(int64_t m, double rate, uint64_t seed, double* out) {
-  if (m < 1 || rate < 0 || rate > 1 || !out) return ICNNM_INVALID_ARGUMENT;
+  if (m < 1 || rate < 0 || rate > 1 || !out) return ICNNM_SYNTH_INVALID;
   const int64_t observed = static_cast<int64_t>(std::llround(rate * static_cast<double>(m)));
   std::vector<int64_t> order(static_cast<size_t>(m));
   std::iota(order.begin(), order.end(), int64_t{0});
@@ -128,7 +128,7 @@ int icnnm_reference_bernoulli_mask(int64_t m, double rate, uint64_t seed, double
   std::shuffle(order.begin(), order.end(), rng);
   std::fill(out, out + m, 0.0);
   for (int64_t i = 0; i < observed; ++i) out[order[static_cast<size_t>(i)]] = 1.0;
-  return ICNNM_OK;
+  return ICNNM_SYNTH_OK;
 }
 
 }  // extern "C"

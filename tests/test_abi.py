@@ -27,6 +27,34 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert lib.icnnm_version().decode().startswith("icnnm_b200")
 
 
+def test_generator_library_is_separate():
+    """The input generator (include/icnnm_synth.h) lives in synthgen's own
+    host-only library: the product library does not carry it, so the oracle
+    and bench.py's reference arm never load libicnnm_b200.so."""
+    import synthgen
+    hdr = os.path.join(os.path.dirname(_lib.HEADER_PATH), "icnnm_synth.h")
+    src = re.sub(r"/\*.*?\*/", "", open(hdr).read(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(icnnm_[a-z0-9_]+)\s*\(", src)))
+    assert len(names) == 8
+    g = synthgen.lib()
+    for n in names:
+        assert hasattr(g, n), n
+        assert not hasattr(P.lib(), n), f"{n} still exported by the product library"
+
+
+def test_reference_arm_imports_do_not_map_the_product_library():
+    """bench.py --impl reference generates its inputs through synthgen and
+    computes with the oracle: neither may map libicnnm_b200.so."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import synthgen, bench; "
+            "from oracle import icnnm_oracle; w = synthgen.WORKLOADS[1]; w.target(); w.mask(); "
+            "m = open('/proc/self/maps').read(); "
+            "assert 'libicnnm_b200' not in m, 'product library mapped'; "
+            "assert 'libicnnm_synth' in m" % os.path.dirname(os.path.dirname(__file__)))
+    subprocess.run([sys.executable, "-c", code], check=True, timeout=300)
+
+
 def test_library_is_sm100a_only():
     out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>/dev/null").read()
     assert "sm_100a" in out

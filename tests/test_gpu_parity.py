@@ -21,6 +21,17 @@ def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
 
 
+def _ab_lib():
+    """The experiments build of the library (environment A/B knobs); the
+    product build ignores the environment, so knob tests run against it."""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = os.path.join(root, "build", "ab", "libicnnm_b200_ab.so")
+    if not os.path.exists(path):
+        pytest.skip("experiments build missing (make -C paper_2604_17001_b200/csrc EXPERIMENTS=1)")
+    return path
+
+
 def _rand_orth(k, seed):
     q, _ = np.linalg.qr(np.random.default_rng(seed).standard_normal((k, k)))
     return q
@@ -575,6 +586,107 @@ def test_full_size_golden(gpu, engine, fname, cfgno, bidx):
     np.testing.assert_allclose(rep.objective, gd["objective"], rtol=1e-4)
 
 
+CFG4_GOLDEN_BATCH = (0, 21, 42, 63)
+
+
+@pytest.mark.parametrize("engine", ["f16x3", "tf32x3"])
+def test_config4_batch_goldens(gpu, engine):
+    """BASELINE config 4 through the library batch call: tensors {0, 21, 42,
+    63} of the 64-tensor batch (each with its own theta0 = 1e-2 max|pm| k,
+    solver.cpp:88-91) against their fp64-oracle goldens, split over two
+    workers on one device (the per-device blocks of icnnm_cuda_solve_batch)."""
+    import os
+    from paper_2604_17001_b200 import synth
+    w = synth.WORKLOADS[4]
+    gds = []
+    for b in CFG4_GOLDEN_BATCH:
+        path = os.path.join(os.path.dirname(__file__), "golden",
+                            "cfg4_it200.npz" if b == 0 else f"cfg4_b{b}_it200.npz")
+        if not os.path.exists(path):
+            pytest.skip(f"{path} not generated")
+        gds.append(np.load(path))
+    mask = w.mask()
+    Xs = [w.target(b=b) for b in CFG4_GOLDEN_BATCH]
+    gd0 = gds[0]
+    B = gpu.EigenBasis(tuple(int(x) for x in gd0["kernel"]), gd0["K"], gd0["eigenvalues"])
+    for gd in gds[1:]:
+        np.testing.assert_array_equal(gd["K"], gd0["K"])
+    cfg = gpu.SolverConfig(max_iters=w.iters, engine=engine, **FIXED)
+    Ls, reps = gpu.icnnm_solve_batch([X * mask for X in Xs], mask, B, cfg, devices=[0, 0])
+    miss = mask == 0
+    psnrs = set()
+    for b, X, L, rep, gd in zip(CFG4_GOLDEN_BATCH, Xs, Ls, reps, gds):
+        Lo = gd["L"].astype(np.float64)
+        assert int(gd["batch_index"]) == b
+        assert rep.iterations == w.iters
+        assert _rel(L, Lo) <= 1e-4, b
+        assert _rel(L[miss], Lo[miss]) <= 1e-3, b
+        assert abs(synth.psnr(X, L) - float(gd["psnr"])) <= 0.01, b
+        np.testing.assert_allclose(rep.objective, gd["objective"], rtol=1e-4)
+        psnrs.add(round(float(gd["psnr"]), 3))
+    assert len(psnrs) == len(CFG4_GOLDEN_BATCH)  # four distinct problems
+
+
+def test_solve_batch_equals_single_calls(gpu):
+    """icnnm_cuda_solve_batch == one icnnm_cuda_solve per tensor (own theta0,
+    own report), for 1, 2 and 3 worker blocks; errors name the problem."""
+    from paper_2604_17001_b200 import synth
+    w = synth.scaled(synth.WORKLOADS[4], (24, 20, 16), iters=40, n_train=2)
+    B = gpu.learn_ensemble_basis(w.training(), w.kernel)
+    mask = w.mask()
+    Ms = [w.target(b=b) * mask * (1.0 + 0.5 * b) for b in range(5)]
+    cfg = gpu.SolverConfig(max_iters=w.iters, **FIXED)
+    single = [gpu.icnnm_solve(M, mask, B, cfg) for M in Ms]
+    for devs in ([0], [0, 0], [0, 0, 0]):
+        Ls, reps = gpu.icnnm_solve_batch(Ms, mask, B, cfg, devices=devs)
+        assert len(Ls) == len(reps) == 5
+        for (L1, r1), L, r in zip(single, Ls, reps):
+            assert r.iterations == r1.iterations == w.iters
+            assert _rel(L, L1) <= 1e-6
+            np.testing.assert_allclose(r.objective, r1.objective, rtol=1e-6)
+    assert gpu.icnnm_solve_batch([], mask, B, cfg) == ([], [])
+    bad = [m.copy() for m in Ms]
+    bad[3].flat[7] = np.nan
+    with pytest.raises(gpu.InvalidArgument, match="problem 3"):
+        gpu.icnnm_solve_batch(bad, mask, B, cfg, devices=[0, 0])
+    with pytest.raises(gpu.InvalidArgument, match="out of range"):
+        gpu.icnnm_solve_batch(Ms, mask, B, cfg, devices=[0, 99])
+    with pytest.raises(gpu.InvalidArgument, match="not orthogonal"):
+        gpu.icnnm_solve_batch(Ms, mask, gpu.EigenBasis(B.kernel_shape, 2 * B.K, B.eigenvalues),
+                              cfg)
+
+
+def test_rejected_upload_leaves_no_problem(gpu):
+    """A rejected upload must not leave the previous problem's scalars next to
+    the overwritten staging buffers: the handle then has no problem."""
+    from paper_2604_17001_b200 import synth
+    w = synth.scaled(synth.WORKLOADS[1], (16, 16, 8), iters=10, n_train=1)
+    B = gpu.learn_ensemble_basis(w.training(), w.kernel)
+    X, mask = w.target(), w.mask()
+    S = gpu.Solver(w.dims, B)
+    try:
+        S.upload(X * mask, mask)
+        S.run(gpu.SolverConfig(max_iters=5, **FIXED))
+        bad = X * mask
+        bad[0, 0, 0] = np.inf
+        with pytest.raises(gpu.InvalidArgument, match="non-finite"):
+            S.upload(bad, mask)
+        with pytest.raises(gpu.InvalidArgument, match="no problem uploaded"):
+            S.run(gpu.SolverConfig(max_iters=5, **FIXED))
+        S.upload(X * mask, mask)
+        S.run(gpu.SolverConfig(max_iters=5, **FIXED))
+        with pytest.raises(gpu.InvalidArgument):
+            S.download(out=np.empty((16, 16, 8), dtype=np.float32))
+        with pytest.raises(gpu.InvalidArgument):
+            S.download(out=np.empty((16, 16, 7)))
+        with pytest.raises(gpu.InvalidArgument):
+            S.download(out=np.empty((16, 16, 16))[:, :, ::2])
+        out = np.empty((16, 16, 8))
+        assert S.download(out=out) is out
+    finally:
+        S.close()
+
+
 def test_config3_full_size_engines_agree(gpu):
     """BASELINE config 3 at full size (256x256x48, k = 1183: six N-tiles, three
     tile groups).  The fp64 oracle cannot hold its m x k state in host RAM, so
@@ -643,8 +755,11 @@ def test_solve_edge_cases(gpu, dims, ks, iters, engine):
 # ICNNM_TC_CS=2) and B multicast (ICNNM_TC_MCB=1)
 # --------------------------------------------------------------------------
 _CLUSTER_CHECK = r"""
-import sys, numpy as np
+import sys, os, numpy as np
 sys.path.insert(0, sys.argv[1])
+import paper_2604_17001_b200._lib as _L
+# the A/B knobs are read only by the experiments build (make EXPERIMENTS=1)
+_L.LIB_PATH = os.path.join(sys.argv[1], "build", "ab", "libicnnm_b200_ab.so")
 import paper_2604_17001_b200 as P
 from oracle import icnnm_oracle as O
 out = []
@@ -672,6 +787,7 @@ print("ok", rel)
 
 @pytest.mark.parametrize("env", [{"ICNNM_TC_CS": "2"}, {"ICNNM_TC_MCB": "1"}])
 def test_cluster_modes_exact_and_solve_parity(gpu, env):
+    _ab_lib()
     import os
     import subprocess
     import sys
@@ -734,8 +850,11 @@ def test_sharded_nccl_one_rank_transport(gpu, engine):
 # 64x64x32 with kernel 9x9x5 and 100 iterations is long enough to split.
 # --------------------------------------------------------------------------
 _LAUNCH_MODES = r"""
-import sys, numpy as np
+import sys, os, numpy as np
 sys.path.insert(0, sys.argv[1])
+import paper_2604_17001_b200._lib as _L
+# the A/B knobs are read only by the experiments build (make EXPERIMENTS=1)
+_L.LIB_PATH = os.path.join(sys.argv[1], "build", "ab", "libicnnm_b200_ab.so")
 import paper_2604_17001_b200 as P
 from paper_2604_17001_b200 import synth
 w = synth.scaled(synth.WORKLOADS[2], (64, 64, 32), iters=100, n_train=2)
@@ -752,6 +871,7 @@ print("ok")
 
 
 def test_launch_modes_do_not_change_results(gpu, tmp_path):
+    _ab_lib()
     import os
     import subprocess
     import sys

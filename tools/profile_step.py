@@ -2,7 +2,7 @@
 import argparse, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2604_17001_b200 as P
-from paper_2604_17001_b200 import synth
+import synthgen as synth
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
