@@ -137,8 +137,12 @@ void devcache_free(void* p, size_t bytes) {
     cudaFree(p);
     return;
   }
-  // unwinding from an error: work on the block may still be in flight
-  if (std::uncaught_exceptions() > 0) cudaDeviceSynchronize();
+  // unwinding from an error: work on the block may still be in flight.  Solver
+  // state is freed after ~Solver synchronised its own stream; the operator
+  // entry points work on the legacy default stream.  (Not cudaDeviceSynchronize:
+  // it would invalidate a stream capture running on another thread of a batch
+  // call on the same device.)
+  if (std::uncaught_exceptions() > 0) cudaStreamSynchronize(cudaStreamLegacy);
   std::lock_guard<std::mutex> lk(g_cache_mu);
   g_cache.push_back({p, bytes, dev});
 }
@@ -668,7 +672,45 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   a.sb = 2;
   a.ws = 2;
   a.ehalf = 1;
+  a.nsplit = 1;
+  a.bres = 0;
+  a.bres_stride = 0;
+  a.bres_bytes = 0;
   bool found = false;
+  // Resident B (F16x3 single CTAs): when the basis tiles of one CTA role fit
+  // in shared memory next to a W ring of >= 4 stages, they are loaded once
+  // per launch instead of once per brick -- the per-brick B stream (the whole
+  // hi/lo basis, e.g. 256 KB at k = 245) disappears from L2 and SMEM.  A
+  // brick's work is split over nsplit CTA roles when the whole basis does not
+  // fit: forward by N-tiles (each role its own columns of W), adjoint by
+  // K-chunks (each role a partial sum over j, added by the atomic flush).
+  // ICNNM_TC_BRES=0 (experiments build) streams B as before.
+  static const int bres_env = env_knob("ICNNM_TC_BRES", -1);
+  if (t.f16 && !pairs && !a.mcb && Bpk != nullptr && bres_env != 0) {
+    const int stride = t.wbase * icnnm_dev::tc::KC * 4;
+    for (int ns = 1; ns <= 4 && !found; ++ns) {
+      if (fwd && ns > t.ntn) break;
+      if (!fwd && ns > 1 && t.nkc / ns < 2) break;
+      int maxb = 0;
+      for (int r = 0; r < ns; ++r) {
+        const int ntiles = fwd ? (r + 1) * t.ntn / ns - r * t.ntn / ns : t.ntn;
+        const int nchunks = fwd ? t.nkc : (r + 1) * t.nkc / ns - r * t.nkc / ns;
+        maxb = std::max(maxb, ntiles * nchunks * stride);
+      }
+      for (int eh = fwd ? 1 : 2; eh >= 1 && !found; --eh)
+        for (int wsv = std::min(ws_cap, icnnm_dev::tc::WS) & ~1; wsv >= 4 && !found; wsv -= 2)
+          if (icnnm_dev::tc::smem_bytes(gtc, fwd, 1, wsv, t.f16, false, eh, maxb) <= 227 * 1024) {
+            a.nsplit = ns;
+            a.bres = 1;
+            a.bres_stride = stride;
+            a.bres_bytes = maxb;
+            a.sb = 1;
+            a.ws = wsv;
+            a.ehalf = eh;
+            found = true;
+          }
+    }
+  }
   for (int eh = fwd ? 1 : (eh_env > 0 ? eh_env : 2); eh >= 1 && !found; --eh) {
     const int sb_min = (eh == 2 && eh_env <= 0) ? std::min(4, sb_cap) : 2;
     for (int sbv = std::min(sb_cap, icnnm_dev::tc::SB); sbv >= sb_min && !found; --sbv)
@@ -685,7 +727,8 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   void* args[] = {&a};
-  const size_t smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16, pairs, a.ehalf);
+  const size_t smem =
+      icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16, pairs, a.ehalf, a.bres_bytes);
   if (smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
   const dim3 block(icnnm_dev::tc::threads(fwd));
   void* fn = fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16, a.cs > 1)
@@ -729,7 +772,9 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
     lc.numAttrs = 1;
     CK(cudaLaunchKernelExC(&lc, fn, args));
   } else {
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(a.nbricks, nsm));
+    // split mode: a multiple of nsplit CTAs, role = blockIdx % nsplit
+    const int64_t want = std::min<int64_t>(a.nbricks * a.nsplit, nsm);
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(a.nsplit, want / a.nsplit * a.nsplit));
     cudaLaunchConfig_t lc{};
     cudaLaunchAttribute at{};
     at.id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -500,7 +500,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   const int sbn = a.sb, wsn = a.ws, san = a.sa;
   const uint32_t a_col0 = 2u * static_cast<uint32_t>(a.accw);
   float* Bst = reinterpret_cast<float*>(p);
-  p += sbn * BSTG;
+  p += a.bres ? a.bres_bytes : sbn * BSTG;
   float* Wst = reinterpret_cast<float*>(p);   // adjoint: W-chunk ring; forward: W-group ring
   p += wsn * (FWD ? WO_STAGE_BYTES : W_STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p);
@@ -679,9 +679,27 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   const int nbr = static_cast<int>(a.nbricks);
   const int ntn = a.ntn;
   const int nkc = a.nkc;
+  // Split mode (a.nsplit > 1, single CTAs only): CTA role = blockIdx % nsplit
+  // owns a slice of the work of every brick -- forward: a range of N-tiles
+  // (its columns of W), adjoint: a range of K-chunks (a partial sum over the
+  // basis columns j, added into adj by the flush like any other partial) --
+  // so that the role's B tiles fit in shared memory and stay resident
+  // (a.bres: loaded once per launch instead of once per brick).
+  const int nsp = a.nsplit > 1 ? a.nsplit : 1;
+  const int role = nsp > 1 ? static_cast<int>(blockIdx.x % static_cast<unsigned>(nsp)) : 0;
+  const int ntb = (FWD && nsp > 1) ? role * ntn / nsp : 0;
+  const int nte = (FWD && nsp > 1) ? (role + 1) * ntn / nsp : ntn;
+  const int kcb = (!FWD && nsp > 1) ? role * nkc / nsp : 0;
+  const int kce = (!FWD && nsp > 1) ? (role + 1) * nkc / nsp : nkc;
+  const int nkr = kce - kcb;                   // K-chunks per tile in this CTA
   const int grp = a.grp > 1 ? 2 : 1;          // N-tiles sharing each A chunk
-  const int ngrp = (ntn + grp - 1) / grp;
-  int skew = a.skew < nkc / 2 ? a.skew : nkc / 2;
+  const int ngrp = (nte - ntb + grp - 1) / grp;
+  // resident B: SMEM offset of tile nt's chunk kc (tiles of the role's range,
+  // chunks of its K range, a.bres_stride bytes each)
+  auto bres_off = [&](int nt, int kc) {
+    return static_cast<uint32_t>(((nt - ntb) * nkr + (kc - kcb)) * a.bres_stride);
+  };
+  int skew = a.skew < nkr / 2 ? a.skew : nkr / 2;
   skew = skew < san ? skew : san;
   skew = skew < 0 ? 0 : skew;
   // Bricks by cluster slot: CTA `crank` of a cs-CTA cluster takes brick
@@ -690,8 +708,8 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   // tail brick is a dummy (brick nbr-1 re-read, nothing written).
   const int ncta = CL2 ? 2 : 1;
   const int crank = ncta > 1 ? static_cast<int>(blockIdx.x & 1u) : 0;
-  const int sfirst = static_cast<int>(blockIdx.x) / ncta;
-  const int sstep = static_cast<int>(gridDim.x) / ncta;
+  const int sfirst = static_cast<int>(blockIdx.x) / (ncta * nsp);
+  const int sstep = static_cast<int>(gridDim.x) / (ncta * nsp);
   const int nslot = (nbr + ncta - 1) / ncta;
   auto brick_of = [&](int sl) {
     const int bb = sl * ncta + crank;
@@ -781,7 +799,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         }
       }
       for (int gi = 0; gi < ngrp; ++gi) {
-        for (int kc = 0; kc < nkc; ++kc, ++cnt, adv_stage()) {
+        for (int kc = kcb; kc < kce; ++kc, ++cnt, adv_stage()) {
           // bsplit = 0: group `half` owns the chunks with cnt % 2 == half and
           // builds all KC columns, so each warp has two chunk periods of MMA
           // time to cover its TMEM-store round trip.
@@ -954,7 +972,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         mbar_wait(SC_full + biter % NSC, (biter / NSC) & 1);
         us = sc_ring[biter % NSC];
       }
-      for (int nt = 0; nt < ntn; ++nt, ++tcount) {
+      for (int nt = ntb; nt < nte; ++nt, ++tcount) {
         const int acc = tcount & 1;
         const uint32_t ph = (tcount >> 1) & 1;
         const int wn = tile_width(a, nt);
@@ -1165,8 +1183,9 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       uint32_t idesc_t[2], dcol_t[2];
       int wn_t[2];
       // MMAs of chunk kc (A stage sa, parity aph) into tile t of the current group
+      int cur_nt0 = 0;  // first N-tile of the current group
       auto issue = [&](int t, int kc, int sa, uint32_t aph, bool first_use, bool last_use) {
-        if (kc == 0) {
+        if (kc == kcb) {
           const uint32_t tci = tcount + static_cast<uint32_t>(t);
           long long q0 = a.dbg ? clk() : 0;
           if (!(TC_SKIP(a) & 32)) {
@@ -1185,7 +1204,9 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             mbar_wait(A_full + sa, aph);
         }
         long long q2 = a.dbg ? clk() : 0;
-        if (!(TC_SKIP(a) & 16)) {
+        if (a.bres) {
+          mbar_wait(B_full, 0);  // resident B: one fill per launch (phase 0)
+        } else if (!(TC_SKIP(a) & 16)) {
           if (PAIR)
             pwait(B_full + sb, bph);
           else
@@ -1198,31 +1219,31 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         }
         tc_fence_after();
         const uint32_t acol = tbase + a_col0 + sa * ASC;
-        const uint32_t bhi = bs0 + sb * BSTG;
+        const uint32_t bhi = a.bres ? bs0 + bres_off(cur_nt0 + t, kc) : bs0 + sb * BSTG;
         const uint32_t dcol = dcol_t[t], idesc = idesc_t[t];
         const int wn = wn_t[t];
-        const bool acc_done = kc == nkc - 1 && !(TC_SKIP(a) & 32);
+        const bool acc_done = kc == kce - 1 && !(TC_SKIP(a) & 32);
         if (PAIR) {
           // this CTA's half of B: hi rows [0, wn/2) then lo rows (wn/2 x 32 B each)
           tc_chunk_f16_pair(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + (wn / 2) * 32), idesc,
-                            kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
+                            kc == kcb ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
                             bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
                             (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
         } else if (MCB && !(TC_SKIP(a) & 24)) {
           tc_chunk_f16_mcb(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + wn * 32), idesc,
-                           kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
+                           kc == kcb ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
                            bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
                            (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
         } else if (F16 && !(TC_SKIP(a) & 24)) {
           tc_chunk_f16(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + wn * 32), idesc,
-                       kc == 0 ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
+                       kc == kcb ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
                        bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
                        (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
         } else {
           if (F16) {
             const uint64_t dh = bdesc(bhi);
             const uint64_t dl = bdesc(bhi + wn * 32);
-            tc_mma_f16_elect(dcol, acol, dh, idesc, kc == 0 ? 0u : 1u);
+            tc_mma_f16_elect(dcol, acol, dh, idesc, kc == kcb ? 0u : 1u);
             tc_mma_f16_elect(dcol, acol + ALO, dh, idesc, 1u);
             tc_mma_f16_elect(dcol, acol, dl, idesc, 1u);
           } else {
@@ -1231,14 +1252,14 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             for (int q = 0; q < KC / 8; ++q) {
               const uint64_t dh = bdesc(bhi + q * wn * 32);
               const uint64_t dl = bdesc(blo + q * wn * 32);
-              const uint32_t first = (kc == 0 && q == 0) ? 0u : 1u;
+              const uint32_t first = (kc == kcb && q == 0) ? 0u : 1u;
               tc_mma_ts_elect(dcol, acol + q * 8, dh, idesc, first);
               tc_mma_ts_elect(dcol, acol + ALO + q * 8, dh, idesc, 1u);
               tc_mma_ts_elect(dcol, acol + q * 8, dl, idesc, 1u);
             }
           }
           if (last_use && !(TC_SKIP(a) & 8)) tc_commit_elect(A_empty + sa);
-          if (!(TC_SKIP(a) & 16)) tc_commit_elect(B_empty + sb);
+          if (!(TC_SKIP(a) & 16) && !a.bres) tc_commit_elect(B_empty + sb);
           if (acc_done) tc_commit_elect(ACC_full + ((tcount + static_cast<uint32_t>(t)) & 1));
         }
         if (++sb == sbn) {
@@ -1264,8 +1285,9 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       };
       for (int sl = sfirst; sl < nslot; sl += sstep) {
         for (int gi = 0; gi < ngrp; ++gi) {
-          const int nt0 = gi * grp;
-          const int gsz = (ntn - nt0) < grp ? (ntn - nt0) : grp;
+          const int nt0 = ntb + gi * grp;
+          const int gsz = (nte - nt0) < grp ? (nte - nt0) : grp;
+          cur_nt0 = nt0;
           for (int t = 0; t < gsz; ++t) {
             wn_t[t] = tile_width(a, nt0 + t);
             idesc_t[t] = PAIR ? idesc_f16_m256(wn_t[t]) : (F16 ? idesc_f16(wn_t[t]) : idesc_tf32(wn_t[t]));
@@ -1273,22 +1295,22 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           }
           if (gsz == 1) {
             StageIt x = stage_of(cnt);
-            for (int kc = 0; kc < nkc; ++kc, next(x)) issue(0, kc, x.s, x.ph, true, true);
+            for (int kc = kcb; kc < kce; ++kc, next(x)) issue(0, kc, x.s, x.ph, true, true);
           } else {  // the tg_seq order, phase by phase
             StageIt x = stage_of(cnt);
-            for (int kc = 0; kc < skew; ++kc, next(x)) issue(0, kc, x.s, x.ph, true, false);
+            for (int kc = kcb; kc < kcb + skew; ++kc, next(x)) issue(0, kc, x.s, x.ph, true, false);
             x = stage_of(cnt);
-            for (int kc = 0; kc < skew; ++kc, next(x)) issue(1, kc, x.s, x.ph, false, true);
-            for (int kc = skew; kc < nkc - skew; ++kc, next(x)) {
+            for (int kc = kcb; kc < kcb + skew; ++kc, next(x)) issue(1, kc, x.s, x.ph, false, true);
+            for (int kc = kcb + skew; kc < kce - skew; ++kc, next(x)) {
               issue(0, kc, x.s, x.ph, true, false);
               issue(1, kc, x.s, x.ph, false, true);
             }
             const StageIt y = x;
-            for (int kc = nkc - skew; kc < nkc; ++kc, next(x)) issue(0, kc, x.s, x.ph, true, false);
+            for (int kc = kce - skew; kc < kce; ++kc, next(x)) issue(0, kc, x.s, x.ph, true, false);
             x = y;
-            for (int kc = nkc - skew; kc < nkc; ++kc, next(x)) issue(1, kc, x.s, x.ph, false, true);
+            for (int kc = kce - skew; kc < kce; ++kc, next(x)) issue(1, kc, x.s, x.ph, false, true);
           }
-          cnt += static_cast<uint32_t>(nkc);
+          cnt += static_cast<uint32_t>(nkr);
           tcount += static_cast<uint32_t>(gsz);
         }
       }
@@ -1302,16 +1324,34 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     __syncwarp();
   } else if (warp == WLOAD) {
     // ===================== B loader =====================
-    if (lane == 0 && !(TC_SKIP(a) & 16)) {
+    if (lane == 0 && a.bres) {
+      // resident B: this CTA's tiles x chunks, loaded once (one barrier phase)
+      // and read by every brick's MMAs; only when the CTA has a brick (its
+      // MMA warp then waits for the fill before the CTA can exit)
+      if (sfirst < nslot) {
+        uint32_t total = 0;
+        for (int nt = ntb; nt < nte; ++nt)
+          total += static_cast<uint32_t>(nkr * tile_width(a, nt) * KC * (F16 ? 4 : 8));
+        mbar_arrive_expect_tx(B_full, total);
+        for (int nt = ntb; nt < nte; ++nt) {
+          const uint32_t bytes = static_cast<uint32_t>(tile_width(a, nt)) * KC * (F16 ? 4 : 8);
+          for (int kc = kcb; kc < kce; ++kc)
+            bulk_g2s(reinterpret_cast<uint8_t*>(Bst) + bres_off(nt, kc),
+                     a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4), bytes,
+                     B_full);
+        }
+      }
+    } else if (lane == 0 && !(TC_SKIP(a) & 16)) {
       uint32_t bcnt = 0;
       long long wl = 0;
       for (int sl = sfirst; sl < nslot; sl += sstep) {
         for (int gi = 0; gi < ngrp; ++gi) {
-          const int nt0 = gi * grp;
-          const int gsz = (ntn - nt0) < grp ? (ntn - nt0) : grp;
-          for (int i = 0; i < gsz * nkc; ++i, ++bcnt) {
+          const int nt0 = ntb + gi * grp;
+          const int gsz = (nte - nt0) < grp ? (nte - nt0) : grp;
+          for (int i = 0; i < gsz * nkr; ++i, ++bcnt) {
             int t, kc;
-            tg_seq(i, gsz, nkc, skew, t, kc);
+            tg_seq(i, gsz, nkr, skew, t, kc);
+            kc += kcb;
             const int nt = nt0 + t;
             const int wn = tile_width(a, nt);
             const uint32_t bytes = static_cast<uint32_t>(wn) * KC * (F16 ? 4 : 8);
@@ -1380,7 +1420,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       uint32_t gs = 0;
       for (int sl = sfirst; sl < nslot; sl += sstep) {
         const int b = brick_of(sl);
-        for (int nt = 0; nt < ntn; ++nt) {
+        for (int nt = ntb; nt < nte; ++nt) {
           const int wn = tile_width(a, nt);
           const int ng = (wn + 31) / 32, ngp = ng + (ng & 1);
           for (int gq = 0; gq < ngp; ++gq, ++gs) {
@@ -1409,7 +1449,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       for (int sl = sfirst; sl < nslot; sl += sstep) {
         const int b = brick_of(sl);
         for (int gi = 0; gi < ngrp; ++gi) {
-          for (int kc = 0; kc < nkc; ++kc, ++wcnt) {
+          for (int kc = kcb; kc < kce; ++kc, ++wcnt) {
             const int wsi = wcnt % wsn;
             mbar_wait(W_empty + wsi, ((wcnt / wsn) & 1) ^ 1);
             mbar_arrive_expect_tx(W_full + wsi, W_STAGE_BYTES);

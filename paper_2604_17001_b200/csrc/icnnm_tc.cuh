@@ -69,6 +69,11 @@ struct alignas(64) TcArgs {
   int mcb;                  // F16x3 single CTAs in 2-CTA clusters sharing one multicast B stream
   int ehalf;                // adjoint: epilogue halves in use (1 or 2; 4 warps and 4 output
                             // bricks each -- 2 when the extra output bricks fit in SMEM)
+  int nsplit;               // CTA roles per brick (1: a CTA does whole bricks); forward: N-tile
+                            // ranges, adjoint: K-chunk ranges (single CTAs only)
+  int bres;                 // 1: the role's B tiles are resident in SMEM (one load per launch)
+  int bres_stride;          // resident B: bytes per (tile, chunk) block
+  int bres_bytes;           // resident B: SMEM bytes of the role's tiles x chunks
 };
 
 // dbg slots (cycles summed over CTAs)
@@ -85,10 +90,11 @@ void* adj_kernel_ptr(bool f16, bool pair = false);
 inline int threads(bool) { return 608; }
 
 inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16, bool pair = false,
-                         int ehalf = 1) {
+                         int ehalf = 1, int bres_bytes = 0) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
   const size_t nobp = ((nob + 3) / 4) * 4;
-  size_t b = static_cast<size_t>(sb) * b_stage_bytes(f16, pair) +
+  size_t b = (bres_bytes > 0 ? static_cast<size_t>(bres_bytes)
+                             : static_cast<size_t>(sb) * b_stage_bytes(f16, pair)) +
              static_cast<size_t>(ws) * (fwd ? WO_STAGE_BYTES : W_STAGE_BYTES) + BAR_BYTES + 16;
   b += ((g.ktp * 4 + 15) / 16) * 16;
   b += ((g.kp * 4 + 15) / 16) * 16;

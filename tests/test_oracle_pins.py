@@ -395,3 +395,26 @@ def test_exact_basis_icnnm_and_cnnm_agree():            # test_solver.cpp:170-19
 def test_svt_rejects_negative_tau():
     with pytest.raises(ValueError):
         O.svt(np.eye(3), -1.0)
+
+
+@pytest.mark.parametrize("dims,ks,iters,store", [((12, 10, 8), (3, 3, 2), 25, False),
+                                                 ((9, 7, 6), (4, 2, 3), 15, True),
+                                                 ((16, 12), (5, 3), 20, False)])
+def test_blocked_oracle_matches_in_core(tmp_path, dims, ks, iters, store):
+    """The blocked / out-of-core restatement (used for the config-3 golden,
+    whose m x k state exceeds host RAM) runs the same literal loop as the
+    in-core oracle: identical to fp64 summation-order rounding."""
+    from oracle import icnnm_oracle_blocked as OB
+    rng = np.random.default_rng(7)
+    X = rng.uniform(0, 1, size=dims)
+    mask = (rng.uniform(size=dims) < 0.4).astype(np.float64)
+    B = O.learn_ensemble_basis([rng.uniform(0, 1, size=dims) for _ in range(2)], ks)
+    cfg = O.SolverConfig(max_iters=iters, tol_primal=1e-300, tol_change=1e-300)
+    L1, r1 = O.icnnm_solve(X * mask, mask, B, cfg)
+    L2, r2 = OB.icnnm_solve_blocked(X * mask, mask, B, cfg, chunk=5, slab_rows=3,
+                                    store_dir=str(tmp_path) if store else None)
+    assert r2.iterations == r1.iterations == iters
+    assert np.linalg.norm(L2 - L1) <= 1e-12 * np.linalg.norm(L1)
+    np.testing.assert_allclose(r2.objective, r1.objective, rtol=1e-11)
+    np.testing.assert_allclose(r2.primal_residual, r1.primal_residual, rtol=1e-8)
+    np.testing.assert_allclose(r2.l_change, r1.l_change, rtol=1e-8)
