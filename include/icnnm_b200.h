@@ -156,9 +156,10 @@ int64_t icnnm_solver_device_bytes(icnnm_solver_t h);
 int icnnm_solver_set_profile(icnnm_solver_t h, int enable);
 int icnnm_solver_kernel_times(icnnm_solver_t h, double* out_ms4);
 /* tcgen05 pipeline counters of the last run() with set_profile(h, 2):
- * 2 x 9 cycle sums (forward, adjoint): builder wait/work, MMA wait on A /
- * B / accumulator, epilogue wait/work, loader wait, MMA-thread total. */
-int icnnm_solver_tc_counters(icnnm_solver_t h, unsigned long long* out18);
+ * 2 x 10 cycle sums (forward, adjoint): builder wait/work, MMA wait on A /
+ * B / accumulator, epilogue wait/work, loader wait, MMA-thread total,
+ * builder per-brick preparation (halo, operand scale). */
+int icnnm_solver_tc_counters(icnnm_solver_t h, unsigned long long* out20);
 void icnnm_solver_destroy(icnnm_solver_t h);
 
 /* ------------------------------------------------------------------------

@@ -269,11 +269,11 @@ class Solver:
         check(lib().icnnm_solver_set_profile(self._h, (1 if on else 0) | (2 if tc_counters else 0)))
 
     def tc_counters(self) -> dict:
-        out = (C.c_uint64 * 18)()
+        out = (C.c_uint64 * 20)()
         check(lib().icnnm_solver_tc_counters(self._h, out))
         names = ["build_wait", "build_work", "mma_wait_a", "mma_wait_b", "mma_wait_acc",
-                 "epi_wait", "epi_work", "load_wait", "mma_total"]
-        return {"forward": dict(zip(names, out[:9])), "adjoint": dict(zip(names, out[9:]))}
+                 "epi_wait", "epi_work", "load_wait", "mma_total", "build_prep"]
+        return {"forward": dict(zip(names, out[:10])), "adjoint": dict(zip(names, out[10:]))}
 
     def kernel_times_ms(self) -> dict:
         out = np.zeros(4)

@@ -581,14 +581,22 @@ CUtensorMap pair_b_map(const float* Bpk, const TcPlan& t, int rows) {
   return m;
 }
 
-void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const float* src,
-                      float* W, const float* Bpk, const float* cvec, float* adj, double* norm2,
-                      const IterState* st, cudaStream_t stream,
-                      unsigned long long* dbg = nullptr, float amax = 0.f, bool pdl = false) {
+// Launch configuration of one tcgen05 kernel: knobs, tile groups, CTA pairs /
+// multicast, split + resident-B mode, shared-memory carve-up and grid.  Pure
+// function of the geometry and plan (the solver also uses it to size the
+// deterministic adjoint's scratch before capturing its graphs).
+struct TcConfig {
   icnnm_dev::tc::TcArgs a{};
+  unsigned grid = 0;
+  size_t smem = 0;
+  bool cluster = false;  // 2-CTA clusters (pairs / B multicast)
+  void* fn = nullptr;
+};
+
+TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
+  TcConfig cfg;
+  icnnm_dev::tc::TcArgs& a = cfg.a;
   a.bunscale = t.bunscale;
-  a.amax = amax;
-  a.dbg = dbg;
   static const int skip_env = env_knob("ICNNM_TC_SKIP", 0);  // timing experiments only (results invalid)
   a.skip = skip_env;
   static const int bsplit_env = env_knob("ICNNM_TC_BSPLIT", 0);
@@ -596,15 +604,6 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   static const int bpair_env = env_knob("ICNNM_TC_BPAIR", 0);
   a.bpair = bpair_env;
   a.g = gtc;
-  a.src = src;
-  a.Win = W;
-  a.Wout = W;
-  a.Bpk = Bpk;
-  a.cvec = cvec;
-  a.adj = adj;
-  a.norm2 = norm2;
-  a.st = st;
-  a.mode = mode;
   a.ntn = t.ntn;
   a.nkc = t.nkc;
   a.nlast = t.nlast;
@@ -644,11 +643,7 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   // directly through 2-SM tensor copies (ICNNM_TC_TMAPAIR=0: bulk copies and a
   // relay thread, the first pair design)
   static const int tmapair_env = env_knob("ICNNM_TC_TMAPAIR", 1);
-  a.tma_pair = (pairs && tmapair_env != 0 && Bpk != nullptr) ? 1 : 0;
-  if (a.tma_pair) {
-    a.tmB[0] = pair_b_map(Bpk, t, t.wbase / 2);
-    a.tmB[1] = pair_b_map(Bpk, t, std::max(8, t.nlast / 2));
-  }
+  a.tma_pair = (pairs && tmapair_env != 0 && have_b) ? 1 : 0;
   // B multicast (F16x3 single CTAs in 2-CTA clusters sharing one B stream, each
   // CTA loading half of every stage): ICNNM_TC_MCB=1 (A/B experiment)
   static const int mcb_env = env_knob("ICNNM_TC_MCB", 0);
@@ -684,9 +679,13 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   // brick's work is split over nsplit CTA roles when the whole basis does not
   // fit: forward by N-tiles (each role its own columns of W), adjoint by
   // K-chunks (each role a partial sum over j, added by the atomic flush).
-  // ICNNM_TC_BRES=0 (experiments build) streams B as before.
-  static const int bres_env = env_knob("ICNNM_TC_BRES", -1);
-  if (t.f16 && !pairs && !a.mcb && Bpk != nullptr && bres_env != 0) {
+  // Measured at config 4 (k = 245, 2 N-tiles; profiles/ab_r2/bres): the
+  // split costs more than the B stream it removes (forward 0.353 -> 0.399 ms,
+  // adjoint 0.382 -> 0.503 ms: per-brick preparation runs once per tile, and
+  // the adjoint's K-split doubles its col2im epilogue), so it is off by
+  // default; ICNNM_TC_BRES=1 (experiments build) enables it.
+  static const int bres_env = env_knob("ICNNM_TC_BRES", 0);
+  if (t.f16 && !pairs && !a.mcb && have_b && bres_env != 0) {
     const int stride = t.wbase * icnnm_dev::tc::KC * 4;
     for (int ns = 1; ns <= 4 && !found; ++ns) {
       if (fwd && ns > t.ntn) break;
@@ -726,19 +725,18 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   int dev = 0, nsm = 148;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  void* args[] = {&a};
-  const size_t smem =
+  cfg.smem =
       icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16, pairs, a.ehalf, a.bres_bytes);
-  if (smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
-  const dim3 block(icnnm_dev::tc::threads(fwd));
-  void* fn = fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16, a.cs > 1)
-                 : icnnm_dev::tc::adj_kernel_ptr(t.f16, a.cs > 1);
-  if (a.cs > 1 || a.mcb) {
+  if (cfg.smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
+  cfg.fn = fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16, a.cs > 1)
+               : icnnm_dev::tc::adj_kernel_ptr(t.f16, a.cs > 1);
+  cfg.cluster = a.cs > 1 || a.mcb;
+  if (cfg.cluster) {
     // persistent grid: as many 2-CTA clusters as can be co-resident (one GPC each)
     static std::map<std::pair<void*, size_t>, int> max_pairs;
     static std::mutex mp_mu;
     std::lock_guard<std::mutex> lk(mp_mu);
-    auto key = std::make_pair(fn, smem);
+    auto key = std::make_pair(cfg.fn, cfg.smem);
     auto it = max_pairs.find(key);
     if (it == max_pairs.end()) {
       cudaLaunchConfig_t qc{};
@@ -748,45 +746,69 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
       at.val.clusterDim.y = 1;
       at.val.clusterDim.z = 1;
       qc.gridDim = dim3(static_cast<unsigned>(nsm));
-      qc.blockDim = block;
-      qc.dynamicSmemBytes = smem;
+      qc.blockDim = dim3(icnnm_dev::tc::threads(fwd));
+      qc.dynamicSmemBytes = cfg.smem;
       qc.attrs = &at;
       qc.numAttrs = 1;
       int n = 0;
-      CK(cudaOccupancyMaxActiveClusters(&n, fn, &qc));
+      CK(cudaOccupancyMaxActiveClusters(&n, cfg.fn, &qc));
       it = max_pairs.emplace(key, std::max(1, n)).first;
     }
     const int64_t nslot = (a.nbricks + 1) / 2;
-    const unsigned pairs = static_cast<unsigned>(std::min<int64_t>(nslot, it->second));
-    cudaLaunchConfig_t lc{};
-    cudaLaunchAttribute at{};
+    cfg.grid = 2u * static_cast<unsigned>(std::min<int64_t>(nslot, it->second));
+  } else {
+    // split mode: a multiple of nsplit CTAs, role = blockIdx % nsplit
+    const int64_t want = std::min<int64_t>(a.nbricks * a.nsplit, nsm);
+    cfg.grid = static_cast<unsigned>(std::max<int64_t>(a.nsplit, want / a.nsplit * a.nsplit));
+  }
+  return cfg;
+}
+
+void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const float* src,
+                      float* W, const float* Bpk, const float* cvec, float* adj, double* norm2,
+                      const IterState* st, cudaStream_t stream,
+                      unsigned long long* dbg = nullptr, float amax = 0.f, bool pdl = false,
+                      float* adj_scr = nullptr, double* npart = nullptr) {
+  TcConfig cfg = tc_config(gtc, t, fwd, Bpk != nullptr);
+  icnnm_dev::tc::TcArgs& a = cfg.a;
+  a.amax = amax;
+  a.dbg = dbg;
+  a.src = src;
+  a.Win = W;
+  a.Wout = W;
+  a.Bpk = Bpk;
+  a.cvec = cvec;
+  a.adj = adj;
+  a.norm2 = norm2;
+  a.st = st;
+  a.mode = mode;
+  a.adj_scr = adj_scr;
+  a.npart = npart;
+  if (a.tma_pair) {
+    a.tmB[0] = pair_b_map(Bpk, t, t.wbase / 2);
+    a.tmB[1] = pair_b_map(Bpk, t, std::max(8, t.nlast / 2));
+  }
+  void* args[] = {&a};
+  const dim3 block(icnnm_dev::tc::threads(fwd));
+  cudaLaunchConfig_t lc{};
+  cudaLaunchAttribute at{};
+  lc.gridDim = dim3(cfg.grid);
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = cfg.smem;
+  lc.stream = stream;
+  lc.attrs = &at;
+  if (cfg.cluster) {
     at.id = cudaLaunchAttributeClusterDimension;
     at.val.clusterDim.x = 2;
     at.val.clusterDim.y = 1;
     at.val.clusterDim.z = 1;
-    lc.gridDim = dim3(2 * pairs);
-    lc.blockDim = block;
-    lc.dynamicSmemBytes = smem;
-    lc.stream = stream;
-    lc.attrs = &at;
     lc.numAttrs = 1;
-    CK(cudaLaunchKernelExC(&lc, fn, args));
   } else {
-    // split mode: a multiple of nsplit CTAs, role = blockIdx % nsplit
-    const int64_t want = std::min<int64_t>(a.nbricks * a.nsplit, nsm);
-    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(a.nsplit, want / a.nsplit * a.nsplit));
-    cudaLaunchConfig_t lc{};
-    cudaLaunchAttribute at{};
     at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at.val.programmaticStreamSerializationAllowed = 1;
-    lc.gridDim = dim3(grid);
-    lc.blockDim = block;
-    lc.dynamicSmemBytes = smem;
-    lc.stream = stream;
-    lc.attrs = &at;
     lc.numAttrs = pdl ? 1 : 0;
-    CK(cudaLaunchKernelExC(&lc, fn, args));
   }
+  CK(cudaLaunchKernelExC(&lc, cfg.fn, args));
 }
 
 // EigenBasis::validate (spectral.cpp:25-41), run on every call that takes a
@@ -878,6 +900,8 @@ struct Slab {
   int64_t halo_elems = 0;       // (kh-1) * W * T (slab mode)
   DBuf<float> Lt, adj, pm, mask, W;
   DBuf<float> Lr;                 // exact-residual mode: L_{t+1} (fp32, with halo rows)
+  DBuf<float> adj_scr;            // deterministic adjoint: per-(brick, role) output slots
+  int adj_nsp = 1, adj_nobp = 0;  // roles per brick / padded slot size of the adjoint launch
   DBuf<double> L, V;
 };
 
@@ -899,6 +923,12 @@ struct Solver {
   DBuf<IterState> st;
   DBuf<IterStats> stats;
   DBuf<double> Mstage, maskstage;  // f64 staging of the current problem
+  // Deterministic reductions (tcgen05 engines): per-CTA / per-block partial
+  // rows, folded in a fixed order; slab i owns rows
+  // [i * rows_per_slab, (i + 1) * rows_per_slab), unused rows stay zero.
+  bool det = false;
+  DBuf<double> npart, upart, gpart;
+  int nsm = 148, upd_rows = 0;
   DBuf<float> xfer_send, xfer_recv;  // cross-process halo buffers
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
@@ -1081,6 +1111,7 @@ void exchange_adj(Solver& S) {
 }
 
 int engine_kp(const Solver& S);
+int slab_index(const Solver& S, const Slab& s) { return static_cast<int>(&s - S.slabs.data()); }
 
 // Debugging only (experiments build): ICNNM_F16_OFF=1 runs the F16x3 engine's adjoint in TF32x3,
 // =2 its forward (isolates a kernel when bisecting a failure).
@@ -1151,9 +1182,15 @@ void launch_fwd(Solver& S, Slab& s, int mode) {
   double* acc = mode == 2 ? S.red.p + engine_kp(S) + 5 : S.red.p;
   if (is_tc(S.engine)) {
     const bool f16 = S.engine == ICNNM_ENGINE_F16X3 && !(f16_debug_mask() & 2);
+    double* part = nullptr;
+    if (S.det) {
+      const size_t row0 = static_cast<size_t>(slab_index(S, s)) * S.nsm;
+      part = mode == 2 ? S.gpart.p + row0 : S.npart.p + row0 * engine_kp(S);
+    }
     launch_tc_kernel(s.gtc, f16 ? S.tp16 : S.tp, true, mode, src, s.W.p,
                      f16 ? S.BpkF16.p : S.BpkF.p, S.cvec.p, s.adj.p, acc, S.st.p, S.stream,
-                     S.tc_counters ? S.dbg.p : nullptr, 0.f, mode != 0 && use_pdl(S));
+                     S.tc_counters ? S.dbg.p : nullptr, 0.f, mode != 0 && use_pdl(S), nullptr,
+                     part);
     ++S.launches;
     return;
   }
@@ -1168,8 +1205,24 @@ void launch_adj(Solver& S, Slab& s) {
     launch_tc_kernel(s.gtc, f16 ? S.tp16 : S.tp, false, 1, s.Lt.p, s.W.p,
                      f16 ? S.BpkA16.p : S.BpkA.p, S.cvec.p, s.adj.p, S.red.p, S.st.p, S.stream,
                      S.tc_counters ? S.dbg.p + icnnm_dev::tc::DBG_SLOTS : nullptr, 0.f,
-                     use_pdl(S));
+                     use_pdl(S), S.det ? s.adj_scr.p : nullptr);
     ++S.launches;
+    if (S.det) {
+      // fixed-order sum of the output slots covering each voxel -> adj
+      const int64_t n = static_cast<int64_t>(s.gtc.Hsrc) * s.gtc.W * s.gtc.T;
+      cudaLaunchConfig_t lc{};
+      cudaLaunchAttribute at{};
+      at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at.val.programmaticStreamSerializationAllowed = 1;
+      lc.gridDim = dim3(static_cast<unsigned>((n + 255) / 256));
+      lc.blockDim = dim3(256);
+      lc.stream = S.stream;
+      lc.attrs = &at;
+      lc.numAttrs = use_pdl(S) ? 1 : 0;
+      CK(cudaLaunchKernelEx(&lc, icnnm_dev::icnnm_adj_gather, s.gtc, s.adj_nsp, s.adj_nobp,
+                            static_cast<const float*>(s.adj_scr.p), s.adj.p));
+      ++S.launches;
+    }
     return;
   }
   icnnm_dev::icnnm_adj_ffma<<<static_cast<unsigned>(n_bricks(s.g)), 128, adj_smem(s.g),
@@ -1182,7 +1235,95 @@ int engine_kp(const Solver& S) {
   return is_tc(S.engine) ? S.tp.kp : S.p.kp;
 }
 
+// The iteration's partial rows for the fold (or none in the atomic mode).
+icnnm_dev::Partials partials(const Solver& S) {
+  icnnm_dev::Partials P{};
+  if (!S.det) return P;
+  const int ns = static_cast<int>(S.slabs.size());
+  P.npart = S.npart.p;
+  P.nrows = ns * S.nsm;
+  P.upart = S.upart.p;
+  P.urows = ns * S.upd_rows;
+  if (S.exact_res) {
+    P.gpart = S.gpart.p;
+    P.grows = ns * S.nsm;
+  }
+  return P;
+}
+
+// Deterministic buffers of a tcgen05 run, allocated before any graph capture.
+void prepare_det(Solver& S) {
+  S.det = is_tc(S.engine);
+  if (!S.det) return;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&S.nsm, cudaDevAttrMultiProcessorCount, dev));
+  S.upd_rows = 0;
+  for (auto& s : S.slabs) S.upd_rows = std::max(S.upd_rows, update_grid(s.m_own));
+  const int ns = static_cast<int>(S.slabs.size());
+  const int kpe = engine_kp(S);
+  const bool f16 = S.engine == ICNNM_ENGINE_F16X3;
+  const TcPlan& t = f16 ? S.tp16 : S.tp;
+  const size_t nrow = static_cast<size_t>(ns) * S.nsm;
+  auto zero = [&](DBuf<double>& b, size_t n) {
+    if (b.n != n) {
+      b.alloc(n);
+      CK(cudaMemsetAsync(b.p, 0, b.bytes(), S.stream));
+    }
+  };
+  zero(S.npart, nrow * kpe);
+  zero(S.gpart, nrow);
+  zero(S.upart, static_cast<size_t>(ns) * S.upd_rows * 8);
+  for (auto& s : S.slabs) {
+    const TcConfig c = tc_config(s.gtc, t, false, true);
+    s.adj_nsp = c.a.nsplit;
+    const int nob = s.gtc.HH * s.gtc.HW * s.gtc.HT;
+    s.adj_nobp = (nob + 3) / 4 * 4;
+    const size_t need = static_cast<size_t>(n_bricks(s.gtc)) * s.adj_nsp * s.adj_nobp;
+    if (s.adj_scr.n != need) s.adj_scr.alloc(need);
+  }
+}
+
+void launch_coef(Solver& S, const icnnm_solver_config& cfg, double kd, double res_scale,
+                 double floor_rel) {
+  // sharded solves fold before the all-reduce (icnnm_fold); else the coef
+  // kernel folds
+  const icnnm_dev::Partials P = S.sharded ? icnnm_dev::Partials{} : partials(S);
+  icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
+                                                  S.stats.p, S.p.k, engine_kp(S), kd, res_scale,
+                                                  cfg.tol_primal, cfg.tol_change, floor_rel,
+                                                  S.exact_res ? 1 : 0, P);
+  CKL();
+}
+
+void launch_update(Solver& S, Slab& s, const icnnm_solver_config& cfg, double kd, bool pdl) {
+  cudaLaunchConfig_t lc{};
+  cudaLaunchAttribute at{};
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+  lc.gridDim = dim3(update_grid(s.m_own));
+  lc.blockDim = dim3(256);
+  lc.stream = S.stream;
+  lc.attrs = &at;
+  lc.numAttrs = pdl ? 1 : 0;
+  double* upart =
+      S.det ? S.upart.p + static_cast<size_t>(slab_index(S, s)) * S.upd_rows * 8 : nullptr;
+  CK(cudaLaunchKernelEx(&lc, icnnm_dev::icnnm_update, s.m_own,
+                        static_cast<const icnnm_dev::IterState*>(S.st.p), cfg.lambda, kd,
+                        s.adj.p + s.halo_elems, s.L.p, s.V.p, static_cast<const float*>(s.pm.p),
+                        static_cast<const float*>(s.mask.p), s.Lt.p + s.halo_elems,
+                        S.red.p + engine_kp(S),
+                        S.exact_res ? s.Lr.p + s.halo_elems : static_cast<float*>(nullptr),
+                        upart));
+}
+
 void allreduce_red(Solver& S) {
+  if (S.sharded && S.det) {
+    // fold the slabs' partial rows into red before the cross-rank sum
+    icnnm_dev::icnnm_fold<<<1, 1024, 0, S.stream>>>(partials(S), engine_kp(S), S.red.p);
+    CKL();
+    ++S.launches;
+  }
   if (S.comm) S.comm->allreduce_sum(S.red.p, engine_kp(S) + 8, S.stream);
 }
 
@@ -1200,7 +1341,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   S.engine = cfg.engine;
   ensure_engine_basis(S, S.engine);
   S.exact_res = cfg.exact_residual != 0;
-  const int kpe = engine_kp(S);
+  prepare_det(S);
   if (S.exact_res)
     for (auto& s : S.slabs)
       if (!s.Lr.p) s.Lr.alloc(s.Lt.n);
@@ -1222,30 +1363,10 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   // One ADMM iteration as a graph: coef -> adjoint -> update -> forward.
   const double floor_rel = 1e-5;
   auto iteration = [&]() {
-    icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
-                                                    S.stats.p, p.k, kpe, kd, res_scale,
-                                                    cfg.tol_primal, cfg.tol_change, floor_rel,
-                                                    S.exact_res ? 1 : 0);
-    CKL();
+    launch_coef(S, cfg, kd, res_scale, floor_rel);
     for (auto& s : S.slabs) launch_adj(S, s);
     exchange_adj(S);
-    for (auto& s : S.slabs) {
-      cudaLaunchConfig_t lc{};
-      cudaLaunchAttribute at{};
-      at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      at.val.programmaticStreamSerializationAllowed = 1;
-      lc.gridDim = dim3(update_grid(s.m_own));
-      lc.blockDim = dim3(256);
-      lc.stream = S.stream;
-      lc.attrs = &at;
-      lc.numAttrs = use_pdl(S) ? 1 : 0;
-      CK(cudaLaunchKernelEx(&lc, icnnm_dev::icnnm_update, s.m_own,
-                            static_cast<const icnnm_dev::IterState*>(S.st.p), cfg.lambda, kd,
-                            s.adj.p + s.halo_elems, s.L.p, s.V.p,
-                            static_cast<const float*>(s.pm.p), static_cast<const float*>(s.mask.p),
-                            s.Lt.p + s.halo_elems, S.red.p + kpe,
-                            S.exact_res ? s.Lr.p + s.halo_elems : static_cast<float*>(nullptr)));
-    }
+    for (auto& s : S.slabs) launch_update(S, s, cfg, kd, use_pdl(S));
     exchange_lt(S);
     if (S.exact_res) {
       exchange_lt(S, &Slab::Lr);
@@ -1323,11 +1444,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
   };
   // final coef: moves the last update slot into stats, evaluates the stop test.
   auto finish = [&]() {
-    icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
-                                                    S.stats.p, p.k, kpe, kd, res_scale,
-                                                    cfg.tol_primal, cfg.tol_change, floor_rel,
-                                                    S.exact_res ? 1 : 0);
-    CKL();
+    launch_coef(S, cfg, kd, res_scale, floor_rel);
     ++S.launches;
     record(S.ev1);
   };
@@ -1343,20 +1460,12 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     double acc[4] = {0, 0, 0, 0};
     for (int it = 0; it < iters; ++it) {
       CK(cudaEventRecord(e[0], S.stream));
-      icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
-                                                      S.stats.p, p.k, kpe, kd, res_scale,
-                                                      cfg.tol_primal, cfg.tol_change,
-                                                      floor_rel, S.exact_res ? 1 : 0);
+      launch_coef(S, cfg, kd, res_scale, floor_rel);
       CK(cudaEventRecord(e[1], S.stream));
       for (auto& s : S.slabs) launch_adj(S, s);
       exchange_adj(S);
       CK(cudaEventRecord(e[2], S.stream));
-      for (auto& s : S.slabs) {
-        icnnm_dev::icnnm_update<<<update_grid(s.m_own), 256, 0, S.stream>>>(
-            s.m_own, S.st.p, cfg.lambda, kd, s.adj.p + s.halo_elems, s.L.p, s.V.p, s.pm.p,
-            s.mask.p, s.Lt.p + s.halo_elems, S.red.p + kpe,
-            S.exact_res ? s.Lr.p + s.halo_elems : nullptr);
-      }
+      for (auto& s : S.slabs) launch_update(S, s, cfg, kd, false);
       exchange_lt(S);
       if (S.exact_res) {
         exchange_lt(S, &Slab::Lr);
@@ -1646,7 +1755,7 @@ int icnnm_solver_set_profile(icnnm_solver_t h, int enable) {
   });
 }
 
-int icnnm_solver_tc_counters(icnnm_solver_t h, unsigned long long* out) {
+int icnnm_solver_tc_counters(icnnm_solver_t h, unsigned long long* out) {  // 2 x DBG_SLOTS
   return guard([&] {
     if (!h || !out) invalid("null argument");
     const int n = 2 * icnnm_dev::tc::DBG_SLOTS;

@@ -407,6 +407,113 @@ __device__ __forceinline__ void block_reduce_add(double (&v)[N], double* dst) {
 }
 
 // ---------------------------------------------------------------------------
+// Deterministic reductions.  The forward kernel writes one row of column
+// partials per CTA, the update kernel one row of its 5 report sums per block,
+// the exact-residual forward one gap partial per CTA; these fold them in a
+// fixed order (thread t sums rows t, t + blockDim, ... sequentially, then a
+// fixed shuffle tree and a fixed sum over warps), so a solve is bit-for-bit
+// reproducible run to run (the reference is deterministic).
+// ---------------------------------------------------------------------------
+__device__ double block_sum_fixed(double v) {
+  __shared__ double sh[32];
+  __shared__ double out;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();  // sh / out reuse across calls
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += sh[w];
+    out = t;
+  }
+  __syncthreads();
+  return out;
+}
+
+__device__ void fold_partials(const Partials& P, int kp, double* red) {
+  if (P.npart != nullptr) {
+    for (int j = threadIdx.x; j < kp; j += blockDim.x) {
+      double t = 0.0;
+      for (int r = 0; r < P.nrows; ++r) t += P.npart[static_cast<size_t>(r) * kp + j];
+      red[j] = t;
+    }
+  }
+  double* slot = red + kp;
+  if (P.upart != nullptr) {
+    for (int q = 0; q < 5; ++q) {
+      double v = 0.0;
+      for (int r = threadIdx.x; r < P.urows; r += blockDim.x) v += P.upart[r * 8 + q];
+      v = block_sum_fixed(v);
+      if (threadIdx.x == 0) slot[q] = v;
+    }
+  }
+  if (P.gpart != nullptr) {
+    double v = 0.0;
+    for (int r = threadIdx.x; r < P.grows; r += blockDim.x) v += P.gpart[r];
+    v = block_sum_fixed(v);
+    if (threadIdx.x == 0) slot[5] = v;
+  }
+  __syncthreads();
+}
+
+// Sharded solves fold before the cross-rank all-reduce of `red`.
+__global__ void icnnm_fold(Partials P, int kp, double* red) {
+  pdl_wait();
+  pdl_trigger();
+  fold_partials(P, kp, red);
+}
+
+// Deterministic adjoint output: adj[i] = sum over the (brick, role) output
+// slots whose halo box covers i, in a fixed order (halo row aa, column bb,
+// time c, role).  A brick at (h0, w0, t0) writes slot element
+// ((aa*HW + bb)*HT + c) to voxel (h0-(kh-1)+aa, w0-(kw-1)+bb, t0-(kt-1)+c)
+// (periodic in W and T; in H periodic over the tensor or, in slab mode, the
+// buffer row hoff + h with kh-1 halo rows first) -- the col2im of the
+// tcgen05 adjoint (icnnm_tc.cu), conv_adjoint's map (conv_op.cpp:57-77).
+__global__ void __launch_bounds__(256)
+icnnm_adj_gather(Geo g, int nsp, int nobp, const float* __restrict__ scr,
+                 float* __restrict__ adj) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t n = static_cast<int64_t>(g.Hsrc) * g.W * g.T;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int t = static_cast<int>(i % g.T);
+  const int64_t q = i / g.T;
+  const int w = static_cast<int>(q % g.W);
+  const int hb = static_cast<int>(q / g.W);
+  float acc = 0.f;
+  for (int aa = 0; aa < g.HH; ++aa) {
+    int h0 = hb - g.hoff + g.kh - 1 - aa;
+    if (g.wrapH) {
+      h0 %= g.H;
+      if (h0 < 0) h0 += g.H;
+    } else if (h0 < 0 || h0 >= g.H) {
+      continue;
+    }
+    if (h0 % g.bh != 0) continue;
+    const int qh = h0 / g.bh;
+    for (int bb = 0; bb < g.HW; ++bb) {
+      int w0 = (w + g.kw - 1 - bb) % g.W;
+      if (w0 < 0) w0 += g.W;
+      if (w0 % g.bw != 0) continue;
+      const int64_t bhw = static_cast<int64_t>(qh) * g.nbw + w0 / g.bw;
+      for (int c = 0; c < g.HT; ++c) {
+        int t0 = (t + g.kt - 1 - c) % g.T;
+        if (t0 < 0) t0 += g.T;
+        if (t0 % g.bt != 0) continue;
+        const int64_t b = bhw * g.nbt + t0 / g.bt;
+        const int e = (aa * g.HW + bb) * g.HT + c;
+        for (int r = 0; r < nsp; ++r) acc += scr[(b * nsp + r) * nobp + e];
+      }
+    }
+  }
+  adj[i] = acc;
+}
+
+// ---------------------------------------------------------------------------
 // Shrink coefficients (prox_l21, solver.cpp:42-50, folded): c_j = tau/n_j if
 // n_j > tau else 1, tau = 1/theta.  Also evaluates the stopping test of the
 // previous iteration (solver.cpp:136-139) and advances the iteration state.
@@ -416,9 +523,12 @@ __global__ void icnnm_coef(IterState* st, const double* __restrict__ theta,
                            double* __restrict__ red, float* __restrict__ cvec,
                            IterStats* __restrict__ stats, int k, int kp, double kd,
                            double res_scale, double tol_p, double tol_c, double floor_rel,
-                           int exact) {
+                           int exact, Partials P) {
   pdl_wait();
   pdl_trigger();
+  // deterministic mode: fold the per-CTA / per-block partials of the
+  // iteration that just finished into red (fixed order)
+  fold_partials(P, kp, red);
   // red = [norm2 (kp) | update slot (dl2, l2o, fit, ip, ln2) | pad]
   __shared__ int go;
   __shared__ int cur;
@@ -503,7 +613,8 @@ __global__ void __launch_bounds__(256)
 icnnm_update(int64_t m, const IterState* __restrict__ st, double lambda, double kd,
              float* __restrict__ adj, double* __restrict__ L, double* __restrict__ V,
              const float* __restrict__ pm, const float* __restrict__ mask,
-             float* __restrict__ Lt, double* __restrict__ slot, float* __restrict__ Lr) {
+             float* __restrict__ Lt, double* __restrict__ slot, float* __restrict__ Lr,
+             double* __restrict__ upart) {
   pdl_wait();
   pdl_trigger();
   if (!st->active) return;
@@ -550,6 +661,15 @@ icnnm_update(int64_t m, const IterState* __restrict__ st, double lambda, double 
       acc[3] += (kd * lo - v - a) * ln;
       acc[4] += ln * ln;
     }
+  }
+  if (upart != nullptr) {
+    // deterministic: this block's sums in its own row (fixed-order tree)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const double v = block_sum_fixed(acc[q]);
+      if (threadIdx.x == 0) upart[blockIdx.x * 8 + q] = v;
+    }
+    return;
   }
   block_reduce_add<5>(acc, slot);
 }

@@ -75,6 +75,16 @@ struct IterStats {
   double gap2;  // exact ||Z_t - A(L_{t+1})K||^2 (exact_residual mode), else 0
 };
 
+// Deterministic-reduction buffers of one iteration (null: not used).
+struct Partials {
+  const double* npart;  // forward column partials [nrows][kp]
+  int nrows;
+  const double* upart;  // update report partials [urows][8]
+  int urows;
+  const double* gpart;  // exact-residual gap partials [grows]
+  int grows;
+};
+
 }  // namespace icnnm_dev
 
 // Kernel declarations (defined in icnnm_kernels.cu; launched from the host
@@ -87,11 +97,14 @@ __global__ void icnnm_adj_ffma(Geo g, const float* Wm, const float* KT, const fl
                                float* adj, const IterState* st, int mode);
 __global__ void icnnm_coef(IterState* st, const double* theta, double* red, float* cvec,
                            IterStats* stats, int k, int kp, double kd, double res_scale,
-                           double tol_p, double tol_c, double floor_rel, int exact);
+                           double tol_p, double tol_c, double floor_rel, int exact, Partials P);
+__global__ void icnnm_fold(Partials P, int kp, double* red);
+__global__ void icnnm_adj_gather(Geo g, int nsp, int nobp, const float* scr, float* adj);
 constexpr int UPD_U = 4;  // elements in flight per thread (icnnm_update)
 __global__ void icnnm_update(int64_t m, const IterState* st, double lambda, double kd,
                              float* adj, double* L, double* V, const float* pm,
-                             const float* mask, float* Lt, double* slot, float* Lr);
+                             const float* mask, float* Lt, double* slot, float* Lr,
+                             double* upart);
 __global__ void icnnm_add_rows(int64_t n, float* dst, float* src);
 __global__ void icnnm_setup(int64_t m, const double* M, const double* msk, int mean_fill,
                             double mean, float* pm, float* maskf, double* L, double* V,

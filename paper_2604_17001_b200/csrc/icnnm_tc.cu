@@ -765,8 +765,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         st_wph ^= 1u;
       }
     };
+    long long prep = 0;
     for (int sl = sfirst; sl < nslot; sl += sstep, ++iter) {
       float* hcur = halo + (iter & 1) * nobp;
+      const long long tp0 = dbg.p ? clk() : 0;
       if (FWD) {
         cp_async_wait_all();
         named_sync(1, NB * 32);  // this brick's halo landed; previous brick fully built
@@ -798,6 +800,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           named_sync(1, NB * 32);  // halo scaled
         }
       }
+      if (dbg.p) prep += clk() - tp0;
       for (int gi = 0; gi < ngrp; ++gi) {
         for (int kc = kcb; kc < kce; ++kc, ++cnt, adv_stage()) {
           // bsplit = 0: group `half` owns the chunks with cnt % 2 == half and
@@ -937,6 +940,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       }
     }
     dbg.flush(DBG_BUILD_WAIT, DBG_BUILD_WORK);
+    if (dbg.p) atomicAdd(dbg.p + DBG_BUILD_PREP, static_cast<unsigned long long>(prep));
   } else if (warp < NB) {
   } else if (warp < NB + nepi_act && !(TC_SKIP(a) & 32)) {
     // ===================== epilogue =====================
@@ -1128,6 +1132,13 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             ob[q * obs + e] = 0.f;
           }
           if (!breal) continue;  // dummy brick: output bricks cleared, nothing written
+          if (a.adj_scr != nullptr) {
+            // deterministic: the brick's (role's) partial output brick goes to
+            // its own scratch slot; icnnm_adj_gather sums the slots covering
+            // each voxel in a fixed order
+            a.adj_scr[(static_cast<size_t>(b) * nsp + role) * nobp + e] = s;
+            continue;
+          }
           if (s == 0.f) continue;
           int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
           int hs = h0 - (g.kh - 1) + aa + g.hoff;
@@ -1145,7 +1156,25 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     if (FWD && a.mode == 2) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) gacc += __shfl_xor_sync(0xffffffffu, gacc, o);
-      if (lane == 0) atomicAdd(a.norm2, static_cast<double>(gacc));
+      if (a.npart != nullptr) {
+        // deterministic: the CTA's partial (warps summed in a fixed order)
+        if (lane == 0) nrm[ew] = static_cast<double>(gacc);
+        named_sync(2, NEPI * 32);
+        if (ew == 0 && lane == 0) {
+          double t = 0.0;
+          for (int w = 0; w < NEPI; ++w) t += nrm[w];
+          a.npart[blockIdx.x] = t;
+        }
+      } else if (lane == 0) {
+        atomicAdd(a.norm2, static_cast<double>(gacc));
+      }
+    } else if (FWD && a.npart != nullptr) {
+      // deterministic: the CTA's column partials (its bricks, its columns;
+      // zeros elsewhere) in its own row, summed over the rows in a fixed
+      // order by the coefficient / fold kernel
+      named_sync(2, NEPI * 32);
+      for (int j = ew * 32 + lane; j < g.kp; j += NEPI * 32)
+        a.npart[static_cast<size_t>(blockIdx.x) * g.kp + j] = nrm[j];
     } else if (FWD && a.norm2 != nullptr) {
       named_sync(2, NEPI * 32);
       for (int j = ew * 32 + lane; j < g.kp; j += NEPI * 32)

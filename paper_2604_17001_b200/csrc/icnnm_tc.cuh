@@ -74,11 +74,14 @@ struct alignas(64) TcArgs {
   int bres;                 // 1: the role's B tiles are resident in SMEM (one load per launch)
   int bres_stride;          // resident B: bytes per (tile, chunk) block
   int bres_bytes;           // resident B: SMEM bytes of the role's tiles x chunks
+  // deterministic reductions (null: fp32 / fp64 atomics as before)
+  float* adj_scr;           // adjoint: per-(brick, role) output-brick slots [nbricks][nsplit][nobp]
+  double* npart;            // forward: per-CTA column partials [grid][kp] (mode 2: [grid])
 };
 
 // dbg slots (cycles summed over CTAs)
 enum { DBG_BUILD_WAIT = 0, DBG_BUILD_WORK, DBG_MMA_WAIT_A, DBG_MMA_WAIT_B, DBG_MMA_WAIT_ACC,
-       DBG_EPI_WAIT, DBG_EPI_WORK, DBG_LOAD_WAIT, DBG_TOTAL, DBG_SLOTS };
+       DBG_EPI_WAIT, DBG_EPI_WORK, DBG_LOAD_WAIT, DBG_TOTAL, DBG_BUILD_PREP, DBG_SLOTS };
 
 template <bool FWD, bool F16>
 __global__ void icnnm_tc_kernel(TcArgs a);

@@ -656,6 +656,34 @@ def test_solve_batch_equals_single_calls(gpu):
                               cfg)
 
 
+@pytest.mark.parametrize("engine", ["f16x3", "tf32x3"])
+@pytest.mark.parametrize("cfgno,dims,iters", [(4, (32, 32, 16), 40), (2, (24, 24, 16), 30),
+                                              (1, (32, 32, 8), 30)])
+def test_solve_bit_reproducible(gpu, engine, cfgno, dims, iters):
+    """Two solves of the same problem are bit-identical (the reference is
+    deterministic): the tcgen05 engines reduce the adjoint's
+    output bricks, the column norms and the report sums in a fixed order
+    (no floating-point atomics).  Covers the resident-B split mode (config-4
+    and config-1 recipes) and the streamed-B mode (config-2 recipe)."""
+    from paper_2604_17001_b200 import synth
+    w = synth.scaled(synth.WORKLOADS[cfgno], dims, iters=iters, n_train=2)
+    X, mask = w.target(), w.mask()
+    B = gpu.learn_ensemble_basis(w.training(), w.kernel)
+    cfg = gpu.SolverConfig(max_iters=iters, engine=engine, **FIXED)
+    L1, r1 = gpu.icnnm_solve(X * mask, mask, B, cfg)
+    L2, r2 = gpu.icnnm_solve(X * mask, mask, B, cfg)
+    np.testing.assert_array_equal(L1, L2)
+    np.testing.assert_array_equal(np.asarray(r1.objective), np.asarray(r2.objective))
+    cfg_x = gpu.SolverConfig(max_iters=iters, engine=engine, exact_residual=True, **FIXED)
+    L3, r3 = gpu.icnnm_solve(X * mask, mask, B, cfg_x)
+    L4, r4 = gpu.icnnm_solve(X * mask, mask, B, cfg_x)
+    np.testing.assert_array_equal(L3, L4)
+    np.testing.assert_array_equal(np.asarray(r3.primal_residual), np.asarray(r4.primal_residual))
+    Lo, _ = O.icnnm_solve(X * mask, mask, _oracle_basis(B),
+                          O.SolverConfig(max_iters=iters, **FIXED))
+    assert _rel(L1, Lo) <= 1e-4
+
+
 def test_rejected_upload_leaves_no_problem(gpu):
     """A rejected upload must not leave the previous problem's scalars next to
     the overwritten staging buffers: the handle then has no problem."""
