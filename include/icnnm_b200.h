@@ -317,10 +317,10 @@ int icnnm_cuda_analyze_recovery(int order, const int64_t* dims, const double* L0
 int icnnm_dist_unique_id(char* out128);
 
 /* Solve with `local_slabs` slabs per process and `world` processes
- * (G = local_slabs * world slabs).  Each process passes the FULL tensor
- * (M_obs, mask: m doubles) and receives its own slabs' rows of L in
- * L_out (rows [row0, row0 + nrows) of the H axis, written to
- * L_out[0 .. nrows*W*T)).  world == 1 needs no NCCL id (pass NULL: the
+ * (G = local_slabs * world slabs), every process passing the FULL tensor
+ * (M_obs, mask: m doubles); each process reads only its own rows and
+ * receives them in L_out (rows [row0, row0 + nrows) of the H axis, written
+ * to L_out[0 .. nrows*W*T)).  world == 1 needs no NCCL id (pass NULL: the
  * exchange is device copies); world == 1 WITH an id (icnnm_dist_unique_id)
  * runs the exchange through a one-rank NCCL communicator (self send/recv,
  * all-reduce) -- the multi-process transport, exercised on one GPU.
@@ -334,6 +334,27 @@ int icnnm_sharded_solve(int order, const int64_t* dims, const double* M_obs,
                         int world, int rank, const char* nccl_id128,
                         int device, double* L_out, int64_t* row0,
                         int64_t* nrows, icnnm_solve_report* report);
+
+/* The rows [row0, row0 + nrows) of the H axis that rank `rank` owns (its
+ * local_slabs consecutive slabs of the G-slab plan). */
+int icnnm_sharded_rows(int order, const int64_t* dims, const int64_t* kdims,
+                       int local_slabs, int world, int rank, int64_t* row0,
+                       int64_t* nrows);
+
+/* The same solve with slab-local inputs: M_rows / mask_rows hold only this
+ * rank's rows [row0, row0 + nrows) (nrows*W*T doubles each, as
+ * icnnm_sharded_rows returns them) -- no process holds the full tensor.  The
+ * global setup scalars (theta0 from max|pm|, solver.cpp:88-91; res_scale
+ * from ||pm||, :97; the mean fill, :83-86; the empty-set check, :70-71)
+ * are all-reduced over the ranks, and an invalid slab fails every rank. */
+int icnnm_sharded_solve_local(int order, const int64_t* dims, int64_t row0,
+                              int64_t nrows, const double* M_rows,
+                              const double* mask_rows, const int64_t* kdims,
+                              const double* K_colmajor,
+                              const icnnm_solver_config* cfg, int local_slabs,
+                              int world, int rank, const char* nccl_id128,
+                              int device, double* L_out,
+                              icnnm_solve_report* report);
 
 /* Slab plan (host logic, exported for CPU tests): slab g of G over H rows
  * gets rows [start, start+count); returns 1 (invalid) when a slab would be

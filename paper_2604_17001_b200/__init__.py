@@ -7,7 +7,7 @@ package is the Python mirror of the reference's solver/operator interface.
 from ._lib import IcnnmError, InvalidArgument, CudaError, LIB_PATH, lib
 from .api import (SolverConfig, SolveReport, EigenBasis, Solver, BasisConvolver,
                   icnnm_solve, icnnm_solve_batch, cnnm_solve, learn_ensemble_basis, conv_adjoint, prox_l21, conv_gram,
-                  objective_icnnm, symeig, sharded_solve, shard_plan, dist_unique_id,
+                  objective_icnnm, symeig, sharded_solve, sharded_solve_local, sharded_rows, shard_plan, dist_unique_id,
                   device_count, empty_cache, probe_ffma_tflops)
 from . import synth, analysis
 
@@ -15,6 +15,6 @@ __all__ = [
     "IcnnmError", "InvalidArgument", "CudaError", "LIB_PATH", "lib",
     "SolverConfig", "SolveReport", "EigenBasis", "Solver", "BasisConvolver",
     "icnnm_solve", "icnnm_solve_batch", "cnnm_solve", "learn_ensemble_basis", "conv_adjoint", "prox_l21", "conv_gram",
-    "objective_icnnm", "symeig", "sharded_solve", "shard_plan", "dist_unique_id",
+    "objective_icnnm", "symeig", "sharded_solve", "sharded_solve_local", "sharded_rows", "shard_plan", "dist_unique_id",
     "device_count", "empty_cache", "probe_ffma_tflops", "synth", "analysis",
 ]

@@ -135,6 +135,11 @@ SIGNATURES = {
                                       C.POINTER(SolverConfigC), C.c_int, C.c_int,
                                       C.c_int, C.c_char_p, C.c_int, _dp, _lp, _lp,
                                       C.POINTER(SolveReportC)]),
+    "icnnm_sharded_rows": (C.c_int, [C.c_int, _lp, _lp, C.c_int, C.c_int, C.c_int, _lp, _lp]),
+    "icnnm_sharded_solve_local": (C.c_int, [C.c_int, _lp, C.c_int64, C.c_int64, _dp, _dp, _lp,
+                                            _dp, C.POINTER(SolverConfigC), C.c_int, C.c_int,
+                                            C.c_int, C.c_char_p, C.c_int, _dp,
+                                            C.POINTER(SolveReportC)]),
     "icnnm_shard_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int64, C.c_int, _lp, _lp]),
     "icnnm_probe_ffma_tflops": (C.c_int, [C.c_int, _dp]),
     "icnnm_io_last_error": (C.c_char_p, []),

@@ -466,6 +466,45 @@ def sharded_solve(M_obs, mask, basis: EigenBasis, cfg: Optional[SolverConfig] = 
     return r0.value, rows.copy(), _report_from_c(rep, obj, res, lc)
 
 
+def sharded_rows(dims, kernel_shape, local_slabs: int = 1, world: int = 1, rank: int = 0):
+    """(row0, nrows): the H rows a rank owns in the sharded solve."""
+    r0 = C.c_int64()
+    nr = C.c_int64()
+    check(lib().icnnm_sharded_rows(len(dims), lptr(_dims(dims)), lptr(_dims(kernel_shape)),
+                                   int(local_slabs), int(world), int(rank), C.byref(r0),
+                                   C.byref(nr)))
+    return r0.value, nr.value
+
+
+def sharded_solve_local(dims, M_rows, mask_rows, basis: EigenBasis,
+                        cfg: Optional[SolverConfig] = None, local_slabs: int = 1,
+                        world: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None,
+                        device: int = 0):
+    """H-sharded solve from slab-local inputs: M_rows / mask_rows are this
+    rank's rows (sharded_rows) of the full `dims` tensor; no process holds
+    the whole tensor.  Returns (L_rows, report)."""
+    cfg = cfg or SolverConfig()
+    dims = tuple(int(d) for d in dims)
+    M, W = _f64(M_rows), _f64(mask_rows)
+    if M.shape != W.shape:
+        raise InvalidArgument("solve: mask dims != observation dims")
+    _check_basis_shape(basis, dims)
+    r0, nr = sharded_rows(dims, basis.kernel_shape, local_slabs, world, rank)
+    if M.shape != (nr,) + dims[1:]:
+        raise InvalidArgument(f"sharded solve: rank {rank} owns rows [{r0}, {r0 + nr}) -> "
+                              f"inputs of shape {(nr,) + dims[1:]}, got {M.shape}")
+    c = cfg.to_c()
+    out = np.empty_like(M)
+    rep, obj, res, lc = _report_buffers(max(int(cfg.max_iters), 1))
+    idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+    check(lib().icnnm_sharded_solve_local(len(dims), lptr(_dims(dims)), r0, nr, dptr(M), dptr(W),
+                                          lptr(_dims(basis.kernel_shape)),
+                                          dptr(_colmajor(basis.K)), C.byref(c),
+                                          int(local_slabs), int(world), int(rank), idbuf,
+                                          device, dptr(out), C.byref(rep)))
+    return out, _report_from_c(rep, obj, res, lc)
+
+
 def cnnm_solve(M_obs, mask, kernel_shape, cfg: Optional[SolverConfig] = None,
                device: int = 0) -> Tuple[np.ndarray, SolveReport]:
     """cnnm_solve (solver.cpp:161-170): the CNNM baseline (K = I, SVT

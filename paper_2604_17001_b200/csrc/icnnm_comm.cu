@@ -50,6 +50,9 @@ class NcclComm final : public Comm {
   void allreduce_sum(double* buf, size_t n, cudaStream_t s) override {
     NK(ncclAllReduce(buf, buf, n, ncclFloat64, ncclSum, comm_, s));
   }
+  void allreduce_max(double* buf, size_t n, cudaStream_t s) override {
+    NK(ncclAllReduce(buf, buf, n, ncclFloat64, ncclMax, comm_, s));
+  }
 
  private:
   ncclComm_t comm_ = nullptr;

@@ -17,6 +17,7 @@ class Comm {
   // send n floats to rank-1, receive n floats from rank+1
   virtual void shift_backward(const float* send, float* recv, size_t n, cudaStream_t s) = 0;
   virtual void allreduce_sum(double* buf, size_t n, cudaStream_t s) = 0;
+  virtual void allreduce_max(double* buf, size_t n, cudaStream_t s) = 0;
 };
 
 void comm_unique_id(char* out128);

@@ -676,9 +676,9 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   // in shared memory next to a W ring of >= 4 stages, they are loaded once
   // per launch instead of once per brick -- the per-brick B stream (the whole
   // hi/lo basis, e.g. 256 KB at k = 245) disappears from L2 and SMEM.  A
-  // brick's work is split over nsplit CTA roles when the whole basis does not
-  // fit: forward by N-tiles (each role its own columns of W), adjoint by
-  // K-chunks (each role a partial sum over j, added by the atomic flush).
+  // brick's work is split over nsplit CTA roles by N-tiles when the whole
+  // basis does not fit (forward: each role its own columns of W; adjoint: its
+  // own taps, partial output bricks summed by the flush).
   // Measured at config 4 (k = 245, 2 N-tiles; profiles/ab_r2/bres): the
   // split costs more than the B stream it removes (forward 0.353 -> 0.399 ms,
   // adjoint 0.382 -> 0.503 ms: per-brick preparation runs once per tile, and
@@ -688,13 +688,11 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   if (t.f16 && !pairs && !a.mcb && have_b && bres_env != 0) {
     const int stride = t.wbase * icnnm_dev::tc::KC * 4;
     for (int ns = 1; ns <= 4 && !found; ++ns) {
-      if (fwd && ns > t.ntn) break;
-      if (!fwd && ns > 1 && t.nkc / ns < 2) break;
+      if (ns > t.ntn) break;
       int maxb = 0;
       for (int r = 0; r < ns; ++r) {
-        const int ntiles = fwd ? (r + 1) * t.ntn / ns - r * t.ntn / ns : t.ntn;
-        const int nchunks = fwd ? t.nkc : (r + 1) * t.nkc / ns - r * t.nkc / ns;
-        maxb = std::max(maxb, ntiles * nchunks * stride);
+        const int ntiles = (r + 1) * t.ntn / ns - r * t.ntn / ns;
+        maxb = std::max(maxb, ntiles * t.nkc * stride);
       }
       for (int eh = fwd ? 1 : 2; eh >= 1 && !found; --eh)
         for (int wsv = std::min(ws_cap, icnnm_dev::tc::WS) & ~1; wsv >= 4 && !found; wsv -= 2)
@@ -930,6 +928,8 @@ struct Solver {
   DBuf<double> npart, upart, gpart;
   int nsm = 148, upd_rows = 0;
   DBuf<float> xfer_send, xfer_recv;  // cross-process halo buffers
+  DBuf<double> comb;                 // cross-rank combine of the upload scalars
+  double h_comb[5] = {0, 0, 0, 0, 0};
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs = nullptr;
   double* h_theta = nullptr;  // pinned staging of the theta schedule (thread's pool)
@@ -993,10 +993,13 @@ void solver_alloc(Solver& S) {
   S.cvec.alloc(kpmax);
   S.red.alloc(kpmax + 8);
   S.st.alloc(1);
-  int64_t mtot = p.m;
+  // staging of this process' own rows only (all slabs: the whole tensor)
+  int64_t mtot = 0;
+  for (auto& s : S.slabs) mtot += s.m_own;
   S.Mstage.alloc(mtot);
   S.maskstage.alloc(mtot);
   if (S.comm) {
+    S.comb.alloc(8);
     S.xfer_send.alloc((p.kd[0] - 1) * WT + 1);
     S.xfer_recv.alloc((p.kd[0] - 1) * WT + 1);
   }
@@ -1006,7 +1009,9 @@ void solver_alloc(Solver& S) {
 // Upload: validation of solver.cpp:66-72 / tensor.hpp:115-121, host scalars.
 void solver_upload(Solver& S, const double* M, const double* mask) {
   if (!M || !mask) invalid("solve: null input");
-  const int64_t m = S.p.m;
+  // this process' own rows (every slab of an unsharded or single-process solve)
+  int64_t m = 0;
+  for (auto& s : S.slabs) m += s.m_own;
   // The staging buffers are overwritten below before the scan has finished:
   // the handle holds no problem until this upload has validated (a rejected
   // upload leaves "no problem uploaded", never the previous problem's scalars
@@ -1045,6 +1050,31 @@ void solver_upload(Solver& S, const double* M, const double* mask) {
                                      : e1;
   cudaError_t e3 = e2 == cudaSuccess ? cudaStreamSynchronize(S.stream) : e2;
   scan.join();
+  if (S.comm) {
+    // slab-local inputs: theta0 (max |pm|, solver.cpp:88-91), res_scale
+    // (||pm||, :97), the mean fill (:83-86) and the empty-set / validity
+    // checks (:68-72) are global -- combined over the ranks (max / sum);
+    // an invalid slab fails every rank (no rank is left waiting in a
+    // collective)
+    CK(e3);
+    double* h = S.h_comb;
+    h[0] = amax;
+    h[1] = err ? 1.0 : 0.0;
+    h[2] = n2;
+    h[3] = sum;
+    h[4] = static_cast<double>(obs);
+    CK(cudaMemcpyAsync(S.comb.p, h, 5 * sizeof(double), cudaMemcpyHostToDevice, S.stream));
+    S.comm->allreduce_max(S.comb.p, 2, S.stream);
+    S.comm->allreduce_sum(S.comb.p + 2, 3, S.stream);
+    CK(cudaMemcpyAsync(h, S.comb.p, 5 * sizeof(double), cudaMemcpyDeviceToHost, S.stream));
+    CK(cudaStreamSynchronize(S.stream));
+    if (err) invalid(err);
+    if (h[1] != 0.0) invalid("solve: invalid input on another rank");
+    amax = h[0];
+    n2 = h[2];
+    sum = h[3];
+    obs = static_cast<int64_t>(h[4] + 0.5);
+  }
   if (err) invalid(err);
   CK(e3);
   if (obs == 0) invalid("solve: empty sampling set");
@@ -1429,7 +1459,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
     CK(cudaMemcpyAsync(S.st.p, S.h_st, sizeof(IterState), cudaMemcpyHostToDevice, S.stream));
     if (S.tc_counters) CK(cudaMemsetAsync(S.dbg.p, 0, S.dbg.bytes(), S.stream));
     for (auto& s : S.slabs) {
-      const int64_t off = s.row0 * WT;
+      const int64_t off = (s.row0 - S.slabs[0].row0) * WT;
       icnnm_dev::icnnm_setup<<<grid_for(s.m_own, 256), 256, 0, S.stream>>>(
           s.m_own, S.Mstage.p + off, S.maskstage.p + off, cfg.init_fill == ICNNM_INIT_MEAN,
           mean, s.pm.p, s.mask.p, s.L.p, s.V.p, s.Lt.p + s.halo_elems);
@@ -2232,6 +2262,78 @@ int icnnm_dist_unique_id(char* out128) {
   });
 }
 
+namespace {
+// The H-sharded solve of one process: `M_rows` / `mask_rows` hold exactly the
+// process' own rows [row0, row0 + nrows) of the tensor (its local_slabs
+// consecutive slabs of the G-slab plan); halo rows arrive through the
+// exchange, the global setup scalars through the upload's all-reduce.
+void sharded_solve_rows(const Problem& p, const double* M_rows, const double* mask_rows,
+                        const double* K_colmajor, const icnnm_solver_config* cfg,
+                        int local_slabs, int world, int rank, const char* nccl_id128,
+                        int device, double* L_out, int64_t* row0_out, int64_t* nrows_out,
+                        icnnm_solve_report* report, std::chrono::steady_clock::time_point t0) {
+  const int G = local_slabs * world;
+  DeviceScope ds(device);
+  Solver S;
+  S.p = p;
+  S.device = device;
+  S.sharded = true;
+  S.G = G;
+  S.world = world;
+  S.rank = rank;
+  S.local = local_slabs;
+  S.K.assign(K_colmajor, K_colmajor + static_cast<size_t>(p.k) * p.k);
+  S.slabs.resize(local_slabs);
+  for (int i = 0; i < local_slabs; ++i) {
+    int64_t s = 0, c = 0;
+    const int gi = rank * local_slabs + i;
+    if (icnnm_shard_plan(p.dims[0], G, p.kd[0], gi, &s, &c) != ICNNM_OK) invalid(g_last_error);
+    S.slabs[i].row0 = s;
+    S.slabs[i].rows = c;
+  }
+  // world == 1 with an id: a one-rank communicator carries the exchange
+  // (self send/recv + all-reduce), so the NCCL transport runs on one GPU
+  if (world > 1 || nccl_id128) {
+    if (!nccl_id128) invalid("sharded solve: NCCL unique id required for world > 1");
+    S.comm = comm_create(nccl_id128, world, rank);
+  }
+  solver_alloc(S);
+  solver_upload(S, M_rows, mask_rows);
+  RunResult R = solver_run(S, *cfg);
+  solver_download(S, L_out);
+  if (row0_out) *row0_out = S.slabs[0].row0;
+  if (nrows_out) {
+    int64_t n = 0;
+    for (auto& s : S.slabs) n += s.rows;
+    *nrows_out = n;
+  }
+  double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  fill_report(S, *cfg, R, report, wall);
+}
+
+void rank_rows(const Problem& p, int local_slabs, int world, int rank, int64_t* row0,
+               int64_t* nrows) {
+  const int G = local_slabs * world;
+  int64_t s0 = 0, c0 = 0, s1 = 0, c1 = 0;
+  if (icnnm_shard_plan(p.dims[0], G, p.kd[0], rank * local_slabs, &s0, &c0) != ICNNM_OK ||
+      icnnm_shard_plan(p.dims[0], G, p.kd[0], rank * local_slabs + local_slabs - 1, &s1, &c1) !=
+          ICNNM_OK)
+    invalid(g_last_error);
+  *row0 = s0;
+  *nrows = s1 + c1 - s0;
+}
+}  // namespace
+
+int icnnm_sharded_rows(int order, const int64_t* dims, const int64_t* kdims, int local_slabs,
+                       int world, int rank, int64_t* row0, int64_t* nrows) {
+  return guard([&] {
+    Problem p = make_problem(order, dims, kdims);
+    if (local_slabs < 1 || world < 1 || rank < 0 || rank >= world || !row0 || !nrows)
+      invalid("sharded solve: bad slab / rank arguments");
+    rank_rows(p, local_slabs, world, rank, row0, nrows);
+  });
+}
+
 int icnnm_sharded_solve(int order, const int64_t* dims, const double* M_obs, const double* mask,
                         const int64_t* kdims, const double* K_colmajor,
                         const icnnm_solver_config* cfg, int local_slabs, int world, int rank,
@@ -2243,46 +2345,39 @@ int icnnm_sharded_solve(int order, const int64_t* dims, const double* M_obs, con
     Problem p = make_problem(order, dims, kdims);
     if (local_slabs < 1 || world < 1 || rank < 0 || rank >= world)
       invalid("sharded solve: bad slab / rank arguments");
-    if (!L_out) invalid("null output");
+    if (!L_out || !M_obs || !mask) invalid("null argument");
     validate_basis(p.k, K_colmajor, nullptr);
-    const int G = local_slabs * world;
-    DeviceScope ds(device);
-    Solver S;
-    S.p = p;
-    S.device = device;
-    S.sharded = true;
-    S.G = G;
-    S.world = world;
-    S.rank = rank;
-    S.local = local_slabs;
-    S.K.assign(K_colmajor, K_colmajor + static_cast<size_t>(p.k) * p.k);
-    S.slabs.resize(local_slabs);
-    for (int i = 0; i < local_slabs; ++i) {
-      int64_t s = 0, c = 0;
-      const int gi = rank * local_slabs + i;
-      if (icnnm_shard_plan(p.dims[0], G, p.kd[0], gi, &s, &c) != ICNNM_OK)
-        invalid(g_last_error);
-      S.slabs[i].row0 = s;
-      S.slabs[i].rows = c;
-    }
-    // world == 1 with an id: a one-rank communicator carries the exchange
-    // (self send/recv + all-reduce), so the NCCL transport runs on one GPU
-    if (world > 1 || nccl_id128) {
-      if (!nccl_id128) invalid("sharded solve: NCCL unique id required for world > 1");
-      S.comm = comm_create(nccl_id128, world, rank);
-    }
-    solver_alloc(S);
-    solver_upload(S, M_obs, mask);
-    RunResult R = solver_run(S, *cfg);
-    solver_download(S, L_out);
-    if (row0_out) *row0_out = S.slabs[0].row0;
-    if (nrows_out) {
-      int64_t n = 0;
-      for (auto& s : S.slabs) n += s.rows;
-      *nrows_out = n;
-    }
-    double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    fill_report(S, *cfg, R, report, wall);
+    int64_t r0 = 0, nr = 0;
+    rank_rows(p, local_slabs, world, rank, &r0, &nr);
+    const int64_t WT = p.dims[1] * p.dims[2];
+    // the full tensor was passed: this rank reads (and validates) its own rows
+    sharded_solve_rows(p, M_obs + r0 * WT, mask + r0 * WT, K_colmajor, cfg, local_slabs, world,
+                       rank, nccl_id128, device, L_out, row0_out, nrows_out, report, t0);
+  });
+}
+
+int icnnm_sharded_solve_local(int order, const int64_t* dims, int64_t row0, int64_t nrows,
+                              const double* M_rows, const double* mask_rows,
+                              const int64_t* kdims, const double* K_colmajor,
+                              const icnnm_solver_config* cfg, int local_slabs, int world,
+                              int rank, const char* nccl_id128, int device, double* L_out,
+                              icnnm_solve_report* report) {
+  return guard([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    validate_cfg(cfg);
+    Problem p = make_problem(order, dims, kdims);
+    if (local_slabs < 1 || world < 1 || rank < 0 || rank >= world)
+      invalid("sharded solve: bad slab / rank arguments");
+    if (!L_out || !M_rows || !mask_rows) invalid("null argument");
+    validate_basis(p.k, K_colmajor, nullptr);
+    int64_t r0 = 0, nr = 0;
+    rank_rows(p, local_slabs, world, rank, &r0, &nr);
+    if (row0 != r0 || nrows != nr)
+      invalid("sharded solve: rows [" + std::to_string(row0) + ", " + std::to_string(row0 + nrows) +
+              ") are not this rank's slab rows [" + std::to_string(r0) + ", " +
+              std::to_string(r0 + nr) + ") (icnnm_sharded_rows)");
+    sharded_solve_rows(p, M_rows, mask_rows, K_colmajor, cfg, local_slabs, world, rank,
+                       nccl_id128, device, L_out, nullptr, nullptr, report, t0);
   });
 }
 

@@ -472,6 +472,38 @@ __global__ void icnnm_fold(Partials P, int kp, double* red) {
 // (periodic in W and T; in H periodic over the tensor or, in slab mode, the
 // buffer row hoff + h with kh-1 halo rows first) -- the col2im of the
 // tcgen05 adjoint (icnnm_tc.cu), conv_adjoint's map (conv_op.cpp:57-77).
+// Valid (brick index q, halo offset off) pairs of one axis for output
+// coordinate x: brick start x0 = q * bx with x0 - (kx-1) + off == x (mod X
+// when periodic; in slab mode x is the buffer row and x0 + hoff... the
+// caller passes the own-row coordinate), off in [0, bx + kx - 1).  Returns
+// the count (<= GMAX), or -1 when more pairs exist (tiny tensors that wrap
+// the halo box several times; the caller then takes the generic path).
+constexpr int GMAX = 12;
+__device__ __forceinline__ int axis_pairs(int x, int kx, int bx, int X, bool periodic,
+                                          int (&q)[GMAX], int (&off)[GMAX]) {
+  const int HX = bx + kx - 1;
+  int n = 0;
+  for (int o = 0; o < HX; ++o) {
+    int x0 = x + kx - 1 - o;
+    if (periodic) {
+      if (x0 >= X) x0 -= X;
+      if (x0 < 0) x0 += X;
+      if (x0 < 0 || x0 >= X) {  // wraps more than once (X < HX)
+        x0 %= X;
+        if (x0 < 0) x0 += X;
+      }
+    } else if (x0 < 0 || x0 >= X) {
+      continue;
+    }
+    if (x0 % bx != 0) continue;
+    if (n == GMAX) return -1;
+    q[n] = x0 / bx;
+    off[n] = o;
+    ++n;
+  }
+  return n;
+}
+
 __global__ void __launch_bounds__(256)
 icnnm_adj_gather(Geo g, int nsp, int nobp, const float* __restrict__ scr,
                  float* __restrict__ adj) {
@@ -481,32 +513,50 @@ icnnm_adj_gather(Geo g, int nsp, int nobp, const float* __restrict__ scr,
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int t = static_cast<int>(i % g.T);
-  const int64_t q = i / g.T;
-  const int w = static_cast<int>(q % g.W);
-  const int hb = static_cast<int>(q / g.W);
+  const int64_t qq = i / g.T;
+  const int w = static_cast<int>(qq % g.W);
+  const int hb = static_cast<int>(qq / g.W);
+  int qh[GMAX], oh[GMAX], qw[GMAX], ow[GMAX], qt[GMAX], ot[GMAX];
+  const int nh = axis_pairs(hb - g.hoff, g.kh, g.bh, g.H, g.wrapH != 0, qh, oh);
+  const int nw = axis_pairs(w, g.kw, g.bw, g.W, true, qw, ow);
+  const int nt = axis_pairs(t, g.kt, g.bt, g.T, true, qt, ot);
   float acc = 0.f;
-  for (int aa = 0; aa < g.HH; ++aa) {
-    int h0 = hb - g.hoff + g.kh - 1 - aa;
-    if (g.wrapH) {
-      h0 %= g.H;
-      if (h0 < 0) h0 += g.H;
-    } else if (h0 < 0 || h0 >= g.H) {
-      continue;
-    }
-    if (h0 % g.bh != 0) continue;
-    const int qh = h0 / g.bh;
-    for (int bb = 0; bb < g.HW; ++bb) {
-      int w0 = (w + g.kw - 1 - bb) % g.W;
-      if (w0 < 0) w0 += g.W;
-      if (w0 % g.bw != 0) continue;
-      const int64_t bhw = static_cast<int64_t>(qh) * g.nbw + w0 / g.bw;
-      for (int c = 0; c < g.HT; ++c) {
-        int t0 = (t + g.kt - 1 - c) % g.T;
-        if (t0 < 0) t0 += g.T;
-        if (t0 % g.bt != 0) continue;
-        const int64_t b = bhw * g.nbt + t0 / g.bt;
-        const int e = (aa * g.HW + bb) * g.HT + c;
-        for (int r = 0; r < nsp; ++r) acc += scr[(b * nsp + r) * nobp + e];
+  if (nh >= 0 && nw >= 0 && nt >= 0) {
+    // fixed order: h pairs, w pairs, t pairs (ascending halo offset), roles
+    for (int a = 0; a < nh; ++a)
+      for (int b2 = 0; b2 < nw; ++b2) {
+        const int64_t bhw = static_cast<int64_t>(qh[a]) * g.nbw + qw[b2];
+        const int ehw = (oh[a] * g.HW + ow[b2]) * g.HT;
+        for (int c = 0; c < nt; ++c) {
+          const int64_t b = bhw * g.nbt + qt[c];
+          const float* sp = scr + b * nsp * nobp + ehw + ot[c];
+          for (int r = 0; r < nsp; ++r) acc += sp[static_cast<int64_t>(r) * nobp];
+        }
+      }
+  } else {
+    // generic path (the halo box wraps a tiny tensor many times)
+    for (int aa = 0; aa < g.HH; ++aa) {
+      int h0 = hb - g.hoff + g.kh - 1 - aa;
+      if (g.wrapH) {
+        h0 %= g.H;
+        if (h0 < 0) h0 += g.H;
+      } else if (h0 < 0 || h0 >= g.H) {
+        continue;
+      }
+      if (h0 % g.bh != 0) continue;
+      for (int bb = 0; bb < g.HW; ++bb) {
+        int w0 = (w + g.kw - 1 - bb) % g.W;
+        if (w0 < 0) w0 += g.W;
+        if (w0 % g.bw != 0) continue;
+        const int64_t bhw = static_cast<int64_t>(h0 / g.bh) * g.nbw + w0 / g.bw;
+        for (int c = 0; c < g.HT; ++c) {
+          int t0 = (t + g.kt - 1 - c) % g.T;
+          if (t0 < 0) t0 += g.T;
+          if (t0 % g.bt != 0) continue;
+          const int64_t b = bhw * g.nbt + t0 / g.bt;
+          const int e = (aa * g.HW + bb) * g.HT + c;
+          for (int r = 0; r < nsp; ++r) acc += scr[(b * nsp + r) * nobp + e];
+        }
       }
     }
   }

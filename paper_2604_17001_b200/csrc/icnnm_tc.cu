@@ -680,17 +680,19 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   const int ntn = a.ntn;
   const int nkc = a.nkc;
   // Split mode (a.nsplit > 1, single CTAs only): CTA role = blockIdx % nsplit
-  // owns a slice of the work of every brick -- forward: a range of N-tiles
-  // (its columns of W), adjoint: a range of K-chunks (a partial sum over the
-  // basis columns j, added into adj by the flush like any other partial) --
-  // so that the role's B tiles fit in shared memory and stay resident
-  // (a.bres: loaded once per launch instead of once per brick).
+  // owns a range of the N-tiles of every brick -- forward: its columns j of
+  // W; adjoint: its taps s, whose col2im partial output brick is summed with
+  // the other roles' by the flush -- so that the role's B tiles fit in shared
+  // memory and stay resident (a.bres: loaded once per launch instead of once
+  // per brick).  Each role builds the brick's A operand itself (the adjoint's
+  // builders idle ~80% of the time).  The K-chunk range
+  // [kcb, kce) is the whole basis (kept general for the loops below).
   const int nsp = a.nsplit > 1 ? a.nsplit : 1;
   const int role = nsp > 1 ? static_cast<int>(blockIdx.x % static_cast<unsigned>(nsp)) : 0;
-  const int ntb = (FWD && nsp > 1) ? role * ntn / nsp : 0;
-  const int nte = (FWD && nsp > 1) ? (role + 1) * ntn / nsp : ntn;
-  const int kcb = (!FWD && nsp > 1) ? role * nkc / nsp : 0;
-  const int kce = (!FWD && nsp > 1) ? (role + 1) * nkc / nsp : nkc;
+  const int ntb = nsp > 1 ? role * ntn / nsp : 0;
+  const int nte = nsp > 1 ? (role + 1) * ntn / nsp : ntn;
+  const int kcb = 0;
+  const int kce = nkc;
   const int nkr = kce - kcb;                   // K-chunks per tile in this CTA
   const int grp = a.grp > 1 ? 2 : 1;          // N-tiles sharing each A chunk
   const int ngrp = (nte - ntb + grp - 1) / grp;

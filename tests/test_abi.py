@@ -113,6 +113,20 @@ def test_shard_plan_partitions_rows(H, G, kh):
     assert max(c for _, c in rows) - min(c for _, c in rows) <= 1
 
 
+@pytest.mark.parametrize("H,G,world", [(1024, 8, 8), (1024, 2, 4), (100, 3, 2), (48, 1, 4)])
+def test_sharded_rows_partition_H(H, G, world):
+    """icnnm_sharded_rows: each rank's rows are its local_slabs consecutive
+    slabs of the G*world-slab plan; the ranks tile [0, H) in order."""
+    nxt = 0
+    for r in range(world):
+        r0, n = P.sharded_rows((H, 16, 8), (9, 3, 3), local_slabs=G, world=world, rank=r)
+        assert r0 == nxt and n >= 1
+        s0, _ = P.shard_plan(H, G * world, 9, r * G)
+        assert s0 == r0
+        nxt = r0 + n
+    assert nxt == H
+
+
 def test_shard_plan_rejects_thin_slabs():
     with pytest.raises(P.InvalidArgument):
         P.shard_plan(16, 8, 9, 0)      # 2 rows < 8-row halo

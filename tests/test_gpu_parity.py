@@ -473,6 +473,66 @@ def test_config5_sharded_recipe(gpu, engine):
         assert _rel(rows, L1) <= 1e-5, G
 
 
+@pytest.mark.parametrize("engine", ["f16x3", "tf32x3"])
+def test_config5_recipe_golden_sharded(gpu, engine):
+    """Config 5's recipe (kernel 9x9x9, k = 729; 30% i.i.d. minus boxes) at
+    128x128x64, 100 iterations, against the fp64 oracle golden
+    (cfg5_128x128x64_it100.npz, blocked oracle): the unsharded solve, G = 1,
+    2, 4, 8 virtual slabs, and G = 2 through the one-rank NCCL transport --
+    the adjoint wrap across slab boundaries (conv_op.cpp:57-77) and the loop
+    (solver.cpp:107-139) at the survey's size."""
+    import os
+    from paper_2604_17001_b200 import synth
+    path = os.path.join(os.path.dirname(__file__), "golden", "cfg5_128x128x64_it100.npz")
+    if not os.path.exists(path):
+        pytest.skip("cfg5_128x128x64_it100.npz not generated")
+    gd = np.load(path)
+    w = synth.scaled(synth.WORKLOADS[5], (128, 128, 64), iters=100)
+    assert tuple(gd["dims"]) == w.dims and tuple(gd["kernel"]) == w.kernel
+    X, mask = w.target(), w.mask()
+    B = gpu.EigenBasis(w.kernel, gd["K"], gd["eigenvalues"])
+    Lo = gd["L"].astype(np.float64)
+    miss = mask == 0
+    cfg = gpu.SolverConfig(max_iters=100, engine=engine, **FIXED)
+
+    def check(L, rep, tag):
+        assert rep.iterations == 100, tag
+        assert _rel(L, Lo) <= 1e-4, tag
+        assert _rel(L[miss], Lo[miss]) <= 1e-3, tag
+        assert abs(synth.psnr(X, L) - float(gd["psnr"])) <= 0.01, tag
+        np.testing.assert_allclose(rep.objective, gd["objective"], rtol=1e-4)
+    L1, r1 = gpu.icnnm_solve(X * mask, mask, B, cfg)
+    check(L1, r1, "unsharded")
+    for G in (1, 2, 4, 8):
+        row0, rows, rep = gpu.sharded_solve(X * mask, mask, B, cfg, local_slabs=G)
+        assert row0 == 0 and rows.shape == X.shape
+        check(rows, rep, f"G={G}")
+    rows, rep = gpu.sharded_solve_local(X.shape, X * mask, mask, B, cfg, local_slabs=2,
+                                        nccl_id=gpu.dist_unique_id())
+    check(rows, rep, "G=2 NCCL one-rank, slab-local inputs")
+
+
+def test_sharded_local_inputs_errors(gpu):
+    """Slab-local inputs must be exactly the rank's rows; an invalid entry on
+    any slab fails the call."""
+    from paper_2604_17001_b200 import synth
+    X = synth.synth_video(32, 16, 16, 4, 1, 5)
+    mask = synth.synth_mask(32, 16, 16, synth.MASK_IID, 0.4, 6)
+    B = gpu.learn_ensemble_basis([X], (5, 3, 3))
+    cfg = gpu.SolverConfig(max_iters=5, **FIXED)
+    assert gpu.sharded_rows(X.shape, (5, 3, 3), local_slabs=4) == (0, 32)
+    with pytest.raises(gpu.InvalidArgument, match="owns rows"):
+        gpu.sharded_solve_local(X.shape, (X * mask)[:16], mask[:16], B, cfg, local_slabs=4)
+    bad = X * mask
+    bad[20, 3, 3] = np.nan
+    with pytest.raises(gpu.InvalidArgument, match="non-finite"):
+        gpu.sharded_solve_local(X.shape, bad, mask, B, cfg, local_slabs=2,
+                                nccl_id=gpu.dist_unique_id())
+    L, _ = gpu.sharded_solve_local(X.shape, X * mask, mask, B, cfg, local_slabs=2)
+    Lf, _ = gpu.icnnm_solve(X * mask, mask, B, cfg)
+    assert _rel(L, Lf) <= 1e-5
+
+
 @pytest.mark.parametrize("engine", ENGINES)
 def test_exact_residual_trace(gpu, engine):
     """exact_residual=True reproduces the reference's primal_residual trace
