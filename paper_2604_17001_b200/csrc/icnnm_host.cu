@@ -899,6 +899,7 @@ struct Slab {
   DBuf<float> Lt, adj, pm, mask, W;
   DBuf<float> Lr;                 // exact-residual mode: L_{t+1} (fp32, with halo rows)
   DBuf<float> adj_scr;            // deterministic adjoint: per-(brick, role) output slots
+  DBuf<int> gtab;                 // deterministic adjoint: gather table (icnnm_adj_gather)
   int adj_nsp = 1, adj_nobp = 0;  // roles per brick / padded slot size of the adjoint launch
   DBuf<double> L, V;
 };
@@ -1250,6 +1251,7 @@ void launch_adj(Solver& S, Slab& s) {
       lc.attrs = &at;
       lc.numAttrs = use_pdl(S) ? 1 : 0;
       CK(cudaLaunchKernelEx(&lc, icnnm_dev::icnnm_adj_gather, s.gtc, s.adj_nsp, s.adj_nobp,
+                            static_cast<const int*>(s.gtab.p),
                             static_cast<const float*>(s.adj_scr.p), s.adj.p));
       ++S.launches;
     }
@@ -1279,6 +1281,42 @@ icnnm_dev::Partials partials(const Solver& S) {
     P.grows = ns * S.nsm;
   }
   return P;
+}
+
+// Gather table of icnnm_adj_gather: for every buffer row (slab: own rows after
+// hoff halo rows), W and T coordinate, the (brick index, halo offset) pairs of
+// the output slots covering it, in ascending offset order (the kernel's fixed
+// summation order) -- the inverse of the tcgen05 adjoint's col2im map.
+std::vector<int> gather_table(const Geo& g) {
+  using icnnm_dev::GATHER_PAIRS;
+  using icnnm_dev::GATHER_S;
+  std::vector<int> tab(static_cast<size_t>(g.Hsrc + g.W + g.T) * GATHER_S, 0);
+  auto axis = [&](int row, int x, int kx, int bx, int X, bool periodic) {
+    int* e = tab.data() + static_cast<size_t>(row) * GATHER_S;
+    int n = 0;
+    for (int o = 0; o < bx + kx - 1; ++o) {
+      int x0 = x + kx - 1 - o;
+      if (periodic) {
+        x0 %= X;
+        if (x0 < 0) x0 += X;
+      } else if (x0 < 0 || x0 >= X) {
+        continue;
+      }
+      if (x0 % bx != 0) continue;
+      if (n == GATHER_PAIRS) {
+        n = -1;
+        break;
+      }
+      e[1 + 2 * n] = x0 / bx;
+      e[2 + 2 * n] = o;
+      ++n;
+    }
+    e[0] = n;
+  };
+  for (int hb = 0; hb < g.Hsrc; ++hb) axis(hb, hb - g.hoff, g.kh, g.bh, g.H, g.wrapH != 0);
+  for (int w = 0; w < g.W; ++w) axis(g.Hsrc + w, w, g.kw, g.bw, g.W, true);
+  for (int t = 0; t < g.T; ++t) axis(g.Hsrc + g.W + t, t, g.kt, g.bt, g.T, true);
+  return tab;
 }
 
 // Deterministic buffers of a tcgen05 run, allocated before any graph capture.
@@ -1311,6 +1349,12 @@ void prepare_det(Solver& S) {
     s.adj_nobp = (nob + 3) / 4 * 4;
     const size_t need = static_cast<size_t>(n_bricks(s.gtc)) * s.adj_nsp * s.adj_nobp;
     if (s.adj_scr.n != need) s.adj_scr.alloc(need);
+    if (!s.gtab.p) {
+      const std::vector<int> tab = gather_table(s.gtc);
+      s.gtab.alloc(tab.size());
+      CK(cudaMemcpyAsync(s.gtab.p, tab.data(), s.gtab.bytes(), cudaMemcpyHostToDevice, S.stream));
+      CK(cudaStreamSynchronize(S.stream));
+    }
   }
 }
 

@@ -472,41 +472,15 @@ __global__ void icnnm_fold(Partials P, int kp, double* red) {
 // (periodic in W and T; in H periodic over the tensor or, in slab mode, the
 // buffer row hoff + h with kh-1 halo rows first) -- the col2im of the
 // tcgen05 adjoint (icnnm_tc.cu), conv_adjoint's map (conv_op.cpp:57-77).
-// Valid (brick index q, halo offset off) pairs of one axis for output
-// coordinate x: brick start x0 = q * bx with x0 - (kx-1) + off == x (mod X
-// when periodic; in slab mode x is the buffer row and x0 + hoff... the
-// caller passes the own-row coordinate), off in [0, bx + kx - 1).  Returns
-// the count (<= GMAX), or -1 when more pairs exist (tiny tensors that wrap
-// the halo box several times; the caller then takes the generic path).
-constexpr int GMAX = 12;
-__device__ __forceinline__ int axis_pairs(int x, int kx, int bx, int X, bool periodic,
-                                          int (&q)[GMAX], int (&off)[GMAX]) {
-  const int HX = bx + kx - 1;
-  int n = 0;
-  for (int o = 0; o < HX; ++o) {
-    int x0 = x + kx - 1 - o;
-    if (periodic) {
-      if (x0 >= X) x0 -= X;
-      if (x0 < 0) x0 += X;
-      if (x0 < 0 || x0 >= X) {  // wraps more than once (X < HX)
-        x0 %= X;
-        if (x0 < 0) x0 += X;
-      }
-    } else if (x0 < 0 || x0 >= X) {
-      continue;
-    }
-    if (x0 % bx != 0) continue;
-    if (n == GMAX) return -1;
-    q[n] = x0 / bx;
-    off[n] = o;
-    ++n;
-  }
-  return n;
-}
-
+// The (brick, halo offset) pairs covering each coordinate come from a host
+// table (gather_table(), icnnm_host.cu): per axis and coordinate x, GATHER_S
+// ints = [n, q_0, off_0, q_1, off_1, ...] in ascending offset order, n = -1
+// when more than GATHER_PAIRS pairs exist (a tiny tensor wrapped several times
+// by the halo box: the generic path below).  Rows: Hsrc buffer rows, then W,
+// then T coordinates.
 __global__ void __launch_bounds__(256)
-icnnm_adj_gather(Geo g, int nsp, int nobp, const float* __restrict__ scr,
-                 float* __restrict__ adj) {
+icnnm_adj_gather(Geo g, int nsp, int nobp, const int* __restrict__ tab,
+                 const float* __restrict__ scr, float* __restrict__ adj) {
   pdl_wait();
   pdl_trigger();
   const int64_t n = static_cast<int64_t>(g.Hsrc) * g.W * g.T;
@@ -516,25 +490,27 @@ icnnm_adj_gather(Geo g, int nsp, int nobp, const float* __restrict__ scr,
   const int64_t qq = i / g.T;
   const int w = static_cast<int>(qq % g.W);
   const int hb = static_cast<int>(qq / g.W);
-  int qh[GMAX], oh[GMAX], qw[GMAX], ow[GMAX], qt[GMAX], ot[GMAX];
-  const int nh = axis_pairs(hb - g.hoff, g.kh, g.bh, g.H, g.wrapH != 0, qh, oh);
-  const int nw = axis_pairs(w, g.kw, g.bw, g.W, true, qw, ow);
-  const int nt = axis_pairs(t, g.kt, g.bt, g.T, true, qt, ot);
+  const int* th = tab + static_cast<int64_t>(hb) * GATHER_S;
+  const int* tw = tab + static_cast<int64_t>(g.Hsrc + w) * GATHER_S;
+  const int* tt = tab + static_cast<int64_t>(g.Hsrc + g.W + t) * GATHER_S;
+  const int nh = th[0], nw = tw[0], nt = tt[0];
   float acc = 0.f;
   if (nh >= 0 && nw >= 0 && nt >= 0) {
     // fixed order: h pairs, w pairs, t pairs (ascending halo offset), roles
-    for (int a = 0; a < nh; ++a)
+    for (int a = 0; a < nh; ++a) {
+      const int qh = th[1 + 2 * a], oh = th[2 + 2 * a];
       for (int b2 = 0; b2 < nw; ++b2) {
-        const int64_t bhw = static_cast<int64_t>(qh[a]) * g.nbw + qw[b2];
-        const int ehw = (oh[a] * g.HW + ow[b2]) * g.HT;
+        const int64_t bhw = static_cast<int64_t>(qh) * g.nbw + tw[1 + 2 * b2];
+        const int ehw = (oh * g.HW + tw[2 + 2 * b2]) * g.HT;
         for (int c = 0; c < nt; ++c) {
-          const int64_t b = bhw * g.nbt + qt[c];
-          const float* sp = scr + b * nsp * nobp + ehw + ot[c];
+          const int64_t b = bhw * g.nbt + tt[1 + 2 * c];
+          const float* sp = scr + b * nsp * nobp + ehw + tt[2 + 2 * c];
           for (int r = 0; r < nsp; ++r) acc += sp[static_cast<int64_t>(r) * nobp];
         }
       }
+    }
   } else {
-    // generic path (the halo box wraps a tiny tensor many times)
+    // generic path (the halo box wraps a tiny tensor many times): same order
     for (int aa = 0; aa < g.HH; ++aa) {
       int h0 = hb - g.hoff + g.kh - 1 - aa;
       if (g.wrapH) {

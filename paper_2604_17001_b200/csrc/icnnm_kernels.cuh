@@ -99,7 +99,10 @@ __global__ void icnnm_coef(IterState* st, const double* theta, double* red, floa
                            IterStats* stats, int k, int kp, double kd, double res_scale,
                            double tol_p, double tol_c, double floor_rel, int exact, Partials P);
 __global__ void icnnm_fold(Partials P, int kp, double* red);
-__global__ void icnnm_adj_gather(Geo g, int nsp, int nobp, const float* scr, float* adj);
+constexpr int GATHER_PAIRS = 12;                 // max (brick, offset) pairs per axis coordinate
+constexpr int GATHER_S = 1 + 2 * GATHER_PAIRS;   // ints per table entry
+__global__ void icnnm_adj_gather(Geo g, int nsp, int nobp, const int* tab, const float* scr,
+                                 float* adj);
 constexpr int UPD_U = 4;  // elements in flight per thread (icnnm_update)
 __global__ void icnnm_update(int64_t m, const IterState* st, double lambda, double kd,
                              float* adj, double* L, double* V, const float* pm,

@@ -485,7 +485,7 @@ __device__ __forceinline__ void tg_seq(int i, int gsz, int nkc, int D, int& t, i
 //   warp  9 + NEPI          B loader
 // ---------------------------------------------------------------------------
 template <bool FWD, bool F16, bool PAIR>
-__global__ void __launch_bounds__(608, 1)
+__global__ void __launch_bounds__(608 + 32 * NPREP, 1)
 icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   constexpr int ASC = F16 ? KC : 2 * KC;  // TMEM columns per A stage
   constexpr int ALO = ASC / 2;            // column offset of the lo half
@@ -493,6 +493,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   constexpr int NEPI = 8;                // epilogue warps (adjoint: 4 * a.ehalf active)
   constexpr int WMMA = NB + NEPI;        // MMA warp
   constexpr int WLOAD = NB + NEPI + 1;   // B loader warp; W loader warp after it
+  constexpr int WPREP = WLOAD + 2;       // forward: NPREP halo-preparation warps
   constexpr int BSTG = F16 ? (PAIR ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES;  // B stage stride
   const Geo& g = a.g;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -514,7 +515,9 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   uint64_t* W_empty = W_full + WS;
   uint64_t* SC_full = W_empty + WS;   // F16x3 forward: per-brick scale slots
   float* sc_ring = reinterpret_cast<float*>(SC_full + NSC);
-  float* wmax = sc_ring + NSC;        // 2 x 8 builder-warp maxima
+  float* wmax = sc_ring + NSC;        // 2 x 8 halo-warp maxima
+  uint64_t* HALO_full = reinterpret_cast<uint64_t*>(wmax + 16);  // forward: halo buffer ready
+  uint64_t* HALO_empty = HALO_full + 2;                           // forward: halo buffer read
   p += BAR_BYTES;  // 2*SA + 2*SB + 4 + 2*WS + NSC mbarriers, NSC scales, 16 maxima
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p);
   p += 16;
@@ -587,6 +590,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       mbar_init(W_empty + i, FWD ? 4 * 32 : nbuild);  // forward: the half's 4 epilogue warps
     }
     for (int i = 0; i < NSC; ++i) mbar_init(SC_full + i, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(HALO_full + i, 1);             // the prep warps' leader, after their barrier
+      mbar_init(HALO_empty + i, NB * 32);      // every builder thread, after the brick
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int s = tid; s < g.ktp; s += blockDim.x) {
@@ -731,22 +738,6 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
     uint32_t cnt = 0;
     Dbg dbg(lane == 0 ? a.dbg : nullptr);
-    auto issue_halo = [&](float* dst, int b) {
-      int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
-      const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
-      for (int e = bt_tid; e < nob; e += NB * 32) {
-        int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
-        int hs = h0 - (g.kh - 1) + aa + g.hoff;
-        hs = g.wrapH ? wrapi(hs, g.Hsrc) : (hs < 0 ? 0 : (hs >= g.Hsrc ? g.Hsrc - 1 : hs));
-        int ws = wrapi(w0 - (g.kw - 1) + bb, g.W);
-        int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
-        cp_async4(dst + e, a.src + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts);
-      }
-      cp_async_commit();
-    };
-    if (FWD) {
-      if (sfirst < nslot) issue_halo(halo, brick_of(sfirst));
-    }
     // F16x3 operand scale: forward per brick (the halo is prescaled in place);
     // adjoint: folded into cs
     // (the held chunk c and the next owned chunk c+2 must use different A and
@@ -771,37 +762,9 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     for (int sl = sfirst; sl < nslot; sl += sstep, ++iter) {
       float* hcur = halo + (iter & 1) * nobp;
       const long long tp0 = dbg.p ? clk() : 0;
-      if (FWD) {
-        cp_async_wait_all();
-        named_sync(1, NB * 32);  // this brick's halo landed; previous brick fully built
-        if (sl + sstep < nslot) issue_halo(halo + ((iter + 1) & 1) * nobp, brick_of(sl + sstep));
-        if (F16) {
-          float mx = 0.f;
-          for (int e = bt_tid; e < nob; e += NB * 32) mx = fmaxf(mx, fabsf(hcur[e]));
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          if (lane == 0) wmax[(iter & 1) * 8 + warp] = mx;
-          named_sync(1, NB * 32);
-          float bm = 0.f;
-#pragma unroll
-          for (int w = 0; w < NB; ++w) bm = fmaxf(bm, wmax[(iter & 1) * 8 + w]);
-          const float fscale = f16_scale(bm);
-          // prescale and pre-split in place: word = rn_f16(x) | rn_f16(x - hi) << 16,
-          // so each chunk's build is gathers + byte permutes (same bits as
-          // splitting per chunk, once per halo element instead of once per tap)
-          uint32_t* hw = reinterpret_cast<uint32_t*>(hcur);
-          for (int e = bt_tid; e < nob; e += NB * 32) {
-            const float x = hcur[e] * fscale;
-            const float xh = __half2float(__float2half_rn(x));
-            hw[e] = pack_f16x2(x, x - xh);
-          }
-          if (bt_tid == 0) {  // the epilogue unscales this brick by 2^-(eA + eB)
-            sc_ring[iter % NSC] = a.bunscale / fscale;
-            mbar_arrive(SC_full + iter % NSC);
-          }
-          named_sync(1, NB * 32);  // halo scaled
-        }
-      }
+      // forward: this brick's halo (prescaled / pre-split for F16x3) is
+      // prepared by the prep warps while the previous brick is built
+      if (FWD) mbar_wait(HALO_full + (iter & 1), (static_cast<uint32_t>(iter) >> 1) & 1u);
       if (dbg.p) prep += clk() - tp0;
       for (int gi = 0; gi < ngrp; ++gi) {
         for (int kc = kcb; kc < kce; ++kc, ++cnt, adv_stage()) {
@@ -940,9 +903,66 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         if (!FWD) mbar_arrive(W_empty + pend_wsi);
         pend_sa = -1;
       }
+      if (FWD) mbar_arrive(HALO_empty + (iter & 1));  // this thread's reads of the halo are done
     }
     dbg.flush(DBG_BUILD_WAIT, DBG_BUILD_WORK);
     if (dbg.p) atomicAdd(dbg.p + DBG_BUILD_PREP, static_cast<unsigned long long>(prep));
+  } else if (FWD && warp >= WPREP && warp < WPREP + NPREP) {
+    // ===================== halo preparation (forward) =====================
+    // Brick i's halo box (periodic L~ gather) into halo[i & 1], its max|x|,
+    // the F16x3 operand scale (published to the epilogue's scale ring), and
+    // the in-place prescale / hi-lo pre-split -- off the builders' critical
+    // path (the all-builder barrier phase this replaces took ~25-33% of the
+    // builders' time at brick transitions, profiles/README_r2.md)
+    const int pt = tid - WPREP * 32;  // 0 .. 32*NPREP-1
+    const int pw = warp - WPREP;
+    int iter = 0;
+    for (int sl = sfirst; sl < nslot; sl += sstep, ++iter) {
+      const int buf = iter & 1;
+      float* hcur = halo + buf * nobp;
+      mbar_wait(HALO_empty + buf, ((static_cast<uint32_t>(iter) >> 1) & 1u) ^ 1u);
+      const int b = brick_of(sl);
+      const int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
+      const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
+      for (int e = pt; e < nob; e += NPREP * 32) {
+        int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
+        int hs = h0 - (g.kh - 1) + aa + g.hoff;
+        hs = g.wrapH ? wrapi(hs, g.Hsrc) : (hs < 0 ? 0 : (hs >= g.Hsrc ? g.Hsrc - 1 : hs));
+        int ws = wrapi(w0 - (g.kw - 1) + bb, g.W);
+        int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
+        cp_async4(hcur + e, a.src + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts);
+      }
+      cp_async_commit();
+      cp_async_wait_all();
+      named_sync(5, NPREP * 32);  // the whole halo landed
+      if (F16) {
+        float mx = 0.f;
+        for (int e = pt; e < nob; e += NPREP * 32) mx = fmaxf(mx, fabsf(hcur[e]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) wmax[buf * 8 + pw] = mx;
+        named_sync(5, NPREP * 32);
+        float bm = 0.f;
+#pragma unroll
+        for (int w = 0; w < NPREP; ++w) bm = fmaxf(bm, wmax[buf * 8 + w]);
+        const float fscale = f16_scale(bm);
+        // prescale and pre-split in place: word = rn_f16(x) | rn_f16(x - hi) << 16,
+        // so each chunk's build is gathers + byte permutes (same bits as
+        // splitting per chunk, once per halo element instead of once per tap)
+        uint32_t* hw = reinterpret_cast<uint32_t*>(hcur);
+        for (int e = pt; e < nob; e += NPREP * 32) {
+          const float x = hcur[e] * fscale;
+          const float xh = __half2float(__float2half_rn(x));
+          hw[e] = pack_f16x2(x, x - xh);
+        }
+        if (pt == 0) {  // the epilogue unscales this brick by 2^-(eA + eB)
+          sc_ring[iter % NSC] = a.bunscale / fscale;
+          mbar_arrive(SC_full + iter % NSC);
+        }
+        named_sync(5, NPREP * 32);  // halo scaled
+      }
+      if (pt == 0) mbar_arrive(HALO_full + buf);
+    }
   } else if (warp < NB) {
   } else if (warp < NB + nepi_act && !(TC_SKIP(a) & 32)) {
     // ===================== epilogue =====================

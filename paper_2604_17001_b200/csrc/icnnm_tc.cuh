@@ -23,9 +23,10 @@ constexpr int NTMAX = 208;                     // max accumulator width (N per t
 constexpr int B_STAGE_BYTES = 256 * KC * 4 * 2;    // hi + lo, up to 256 rows = 32 KB (tf32;
                                                    // also the packed-block stride in global)
 constexpr int B_STAGE_F16 = 256 * KC * 2 * 2;      // f16 hi + lo: 16 KB SMEM stage
-constexpr int BAR_BYTES = 640;                     // mbarriers + scale ring + builder maxima
-static_assert((2 * SA + 2 * SB + 4 + 2 * WS + NSC) * 8 + NSC * 4 + 16 * 4 <= BAR_BYTES,
+constexpr int BAR_BYTES = 768;  // mbarriers + scale ring + halo maxima + halo barriers
+static_assert((2 * SA + 2 * SB + 4 + 2 * WS + NSC) * 8 + NSC * 4 + 16 * 4 + 4 * 8 <= BAR_BYTES,
               "barrier block overflows BAR_BYTES");
+constexpr int NPREP = 4;  // forward: halo-preparation warps
 // CTA pairs hold half of every B tile (N split across the pair)
 inline int b_stage_bytes(bool f16, bool pair = false) {
   return f16 ? (pair ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES;
@@ -89,8 +90,9 @@ __global__ void icnnm_tc_kernel(TcArgs a);
 void* fwd_kernel_ptr(bool f16, bool pair = false);
 void* adj_kernel_ptr(bool f16, bool pair = false);
 
-// 8 builder + 8 epilogue + MMA + B loader + W loader warps (both kernels)
-inline int threads(bool) { return 608; }
+// 8 builder + 8 epilogue + MMA + B loader + W loader warps (both kernels);
+// the forward adds NPREP halo-preparation warps
+inline int threads(bool fwd) { return fwd ? 608 + 32 * NPREP : 608; }
 
 inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16, bool pair = false,
                          int ehalf = 1, int bres_bytes = 0) {
