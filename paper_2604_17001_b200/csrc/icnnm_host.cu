@@ -685,6 +685,11 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   // the adjoint's K-split doubles its col2im epilogue), so it is off by
   // default; ICNNM_TC_BRES=1 (experiments build) enables it.
   static const int bres_env = env_knob("ICNNM_TC_BRES", 0);
+  // forward: halo buffers for the prep warps' software pipeline (4: they run
+  // two bricks ahead of the builders), fewer when shared memory is short
+  static const int nhb_env = env_knob("ICNNM_TC_NHB", icnnm_dev::tc::NHB_MAX);
+  for (int nhb = fwd ? std::min(nhb_env, icnnm_dev::tc::NHB_MAX) : 2; nhb >= 2 && !found; --nhb) {
+  a.nhb = nhb;
   if (t.f16 && !pairs && !a.mcb && have_b && bres_env != 0) {
     const int stride = t.wbase * icnnm_dev::tc::KC * 4;
     for (int ns = 1; ns <= 4 && !found; ++ns) {
@@ -696,7 +701,8 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
       }
       for (int eh = fwd ? 1 : 2; eh >= 1 && !found; --eh)
         for (int wsv = std::min(ws_cap, icnnm_dev::tc::WS) & ~1; wsv >= 4 && !found; wsv -= 2)
-          if (icnnm_dev::tc::smem_bytes(gtc, fwd, 1, wsv, t.f16, false, eh, maxb) <= 227 * 1024) {
+          if (icnnm_dev::tc::smem_bytes(gtc, fwd, 1, wsv, t.f16, false, eh, maxb, nhb) <=
+              227 * 1024) {
             a.nsplit = ns;
             a.bres = 1;
             a.bres_stride = stride;
@@ -712,19 +718,21 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
     const int sb_min = (eh == 2 && eh_env <= 0) ? std::min(4, sb_cap) : 2;
     for (int sbv = std::min(sb_cap, icnnm_dev::tc::SB); sbv >= sb_min && !found; --sbv)
       for (int wsv = std::min(ws_cap, icnnm_dev::tc::WS) & ~1; wsv >= 2 && !found; wsv -= 2)
-        if (icnnm_dev::tc::smem_bytes(gtc, fwd, sbv, wsv, t.f16, pairs, eh) <= 227 * 1024) {
+        if (icnnm_dev::tc::smem_bytes(gtc, fwd, sbv, wsv, t.f16, pairs, eh, 0, nhb) <=
+            227 * 1024) {
           a.sb = sbv;
           a.ws = wsv;
           a.ehalf = eh;
           found = true;
         }
   }
+  }  // nhb
   a.nbricks = n_bricks(gtc);
   int dev = 0, nsm = 148;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  cfg.smem =
-      icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16, pairs, a.ehalf, a.bres_bytes);
+  cfg.smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16, pairs, a.ehalf, a.bres_bytes,
+                                       a.nhb);
   if (cfg.smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
   cfg.fn = fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16, a.cs > 1)
                : icnnm_dev::tc::adj_kernel_ptr(t.f16, a.cs > 1);

@@ -517,7 +517,8 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   float* sc_ring = reinterpret_cast<float*>(SC_full + NSC);
   float* wmax = sc_ring + NSC;        // 2 x 8 halo-warp maxima
   uint64_t* HALO_full = reinterpret_cast<uint64_t*>(wmax + 16);  // forward: halo buffer ready
-  uint64_t* HALO_empty = HALO_full + 2;                           // forward: halo buffer read
+  uint64_t* HALO_empty = HALO_full + NHB_MAX;                     // forward: halo buffer read
+  const int nhb = a.nhb >= 2 ? a.nhb : 2;                         // forward: halo buffers
   p += BAR_BYTES;  // 2*SA + 2*SB + 4 + 2*WS + NSC mbarriers, NSC scales, 16 maxima
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p);
   p += 16;
@@ -527,10 +528,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   p += ((g.kp * 4 + 15) / 16) * 16;
   const int nob = g.HH * g.HW * g.HT;
   const int nobp = ((nob + 3) / 4) * 4;
-  // FWD: halo[2] (2 x nobp) | nrm (kp doubles)
+  // FWD: halo[nhb] (nhb x nobp) | nrm (kp doubles)
   // ADJ: 4 * ehalf output bricks (nobp + 32 each)
   float* halo = reinterpret_cast<float*>(p);
-  double* nrm = reinterpret_cast<double*>(halo + 2 * nobp);
+  double* nrm = reinterpret_cast<double*>(halo + (FWD ? nhb : 2) * nobp);
   float* ob = reinterpret_cast<float*>(p);
 
   const int tid = threadIdx.x;
@@ -590,7 +591,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       mbar_init(W_empty + i, FWD ? 4 * 32 : nbuild);  // forward: the half's 4 epilogue warps
     }
     for (int i = 0; i < NSC; ++i) mbar_init(SC_full + i, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NHB_MAX; ++i) {
       mbar_init(HALO_full + i, 1);             // the prep warps' leader, after their barrier
       mbar_init(HALO_empty + i, NB * 32);      // every builder thread, after the brick
     }
@@ -760,11 +761,12 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     };
     long long prep = 0;
     for (int sl = sfirst; sl < nslot; sl += sstep, ++iter) {
-      float* hcur = halo + (iter & 1) * nobp;
+      const int hbuf = iter % nhb;
+      float* hcur = halo + hbuf * nobp;
       const long long tp0 = dbg.p ? clk() : 0;
       // forward: this brick's halo (prescaled / pre-split for F16x3) is
       // prepared by the prep warps while the previous brick is built
-      if (FWD) mbar_wait(HALO_full + (iter & 1), (static_cast<uint32_t>(iter) >> 1) & 1u);
+      if (FWD) mbar_wait(HALO_full + hbuf, static_cast<uint32_t>(iter / nhb) & 1u);
       if (dbg.p) prep += clk() - tp0;
       for (int gi = 0; gi < ngrp; ++gi) {
         for (int kc = kcb; kc < kce; ++kc, ++cnt, adv_stage()) {
@@ -903,24 +905,27 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         if (!FWD) mbar_arrive(W_empty + pend_wsi);
         pend_sa = -1;
       }
-      if (FWD) mbar_arrive(HALO_empty + (iter & 1));  // this thread's reads of the halo are done
+      if (FWD) mbar_arrive(HALO_empty + hbuf);  // this thread's reads of the halo are done
     }
     dbg.flush(DBG_BUILD_WAIT, DBG_BUILD_WORK);
     if (dbg.p) atomicAdd(dbg.p + DBG_BUILD_PREP, static_cast<unsigned long long>(prep));
   } else if (FWD && warp >= WPREP && warp < WPREP + NPREP) {
     // ===================== halo preparation (forward) =====================
-    // Brick i's halo box (periodic L~ gather) into halo[i & 1], its max|x|,
+    // Brick i's halo box (periodic L~ gather) into halo[i % nhb], its max|x|,
     // the F16x3 operand scale (published to the epilogue's scale ring), and
     // the in-place prescale / hi-lo pre-split -- off the builders' critical
     // path (the all-builder barrier phase this replaces took ~25-33% of the
     // builders' time at brick transitions, profiles/README_r2.md)
     const int pt = tid - WPREP * 32;  // 0 .. 32*NPREP-1
     const int pw = warp - WPREP;
-    int iter = 0;
-    for (int sl = sfirst; sl < nslot; sl += sstep, ++iter) {
-      const int buf = iter & 1;
-      float* hcur = halo + buf * nobp;
-      mbar_wait(HALO_empty + buf, ((static_cast<uint32_t>(iter) >> 1) & 1u) ^ 1u);
+    // software pipeline over nhb halo buffers: the gather of brick i is issued
+    // (cp.async group i) LAG bricks before its scale / split pass, so its
+    // L2/HBM latency overlaps the preparation of the bricks before it
+    const int LAG = nhb - 2 >= 1 ? (nhb - 2 > 2 ? 2 : nhb - 2) : 0;
+    auto issue = [&](int i, int sl) {
+      const int buf = i % nhb;
+      float* hdst = halo + buf * nobp;
+      mbar_wait(HALO_empty + buf, (static_cast<uint32_t>(i / nhb) & 1u) ^ 1u);
       const int b = brick_of(sl);
       const int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
       const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
@@ -930,21 +935,30 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         hs = g.wrapH ? wrapi(hs, g.Hsrc) : (hs < 0 ? 0 : (hs >= g.Hsrc ? g.Hsrc - 1 : hs));
         int ws = wrapi(w0 - (g.kw - 1) + bb, g.W);
         int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
-        cp_async4(hcur + e, a.src + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts);
+        cp_async4(hdst + e, a.src + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts);
       }
       cp_async_commit();
-      cp_async_wait_all();
-      named_sync(5, NPREP * 32);  // the whole halo landed
+    };
+    auto finish = [&](int i, int pending) {
+      const int buf = i % nhb;
+      float* hcur = halo + buf * nobp;
+      if (pending >= 2)
+        asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+      else if (pending == 1)
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      else
+        cp_async_wait_all();
+      named_sync(5, NPREP * 32);  // brick i's halo landed (every prep thread's copies)
       if (F16) {
         float mx = 0.f;
         for (int e = pt; e < nob; e += NPREP * 32) mx = fmaxf(mx, fabsf(hcur[e]));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (lane == 0) wmax[buf * 8 + pw] = mx;
+        if (lane == 0) wmax[(i & 1) * 8 + pw] = mx;
         named_sync(5, NPREP * 32);
         float bm = 0.f;
 #pragma unroll
-        for (int w = 0; w < NPREP; ++w) bm = fmaxf(bm, wmax[buf * 8 + w]);
+        for (int w = 0; w < NPREP; ++w) bm = fmaxf(bm, wmax[(i & 1) * 8 + w]);
         const float fscale = f16_scale(bm);
         // prescale and pre-split in place: word = rn_f16(x) | rn_f16(x - hi) << 16,
         // so each chunk's build is gathers + byte permutes (same bits as
@@ -956,12 +970,21 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           hw[e] = pack_f16x2(x, x - xh);
         }
         if (pt == 0) {  // the epilogue unscales this brick by 2^-(eA + eB)
-          sc_ring[iter % NSC] = a.bunscale / fscale;
-          mbar_arrive(SC_full + iter % NSC);
+          sc_ring[i % NSC] = a.bunscale / fscale;
+          mbar_arrive(SC_full + i % NSC);
         }
         named_sync(5, NPREP * 32);  // halo scaled
       }
       if (pt == 0) mbar_arrive(HALO_full + buf);
+    };
+    const int nmine = sfirst < nslot ? (nslot - sfirst + sstep - 1) / sstep : 0;
+    for (int i = 0; i < nmine + LAG; ++i) {
+      if (i < nmine) issue(i, sfirst + i * sstep);
+      if (i >= LAG) {
+        const int j = i - LAG;
+        const int pend = (i < nmine ? LAG : LAG - (i - nmine) - 1);
+        finish(j, pend < 0 ? 0 : pend);
+      }
     }
   } else if (warp < NB) {
   } else if (warp < NB + nepi_act && !(TC_SKIP(a) & 32)) {

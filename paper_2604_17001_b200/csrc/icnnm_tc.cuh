@@ -24,9 +24,10 @@ constexpr int B_STAGE_BYTES = 256 * KC * 4 * 2;    // hi + lo, up to 256 rows = 
                                                    // also the packed-block stride in global)
 constexpr int B_STAGE_F16 = 256 * KC * 2 * 2;      // f16 hi + lo: 16 KB SMEM stage
 constexpr int BAR_BYTES = 768;  // mbarriers + scale ring + halo maxima + halo barriers
-static_assert((2 * SA + 2 * SB + 4 + 2 * WS + NSC) * 8 + NSC * 4 + 16 * 4 + 4 * 8 <= BAR_BYTES,
+static_assert((2 * SA + 2 * SB + 4 + 2 * WS + NSC) * 8 + NSC * 4 + 16 * 4 + 2 * 4 * 8 <= BAR_BYTES,
               "barrier block overflows BAR_BYTES");
 constexpr int NPREP = 4;  // forward: halo-preparation warps
+constexpr int NHB_MAX = 4;  // forward: halo buffers (max; runtime a.nhb)
 // CTA pairs hold half of every B tile (N split across the pair)
 inline int b_stage_bytes(bool f16, bool pair = false) {
   return f16 ? (pair ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES;
@@ -78,6 +79,7 @@ struct alignas(64) TcArgs {
   // deterministic reductions (null: fp32 / fp64 atomics as before)
   float* adj_scr;           // adjoint: per-(brick, role) output-brick slots [nbricks][nsplit][nobp]
   double* npart;            // forward: per-CTA column partials [grid][kp] (mode 2: [grid])
+  int nhb;                  // forward: halo buffers (2..NHB_MAX; the prep warps run nhb-2 ahead)
 };
 
 // dbg slots (cycles summed over CTAs)
@@ -95,7 +97,7 @@ void* adj_kernel_ptr(bool f16, bool pair = false);
 inline int threads(bool fwd) { return fwd ? 608 + 32 * NPREP : 608; }
 
 inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16, bool pair = false,
-                         int ehalf = 1, int bres_bytes = 0) {
+                         int ehalf = 1, int bres_bytes = 0, int nhb = 2) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
   const size_t nobp = ((nob + 3) / 4) * 4;
   size_t b = (bres_bytes > 0 ? static_cast<size_t>(bres_bytes)
@@ -104,7 +106,7 @@ inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16, bool 
   b += ((g.ktp * 4 + 15) / 16) * 16;
   b += ((g.kp * 4 + 15) / 16) * 16;
   if (fwd)
-    b += 2 * nobp * 4 + static_cast<size_t>(g.kp) * 8;
+    b += static_cast<size_t>(nhb) * nobp * 4 + static_cast<size_t>(g.kp) * 8;
   else
     b += static_cast<size_t>(4 * ehalf) * (nobp + 32) * 4;
   return b;
