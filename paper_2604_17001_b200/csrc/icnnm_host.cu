@@ -679,18 +679,20 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   // brick's work is split over nsplit CTA roles by N-tiles when the whole
   // basis does not fit (forward: each role its own columns of W; adjoint: its
   // own taps, partial output bricks summed by the flush).
-  // Measured at config 4 (k = 245, 2 N-tiles; profiles/ab_r2/bres): the
-  // split costs more than the B stream it removes (forward 0.353 -> 0.399 ms,
-  // adjoint 0.382 -> 0.503 ms: per-brick preparation runs once per tile, and
-  // the adjoint's K-split doubles its col2im epilogue), so it is off by
-  // default; ICNNM_TC_BRES=1 (experiments build) enables it.
-  static const int bres_env = env_knob("ICNNM_TC_BRES", 0);
+  // Measured at config 4 (k = 245, 2 N-tiles; profiles/README_r2.md): the
+  // adjoint gains (0.408 -> 0.383 ms with the deterministic gather: its MMA
+  // waited on B 45% of the time), the forward loses (0.354 -> 0.387 ms: its
+  // per-brick halo preparation, now done once per tile, outlasts a tile's
+  // MMAs), so resident B is the adjoint's default only.  ICNNM_TC_BRES=0|1
+  // (experiments build) forces it off / on for both kernels.
+  static const int bres_env = env_knob("ICNNM_TC_BRES", -1);
+  const bool bres_on = bres_env < 0 ? !fwd : bres_env != 0;
   // forward: halo buffers for the prep warps' software pipeline (4: they run
   // two bricks ahead of the builders), fewer when shared memory is short
   static const int nhb_env = env_knob("ICNNM_TC_NHB", icnnm_dev::tc::NHB_MAX);
   for (int nhb = fwd ? std::min(nhb_env, icnnm_dev::tc::NHB_MAX) : 2; nhb >= 2 && !found; --nhb) {
   a.nhb = nhb;
-  if (t.f16 && !pairs && !a.mcb && have_b && bres_env != 0) {
+  if (t.f16 && !pairs && !a.mcb && have_b && bres_on) {
     const int stride = t.wbase * icnnm_dev::tc::KC * 4;
     for (int ns = 1; ns <= 4 && !found; ++ns) {
       if (ns > t.ntn) break;
@@ -714,11 +716,19 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
           }
     }
   }
+  // tight B stages (ICNNM_TC_BTIGHT=1, experiments): the ring's stage stride is
+  // the widest tile's bytes (8 KB at k = 245 instead of 16 KB), so the same
+  // shared memory holds up to twice as many chunks of lookahead
+  static const int btight_env = env_knob("ICNNM_TC_BTIGHT", 0);
+  const bool tight = t.f16 && !pairs && btight_env != 0;
+  a.bstride = tight ? t.wbase * icnnm_dev::tc::KC * 4 : 0;
+  const int sbc = tight ? std::max(sb_cap, icnnm_dev::tc::B_STAGE_F16 / std::max(1, a.bstride) * sb_cap)
+                        : sb_cap;
   for (int eh = fwd ? 1 : (eh_env > 0 ? eh_env : 2); eh >= 1 && !found; --eh) {
-    const int sb_min = (eh == 2 && eh_env <= 0) ? std::min(4, sb_cap) : 2;
-    for (int sbv = std::min(sb_cap, icnnm_dev::tc::SB); sbv >= sb_min && !found; --sbv)
+    const int sb_min = (eh == 2 && eh_env <= 0) ? std::min(4, sbc) : 2;
+    for (int sbv = std::min(sbc, icnnm_dev::tc::SB); sbv >= sb_min && !found; --sbv)
       for (int wsv = std::min(ws_cap, icnnm_dev::tc::WS) & ~1; wsv >= 2 && !found; wsv -= 2)
-        if (icnnm_dev::tc::smem_bytes(gtc, fwd, sbv, wsv, t.f16, pairs, eh, 0, nhb) <=
+        if (icnnm_dev::tc::smem_bytes(gtc, fwd, sbv, wsv, t.f16, pairs, eh, 0, nhb, a.bstride) <=
             227 * 1024) {
           a.sb = sbv;
           a.ws = wsv;
@@ -732,7 +742,7 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   cfg.smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16, pairs, a.ehalf, a.bres_bytes,
-                                       a.nhb);
+                                       a.nhb, a.bres ? 0 : a.bstride);
   if (cfg.smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
   cfg.fn = fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16, a.cs > 1)
                : icnnm_dev::tc::adj_kernel_ptr(t.f16, a.cs > 1);

@@ -434,10 +434,19 @@ __device__ double block_sum_fixed(double v) {
 
 __device__ void fold_partials(const Partials& P, int kp, double* red) {
   if (P.npart != nullptr) {
+    // four independent partial sums per column (rows r = 4i + q), combined in
+    // a fixed order: the dependent-add chain is a quarter as long
     for (int j = threadIdx.x; j < kp; j += blockDim.x) {
-      double t = 0.0;
-      for (int r = 0; r < P.nrows; ++r) t += P.npart[static_cast<size_t>(r) * kp + j];
-      red[j] = t;
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+      int r = 0;
+      for (; r + 4 <= P.nrows; r += 4) {
+        t0 += P.npart[static_cast<size_t>(r) * kp + j];
+        t1 += P.npart[static_cast<size_t>(r + 1) * kp + j];
+        t2 += P.npart[static_cast<size_t>(r + 2) * kp + j];
+        t3 += P.npart[static_cast<size_t>(r + 3) * kp + j];
+      }
+      for (; r < P.nrows; ++r) t0 += P.npart[static_cast<size_t>(r) * kp + j];
+      red[j] = (t0 + t1) + (t2 + t3);
     }
   }
   double* slot = red + kp;

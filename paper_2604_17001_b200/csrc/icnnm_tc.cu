@@ -494,7 +494,11 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   constexpr int WMMA = NB + NEPI;        // MMA warp
   constexpr int WLOAD = NB + NEPI + 1;   // B loader warp; W loader warp after it
   constexpr int WPREP = WLOAD + 2;       // forward: NPREP halo-preparation warps
-  constexpr int BSTG = F16 ? (PAIR ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES;  // B stage stride
+  // B stage stride: the widest tile's hi/lo bytes when the host packs the
+  // ring tightly (a.bstride, F16x3 single CTAs), else the fixed stage size
+  const int BSTG = (F16 && !PAIR && a.bstride > 0)
+                       ? a.bstride
+                       : (F16 ? (PAIR ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES);
   const Geo& g = a.g;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* p = smem;
@@ -922,20 +926,39 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     // (cp.async group i) LAG bricks before its scale / split pass, so its
     // L2/HBM latency overlaps the preparation of the bricks before it
     const int LAG = nhb - 2 >= 1 ? (nhb - 2 > 2 ? 2 : nhb - 2) : 0;
+    // halo element e = (aa*HW + bb)*HT + c of this thread: decomposed once,
+    // then advanced by NPREP*32 in mixed radix (no divisions per element)
+    constexpr int PSTEP = NPREP * 32;
+    const int dc = PSTEP % g.HT, dbb = (PSTEP / g.HT) % g.HW, daa = PSTEP / (g.HT * g.HW);
+    const int c0 = pt % g.HT, bb0 = (pt / g.HT) % g.HW, aa0 = pt / (g.HT * g.HW);
+    // one conditional wrap suffices unless a dimension is smaller than its halo
+    auto wrap1 = [](int x, int n) {
+      x = x < 0 ? x + n : x;
+      x = x >= n ? x - n : x;
+      return (static_cast<unsigned>(x) < static_cast<unsigned>(n)) ? x : wrapi(x, n);
+    };
     auto issue = [&](int i, int sl) {
       const int buf = i % nhb;
       float* hdst = halo + buf * nobp;
       mbar_wait(HALO_empty + buf, (static_cast<uint32_t>(i / nhb) & 1u) ^ 1u);
       const int b = brick_of(sl);
       const int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
-      const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
-      for (int e = pt; e < nob; e += NPREP * 32) {
-        int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
-        int hs = h0 - (g.kh - 1) + aa + g.hoff;
-        hs = g.wrapH ? wrapi(hs, g.Hsrc) : (hs < 0 ? 0 : (hs >= g.Hsrc ? g.Hsrc - 1 : hs));
-        int ws = wrapi(w0 - (g.kw - 1) + bb, g.W);
-        int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
+      const int hb0 = bh_i * g.bh - (g.kh - 1) + g.hoff, wb0 = bw_i * g.bw - (g.kw - 1),
+                tb0 = bt_i * g.bt - (g.kt - 1);
+      int c = c0, bb = bb0, aa = aa0;
+      for (int e = pt; e < nob; e += PSTEP) {
+        int hs = hb0 + aa;
+        hs = g.wrapH ? wrap1(hs, g.Hsrc) : (hs < 0 ? 0 : (hs >= g.Hsrc ? g.Hsrc - 1 : hs));
+        const int ws = wrap1(wb0 + bb, g.W);
+        const int ts = wrap1(tb0 + c, g.T);
         cp_async4(hdst + e, a.src + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts);
+        c += dc;
+        int cy = c >= g.HT ? 1 : 0;
+        c -= cy * g.HT;
+        bb += dbb + cy;
+        cy = bb >= g.HW ? 1 : 0;
+        bb -= cy * g.HW;
+        aa += daa + cy;
       }
       cp_async_commit();
     };

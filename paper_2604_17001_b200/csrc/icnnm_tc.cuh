@@ -15,7 +15,7 @@ constexpr int KC = 16;                         // K per chunk (tf32: 2 MMA K-ste
 constexpr int SA = 6;                          // TMEM A stages (max; runtime a.sa); tf32: 2*KC
                                                // columns each, f16: KC columns (2 halves / column)
 constexpr int NSC = 8;                         // F16x3 forward: per-brick scale ring
-constexpr int SB = 12;                         // SMEM B stages (max; runtime a.sb)
+constexpr int SB = 16;                         // SMEM B stages (max; runtime a.sb)
 constexpr int WS = 8;                          // SMEM W stages (max; runtime a.ws, even)
 constexpr int W_STAGE_BYTES = 128 * KC * 4;    // adjoint: 8 KB W chunk, 16 columns x 128 rows
 constexpr int WO_STAGE_BYTES = 128 * 32 * 4;   // forward: 16 KB W group, 32 columns x 128 rows
@@ -80,6 +80,7 @@ struct alignas(64) TcArgs {
   float* adj_scr;           // adjoint: per-(brick, role) output-brick slots [nbricks][nsplit][nobp]
   double* npart;            // forward: per-CTA column partials [grid][kp] (mode 2: [grid])
   int nhb;                  // forward: halo buffers (2..NHB_MAX; the prep warps run nhb-2 ahead)
+  int bstride;              // F16x3 single CTAs: B ring stage stride in bytes (0: B_STAGE_F16)
 };
 
 // dbg slots (cycles summed over CTAs)
@@ -97,11 +98,11 @@ void* adj_kernel_ptr(bool f16, bool pair = false);
 inline int threads(bool fwd) { return fwd ? 608 + 32 * NPREP : 608; }
 
 inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16, bool pair = false,
-                         int ehalf = 1, int bres_bytes = 0, int nhb = 2) {
+                         int ehalf = 1, int bres_bytes = 0, int nhb = 2, int bstride = 0) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
   const size_t nobp = ((nob + 3) / 4) * 4;
-  size_t b = (bres_bytes > 0 ? static_cast<size_t>(bres_bytes)
-                             : static_cast<size_t>(sb) * b_stage_bytes(f16, pair)) +
+  const size_t stage = bstride > 0 ? static_cast<size_t>(bstride) : b_stage_bytes(f16, pair);
+  size_t b = (bres_bytes > 0 ? static_cast<size_t>(bres_bytes) : static_cast<size_t>(sb) * stage) +
              static_cast<size_t>(ws) * (fwd ? WO_STAGE_BYTES : W_STAGE_BYTES) + BAR_BYTES + 16;
   b += ((g.ktp * 4 + 15) / 16) * 16;
   b += ((g.kp * 4 + 15) / 16) * 16;
