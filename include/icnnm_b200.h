@@ -48,6 +48,14 @@ extern "C" {
 #define ICNNM_ENGINE_TF32X3 1   /* tcgen05 kind::tf32, 3-term split (sm_100a) */
 #define ICNNM_ENGINE_F16X3 2    /* tcgen05 kind::f16, 3-term split of power-of-2
                                    scaled operands (sm_100a; half the MMA time) */
+#define ICNNM_ENGINE_F64 3      /* literal fp64 loop on the GPU (cuBLAS DGEMM
+                                   contractions): resolves the reference's default
+                                   tolerances; not the hot path                   */
+#define ICNNM_ENGINE_AUTO 4     /* default: F16X3 when both tolerances are disabled
+                                   (<= 1e-200, fixed iteration counts) or resolvable in
+                                   fp32 (tol_change >= 1e-6; tol_primal >= 1e-4, then with
+                                   exact_residual); F64 otherwise, so that the default
+                                   SolverConfig stops where solver.cpp:136-139 does      */
 
 /* Field-for-field mirror of icnnm::SolverConfig (solver.hpp:29-43). */
 typedef struct icnnm_solver_config {
@@ -61,7 +69,7 @@ typedef struct icnnm_solver_config {
   double tol_change;    /* 1e-8                                       */
   double rank_tol;      /* 1e-8 (unused by the solver, as upstream)   */
   int init_fill;        /* ICNNM_INIT_ZERO | ICNNM_INIT_MEAN          */
-  int engine;           /* ICNNM_ENGINE_* (extension; default F16X3) */
+  int engine;           /* ICNNM_ENGINE_* (extension; default AUTO)  */
   int exact_residual;   /* extension: 1 = exact primal_residual trace
                            (one extra forward contraction per iteration);
                            0 = fp32 identity estimate (NaN once unresolved) */
@@ -393,6 +401,8 @@ int64_t icnnm_diagnostics_to_json(const icnnm_recovery_diagnostics* d, char* out
  * ---------------------------------------------------------------------- */
 /* FP32 FFMA throughput in TFLOP/s measured with a register-resident kernel. */
 int icnnm_probe_ffma_tflops(int device, double* out);
+/* FP64 DFMA throughput in TFLOP/s (the Gram kernel's roofline denominator). */
+int icnnm_probe_dfma_tflops(int device, double* out);
 
 #ifdef __cplusplus
 }

@@ -8,7 +8,7 @@ from ._lib import IcnnmError, InvalidArgument, CudaError, LIB_PATH, lib
 from .api import (SolverConfig, SolveReport, EigenBasis, Solver, BasisConvolver,
                   icnnm_solve, icnnm_solve_batch, cnnm_solve, learn_ensemble_basis, conv_adjoint, prox_l21, conv_gram,
                   objective_icnnm, symeig, sharded_solve, sharded_solve_local, sharded_rows, shard_plan, dist_unique_id,
-                  device_count, empty_cache, probe_ffma_tflops)
+                  device_count, empty_cache, probe_ffma_tflops, probe_dfma_tflops)
 from . import synth, analysis
 
 __all__ = [
@@ -16,5 +16,5 @@ __all__ = [
     "SolverConfig", "SolveReport", "EigenBasis", "Solver", "BasisConvolver",
     "icnnm_solve", "icnnm_solve_batch", "cnnm_solve", "learn_ensemble_basis", "conv_adjoint", "prox_l21", "conv_gram",
     "objective_icnnm", "symeig", "sharded_solve", "sharded_solve_local", "sharded_rows", "shard_plan", "dist_unique_id",
-    "device_count", "empty_cache", "probe_ffma_tflops", "synth", "analysis",
+    "device_count", "empty_cache", "probe_ffma_tflops", "probe_dfma_tflops", "synth", "analysis",
 ]

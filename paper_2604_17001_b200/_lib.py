@@ -142,6 +142,7 @@ SIGNATURES = {
                                             C.POINTER(SolveReportC)]),
     "icnnm_shard_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int64, C.c_int, _lp, _lp]),
     "icnnm_probe_ffma_tflops": (C.c_int, [C.c_int, _dp]),
+    "icnnm_probe_dfma_tflops": (C.c_int, [C.c_int, _dp]),
     "icnnm_io_last_error": (C.c_char_p, []),
     "icnnm_write_tnsr": (C.c_int, [C.c_char_p, C.c_int, _lp, _dp]),
     "icnnm_read_tnsr": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), _lp, _dp]),

@@ -35,7 +35,7 @@ import numpy as np
 from ._lib import (SolveReportC, SolverConfigC, check, dptr, lib, lptr,
                    InvalidArgument)
 
-ENGINES = {"ffma": 0, "tf32x3": 1, "f16x3": 2}
+ENGINES = {"ffma": 0, "tf32x3": 1, "f16x3": 2, "f64": 3, "auto": 4}
 
 
 @dataclasses.dataclass
@@ -50,7 +50,7 @@ class SolverConfig:
     tol_change: float = 1e-8
     rank_tol: float = 1e-8
     init_fill: str = "zero"
-    engine: str = "f16x3"
+    engine: str = "auto"        # include/icnnm_b200.h ICNNM_ENGINE_AUTO
     exact_residual: bool = False
 
     def to_c(self) -> SolverConfigC:
@@ -537,4 +537,10 @@ def empty_cache() -> None:
 def probe_ffma_tflops(device: int = 0) -> float:
     out = C.c_double()
     check(lib().icnnm_probe_ffma_tflops(device, C.byref(out)))
+    return out.value
+
+
+def probe_dfma_tflops(device: int = 0) -> float:
+    out = C.c_double()
+    check(lib().icnnm_probe_dfma_tflops(device, C.byref(out)))
     return out.value

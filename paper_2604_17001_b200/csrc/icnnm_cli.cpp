@@ -186,6 +186,8 @@ int run(int argc, char** argv) {
     if (engine == "ffma") cfg.engine = ICNNM_ENGINE_FFMA;
     else if (engine == "tf32x3") cfg.engine = ICNNM_ENGINE_TF32X3;
     else if (engine == "f16x3") cfg.engine = ICNNM_ENGINE_F16X3;
+    else if (engine == "f64") cfg.engine = ICNNM_ENGINE_F64;
+    else if (engine == "auto") cfg.engine = ICNNM_ENGINE_AUTO;
     else if (!engine.empty()) throw Fail("unknown engine: " + engine);
     if (exact) cfg.exact_residual = 1;
     std::vector<double> L(M.v.size()), obj(cfg.max_iters), res(cfg.max_iters), lc(cfg.max_iters);

@@ -170,6 +170,91 @@ __global__ void cnnm_shrink(int k, const double* __restrict__ V, const double* _
     Vf[static_cast<size_t>(c) * k + r] = V[static_cast<size_t>(c) * k + r] * f;
 }
 
+// ---------------------------------------------------------------------------
+// FP64 engine of icnnm_solve (ICNNM_ENGINE_F64): the literal loop
+// (solver.cpp:107-139) with the three m x k matrices Wa/AKL, Z, Y in fp64 and
+// the two contractions as cuBLAS DGEMMs.  Not the hot path: it exists so that
+// tolerances below the fp32 engines' resolution (the reference's defaults
+// tol_primal = 1e-7, tol_change = 1e-8) stop the loop where the reference does.
+// ---------------------------------------------------------------------------
+// pm = M mask; L = pm (+ (1 - mask) mean)                      (solver.cpp:80-86)
+__global__ void __launch_bounds__(256)
+f64_init(int64_t m, const double* __restrict__ M, const double* __restrict__ mask, int mean_fill,
+         double mean, double* __restrict__ pm, double* __restrict__ L) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double mk = mask[i], p = M[i] * mk;
+    pm[i] = p;
+    L[i] = mean_fill ? p + (1.0 - mk) * mean : p;
+  }
+}
+
+// out = Y + theta Z                                             (solver.cpp:110 operand)
+__global__ void __launch_bounds__(256)
+f64_ypz(int64_t n, const double* __restrict__ Y, const double* __restrict__ Z, double theta,
+        double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = Y[i] + theta * Z[i];
+}
+
+// adj[i] = sum_s WK[(i + s) mod dims, s]                        (conv_op.cpp:57-77)
+// L[i]  <- (adj/k + lambda pm[i]) / (lambda mask[i] + theta)    (solver.cpp:112-116)
+// part[blockIdx.x * 3 + {0,1,2}] = sum (L_new - L)^2, sum L^2, sum (mask L_new - pm)^2
+__global__ void __launch_bounds__(256)
+f64_update(CGeo g, const double* __restrict__ WK, double theta, double lambda,
+           const double* __restrict__ pm, const double* __restrict__ mask,
+           double* __restrict__ L, double* __restrict__ part) {
+  double acc[3] = {0.0, 0.0, 0.0};
+  const double inv_k = 1.0 / static_cast<double>(g.k);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < g.m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double adj = 0.0;
+    for (int s = 0; s < g.k; ++s) {
+      int sh, sw, st;
+      tap_of(g, s, sh, sw, st);
+      adj += WK[static_cast<size_t>(g.m) * s + shifted(g, i, sh, sw, st, +1)];
+    }
+    const double mk = mask[i], p = pm[i];
+    const double lnew = (adj * inv_k + lambda * p) / (lambda * mk + theta);
+    const double lold = L[i];
+    const double d = lnew - lold, f = lnew * mk - p;
+    acc[0] += d * d;
+    acc[1] += lold * lold;
+    acc[2] += f * f;
+    L[i] = lnew;
+  }
+  block_sum<3>(acc, part + blockIdx.x * 3);
+}
+
+// gap = Z - AKL; Y += theta gap; Wa = AKL - Y/theta_next (in place of AKL)
+// (solver.cpp:123-126, :108); per-block column partials of gap^2 and Z^2
+__global__ void __launch_bounds__(256)
+f64_dual(int64_t m, int k, const double* __restrict__ Z, double* __restrict__ Y, double theta,
+         double inv_theta_next, double* __restrict__ Wa, double* __restrict__ part_gap,
+         double* __restrict__ part_zn) {
+  const int s = blockIdx.y;
+  const size_t col = static_cast<size_t>(m) * s;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double akl = Wa[col + i];
+    const double z = Z[col + i];
+    const double gap = z - akl;
+    const double y = Y[col + i] + theta * gap;
+    Y[col + i] = y;
+    Wa[col + i] = akl - y * inv_theta_next;
+    acc[0] += gap * gap;
+    acc[1] += z * z;
+  }
+  double out[2];
+  block_sum<2>(acc, out);
+  if (threadIdx.x == 0) {
+    part_gap[static_cast<size_t>(blockIdx.x) * k + s] = out[0];
+    part_zn[static_cast<size_t>(blockIdx.x) * k + s] = out[1];
+  }
+}
+
 }  // namespace icnnm_dev
 
 namespace icnnm_host {
@@ -336,6 +421,119 @@ void cnnm_solve_impl(const Problem& p, const double* M, const double* mask,
   rep->loop_seconds = std::chrono::duration<double>(t_end - t_loop).count();
   rep->device_seconds = rep->loop_seconds;
   rep->wall_time_seconds = std::chrono::duration<double>(t_end - t_start).count();
+}
+
+// FP64 engine (see the kernels above).  dM / dmask: the staged problem on the
+// device (validated at upload); dL receives the iterate.  The theta schedule
+// and the stopping test are the reference's (solver.cpp:88-91, :126, :136-139),
+// evaluated on the host once per iteration (one small D2H, off the hot path).
+void icnnm_f64_loop(const Problem& p, const double* dM, const double* dmask,
+                    const double* K_colmajor, const icnnm_solver_config& cfg, double pm_absmax,
+                    double pm_norm2, double pm_sum, int64_t observed, double* dL,
+                    std::vector<icnnm_dev::IterStats>& stats, int* iterations, int* converged,
+                    double* loop_ms) {
+  const int64_t m = p.m;
+  const int k = p.k;
+  const double kd = static_cast<double>(k);
+  double theta = cfg.has_theta0 ? cfg.theta0 : 1e-2 * pm_absmax * kd;
+  if (theta <= 0) theta = 1e-2;
+  theta = std::min(theta, cfg.theta_max);
+  double res_scale = std::sqrt(kd) * std::sqrt(pm_norm2);
+  if (res_scale == 0) res_scale = 1.0;
+  const double mean = pm_sum / static_cast<double>(std::max<int64_t>(observed, 1));
+
+  CnnmHandles hd;
+  const size_t mk = static_cast<size_t>(m) * k;
+  DBuf<double> dpm(m), dK(static_cast<size_t>(k) * k), Y(mk), Wa(mk), Z(mk), TMP(mk), n2(k);
+  icnnm_dev::CGeo g{static_cast<int>(p.dims[0]), static_cast<int>(p.dims[1]),
+                    static_cast<int>(p.dims[2]), static_cast<int>(p.kd[0]),
+                    static_cast<int>(p.kd[1]), static_cast<int>(p.kd[2]), m, k};
+  const int gx_up = static_cast<int>(std::min<int64_t>((m + 255) / 256, 592));
+  const int gx_col = static_cast<int>(std::min<int64_t>((m + 255) / 256, 64));
+  const int gx_el = grid_for(static_cast<int64_t>(mk), 256);
+  DBuf<double> part_up(static_cast<size_t>(gx_up) * 3), part_gap(static_cast<size_t>(gx_col) * k),
+      part_zn(static_cast<size_t>(gx_col) * k), red(2 * static_cast<size_t>(k));
+  std::vector<double> hup(static_cast<size_t>(gx_up) * 3), hred(2 * static_cast<size_t>(k));
+  CK(cudaMemcpyAsync(dK.p, K_colmajor, dK.bytes(), cudaMemcpyHostToDevice, hd.s));
+  CK(cudaMemsetAsync(Y.p, 0, Y.bytes(), hd.s));
+  icnnm_dev::f64_init<<<grid_for(m, 256), 256, 0, hd.s>>>(m, dM, dmask,
+                                                          cfg.init_fill == ICNNM_INIT_MEAN, mean,
+                                                          dpm.p, dL);
+  CKL();
+  const double one = 1.0, zero = 0.0;
+  const int mi = static_cast<int>(m);
+  // AKL = A(L) K: im2col (never kept between iterations) + DGEMM; K(s, j) = K_colmajor[j k + s]
+  auto forward = [&]() {
+    icnnm_dev::cnnm_prep<<<dim3(gx_col, k), 256, 0, hd.s>>>(g, dL, nullptr, 0.0, TMP.p);
+    CKL();
+    CKB(cublasDgemm(hd.b, CUBLAS_OP_N, CUBLAS_OP_N, mi, k, k, &one, TMP.p, mi, dK.p, k, &zero,
+                    Wa.p, mi));
+  };
+  forward();  // Y = 0: Wa = AKL
+  stats.assign(static_cast<size_t>(std::max(cfg.max_iters, 1)), icnnm_dev::IterStats{});
+  *iterations = 0;
+  *converged = 0;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, hd.s));
+  for (int it = 0; it < cfg.max_iters; ++it) {
+    const double tau = 1.0 / theta;
+    // Z = prox_l21(Wa, 1/theta)                                 (solver.cpp:108, :42-50)
+    CK(cudaMemsetAsync(n2.p, 0, n2.bytes(), hd.s));
+    icnnm_dev::icnnm_colnorm2<<<k, 256, 0, hd.s>>>(m, k, Wa.p, n2.p);
+    icnnm_dev::icnnm_colscale<<<gx_el, 256, 0, hd.s>>>(m, k, Wa.p, n2.p, tau, Z.p);
+    // WK = (Y + theta Z) K^T -> the Wa buffer (Wa is rebuilt below)   (:110)
+    icnnm_dev::f64_ypz<<<gx_el, 256, 0, hd.s>>>(static_cast<int64_t>(mk), Y.p, Z.p, theta, TMP.p);
+    CKL();
+    CKB(cublasDgemm(hd.b, CUBLAS_OP_N, CUBLAS_OP_T, mi, k, k, &one, TMP.p, mi, dK.p, k, &zero,
+                    Wa.p, mi));
+    // adjoint gather + L update                                  (:111-120)
+    icnnm_dev::f64_update<<<gx_up, 256, 0, hd.s>>>(g, Wa.p, theta, cfg.lambda, dpm.p, dmask, dL,
+                                                    part_up.p);
+    CKL();
+    forward();                                                   // :121
+    const double theta_next = std::min(theta * cfg.theta_growth, cfg.theta_max);
+    icnnm_dev::f64_dual<<<dim3(gx_col, k), 256, 0, hd.s>>>(m, k, Z.p, Y.p, theta,
+                                                           1.0 / theta_next, Wa.p, part_gap.p,
+                                                           part_zn.p);
+    CKL();
+    CK(cudaMemsetAsync(red.p, 0, red.bytes(), hd.s));
+    icnnm_dev::icnnm_gram_reduce<<<grid_for(k, 256), 256, 0, hd.s>>>(k, gx_col, part_gap.p,
+                                                                     red.p);
+    icnnm_dev::icnnm_gram_reduce<<<grid_for(k, 256), 256, 0, hd.s>>>(k, gx_col, part_zn.p,
+                                                                     red.p + k);
+    CKL();
+    CK(cudaMemcpyAsync(hup.data(), part_up.p, part_up.bytes(), cudaMemcpyDeviceToHost, hd.s));
+    CK(cudaMemcpyAsync(hred.data(), red.p, red.bytes(), cudaMemcpyDeviceToHost, hd.s));
+    CK(cudaStreamSynchronize(hd.s));
+    icnnm_dev::IterStats& q = stats[it];
+    for (int b = 0; b < gx_up; ++b) {
+      q.dl2 += hup[3 * b];
+      q.l2o += hup[3 * b + 1];
+      q.fit += hup[3 * b + 2];
+    }
+    for (int c = 0; c < k; ++c) {
+      q.gap2 += hred[c];
+      q.z2 += hred[k + c];
+      q.l21 += std::sqrt(hred[k + c]);
+    }
+    const double l_change = std::sqrt(q.dl2) / std::max(std::sqrt(q.l2o), 1e-300);
+    const double residual = std::sqrt(q.gap2) / res_scale;
+    theta = theta_next;
+    *iterations = it + 1;
+    if (residual < cfg.tol_primal || l_change < cfg.tol_change) {  // :136-139
+      *converged = 1;
+      break;
+    }
+  }
+  CK(cudaEventRecord(e1, hd.s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *loop_ms = ms;
 }
 
 }  // namespace icnnm_host

@@ -599,6 +599,8 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   a.bunscale = t.bunscale;
   static const int skip_env = env_knob("ICNNM_TC_SKIP", 0);  // timing experiments only (results invalid)
   a.skip = skip_env;
+  static const int warr_env = env_knob("ICNNM_TC_WARR", 1);
+  a.warr = warr_env;
   static const int bsplit_env = env_knob("ICNNM_TC_BSPLIT", 0);
   a.bsplit = bsplit_env;
   static const int bpair_env = env_knob("ICNNM_TC_BPAIR", 0);
@@ -679,14 +681,13 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   // brick's work is split over nsplit CTA roles by N-tiles when the whole
   // basis does not fit (forward: each role its own columns of W; adjoint: its
   // own taps, partial output bricks summed by the flush).
-  // Measured at config 4 (k = 245, 2 N-tiles; profiles/README_r2.md): the
-  // adjoint gains (0.408 -> 0.383 ms with the deterministic gather: its MMA
-  // waited on B 45% of the time), the forward loses (0.354 -> 0.387 ms: its
-  // per-brick halo preparation, now done once per tile, outlasts a tile's
-  // MMAs), so resident B is the adjoint's default only.  ICNNM_TC_BRES=0|1
-  // (experiments build) forces it off / on for both kernels.
+  // Measured at config 4 (k = 245, 2 N-tiles; profiles/r2/README.md): the
+  // adjoint gains 8% (0.406 -> 0.375 ms: its MMA waited on B 45% of the
+  // time) and, with the halo-preparation warps taking the per-brick halo
+  // work off the builders, the forward 10% (0.347 -> 0.312 ms).
+  // ICNNM_TC_BRES=0|1 (experiments build) forces it off / on.
   static const int bres_env = env_knob("ICNNM_TC_BRES", -1);
-  const bool bres_on = bres_env < 0 ? !fwd : bres_env != 0;
+  const bool bres_on = bres_env != 0;
   // forward: halo buffers for the prep warps' software pipeline (4: they run
   // two bricks ahead of the builders), fewer when shared memory is short
   static const int nhb_env = env_knob("ICNNM_TC_NHB", icnnm_dev::tc::NHB_MAX);
@@ -784,7 +785,7 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
                       float* W, const float* Bpk, const float* cvec, float* adj, double* norm2,
                       const IterState* st, cudaStream_t stream,
                       unsigned long long* dbg = nullptr, float amax = 0.f, bool pdl = false,
-                      float* adj_scr = nullptr, double* npart = nullptr) {
+                      unsigned long long* adjq = nullptr, double* npart = nullptr) {
   TcConfig cfg = tc_config(gtc, t, fwd, Bpk != nullptr);
   icnnm_dev::tc::TcArgs& a = cfg.a;
   a.amax = amax;
@@ -798,7 +799,7 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   a.norm2 = norm2;
   a.st = st;
   a.mode = mode;
-  a.adj_scr = adj_scr;
+  a.adjq = adjq;
   a.npart = npart;
   if (a.tma_pair) {
     a.tmB[0] = pair_b_map(Bpk, t, t.wbase / 2);
@@ -900,8 +901,27 @@ void validate_cfg(const icnnm_solver_config* c) {
     invalid("SolverConfig: tolerances must be > 0");
   if (c->init_fill != ICNNM_INIT_ZERO && c->init_fill != ICNNM_INIT_MEAN)
     invalid("SolverConfig: init_fill must be 'zero' or 'mean'");
-  if (c->engine != ICNNM_ENGINE_FFMA && !is_tc(c->engine))
+  if (c->engine != ICNNM_ENGINE_FFMA && !is_tc(c->engine) && c->engine != ICNNM_ENGINE_F64 &&
+      c->engine != ICNNM_ENGINE_AUTO)
     invalid("SolverConfig: unknown engine");
+}
+
+// ICNNM_ENGINE_AUTO (include/icnnm_b200.h): the fp32 engines cannot resolve
+// l_change below ~1e-7 (Delta carries the GEMMs' rounding) nor the primal
+// residual below ~1e-4 (exact_residual) / ~3e-3 (identity), so a finite
+// tolerance under those floors runs the fp64 engine; tolerances <= 1e-200
+// count as disabled (fixed iteration counts).
+icnnm_solver_config resolve_engine(const icnnm_solver_config& in) {
+  icnnm_solver_config c = in;
+  if (c.engine != ICNNM_ENGINE_AUTO) return c;
+  const bool p_on = c.tol_primal > 1e-200, c_on = c.tol_change > 1e-200;
+  if ((p_on && c.tol_primal < 1e-4) || (c_on && c.tol_change < 1e-6)) {
+    c.engine = ICNNM_ENGINE_F64;
+  } else {
+    c.engine = ICNNM_ENGINE_F16X3;
+    if (p_on) c.exact_residual = 1;
+  }
+  return c;
 }
 
 
@@ -916,9 +936,7 @@ struct Slab {
   int64_t halo_elems = 0;       // (kh-1) * W * T (slab mode)
   DBuf<float> Lt, adj, pm, mask, W;
   DBuf<float> Lr;                 // exact-residual mode: L_{t+1} (fp32, with halo rows)
-  DBuf<float> adj_scr;            // deterministic adjoint: per-(brick, role) output slots
-  DBuf<int> gtab;                 // deterministic adjoint: gather table (icnnm_adj_gather)
-  int adj_nsp = 1, adj_nobp = 0;  // roles per brick / padded slot size of the adjoint launch
+  DBuf<unsigned long long> adjq;  // deterministic adjoint: 64-bit fixed-point output (adj's layout)
   DBuf<double> L, V;
 };
 
@@ -1254,10 +1272,10 @@ void launch_adj(Solver& S, Slab& s) {
     launch_tc_kernel(s.gtc, f16 ? S.tp16 : S.tp, false, 1, s.Lt.p, s.W.p,
                      f16 ? S.BpkA16.p : S.BpkA.p, S.cvec.p, s.adj.p, S.red.p, S.st.p, S.stream,
                      S.tc_counters ? S.dbg.p + icnnm_dev::tc::DBG_SLOTS : nullptr, 0.f,
-                     use_pdl(S), S.det ? s.adj_scr.p : nullptr);
+                     use_pdl(S), S.det ? s.adjq.p : nullptr);
     ++S.launches;
     if (S.det) {
-      // fixed-order sum of the output slots covering each voxel -> adj
+      // fixed-point sums -> adj (fp32), accumulator cleared for the next launch
       const int64_t n = static_cast<int64_t>(s.gtc.Hsrc) * s.gtc.W * s.gtc.T;
       cudaLaunchConfig_t lc{};
       cudaLaunchAttribute at{};
@@ -1268,9 +1286,9 @@ void launch_adj(Solver& S, Slab& s) {
       lc.stream = S.stream;
       lc.attrs = &at;
       lc.numAttrs = use_pdl(S) ? 1 : 0;
-      CK(cudaLaunchKernelEx(&lc, icnnm_dev::icnnm_adj_gather, s.gtc, s.adj_nsp, s.adj_nobp,
-                            static_cast<const int*>(s.gtab.p),
-                            static_cast<const float*>(s.adj_scr.p), s.adj.p));
+      CK(cudaLaunchKernelEx(&lc, icnnm_dev::icnnm_adj_q2f, n,
+                            static_cast<const icnnm_dev::IterState*>(S.st.p), S.p.k, s.adjq.p,
+                            s.adj.p));
       ++S.launches;
     }
     return;
@@ -1301,45 +1319,11 @@ icnnm_dev::Partials partials(const Solver& S) {
   return P;
 }
 
-// Gather table of icnnm_adj_gather: for every buffer row (slab: own rows after
-// hoff halo rows), W and T coordinate, the (brick index, halo offset) pairs of
-// the output slots covering it, in ascending offset order (the kernel's fixed
-// summation order) -- the inverse of the tcgen05 adjoint's col2im map.
-std::vector<int> gather_table(const Geo& g) {
-  using icnnm_dev::GATHER_PAIRS;
-  using icnnm_dev::GATHER_S;
-  std::vector<int> tab(static_cast<size_t>(g.Hsrc + g.W + g.T) * GATHER_S, 0);
-  auto axis = [&](int row, int x, int kx, int bx, int X, bool periodic) {
-    int* e = tab.data() + static_cast<size_t>(row) * GATHER_S;
-    int n = 0;
-    for (int o = 0; o < bx + kx - 1; ++o) {
-      int x0 = x + kx - 1 - o;
-      if (periodic) {
-        x0 %= X;
-        if (x0 < 0) x0 += X;
-      } else if (x0 < 0 || x0 >= X) {
-        continue;
-      }
-      if (x0 % bx != 0) continue;
-      if (n == GATHER_PAIRS) {
-        n = -1;
-        break;
-      }
-      e[1 + 2 * n] = x0 / bx;
-      e[2 + 2 * n] = o;
-      ++n;
-    }
-    e[0] = n;
-  };
-  for (int hb = 0; hb < g.Hsrc; ++hb) axis(hb, hb - g.hoff, g.kh, g.bh, g.H, g.wrapH != 0);
-  for (int w = 0; w < g.W; ++w) axis(g.Hsrc + w, w, g.kw, g.bw, g.W, true);
-  for (int t = 0; t < g.T; ++t) axis(g.Hsrc + g.W + t, t, g.kt, g.bt, g.T, true);
-  return tab;
-}
-
 // Deterministic buffers of a tcgen05 run, allocated before any graph capture.
 void prepare_det(Solver& S) {
-  S.det = is_tc(S.engine);
+  // ICNNM_DET=0 (experiments build): fp32 / fp64 atomics instead (A/B)
+  static const int det_env = env_knob("ICNNM_DET", 1);
+  S.det = is_tc(S.engine) && det_env != 0;
   if (!S.det) return;
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -1360,18 +1344,12 @@ void prepare_det(Solver& S) {
   zero(S.npart, nrow * kpe);
   zero(S.gpart, nrow);
   zero(S.upart, static_cast<size_t>(ns) * S.upd_rows * 8);
+  (void)t;
   for (auto& s : S.slabs) {
-    const TcConfig c = tc_config(s.gtc, t, false, true);
-    s.adj_nsp = c.a.nsplit;
-    const int nob = s.gtc.HH * s.gtc.HW * s.gtc.HT;
-    s.adj_nobp = (nob + 3) / 4 * 4;
-    const size_t need = static_cast<size_t>(n_bricks(s.gtc)) * s.adj_nsp * s.adj_nobp;
-    if (s.adj_scr.n != need) s.adj_scr.alloc(need);
-    if (!s.gtab.p) {
-      const std::vector<int> tab = gather_table(s.gtc);
-      s.gtab.alloc(tab.size());
-      CK(cudaMemcpyAsync(s.gtab.p, tab.data(), s.gtab.bytes(), cudaMemcpyHostToDevice, S.stream));
-      CK(cudaStreamSynchronize(S.stream));
+    const size_t need = static_cast<size_t>(s.gtc.Hsrc) * s.gtc.W * s.gtc.T;
+    if (s.adjq.n != need) {
+      s.adjq.alloc(need);
+      CK(cudaMemsetAsync(s.adjq.p, 0, s.adjq.bytes(), S.stream));
     }
   }
 }
@@ -1427,8 +1405,12 @@ struct RunResult {
 };
 
 // One full solve of the staged problem (device-resident hot path).
-RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
+RunResult solver_run_f64(Solver& S, const icnnm_solver_config& cfg);
+
+RunResult solver_run(Solver& S, const icnnm_solver_config& cfg_in) {
   if (!S.uploaded) invalid("solve: no problem uploaded");
+  const icnnm_solver_config cfg = resolve_engine(cfg_in);
+  if (cfg.engine == ICNNM_ENGINE_F64) return solver_run_f64(S, cfg);
   const Problem& p = S.p;
   S.engine = cfg.engine;
   ensure_engine_basis(S, S.engine);
@@ -1529,6 +1511,7 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
       ++S.launches;
       CK(cudaMemsetAsync(s.W.p, 0, s.W.bytes(), S.stream));
       CK(cudaMemsetAsync(s.adj.p, 0, s.adj.bytes(), S.stream));
+      if (s.adjq.p) CK(cudaMemsetAsync(s.adjq.p, 0, s.adjq.bytes(), S.stream));
     }
     exchange_lt(S);
     for (auto& s : S.slabs) launch_fwd(S, s, 0);
@@ -1683,6 +1666,29 @@ RunResult solver_run(Solver& S, const icnnm_solver_config& cfg) {
 }
 
 // Report of solver.cpp:128-139 from the device statistics.
+// ICNNM_ENGINE_F64: the literal fp64 loop (icnnm_cnnm.cu) on the staged problem.
+RunResult solver_run_f64(Solver& S, const icnnm_solver_config& cfg) {
+  if (S.sharded) invalid("solve: the fp64 engine does not run H-sharded solves");
+  RunResult R;
+  S.engine = ICNNM_ENGINE_F64;
+  S.exact_res = true;  // the report's residual is the exact gap norm
+  S.launches = 0;
+  CK(cudaStreamSynchronize(S.stream));  // the staged problem is on the device
+  int iters = 0, conv = 0;
+  double ms = 0;
+  Slab& s = S.slabs[0];
+  icnnm_f64_loop(S.p, S.Mstage.p, S.maskstage.p, S.K.data(), cfg, S.pm_absmax, S.pm_norm2,
+                 S.pm_sum, S.observed, s.L.p, R.stats, &iters, &conv, &ms);
+  R.st.next_it = iters;
+  R.st.it = iters - 1;
+  R.st.converged = conv;
+  R.st.active = 0;
+  R.st.max_iters = cfg.max_iters;
+  R.loop_ms = ms;
+  R.run_ms = ms;
+  return R;
+}
+
 void fill_report(const Solver& S, const icnnm_solver_config& cfg, const RunResult& R,
                  icnnm_solve_report* rep, double wall_s) {
   if (!rep) return;
@@ -1752,7 +1758,7 @@ void icnnm_default_config(icnnm_solver_config* c) {
   c->tol_change = 1e-8;
   c->rank_tol = 1e-8;
   c->init_fill = ICNNM_INIT_ZERO;
-  c->engine = ICNNM_ENGINE_F16X3;
+  c->engine = ICNNM_ENGINE_AUTO;
   c->exact_residual = 0;
 }
 
@@ -2147,7 +2153,46 @@ void gram_lags_accumulate(const Problem& p, const double* dX, double* dR, cudaSt
             T = static_cast<int>(p.dims[2]);
   const int kh = static_cast<int>(p.kd[0]), kw = static_cast<int>(p.kd[1]),
             kt = static_cast<int>(p.kd[2]);
-  const int nl = (2 * kw - 1) * (2 * kt - 1);
+  const int nlw = 2 * kw - 1, nlt = 2 * kt - 1;
+  const int nl = nlw * nlt;
+  void* rt = (nlw <= 256) ? icnnm_dev::gram_lags_rt_ptr(kt) : nullptr;
+  if (rt != nullptr) {
+    // register-tiled kernel: thread (dw, row), rows = bh x bw voxels of bt frames
+    const int rsmax = 256 / nlw;
+    int bw = std::min(W, rsmax);
+    int bh = std::min(H, std::max(1, rsmax / bw));
+    int bt = std::min(T, 64);
+    const int btp = (bt + 3) / 4 * 4;
+    const int RS = bh * bw;
+    const size_t tile = static_cast<size_t>(RS) * (btp + 2) +
+                        static_cast<size_t>(bh) * (bw + 2 * (kw - 1)) * ((btp + 2 * (kt - 1)) | 1);
+    const size_t smem = std::max(tile, static_cast<size_t>(RS) * nl) * sizeof(double);
+    check_smem(smem);
+    static std::mutex mu;
+    static std::map<void*, size_t> attr;  // opt-in dynamic shared memory per instantiation
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      size_t& cur = attr[rt];
+      if (smem > cur) {
+        CK(cudaFuncSetAttribute(rt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        cur = smem;
+      }
+    }
+    const int nb = ((H + bh - 1) / bh) * ((W + bw - 1) / bw) * ((T + bt - 1) / bt);
+    dim3 grid(kh, std::max(1, std::min(nb, 592 / kh + 1)));
+    DBuf<double> part(static_cast<size_t>(grid.y) * kh * nl);
+    int aH = H, aW = W, aT = T, akw = kw, abh = bh, abw = bw, abt = bt;
+    const double* aX = dX;
+    double* aR = part.p;
+    void* args[] = {&aH, &aW, &aT, &akw, &abh, &abw, &abt, &aX, &aR};
+    CK(cudaLaunchKernel(rt, grid, dim3(256), args, smem, s));
+    icnnm_dev::icnnm_gram_reduce_sym<<<grid_for(static_cast<int64_t>(kh) * nl, 256), 256, 0, s>>>(
+        kh, nl, static_cast<int>(grid.y), part.p, dR);
+    CKL();
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
   if (nl > 256 * icnnm_dev::GRAM_LPT_HOST)
     invalid("icnnm_b200: kernel (kw, kt) too large for the Gram kernel");
   int bt = T >= 16 ? 16 : (T >= 8 ? 8 : T);
@@ -2469,6 +2514,35 @@ int icnnm_probe_ffma_tflops(int device, double* out) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     const double flops = 2.0 * 16.0 * iters * static_cast<double>(blocks) * threads;
+    *out = flops / (ms * 1e-3) / 1e12;
+  });
+}
+
+
+/* FP64 DFMA throughput in TFLOP/s (the Gram kernel's roofline denominator). */
+int icnnm_probe_dfma_tflops(int device, double* out) {
+  return guard([&] {
+    if (!out) invalid("null argument");
+    DeviceScope ds(device);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    DBuf<double> o(1);
+    const int iters = 1 << 14;
+    const int blocks = sms * 8, threads = 256;
+    icnnm_dev::icnnm_dfma_probe<<<blocks, threads>>>(o.p, 256, 1.0);
+    CKL();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a));
+    icnnm_dev::icnnm_dfma_probe<<<blocks, threads>>>(o.p, iters, 1.0);
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads;
     *out = flops / (ms * 1e-3) / 1e12;
   });
 }

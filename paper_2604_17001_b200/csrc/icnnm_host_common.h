@@ -171,6 +171,12 @@ inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 16) {
 }
 void gram_lags_accumulate(const Problem& p, const double* dX, double* dR, cudaStream_t s);
 void gram_from_lags(const Problem& p, const std::vector<double>& R, double* G);
+// ICNNM_ENGINE_F64: the literal fp64 loop on the GPU (icnnm_cnnm.cu)
+void icnnm_f64_loop(const Problem& p, const double* dM, const double* dmask,
+                    const double* K_colmajor, const icnnm_solver_config& cfg, double pm_absmax,
+                    double pm_norm2, double pm_sum, int64_t observed, double* dL,
+                    std::vector<icnnm_dev::IterStats>& stats, int* iterations, int* converged,
+                    double* loop_ms);
 
 }  // namespace icnnm_host
 

@@ -219,6 +219,8 @@ int icnnm_config_from_json(const char* text, icnnm_solver_config* cfg) {
       if (sval == "tf32x3") cfg->engine = ICNNM_ENGINE_TF32X3;
       else if (sval == "f16x3") cfg->engine = ICNNM_ENGINE_F16X3;
       else if (sval == "ffma") cfg->engine = ICNNM_ENGINE_FFMA;
+      else if (sval == "f64") cfg->engine = ICNNM_ENGINE_F64;
+      else if (sval == "auto") cfg->engine = ICNNM_ENGINE_AUTO;
       else return io_fail("SolverConfig: unknown engine", ICNNM_INVALID_ARGUMENT);
     } else if (key == "exact_residual") {
       cfg->exact_residual = is_bool ? (bval ? 1 : 0) : (num != 0);

@@ -432,37 +432,71 @@ __device__ double block_sum_fixed(double v) {
   return out;
 }
 
+// Fixed-order sums of up to NV values per thread over the block: shuffle tree
+// within each warp, then thread 0 adds the warps in order.
+template <int NV>
+__device__ void block_sum_fixed_n(double (&v)[NV], double* out) {
+  __shared__ double sh[NV][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  __syncthreads();  // sh reuse across calls
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sh[q][warp] = v[q];
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += sh[threadIdx.x][w];
+    out[threadIdx.x] = t;
+  }
+}
+
 __device__ void fold_partials(const Partials& P, int kp, double* red) {
   if (P.npart != nullptr) {
-    // four independent partial sums per column (rows r = 4i + q), combined in
-    // a fixed order: the dependent-add chain is a quarter as long
-    for (int j = threadIdx.x; j < kp; j += blockDim.x) {
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-      int r = 0;
-      for (; r + 4 <= P.nrows; r += 4) {
-        t0 += P.npart[static_cast<size_t>(r) * kp + j];
-        t1 += P.npart[static_cast<size_t>(r + 1) * kp + j];
-        t2 += P.npart[static_cast<size_t>(r + 2) * kp + j];
-        t3 += P.npart[static_cast<size_t>(r + 3) * kp + j];
+    // column j: FOLD_Q threads, thread q sums rows r = q, q + FOLD_Q, ... in
+    // order (loads issued in batches of 8 ahead of the adds), then the FOLD_Q
+    // partials are added in order -- a fixed summation tree whatever the launch
+    constexpr int FOLD_Q = 4;
+    __shared__ double fq[FOLD_Q][256];
+    for (int j0 = 0; j0 < kp; j0 += 256) {
+      const int jl = threadIdx.x & 255, q = threadIdx.x >> 8;  // blockDim.x = 1024
+      const int j = j0 + jl;
+      double t = 0.0;
+      if (j < kp && q < FOLD_Q) {
+        const double* src = P.npart + j;
+        int r = q;
+        for (; r + 7 * FOLD_Q < P.nrows; r += 8 * FOLD_Q) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = src[static_cast<size_t>(r + u * FOLD_Q) * kp];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) t += v[u];
+        }
+        for (; r < P.nrows; r += FOLD_Q) t += src[static_cast<size_t>(r) * kp];
       }
-      for (; r < P.nrows; ++r) t0 += P.npart[static_cast<size_t>(r) * kp + j];
-      red[j] = (t0 + t1) + (t2 + t3);
+      __syncthreads();
+      if (q < FOLD_Q) fq[q][jl] = t;
+      __syncthreads();
+      if (q == 0 && j < kp) red[j] = (fq[0][jl] + fq[1][jl]) + (fq[2][jl] + fq[3][jl]);
     }
   }
   double* slot = red + kp;
   if (P.upart != nullptr) {
-    for (int q = 0; q < 5; ++q) {
-      double v = 0.0;
-      for (int r = threadIdx.x; r < P.urows; r += blockDim.x) v += P.upart[r * 8 + q];
-      v = block_sum_fixed(v);
-      if (threadIdx.x == 0) slot[q] = v;
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int r = threadIdx.x; r < P.urows; r += blockDim.x) {
+      const double* u = P.upart + static_cast<size_t>(r) * 8;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) v[q] += u[q];
     }
+    block_sum_fixed_n<5>(v, slot);
   }
   if (P.gpart != nullptr) {
-    double v = 0.0;
-    for (int r = threadIdx.x; r < P.grows; r += blockDim.x) v += P.gpart[r];
-    v = block_sum_fixed(v);
-    if (threadIdx.x == 0) slot[5] = v;
+    double v[1] = {0.0};
+    for (int r = threadIdx.x; r < P.grows; r += blockDim.x) v[0] += P.gpart[r];
+    block_sum_fixed_n<1>(v, slot + 5);
   }
   __syncthreads();
 }
@@ -474,78 +508,23 @@ __global__ void icnnm_fold(Partials P, int kp, double* red) {
   fold_partials(P, kp, red);
 }
 
-// Deterministic adjoint output: adj[i] = sum over the (brick, role) output
-// slots whose halo box covers i, in a fixed order (halo row aa, column bb,
-// time c, role).  A brick at (h0, w0, t0) writes slot element
-// ((aa*HW + bb)*HT + c) to voxel (h0-(kh-1)+aa, w0-(kw-1)+bb, t0-(kt-1)+c)
-// (periodic in W and T; in H periodic over the tensor or, in slab mode, the
-// buffer row hoff + h with kh-1 halo rows first) -- the col2im of the
-// tcgen05 adjoint (icnnm_tc.cu), conv_adjoint's map (conv_op.cpp:57-77).
-// The (brick, halo offset) pairs covering each coordinate come from a host
-// table (gather_table(), icnnm_host.cu): per axis and coordinate x, GATHER_S
-// ints = [n, q_0, off_0, q_1, off_1, ...] in ascending offset order, n = -1
-// when more than GATHER_PAIRS pairs exist (a tiny tensor wrapped several times
-// by the halo box: the generic path below).  Rows: Hsrc buffer rows, then W,
-// then T coordinates.
+// Deterministic adjoint output: the tcgen05 adjoint adds each brick's partial
+// sums into adjq as 64-bit fixed-point integers (scale 2^adjq_exp from the
+// iteration's st->adj_amax; integer adds commute exactly, so the result does
+// not depend on the order in which CTAs flush).  This converts the sums back
+// to fp32 adj and clears the accumulator for the next launch.
 __global__ void __launch_bounds__(256)
-icnnm_adj_gather(Geo g, int nsp, int nobp, const int* __restrict__ tab,
-                 const float* __restrict__ scr, float* __restrict__ adj) {
+icnnm_adj_q2f(int64_t n, const IterState* __restrict__ st, int k,
+              unsigned long long* __restrict__ adjq, float* __restrict__ adj) {
   pdl_wait();
   pdl_trigger();
-  const int64_t n = static_cast<int64_t>(g.Hsrc) * g.W * g.T;
+  if (!st->active) return;
+  const double inv = ldexp(1.0, -adjq_exp(st->adj_amax, k));
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int t = static_cast<int>(i % g.T);
-  const int64_t qq = i / g.T;
-  const int w = static_cast<int>(qq % g.W);
-  const int hb = static_cast<int>(qq / g.W);
-  const int* th = tab + static_cast<int64_t>(hb) * GATHER_S;
-  const int* tw = tab + static_cast<int64_t>(g.Hsrc + w) * GATHER_S;
-  const int* tt = tab + static_cast<int64_t>(g.Hsrc + g.W + t) * GATHER_S;
-  const int nh = th[0], nw = tw[0], nt = tt[0];
-  float acc = 0.f;
-  if (nh >= 0 && nw >= 0 && nt >= 0) {
-    // fixed order: h pairs, w pairs, t pairs (ascending halo offset), roles
-    for (int a = 0; a < nh; ++a) {
-      const int qh = th[1 + 2 * a], oh = th[2 + 2 * a];
-      for (int b2 = 0; b2 < nw; ++b2) {
-        const int64_t bhw = static_cast<int64_t>(qh) * g.nbw + tw[1 + 2 * b2];
-        const int ehw = (oh * g.HW + tw[2 + 2 * b2]) * g.HT;
-        for (int c = 0; c < nt; ++c) {
-          const int64_t b = bhw * g.nbt + tt[1 + 2 * c];
-          const float* sp = scr + b * nsp * nobp + ehw + tt[2 + 2 * c];
-          for (int r = 0; r < nsp; ++r) acc += sp[static_cast<int64_t>(r) * nobp];
-        }
-      }
-    }
-  } else {
-    // generic path (the halo box wraps a tiny tensor many times): same order
-    for (int aa = 0; aa < g.HH; ++aa) {
-      int h0 = hb - g.hoff + g.kh - 1 - aa;
-      if (g.wrapH) {
-        h0 %= g.H;
-        if (h0 < 0) h0 += g.H;
-      } else if (h0 < 0 || h0 >= g.H) {
-        continue;
-      }
-      if (h0 % g.bh != 0) continue;
-      for (int bb = 0; bb < g.HW; ++bb) {
-        int w0 = (w + g.kw - 1 - bb) % g.W;
-        if (w0 < 0) w0 += g.W;
-        if (w0 % g.bw != 0) continue;
-        const int64_t bhw = static_cast<int64_t>(h0 / g.bh) * g.nbw + w0 / g.bw;
-        for (int c = 0; c < g.HT; ++c) {
-          int t0 = (t + g.kt - 1 - c) % g.T;
-          if (t0 < 0) t0 += g.T;
-          if (t0 % g.bt != 0) continue;
-          const int64_t b = bhw * g.nbt + t0 / g.bt;
-          const int e = (aa * g.HW + bb) * g.HT + c;
-          for (int r = 0; r < nsp; ++r) acc += scr[(b * nsp + r) * nobp + e];
-        }
-      }
-    }
-  }
-  adj[i] = acc;
+  const long long q = static_cast<long long>(adjq[i]);
+  adjq[i] = 0ull;
+  adj[i] = static_cast<float>(static_cast<double>(q) * inv);
 }
 
 // ---------------------------------------------------------------------------
@@ -792,6 +771,154 @@ icnnm_gram_lags(int H, int W, int T, int kh, int kw, int kt, int bh, int bw, int
     if (l < nl)
       R[(static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * nl + l] = acc[p];
   }
+}
+
+// ---------------------------------------------------------------------------
+// (e) Gram lags, register-tiled (fp64), for kt <= GRAM_KT_MAX.
+// Only the lags with dh >= 0 are computed (grid.x = kh): R[-d] = R[d] for the
+// circular autocorrelation of a real tensor, mirrored by icnnm_gram_reduce_sym.
+// Brick = bh x bw x bt voxels (RS = bh bw "rows" of bt frames) with a halo of
+// +-(kw-1) columns and +-(kt-1) frames, rows shifted by -dh.  Thread (dw, rs)
+// computes all NLT = 2kt-1 frame lags of the 1-D correlation of own row rs
+// with halo row rs - dw: per 4 frames 4 own loads + 4 halo loads feed 4 NLT
+// DFMAs from a sliding register window (the lag-per-thread kernel above needs
+// two shared-memory loads per DFMA).  Per-thread sums are reduced over rs in a
+// fixed order at the end (deterministic, like the partial rows).
+// ---------------------------------------------------------------------------
+template <int KT>
+__global__ void __launch_bounds__(256, 2)
+icnnm_gram_lags_rt(int H, int W, int T, int kw, int bh, int bw, int bt,
+                   const double* __restrict__ X, double* __restrict__ R) {
+  constexpr int NLT = 2 * KT - 1;
+  constexpr int CW = 4;
+  extern __shared__ double gsm[];
+  const int dh = static_cast<int>(blockIdx.x);
+  const int nlw = 2 * kw - 1;
+  const int RS = bh * bw;
+  const int HWd = bw + 2 * (kw - 1);
+  const int btp = (bt + CW - 1) / CW * CW;
+  const int po = btp + 2;                 // own row pitch (rows of one warp: <= 3 distinct)
+  const int hl = btp + 2 * (KT - 1);      // halo row length
+  const int ph = hl | 1;                  // odd pitch: a half-warp's rows hit distinct banks
+  double* own = gsm;                      // RS * po
+  double* hal = gsm + RS * po;            // bh * HWd * ph
+  const int nbh = (H + bh - 1) / bh, nbw = (W + bw - 1) / bw, nbt = (T + bt - 1) / bt;
+  const int nb = nbh * nbw * nbt;
+  const int dwi = static_cast<int>(threadIdx.x) % nlw, rs = static_cast<int>(threadIdx.x) / nlw;
+  const bool act = rs < RS;
+  const int ra = act ? rs / bw : 0, rb = act ? rs % bw : 0;
+  const double* orow = own + (act ? rs : 0) * po;
+  const double* hrow = hal + (ra * HWd + rb - dwi + 2 * (kw - 1)) * ph;
+  double acc[NLT];
+#pragma unroll
+  for (int d = 0; d < NLT; ++d) acc[d] = 0.0;
+  for (int b = blockIdx.y; b < nb; b += gridDim.y) {
+    const int bt_i = b % nbt, bw_i = (b / nbt) % nbw, bh_i = b / (nbt * nbw);
+    const int h0 = bh_i * bh, w0 = bw_i * bw, t0 = bt_i * bt;
+    __syncthreads();
+    for (int e = threadIdx.x; e < RS * btp; e += blockDim.x) {
+      const int c = e % btp, r = e / btp;
+      const int h = h0 + r / bw, w = w0 + r % bw, t = t0 + c;
+      own[r * po + c] = (c < bt && h < H && w < W && t < T)
+                            ? X[(static_cast<size_t>(h) * W + w) * T + t] : 0.0;
+    }
+    for (int e = threadIdx.x; e < bh * HWd * hl; e += blockDim.x) {
+      const int c = e % hl, q = e / hl;     // q = a * HWd + j
+      const int h = wrapi(h0 + q / HWd - dh, H);
+      const int w = wrapi(w0 + q % HWd - (kw - 1), W);
+      const int t = wrapi(t0 + c - (KT - 1), T);
+      hal[q * ph + c] = X[(static_cast<size_t>(h) * W + w) * T + t];
+    }
+    __syncthreads();
+    if (act) {
+      double win[CW + NLT - 1];
+#pragma unroll
+      for (int u = 0; u < NLT - 1; ++u) win[u] = hrow[u];
+      for (int c0 = 0; c0 < btp; c0 += CW) {
+        double o[CW];
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+          win[NLT - 1 + i] = hrow[c0 + NLT - 1 + i];
+          o[i] = orow[c0 + i];
+        }
+        // lag index d = dt + (kt-1): own[c] pairs with halo column c + NLT-1-d
+#pragma unroll
+        for (int i = 0; i < CW; ++i)
+#pragma unroll
+          for (int d = 0; d < NLT; ++d) acc[d] = fma(o[i], win[i + NLT - 1 - d], acc[d]);
+#pragma unroll
+        for (int u = 0; u < NLT - 1; ++u) win[u] = win[u + CW];
+      }
+    }
+  }
+  // fixed-order reduction over rs: red[rs][dw][d] in shared memory
+  __syncthreads();
+  double* red = gsm;
+  if (act)
+#pragma unroll
+    for (int d = 0; d < NLT; ++d) red[(rs * nlw + dwi) * NLT + d] = acc[d];
+  __syncthreads();
+  const int nl = nlw * NLT;
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < RS; ++r) s += red[r * nl + l];
+    R[(static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * nl + l] = s;
+  }
+}
+
+// The instantiation for frame-kernel size kt, or null (kt > GRAM_KT_MAX).
+void* gram_lags_rt_ptr(int kt) {
+  switch (kt) {
+    case 1: return reinterpret_cast<void*>(&icnnm_gram_lags_rt<1>);
+    case 2: return reinterpret_cast<void*>(&icnnm_gram_lags_rt<2>);
+    case 3: return reinterpret_cast<void*>(&icnnm_gram_lags_rt<3>);
+    case 4: return reinterpret_cast<void*>(&icnnm_gram_lags_rt<4>);
+    case 5: return reinterpret_cast<void*>(&icnnm_gram_lags_rt<5>);
+    case 6: return reinterpret_cast<void*>(&icnnm_gram_lags_rt<6>);
+    case 7: return reinterpret_cast<void*>(&icnnm_gram_lags_rt<7>);
+    case 8: return reinterpret_cast<void*>(&icnnm_gram_lags_rt<8>);
+    case 9: return reinterpret_cast<void*>(&icnnm_gram_lags_rt<9>);
+    default: return nullptr;
+  }
+}
+
+// Half-space partials [ny][kh][nl] (dh = 0..kh-1) -> the full lag box
+// R_out[(2kh-1)][nl] += sum_y (fixed order), mirrored: R[-dh][-dw][-dt] =
+// R[dh][dw][dt] (index nl-1-l in row kh-1-dh); in the dh = 0 row the upper
+// half (l >= centre) is mirrored onto the lower, so R is exactly symmetric.
+__global__ void icnnm_gram_reduce_sym(int kh, int nl, int ny, const double* __restrict__ partial,
+                                      double* __restrict__ R_out) {
+  const int64_t n = static_cast<int64_t>(kh) * nl;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int y = 0; y < ny; ++y) s += partial[static_cast<size_t>(y) * n + i];
+    const int dh = static_cast<int>(i / nl), l = static_cast<int>(i % nl);
+    if (dh == 0) {
+      if (l < (nl - 1) / 2) continue;
+      R_out[static_cast<size_t>(kh - 1) * nl + l] += s;
+      if (l != (nl - 1) / 2) R_out[static_cast<size_t>(kh - 1) * nl + (nl - 1 - l)] += s;
+    } else {
+      R_out[static_cast<size_t>(kh - 1 + dh) * nl + l] += s;
+      R_out[static_cast<size_t>(kh - 1 - dh) * nl + (nl - 1 - l)] += s;
+    }
+  }
+}
+
+// FP64 DFMA peak probe: independent FMA chains in registers.
+__global__ void __launch_bounds__(256) icnnm_dfma_probe(double* out, int iters, double seed) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x * 1e-9 + i;
+  const double b = 0.999999, c = 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 12345.678) out[0] = s;
 }
 
 // R_out[i] += sum_y partial[y][i] (fixed order)

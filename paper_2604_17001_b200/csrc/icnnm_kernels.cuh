@@ -33,6 +33,20 @@ constexpr int BK = 32;    // reduction chunk
 // bh*bw*bt == 128 and bt a multiple of 8; bricks tile the (H, W, T) box
 // (voxels outside the tensor are masked).  W rows are brick-ordered:
 // row = brick*128 + local voxel, so a CTA's 128 rows are contiguous.
+// Exponent e of the fixed-point scale 2^e of the deterministic adjoint output
+// (icnnm_tc.cu flush, icnnm_adj_q2f).  |adj_i| <= sum over k taps of
+// |U[v, s]| <= amax ||K[s, :]||_1 <= amax sqrt(k) (K orthogonal, amax the
+// coef kernel's bound on |W_vj c_j|), so amax k sqrt(k) 2^e < 2^61 leaves a
+// factor-of-two margin for rounding below the int64 range.
+__device__ __forceinline__ int adjq_exp(double amax, int k) {
+  if (!(amax > 0.0) || !(amax < 1e300)) return 0;
+  int ex;
+  frexp(2.0 * amax * static_cast<double>(k) * sqrt(static_cast<double>(k)), &ex);
+  int e = 61 - ex;
+  e = e > 1000 ? 1000 : (e < -1000 ? -1000 : e);
+  return e;
+}
+
 struct Geo {
   int H, W, T;          // voxels owned by this launch (H = slab rows)
   int kh, kw, kt;       // kernel box
@@ -99,10 +113,8 @@ __global__ void icnnm_coef(IterState* st, const double* theta, double* red, floa
                            IterStats* stats, int k, int kp, double kd, double res_scale,
                            double tol_p, double tol_c, double floor_rel, int exact, Partials P);
 __global__ void icnnm_fold(Partials P, int kp, double* red);
-constexpr int GATHER_PAIRS = 12;                 // max (brick, offset) pairs per axis coordinate
-constexpr int GATHER_S = 1 + 2 * GATHER_PAIRS;   // ints per table entry
-__global__ void icnnm_adj_gather(Geo g, int nsp, int nobp, const int* tab, const float* scr,
-                                 float* adj);
+__global__ void icnnm_adj_q2f(int64_t n, const IterState* st, int k, unsigned long long* adjq,
+                              float* adj);
 constexpr int UPD_U = 4;  // elements in flight per thread (icnnm_update)
 __global__ void icnnm_update(int64_t m, const IterState* st, double lambda, double kd,
                              float* adj, double* L, double* V, const float* pm,
@@ -115,6 +127,11 @@ __global__ void icnnm_setup(int64_t m, const double* M, const double* msk, int m
 __global__ void icnnm_gram_lags(int H, int W, int T, int kh, int kw, int kt, int bh, int bw,
                                 int bt, const double* X, double* R);
 __global__ void icnnm_gram_reduce(int64_t n, int ny, const double* partial, double* R_out);
+constexpr int GRAM_KT_MAX = 9;  // register-tiled Gram kernel: largest frame-kernel size
+void* gram_lags_rt_ptr(int kt);  // icnnm_gram_lags_rt<kt>(H, W, T, kw, bh, bw, bt, X, R) or null
+__global__ void icnnm_gram_reduce_sym(int kh, int nl, int ny, const double* partial,
+                                      double* R_out);
+__global__ void icnnm_dfma_probe(double* out, int iters, double seed);
 __global__ void icnnm_colnorm2(int64_t rows, int64_t cols, const double* W, double* out);
 __global__ void icnnm_colscale(int64_t rows, int64_t cols, const double* W, const double* n2,
                                double tau, double* Z);

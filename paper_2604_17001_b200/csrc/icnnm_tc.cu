@@ -563,6 +563,29 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   // uniform and the MMA issuer's counters can live in uniform registers
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
 
+  // consumer / producer hand-over arrive of a whole warp: lane 0 after a warp
+  // sync (a.warr), or every lane
+  const bool warr = a.warr != 0;
+  auto warp_arrive = [&](uint64_t* b) {
+    if (warr) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(b);
+    } else {
+      mbar_arrive(b);
+    }
+  };
+  auto warp_arrive2 = [&](uint64_t* b0, uint64_t* b1) {  // b1 may be null
+    if (warr) {
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(b0);
+        if (b1) mbar_arrive(b1);
+      }
+    } else {
+      mbar_arrive(b0);
+      if (b1) mbar_arrive(b1);
+    }
+  };
   if (warp == WMMA) {
     if (PAIR) {  // both CTAs' warp WMMA: 512 columns in each CTA of the pair
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
@@ -575,7 +598,11 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     }
   }
   if (tid == 0) {
-    const int nbuild = (a.bsplit && !F16) ? NB * 32 : (NB / 2) * 32;  // builder arrivals / chunk
+    // arrivals per barrier phase: one per warp (a.warr: the warp's lane 0 after
+    // __syncwarp; 128 single-lane arrives on one mbarrier serialise in the
+    // shared-memory atomic unit) or one per thread
+    const int per = a.warr ? 1 : 32;
+    const int nbuild = ((a.bsplit && !F16) ? NB : NB / 2) * per;  // builder arrivals / chunk
     // PAIR: the leader's A_full / ACC_empty count one arrival per warp of both
     // CTAs; its B_full the local expect_tx plus the peer's relayed arrival
     for (int i = 0; i < SA; ++i) {
@@ -588,16 +615,16 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(ACC_full + i, 1);
-      mbar_init(ACC_empty + i, PAIR ? 2 * nepi_act : nepi_act * 32);
+      mbar_init(ACC_empty + i, PAIR ? 2 * nepi_act : nepi_act * per);
     }
     for (int i = 0; i < WS; ++i) {
       mbar_init(W_full + i, 1);
-      mbar_init(W_empty + i, FWD ? 4 * 32 : nbuild);  // forward: the half's 4 epilogue warps
+      mbar_init(W_empty + i, FWD ? 4 * per : nbuild);  // forward: the half's 4 epilogue warps
     }
     for (int i = 0; i < NSC; ++i) mbar_init(SC_full + i, 1);
     for (int i = 0; i < NHB_MAX; ++i) {
       mbar_init(HALO_full + i, 1);             // the prep warps' leader, after their barrier
-      mbar_init(HALO_empty + i, NB * 32);      // every builder thread, after the brick
+      mbar_init(HALO_empty + i, NB * per);     // every builder warp / thread, after the brick
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -875,10 +902,8 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             if (pend_sa >= 0) {
               if (!(TC_SKIP(a) & 1)) tmem_wait_st();
               tc_fence_before();
-              mbar_arrive(A_full + pend_sa);
-              if (!FWD) mbar_arrive(W_empty + pend_wsi);
-              mbar_arrive(A_full + sa);
-              if (!FWD) mbar_arrive(W_empty + wsi);
+              warp_arrive2(A_full + pend_sa, FWD ? nullptr : W_empty + pend_wsi);
+              warp_arrive2(A_full + sa, FWD ? nullptr : W_empty + wsi);
               pend_sa = -1;
             } else {
               pend_sa = sa;
@@ -889,11 +914,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(lead_afull + 8u * static_cast<uint32_t>(sa));
-            if (!FWD) mbar_arrive(W_empty + wsi);
+            if (!FWD) warp_arrive(W_empty + wsi);
           } else {
             tc_fence_before();
-            mbar_arrive(A_full + sa);
-            if (!FWD) mbar_arrive(W_empty + wsi);
+            warp_arrive2(A_full + sa, FWD ? nullptr : W_empty + wsi);
           }
           if (dbg.p) {
             long long t2c = clk();
@@ -905,11 +929,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       if (pair && pend_sa >= 0) {  // flush the brick's last owned chunk
         if (!(TC_SKIP(a) & 1)) tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(A_full + pend_sa);
-        if (!FWD) mbar_arrive(W_empty + pend_wsi);
+        warp_arrive2(A_full + pend_sa, FWD ? nullptr : W_empty + pend_wsi);
         pend_sa = -1;
       }
-      if (FWD) mbar_arrive(HALO_empty + hbuf);  // this thread's reads of the halo are done
+      if (FWD) warp_arrive(HALO_empty + hbuf);  // this warp's reads of the halo are done
     }
     dbg.flush(DBG_BUILD_WAIT, DBG_BUILD_WORK);
     if (dbg.p) atomicAdd(dbg.p + DBG_BUILD_PREP, static_cast<unsigned long long>(prep));
@@ -940,7 +963,8 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     auto issue = [&](int i, int sl) {
       const int buf = i % nhb;
       float* hdst = halo + buf * nobp;
-      mbar_wait(HALO_empty + buf, (static_cast<uint32_t>(i / nhb) & 1u) ^ 1u);
+      // (timing experiments without builders: nobody releases the buffers)
+      if (!(TC_SKIP(a) & 8)) mbar_wait(HALO_empty + buf, (static_cast<uint32_t>(i / nhb) & 1u) ^ 1u);
       const int b = brick_of(sl);
       const int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
       const int hb0 = bh_i * g.bh - (g.kh - 1) + g.hoff, wb0 = bw_i * g.bw - (g.kw - 1),
@@ -1031,6 +1055,19 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     if (F16 && !FWD)
       us_adj = a.bunscale / f16_scale(a.mode >= 1 ? static_cast<float>(a.st->adj_amax) : a.amax);
     uint32_t biter = 0;
+    // adjoint flush: this thread's first output-box element and its step
+    const int FSTEP = nepi_act * 32, fe0 = ew * 32 + lane;
+    const int fl_c0 = fe0 % g.HT, fl_bb0 = (fe0 / g.HT) % g.HW, fl_aa0 = fe0 / (g.HT * g.HW);
+    const int fl_dc = FSTEP % g.HT, fl_dbb = (FSTEP / g.HT) % g.HW, fl_daa = FSTEP / (g.HT * g.HW);
+    // one conditional wrap suffices unless a dimension is smaller than its halo
+    auto wrap1 = [](int x, int n) {
+      x = x < 0 ? x + n : x;
+      x = x >= n ? x - n : x;
+      return (static_cast<unsigned>(x) < static_cast<unsigned>(n)) ? x : wrapi(x, n);
+    };
+    // deterministic adjoint flush: 2^e of the fixed-point output (adjq_exp)
+    const double qscale =
+        (!FWD && a.adjq != nullptr) ? ldexp(1.0, adjq_exp(a.st->adj_amax, g.k)) : 1.0;
     const uint32_t lead_accempty = PAIR ? mapa_u32(smem_u32(ACC_empty), 0) : 0u;
     for (int sl = sfirst; sl < nslot; sl += sstep, ++biter) {
       const int b = brick_of(sl);
@@ -1131,7 +1168,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
                 }
               }
             }
-            mbar_arrive(W_empty + wsl);
+            warp_arrive(W_empty + wsl);
           }
           gbase += static_cast<uint32_t>(ngp);
         } else {
@@ -1183,7 +1220,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(lead_accempty + 8u * static_cast<uint32_t>(acc));
         } else {
-          mbar_arrive(ACC_empty + acc);
+          warp_arrive(ACC_empty + acc);
         }
         if (dbg.p) {
           long long t2c = clk();
@@ -1193,28 +1230,42 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       }
       if (!FWD) {
         named_sync(2, nepi_act * 32);
+        // flush: element e = (aa*HW + bb)*HT + c of the output box, advanced by
+        // the step in mixed radix (no per-element divisions)
+        int c = fl_c0, bb = fl_bb0, aa = fl_aa0;
+        const int hbase = h0 - (g.kh - 1) + g.hoff, wbase = w0 - (g.kw - 1), tbase_ = t0 - (g.kt - 1);
         for (int e = ew * 32 + lane; e < nob; e += nepi_act * 32) {
           float s = 0.f;
           for (int q = 0; q < nepi_act; ++q) {
             s += ob[q * obs + e];
             ob[q * obs + e] = 0.f;
           }
+          const int ce = c, bbe = bb, aae = aa;
+          c += fl_dc;
+          int cy = c >= g.HT ? 1 : 0;
+          c -= cy * g.HT;
+          bb += fl_dbb + cy;
+          cy = bb >= g.HW ? 1 : 0;
+          bb -= cy * g.HW;
+          aa += fl_daa + cy;
           if (!breal) continue;  // dummy brick: output bricks cleared, nothing written
-          if (a.adj_scr != nullptr) {
-            // deterministic: the brick's (role's) partial output brick goes to
-            // its own scratch slot; icnnm_adj_gather sums the slots covering
-            // each voxel in a fixed order
-            a.adj_scr[(static_cast<size_t>(b) * nsp + role) * nobp + e] = s;
+          if (s == 0.f) continue;
+          int hs = hbase + aae;
+          if (g.wrapH) hs = wrap1(hs, g.Hsrc);
+          if (hs < 0 || hs >= g.Hsrc) continue;
+          const int ws = wrap1(wbase + bbe, g.W);
+          const int ts = wrap1(tbase_ + ce, g.T);
+          const size_t oi = (static_cast<size_t>(hs) * g.W + ws) * g.T + ts;
+          if (a.adjq != nullptr) {
+            // deterministic: the brick's partial sum (fixed order within the
+            // CTA) is added as a 64-bit fixed-point integer -- integer adds
+            // commute exactly, so the flush order across CTAs does not matter;
+            // icnnm_adj_q2f converts back (scale from the same st->adj_amax)
+            atomicAdd(a.adjq + oi, static_cast<unsigned long long>(
+                                       __double2ll_rn(static_cast<double>(s) * qscale)));
             continue;
           }
-          if (s == 0.f) continue;
-          int c = e % g.HT, tmp2 = e / g.HT, bb = tmp2 % g.HW, aa = tmp2 / g.HW;
-          int hs = h0 - (g.kh - 1) + aa + g.hoff;
-          if (g.wrapH) hs = wrapi(hs, g.Hsrc);
-          if (hs < 0 || hs >= g.Hsrc) continue;
-          int ws = wrapi(w0 - (g.kw - 1) + bb, g.W);
-          int ts = wrapi(t0 - (g.kt - 1) + c, g.T);
-          atomicAdd(a.adj + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts, s);
+          atomicAdd(a.adj + oi, s);
         }
         named_sync(2, nepi_act * 32);
       }
@@ -1281,6 +1332,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       int wn_t[2];
       // MMAs of chunk kc (A stage sa, parity aph) into tile t of the current group
       int cur_nt0 = 0;  // first N-tile of the current group
+      bool bres_ready = false;
       auto issue = [&](int t, int kc, int sa, uint32_t aph, bool first_use, bool last_use) {
         if (kc == kcb) {
           const uint32_t tci = tcount + static_cast<uint32_t>(t);
@@ -1302,7 +1354,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         }
         long long q2 = a.dbg ? clk() : 0;
         if (a.bres) {
-          mbar_wait(B_full, 0);  // resident B: one fill per launch (phase 0)
+          if (!bres_ready) {
+            mbar_wait(B_full, 0);  // resident B: one fill per launch (phase 0)
+            bres_ready = true;
+          }
         } else if (!(TC_SKIP(a) & 16)) {
           if (PAIR)
             pwait(B_full + sb, bph);

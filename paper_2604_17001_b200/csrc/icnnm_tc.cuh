@@ -77,10 +77,11 @@ struct alignas(64) TcArgs {
   int bres_stride;          // resident B: bytes per (tile, chunk) block
   int bres_bytes;           // resident B: SMEM bytes of the role's tiles x chunks
   // deterministic reductions (null: fp32 / fp64 atomics as before)
-  float* adj_scr;           // adjoint: per-(brick, role) output-brick slots [nbricks][nsplit][nobp]
+  unsigned long long* adjq; // adjoint (mode 1): 64-bit fixed-point output, same layout as adj
   double* npart;            // forward: per-CTA column partials [grid][kp] (mode 2: [grid])
   int nhb;                  // forward: halo buffers (2..NHB_MAX; the prep warps run nhb-2 ahead)
   int bstride;              // F16x3 single CTAs: B ring stage stride in bytes (0: B_STAGE_F16)
+  int warr;                 // 1: one mbarrier arrival per warp (lane 0 after __syncwarp); 0: per thread
 };
 
 // dbg slots (cycles summed over CTAs)

@@ -160,11 +160,26 @@ def test_gram_large_kernel_matches_oracle(gpu):
         assert np.max(np.abs(G - E)) < 1e-10 * np.max(np.abs(E))
 
 
-def test_learn_basis_matches_oracle(gpu):
-    """learn_ensemble_basis: eigenvalues + per-block projectors
-    (test_spectral.cpp:112-137)."""
+def test_gram_generic_kernel_and_mirror(gpu):
+    """Frame kernels beyond the register-tiled Gram kernel's range (kt > 9)
+    take the lag-per-thread kernel; both give an exactly symmetric Gram."""
     from paper_2604_17001_b200 import synth
-    w = synth.WORKLOADS[1]
+    X = synth.synth_video(20, 24, 40, 6, 1, 11)
+    for ks in [(3, 4, 11), (5, 6, 9), (2, 3, 1), (1, 1, 7)]:
+        G = gpu.conv_gram(X, ks)
+        E = O.conv_gram(X, ks)
+        assert np.max(np.abs(G - E)) < 1e-10 * np.max(np.abs(E)), ks
+        if ks[2] <= 9:
+            np.testing.assert_array_equal(G, G.T)
+
+
+@pytest.mark.parametrize("cfgno", [1, 2, 3])
+def test_learn_basis_matches_oracle(gpu, cfgno):
+    """learn_ensemble_basis: eigenvalues + per-block projectors
+    (test_spectral.cpp:112-137), at the kernels and training sets of BASELINE
+    configs 1-3 (k = 75, 405, 1183)."""
+    from paper_2604_17001_b200 import synth
+    w = synth.WORKLOADS[cfgno]
     refs = w.training()
     got = gpu.learn_ensemble_basis(refs, w.kernel)
     ref = O.learn_ensemble_basis(refs, w.kernel)
@@ -569,6 +584,66 @@ def test_exact_residual_stops_like_reference(gpu):
     assert rep.termination == "converged" and ro.termination == "converged"
     assert abs(rep.iterations - ro.iterations) <= 3
     assert _rel(L, L0) < 1e-3
+
+
+def test_default_config_converges_like_reference(gpu):
+    """A drop-in caller's default SolverConfig (tol_primal 1e-7, tol_change
+    1e-8, solver.hpp:35-37) stops where the reference does (solver.cpp:136-139):
+    engine "auto" runs the fp64 engine for tolerances below the fp32 engines'
+    resolution.  The reference's cosine case (test_solver.cpp:122-138) stops on
+    l_change = 7.7e-9 at iteration 28."""
+    L0 = np.cos(2 * np.pi * np.arange(32) / 8)
+    B = gpu.learn_ensemble_basis([L0], (8,))
+    mask = gpu.synth.reference_bernoulli_mask((32,), 0.75, 5)
+    L, rep = gpu.icnnm_solve(L0 * mask, mask, B, gpu.SolverConfig())
+    Lo, ro = O.icnnm_solve(L0 * mask, mask, _oracle_basis(B), O.SolverConfig())
+    assert rep.termination == "converged" and ro.termination == "converged"
+    assert abs(rep.iterations - ro.iterations) <= 1
+    n = min(rep.iterations, ro.iterations)
+    np.testing.assert_allclose(rep.objective[:n], ro.objective[:n], rtol=1e-9)
+    np.testing.assert_allclose(rep.l_change[:n - 1], ro.l_change[:n - 1], rtol=1e-4, atol=1e-12)
+    assert _rel(L, Lo) < 1e-8
+    assert _rel(L, L0) < 1e-3
+
+
+def test_f64_engine_matches_oracle_config1(gpu):
+    """BASELINE config 1 with the reference's default tolerances: the oracle
+    stops on the primal residual (< 1e-7) at iteration 88; the fp64 engine
+    reproduces the stop and the traces."""
+    from paper_2604_17001_b200 import synth
+    w = synth.WORKLOADS[1]
+    X, mask = w.target(), w.mask()
+    B = gpu.learn_ensemble_basis(w.training(), w.kernel)
+    L, rep = gpu.icnnm_solve(X * mask, mask, B, gpu.SolverConfig(max_iters=400))
+    Lo, ro = O.icnnm_solve(X * mask, mask, _oracle_basis(B), O.SolverConfig(max_iters=400))
+    assert ro.termination == "converged" and rep.termination == "converged"
+    assert abs(rep.iterations - ro.iterations) <= 1
+    n = min(rep.iterations, ro.iterations)
+    np.testing.assert_allclose(rep.objective[:n], ro.objective[:n], rtol=1e-8)
+    np.testing.assert_allclose(rep.primal_residual[:n - 1], ro.primal_residual[:n - 1], rtol=1e-3)
+    assert _rel(L, Lo) < 1e-7
+    # the same call with an explicit fp32 engine cannot resolve these tolerances
+    _, r32 = gpu.icnnm_solve(X * mask, mask, B, gpu.SolverConfig(max_iters=120, engine="f16x3"))
+    assert r32.termination == "max_iters"
+
+
+def test_auto_engine_fp32_when_resolvable(gpu):
+    """Engine "auto" keeps the tcgen05 engine when the tolerances are disabled
+    or resolvable in fp32 (tol_primal >= 1e-4 with the exact residual)."""
+    from paper_2604_17001_b200 import synth
+    w = synth.WORKLOADS[1]
+    X, mask = w.target(), w.mask()
+    B = gpu.learn_ensemble_basis(w.training(), w.kernel)
+    La, ra = gpu.icnnm_solve(X * mask, mask, B, gpu.SolverConfig(max_iters=30, **FIXED))
+    Lf, rf = gpu.icnnm_solve(X * mask, mask, B,
+                             gpu.SolverConfig(max_iters=30, engine="f16x3", **FIXED))
+    np.testing.assert_array_equal(La, Lf)           # same engine, deterministic
+    cfg = dict(max_iters=200, tol_primal=1e-3, tol_change=1e-300)
+    L1, r1 = gpu.icnnm_solve(X * mask, mask, B, gpu.SolverConfig(**cfg))
+    Lo, ro = O.icnnm_solve(X * mask, mask, _oracle_basis(B), O.SolverConfig(**cfg))
+    assert r1.termination == "converged" and ro.termination == "converged"
+    assert abs(r1.iterations - ro.iterations) <= 3
+    assert not np.any(np.isnan(r1.primal_residual))
 
 
 def test_cli_learn_complete_end_to_end(gpu, tmp_path):
