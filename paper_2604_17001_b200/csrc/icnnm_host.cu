@@ -2162,11 +2162,13 @@ void gram_lags_accumulate(const Problem& p, const double* dX, double* dR, cudaSt
     int bw = std::min(W, rsmax);
     int bh = std::min(H, std::max(1, rsmax / bw));
     int bt = std::min(T, 64);
-    const int btp = (bt + 3) / 4 * 4;
+    const int cw = std::max(2, 2 * kt - 2);              // frames per step (kernel's CW)
+    const int btp = (bt + 2 * cw - 1) / (2 * cw) * (2 * cw);
     const int RS = bh * bw;
     const size_t tile = static_cast<size_t>(RS) * (btp + 2) +
-                        static_cast<size_t>(bh) * (bw + 2 * (kw - 1)) * ((btp + 2 * (kt - 1)) | 1);
-    const size_t smem = std::max(tile, static_cast<size_t>(RS) * nl) * sizeof(double);
+                        static_cast<size_t>(bh) * (bw + 2 * (kw - 1)) * ((btp + cw) | 1);
+    // two tiles: the next brick's copies overlap the current brick's lags
+    const size_t smem = std::max(2 * tile, static_cast<size_t>(RS) * nl) * sizeof(double);
     check_smem(smem);
     static std::mutex mu;
     static std::map<void*, size_t> attr;  // opt-in dynamic shared memory per instantiation
@@ -2180,7 +2182,15 @@ void gram_lags_accumulate(const Problem& p, const double* dX, double* dR, cudaSt
       }
     }
     const int nb = ((H + bh - 1) / bh) * ((W + bw - 1) / bw) * ((T + bt - 1) / bt);
-    dim3 grid(kh, std::max(1, std::min(nb, 592 / kh + 1)));
+    // one resident wave: kh x grid.y CTAs <= resident CTAs (2 per SM for kt <= 6, else 1)
+    int nsm = 148;
+    {
+      int dev = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int resident = nsm * (kt <= 6 ? 2 : 1);
+    dim3 grid(kh, std::max(1, std::min(nb, std::max(1, resident / kh))));
     DBuf<double> part(static_cast<size_t>(grid.y) * kh * nl);
     int aH = H, aW = W, aT = T, akw = kw, abh = bh, abw = bw, abt = bt;
     const double* aX = dX;

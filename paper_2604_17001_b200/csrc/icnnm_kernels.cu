@@ -24,6 +24,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::);
 }
@@ -786,24 +790,27 @@ icnnm_gram_lags(int H, int W, int T, int kh, int kw, int kt, int bh, int bw, int
 // fixed order at the end (deterministic, like the partial rows).
 // ---------------------------------------------------------------------------
 template <int KT>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, (KT <= 6 ? 2 : 1))
 icnnm_gram_lags_rt(int H, int W, int T, int kw, int bh, int bw, int bt,
                    const double* __restrict__ X, double* __restrict__ R) {
   constexpr int NLT = 2 * KT - 1;
-  constexpr int CW = 4;
+  // frames per step: the window of CW + NLT - 1 halo frames lives in two
+  // register arrays of CW that swap roles every step (no register shifting)
+  constexpr int CW = (NLT - 1) < 2 ? 2 : (NLT - 1);
   extern __shared__ double gsm[];
   const int dh = static_cast<int>(blockIdx.x);
   const int nlw = 2 * kw - 1;
   const int RS = bh * bw;
   const int HWd = bw + 2 * (kw - 1);
-  const int btp = (bt + CW - 1) / CW * CW;
+  const int btp = (bt + 2 * CW - 1) / (2 * CW) * (2 * CW);
   const int po = btp + 2;                 // own row pitch (rows of one warp: <= 3 distinct)
-  const int hl = btp + 2 * (KT - 1);      // halo row length
+  const int hl = btp + CW;                // halo row length (>= btp + 2 (KT - 1))
   const int ph = hl | 1;                  // odd pitch: a half-warp's rows hit distinct banks
   double* own = gsm;                      // RS * po
   double* hal = gsm + RS * po;            // bh * HWd * ph
   const int nbh = (H + bh - 1) / bh, nbw = (W + bw - 1) / bw, nbt = (T + bt - 1) / bt;
   const int nb = nbh * nbw * nbt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int dwi = static_cast<int>(threadIdx.x) % nlw, rs = static_cast<int>(threadIdx.x) / nlw;
   const bool act = rs < RS;
   const int ra = act ? rs / bw : 0, rb = act ? rs % bw : 0;
@@ -812,44 +819,85 @@ icnnm_gram_lags_rt(int H, int W, int T, int kw, int bh, int bw, int bt,
   double acc[NLT];
 #pragma unroll
   for (int d = 0; d < NLT; ++d) acc[d] = 0.0;
-  for (int b = blockIdx.y; b < nb; b += gridDim.y) {
+  // one step: own frames c0 .. c0+CW-1 against the window lo ++ hi
+  // (lo = halo frames c0 .. c0+CW-1, hi = the next CW); lag index
+  // d = dt + (kt-1): own[c] pairs with halo frame c + NLT-1-d
+  auto step = [&](const double (&o)[CW], const double (&lo)[CW], const double (&hi)[CW]) {
+#pragma unroll
+    for (int i = 0; i < CW; ++i)
+#pragma unroll
+      for (int d = 0; d < NLT; ++d) {
+        const int u = i + NLT - 1 - d;
+        acc[d] = fma(o[i], u < CW ? lo[u] : hi[u - CW], acc[d]);
+      }
+  };
+  // brick b's own rows and halo into buffer `buf` with 8-byte cp.async copies
+  // (a warp per row: the row's (h, w) once, frames across the lanes); the next
+  // brick's copies fly while the current one is computed
+  const int tile = RS * po + bh * HWd * ph;
+  auto load = [&](int b, int buf) {
     const int bt_i = b % nbt, bw_i = (b / nbt) % nbw, bh_i = b / (nbt * nbw);
     const int h0 = bh_i * bh, w0 = bw_i * bw, t0 = bt_i * bt;
-    __syncthreads();
-    for (int e = threadIdx.x; e < RS * btp; e += blockDim.x) {
-      const int c = e % btp, r = e / btp;
-      const int h = h0 + r / bw, w = w0 + r % bw, t = t0 + c;
-      own[r * po + c] = (c < bt && h < H && w < W && t < T)
-                            ? X[(static_cast<size_t>(h) * W + w) * T + t] : 0.0;
+    double* ownb = own + buf * tile;
+    double* halb = hal + buf * tile;
+    for (int r = warp; r < RS; r += 8) {
+      const int h = h0 + r / bw, w = w0 + r % bw;
+      const bool in = h < H && w < W;
+      const double* src = X + (static_cast<size_t>(in ? h : 0) * W + (in ? w : 0)) * T + t0;
+      for (int c = lane; c < btp; c += 32) {
+        if (in && c < bt && t0 + c < T)
+          cp_async8(ownb + r * po + c, src + c);
+        else
+          ownb[r * po + c] = 0.0;
+      }
     }
-    for (int e = threadIdx.x; e < bh * HWd * hl; e += blockDim.x) {
-      const int c = e % hl, q = e / hl;     // q = a * HWd + j
+    for (int q = warp; q < bh * HWd; q += 8) {
       const int h = wrapi(h0 + q / HWd - dh, H);
       const int w = wrapi(w0 + q % HWd - (kw - 1), W);
-      const int t = wrapi(t0 + c - (KT - 1), T);
-      hal[q * ph + c] = X[(static_cast<size_t>(h) * W + w) * T + t];
+      const double* src = X + (static_cast<size_t>(h) * W + w) * T;
+      for (int c = lane; c < hl; c += 32) {
+        int t = t0 + c - (KT - 1);
+        t = t < 0 ? t + T : t;
+        t = t >= T ? t - T : t;
+        if (static_cast<unsigned>(t) >= static_cast<unsigned>(T)) t = wrapi(t, T);
+        cp_async8(halb + q * ph + c, src + t);
+      }
+    }
+    cp_async_commit();
+  };
+  int buf = 0;
+  if (static_cast<int>(blockIdx.y) < nb) load(blockIdx.y, 0);
+  for (int b = blockIdx.y; b < nb; b += gridDim.y, buf ^= 1) {
+    const int bn = b + static_cast<int>(gridDim.y);
+    if (bn < nb) {
+      load(bn, buf ^ 1);   // its previous reader finished before the barrier below
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
     if (act) {
-      double win[CW + NLT - 1];
+      const double* orw = orow + buf * tile;
+      const double* hrw = hrow + buf * tile;
+      double wa[CW], wb[CW], o[CW];
 #pragma unroll
-      for (int u = 0; u < NLT - 1; ++u) win[u] = hrow[u];
-      for (int c0 = 0; c0 < btp; c0 += CW) {
-        double o[CW];
+      for (int u = 0; u < CW; ++u) wa[u] = hrw[u];
+      for (int c0 = 0; c0 < btp; c0 += 2 * CW) {
 #pragma unroll
-        for (int i = 0; i < CW; ++i) {
-          win[NLT - 1 + i] = hrow[c0 + NLT - 1 + i];
-          o[i] = orow[c0 + i];
+        for (int u = 0; u < CW; ++u) {
+          wb[u] = hrw[c0 + CW + u];
+          o[u] = orw[c0 + u];
         }
-        // lag index d = dt + (kt-1): own[c] pairs with halo column c + NLT-1-d
+        step(o, wa, wb);
 #pragma unroll
-        for (int i = 0; i < CW; ++i)
-#pragma unroll
-          for (int d = 0; d < NLT; ++d) acc[d] = fma(o[i], win[i + NLT - 1 - d], acc[d]);
-#pragma unroll
-        for (int u = 0; u < NLT - 1; ++u) win[u] = win[u + CW];
+        for (int u = 0; u < CW; ++u) {
+          wa[u] = hrw[c0 + 2 * CW + u];   // last step: zero-padded frames of the pitch
+          o[u] = orw[c0 + CW + u];
+        }
+        step(o, wb, wa);
       }
     }
+    __syncthreads();  // buffer `buf` is refilled by the next iteration's load
   }
   // fixed-order reduction over rs: red[rs][dw][d] in shared memory
   __syncthreads();

@@ -428,6 +428,14 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
@@ -780,16 +788,24 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     int iter = 0;
     int st_sa = 0, st_ws = 0;
     uint32_t st_ph = 0, st_wph = 0;
-    auto adv_stage = [&]() {
-      if (++st_sa == san) {
-        st_sa = 0;
+    // A / W stage (index, parity) advanced by n <= 2 chunks (rings of >= 2 stages)
+    auto adv_stage = [&](int n) {
+      st_sa += n;
+      if (st_sa >= san) {
+        st_sa -= san;
         st_ph ^= 1u;
       }
-      if (++st_ws == wsn) {
-        st_ws = 0;
+      st_ws += n;
+      if (st_ws >= wsn) {
+        st_ws -= wsn;
         st_wph ^= 1u;
       }
     };
+    // bsplit = 0: group `half` owns the chunks with cnt % 2 == half and builds
+    // all KC columns, so each warp has two chunk periods of MMA time to cover
+    // its TMEM-store round trip; the loop visits only the owned chunks
+    const int nchunk = ngrp * nkr;
+    const int cstep = (F16 || !a.bsplit) ? 2 : 1;
     long long prep = 0;
     for (int sl = sfirst; sl < nslot; sl += sstep, ++iter) {
       const int hbuf = iter % nhb;
@@ -799,13 +815,13 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       // prepared by the prep warps while the previous brick is built
       if (FWD) mbar_wait(HALO_full + hbuf, static_cast<uint32_t>(iter / nhb) & 1u);
       if (dbg.p) prep += clk() - tp0;
-      for (int gi = 0; gi < ngrp; ++gi) {
-        for (int kc = kcb; kc < kce; ++kc, ++cnt, adv_stage()) {
-          // bsplit = 0: group `half` owns the chunks with cnt % 2 == half and
-          // builds all KC columns, so each warp has two chunk periods of MMA
-          // time to cover its TMEM-store round trip.
-          if ((F16 || !a.bsplit) && static_cast<int>(cnt & 1u) != half) continue;
-          // A / W stage (index, parity) of chunk cnt, advanced incrementally
+      int f = cstep == 2 ? ((static_cast<int>(cnt) ^ half) & 1) : 0;  // my first chunk
+      adv_stage(f);
+      int kc = kcb + f;
+      if (kc >= kce) kc -= nkr;
+      {
+        for (; f < nchunk; f += cstep) {
+          // A / W stage (index, parity) of this chunk, advanced incrementally
           // (cnt % san and cnt / san were a 32-bit division per chunk)
           const int sa = st_sa;
           const uint32_t ph = st_ph;
@@ -924,8 +940,12 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             dbg.acc[0] += t1c - t0c;
             dbg.acc[1] += t2c - t1c;
           }
+          adv_stage((nchunk - f) < cstep ? (nchunk - f) : cstep);
+          kc += cstep;
+          while (kc >= kce) kc -= nkr;
         }
       }
+      cnt += static_cast<uint32_t>(nchunk);
       if (pair && pend_sa >= 0) {  // flush the brick's last owned chunk
         if (!(TC_SKIP(a) & 1)) tmem_wait_st();
         tc_fence_before();
@@ -951,9 +971,15 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     const int LAG = nhb - 2 >= 1 ? (nhb - 2 > 2 ? 2 : nhb - 2) : 0;
     // halo element e = (aa*HW + bb)*HT + c of this thread: decomposed once,
     // then advanced by NPREP*32 in mixed radix (no divisions per element)
+    // Copies are vw = 4, 2 or 1 consecutive frames wide (16 / 8 / 4 bytes): a
+    // box row's frames are contiguous in L~ between wraps, and groups of vw
+    // stay aligned and never straddle a wrap when vw divides T, bt, kt - 1
+    // (then also HT = bt + kt - 1 and every brick's first halo frame)
     constexpr int PSTEP = NPREP * 32;
-    const int dc = PSTEP % g.HT, dbb = (PSTEP / g.HT) % g.HW, daa = PSTEP / (g.HT * g.HW);
-    const int c0 = pt % g.HT, bb0 = (pt / g.HT) % g.HW, aa0 = pt / (g.HT * g.HW);
+    const int vw = ((g.T | g.bt | (g.kt - 1)) & 3) == 0 ? 4 : (((g.T | g.bt | (g.kt - 1)) & 1) == 0 ? 2 : 1);
+    const int nc = g.HT / vw, ngrp_h = nob / vw;   // groups per box row / per box
+    const int dc = PSTEP % nc, dbb = (PSTEP / nc) % g.HW, daa = PSTEP / (nc * g.HW);
+    const int c0 = pt % nc, bb0 = (pt / nc) % g.HW, aa0 = pt / (nc * g.HW);
     // one conditional wrap suffices unless a dimension is smaller than its halo
     auto wrap1 = [](int x, int n) {
       x = x < 0 ? x + n : x;
@@ -970,15 +996,21 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       const int hb0 = bh_i * g.bh - (g.kh - 1) + g.hoff, wb0 = bw_i * g.bw - (g.kw - 1),
                 tb0 = bt_i * g.bt - (g.kt - 1);
       int c = c0, bb = bb0, aa = aa0;
-      for (int e = pt; e < nob; e += PSTEP) {
+      for (int e = pt; e < ngrp_h; e += PSTEP) {
         int hs = hb0 + aa;
         hs = g.wrapH ? wrap1(hs, g.Hsrc) : (hs < 0 ? 0 : (hs >= g.Hsrc ? g.Hsrc - 1 : hs));
         const int ws = wrap1(wb0 + bb, g.W);
-        const int ts = wrap1(tb0 + c, g.T);
-        cp_async4(hdst + e, a.src + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts);
+        const int ts = wrap1(tb0 + c * vw, g.T);
+        const float* src = a.src + (static_cast<size_t>(hs) * g.W + ws) * g.T + ts;
+        if (vw == 4)
+          cp_async16(hdst + 4 * e, src);
+        else if (vw == 2)
+          cp_async8(hdst + 2 * e, src);
+        else
+          cp_async4(hdst + e, src);
         c += dc;
-        int cy = c >= g.HT ? 1 : 0;
-        c -= cy * g.HT;
+        int cy = c >= nc ? 1 : 0;
+        c -= cy * nc;
         bb += dbb + cy;
         cy = bb >= g.HW ? 1 : 0;
         bb -= cy * g.HW;
@@ -1059,6 +1091,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     const int FSTEP = nepi_act * 32, fe0 = ew * 32 + lane;
     const int fl_c0 = fe0 % g.HT, fl_bb0 = (fe0 / g.HT) % g.HW, fl_aa0 = fe0 / (g.HT * g.HW);
     const int fl_dc = FSTEP % g.HT, fl_dbb = (FSTEP / g.HT) % g.HW, fl_daa = FSTEP / (g.HT * g.HW);
+    // the same in groups of 4 frames (HT % 4 == 0): fv_nc groups per box row
+    const int fv_nc = g.HT >> 2 > 0 ? g.HT >> 2 : 1;
+    const int fv_c0 = fe0 % fv_nc, fv_bb0 = (fe0 / fv_nc) % g.HW, fv_aa0 = fe0 / (fv_nc * g.HW);
+    const int fv_dc = FSTEP % fv_nc, fv_dbb = (FSTEP / fv_nc) % g.HW, fv_daa = FSTEP / (fv_nc * g.HW);
     // one conditional wrap suffices unless a dimension is smaller than its halo
     auto wrap1 = [](int x, int n) {
       x = x < 0 ? x + n : x;
@@ -1181,7 +1217,32 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
               return F16 ? __uint_as_float(u[i]) * us : __uint_as_float(u[i]);
             };
             const int s0 = nt * a.wbase + c0;
-            if ((g.vmap ? g.kw : g.kh) >= 4) {
+            if ((g.vmap ? g.kw : g.kh) >= 4 && ncol == 32 && s0 + 32 <= g.k) {
+              // full block of real taps: the 4 tap offsets of a batch in one
+              // broadcast 128-bit load, no per-column predicates
+              float* const obase = myob + hidx;
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) {
+                const int4 t4 = *reinterpret_cast<const int4*>(tapoff + s0 + i);
+                float* const o0 = obase - t4.x;
+                float* const o1 = obase - t4.y;
+                float* const o2 = obase - t4.z;
+                float* const o3 = obase - t4.w;
+                const float x0 = *o0, x1 = *o1, x2 = *o2, x3 = *o3;
+                if (F16) {
+                  *o0 = fmaf(__uint_as_float(u[i]), us, x0);
+                  *o1 = fmaf(__uint_as_float(u[i + 1]), us, x1);
+                  *o2 = fmaf(__uint_as_float(u[i + 2]), us, x2);
+                  *o3 = fmaf(__uint_as_float(u[i + 3]), us, x3);
+                } else {
+                  *o0 = x0 + __uint_as_float(u[i]);
+                  *o1 = x1 + __uint_as_float(u[i + 1]);
+                  *o2 = x2 + __uint_as_float(u[i + 2]);
+                  *o3 = x3 + __uint_as_float(u[i + 3]);
+                }
+                __syncwarp();
+              }
+            } else if ((g.vmap ? g.kw : g.kh) >= 4) {
               // batches of 4 consecutive N columns = 4 distinct sh (vmap 0) or
               // sw (vmap 1), the coordinate the warp's rows share: no hazards
 #pragma unroll
@@ -1232,29 +1293,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         named_sync(2, nepi_act * 32);
         // flush: element e = (aa*HW + bb)*HT + c of the output box, advanced by
         // the step in mixed radix (no per-element divisions)
-        int c = fl_c0, bb = fl_bb0, aa = fl_aa0;
         const int hbase = h0 - (g.kh - 1) + g.hoff, wbase = w0 - (g.kw - 1), tbase_ = t0 - (g.kt - 1);
-        for (int e = ew * 32 + lane; e < nob; e += nepi_act * 32) {
-          float s = 0.f;
-          for (int q = 0; q < nepi_act; ++q) {
-            s += ob[q * obs + e];
-            ob[q * obs + e] = 0.f;
-          }
-          const int ce = c, bbe = bb, aae = aa;
-          c += fl_dc;
-          int cy = c >= g.HT ? 1 : 0;
-          c -= cy * g.HT;
-          bb += fl_dbb + cy;
-          cy = bb >= g.HW ? 1 : 0;
-          bb -= cy * g.HW;
-          aa += fl_daa + cy;
-          if (!breal) continue;  // dummy brick: output bricks cleared, nothing written
-          if (s == 0.f) continue;
-          int hs = hbase + aae;
-          if (g.wrapH) hs = wrap1(hs, g.Hsrc);
-          if (hs < 0 || hs >= g.Hsrc) continue;
-          const int ws = wrap1(wbase + bbe, g.W);
-          const int ts = wrap1(tbase_ + ce, g.T);
+        auto emit = [&](float sv, int hs, int ws, int cc) {
+          if (sv == 0.f) return;
+          const int ts = wrap1(tbase_ + cc, g.T);
           const size_t oi = (static_cast<size_t>(hs) * g.W + ws) * g.T + ts;
           if (a.adjq != nullptr) {
             // deterministic: the brick's partial sum (fixed order within the
@@ -1262,10 +1304,64 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             // commute exactly, so the flush order across CTAs does not matter;
             // icnnm_adj_q2f converts back (scale from the same st->adj_amax)
             atomicAdd(a.adjq + oi, static_cast<unsigned long long>(
-                                       __double2ll_rn(static_cast<double>(s) * qscale)));
-            continue;
+                                       __double2ll_rn(static_cast<double>(sv) * qscale)));
+          } else {
+            atomicAdd(a.adj + oi, sv);
           }
-          atomicAdd(a.adj + oi, s);
+        };
+        if ((g.HT & 3) == 0) {
+          // four consecutive frames of one (aa, bb) box row per step: the
+          // nepi_act per-warp copies are read and cleared with 128-bit accesses
+          int c = fv_c0, bb = fv_bb0, aa = fv_aa0;
+          const int ng4 = nob >> 2;
+          for (int gq = ew * 32 + lane; gq < ng4; gq += nepi_act * 32) {
+            float4 sv = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < nepi_act; ++q) {
+              float4* pq = reinterpret_cast<float4*>(ob + q * obs) + gq;
+              const float4 v = *pq;
+              sv.x += v.x; sv.y += v.y; sv.z += v.z; sv.w += v.w;
+              *pq = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const int ce = 4 * c, bbe = bb, aae = aa;
+            c += fv_dc;
+            int cy = c >= fv_nc ? 1 : 0;
+            c -= cy * fv_nc;
+            bb += fv_dbb + cy;
+            cy = bb >= g.HW ? 1 : 0;
+            bb -= cy * g.HW;
+            aa += fv_daa + cy;
+            if (!breal) continue;  // dummy brick: output bricks cleared, nothing written
+            int hs = hbase + aae;
+            if (g.wrapH) hs = wrap1(hs, g.Hsrc);
+            if (hs < 0 || hs >= g.Hsrc) continue;
+            const int ws = wrap1(wbase + bbe, g.W);
+            emit(sv.x, hs, ws, ce);
+            emit(sv.y, hs, ws, ce + 1);
+            emit(sv.z, hs, ws, ce + 2);
+            emit(sv.w, hs, ws, ce + 3);
+          }
+        } else {
+          int c = fl_c0, bb = fl_bb0, aa = fl_aa0;
+          for (int e = ew * 32 + lane; e < nob; e += nepi_act * 32) {
+            float sv = 0.f;
+            for (int q = 0; q < nepi_act; ++q) {
+              sv += ob[q * obs + e];
+              ob[q * obs + e] = 0.f;
+            }
+            const int ce = c, bbe = bb, aae = aa;
+            c += fl_dc;
+            int cy = c >= g.HT ? 1 : 0;
+            c -= cy * g.HT;
+            bb += fl_dbb + cy;
+            cy = bb >= g.HW ? 1 : 0;
+            bb -= cy * g.HW;
+            aa += fl_daa + cy;
+            if (!breal) continue;  // dummy brick: output bricks cleared, nothing written
+            int hs = hbase + aae;
+            if (g.wrapH) hs = wrap1(hs, g.Hsrc);
+            if (hs < 0 || hs >= g.Hsrc) continue;
+            emit(sv, hs, wrap1(wbase + bbe, g.W), ce);
+          }
         }
         named_sync(2, nepi_act * 32);
       }
