@@ -785,7 +785,7 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
                       float* W, const float* Bpk, const float* cvec, float* adj, double* norm2,
                       const IterState* st, cudaStream_t stream,
                       unsigned long long* dbg = nullptr, float amax = 0.f, bool pdl = false,
-                      unsigned long long* adjq = nullptr, double* npart = nullptr) {
+                      float2* adjq = nullptr, double* npart = nullptr) {
   TcConfig cfg = tc_config(gtc, t, fwd, Bpk != nullptr);
   icnnm_dev::tc::TcArgs& a = cfg.a;
   a.amax = amax;
@@ -936,7 +936,7 @@ struct Slab {
   int64_t halo_elems = 0;       // (kh-1) * W * T (slab mode)
   DBuf<float> Lt, adj, pm, mask, W;
   DBuf<float> Lr;                 // exact-residual mode: L_{t+1} (fp32, with halo rows)
-  DBuf<unsigned long long> adjq;  // deterministic adjoint: 64-bit fixed-point output (adj's layout)
+  DBuf<float2> adjq;              // deterministic adjoint: {hi, lo} fixed-grid pairs (adj's layout)
   DBuf<double> L, V;
 };
 
@@ -1275,7 +1275,7 @@ void launch_adj(Solver& S, Slab& s) {
                      use_pdl(S), S.det ? s.adjq.p : nullptr);
     ++S.launches;
     if (S.det) {
-      // fixed-point sums -> adj (fp32), accumulator cleared for the next launch
+      // {hi, lo} pairs -> adj (fp32), accumulator cleared for the next launch
       const int64_t n = static_cast<int64_t>(s.gtc.Hsrc) * s.gtc.W * s.gtc.T;
       cudaLaunchConfig_t lc{};
       cudaLaunchAttribute at{};
@@ -1287,8 +1287,7 @@ void launch_adj(Solver& S, Slab& s) {
       lc.attrs = &at;
       lc.numAttrs = use_pdl(S) ? 1 : 0;
       CK(cudaLaunchKernelEx(&lc, icnnm_dev::icnnm_adj_q2f, n,
-                            static_cast<const icnnm_dev::IterState*>(S.st.p), S.p.k, s.adjq.p,
-                            s.adj.p));
+                            static_cast<const icnnm_dev::IterState*>(S.st.p), s.adjq.p, s.adj.p));
       ++S.launches;
     }
     return;
@@ -2164,11 +2163,20 @@ void gram_lags_accumulate(const Problem& p, const double* dX, double* dR, cudaSt
     int bt = std::min(T, 64);
     const int cw = std::max(2, 2 * kt - 2);              // frames per step (kernel's CW)
     const int btp = (bt + 2 * cw - 1) / (2 * cw) * (2 * cw);
-    const int RS = bh * bw;
-    const size_t tile = static_cast<size_t>(RS) * (btp + 2) +
-                        static_cast<size_t>(bh) * (bw + 2 * (kw - 1)) * ((btp + cw) | 1);
-    // two tiles: the next brick's copies overlap the current brick's lags
-    const size_t smem = std::max(2 * tile, static_cast<size_t>(RS) * nl) * sizeof(double);
+    // two tiles (the next brick's copies overlap the current brick's lags) within
+    // the shared memory of a resident CTA: fewer rows per brick until they fit
+    const size_t limit = (kt <= 6 ? 110 : 220) * 1024;
+    size_t smem = 0;
+    for (;;) {
+      const size_t tile = static_cast<size_t>(bh) * bw * (btp + 2) +
+                          static_cast<size_t>(bh) * (bw + 2 * (kw - 1)) * ((btp + cw) | 1);
+      smem = std::max(2 * tile, static_cast<size_t>(bh) * bw * nl) * sizeof(double);
+      if (smem <= limit || (bh == 1 && bw == 1)) break;
+      if (bh > 1)
+        bh = (bh + 1) / 2;
+      else
+        bw = (bw + 1) / 2;
+    }
     check_smem(smem);
     static std::mutex mu;
     static std::map<void*, size_t> attr;  // opt-in dynamic shared memory per instantiation

@@ -513,22 +513,21 @@ __global__ void icnnm_fold(Partials P, int kp, double* red) {
 }
 
 // Deterministic adjoint output: the tcgen05 adjoint adds each brick's partial
-// sums into adjq as 64-bit fixed-point integers (scale 2^adjq_exp from the
-// iteration's st->adj_amax; integer adds commute exactly, so the result does
-// not depend on the order in which CTAs flush).  This converts the sums back
-// to fp32 adj and clears the accumulator for the next launch.
+// sums into adjq as {hi, lo} fp32 pairs on fixed grids (adj_grid,
+// icnnm_kernels.cuh: every add is exact, so the result does not depend on the
+// order in which CTAs flush).  This folds the pairs into fp32 adj and clears
+// the accumulator for the next launch.
 __global__ void __launch_bounds__(256)
-icnnm_adj_q2f(int64_t n, const IterState* __restrict__ st, int k,
-              unsigned long long* __restrict__ adjq, float* __restrict__ adj) {
+icnnm_adj_q2f(int64_t n, const IterState* __restrict__ st, float2* __restrict__ adjq,
+              float* __restrict__ adj) {
   pdl_wait();
   pdl_trigger();
   if (!st->active) return;
-  const double inv = ldexp(1.0, -adjq_exp(st->adj_amax, k));
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const long long q = static_cast<long long>(adjq[i]);
-  adjq[i] = 0ull;
-  adj[i] = static_cast<float>(static_cast<double>(q) * inv);
+  const float2 q = adjq[i];
+  adjq[i] = make_float2(0.f, 0.f);
+  adj[i] = static_cast<float>(static_cast<double>(q.x) + static_cast<double>(q.y));
 }
 
 // ---------------------------------------------------------------------------

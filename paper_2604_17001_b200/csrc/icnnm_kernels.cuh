@@ -33,18 +33,32 @@ constexpr int BK = 32;    // reduction chunk
 // bh*bw*bt == 128 and bt a multiple of 8; bricks tile the (H, W, T) box
 // (voxels outside the tensor are masked).  W rows are brick-ordered:
 // row = brick*128 + local voxel, so a CTA's 128 rows are contiguous.
-// Exponent e of the fixed-point scale 2^e of the deterministic adjoint output
-// (icnnm_tc.cu flush, icnnm_adj_q2f).  |adj_i| <= sum over k taps of
-// |U[v, s]| <= amax ||K[s, :]||_1 <= amax sqrt(k) (K orthogonal, amax the
-// coef kernel's bound on |W_vj c_j|), so amax k sqrt(k) 2^e < 2^61 leaves a
-// factor-of-two margin for rounding below the int64 range.
-__device__ __forceinline__ int adjq_exp(double amax, int k) {
-  if (!(amax > 0.0) || !(amax < 1e300)) return 0;
-  int ex;
-  frexp(2.0 * amax * static_cast<double>(k) * sqrt(static_cast<double>(k)), &ex);
-  int e = 61 - ex;
-  e = e > 1000 ? 1000 : (e < -1000 ? -1000 : e);
-  return e;
+// Deterministic adjoint output (icnnm_tc.cu flush, icnnm_adj_q2f).  Every
+// partial sum s a CTA flushes is split into two fp32 numbers on fixed grids,
+//   hi = rint(s / qh) qh,   lo = rint((s - hi) / ql) ql,   ql = qh 2^-17,
+// and added to the voxel's {hi, lo} pair with one vector reduction
+// (red.global.add.v2.f32).  With |adj_i| <= sum over k taps of |U[v, s]| <=
+// amax ||K[s, :]||_1 <= amax sqrt(k) k (K orthogonal, amax the coef kernel's
+// bound on |W_vj c_j|) and qh = 2^eh >= 2 amax k sqrt(k) 2^-23, every running
+// hi sum is a multiple of qh below 2^24 qh and every lo sum (<= 2^6
+// contributions of at most qh/2) a multiple of ql below 2^24 ql: all fp32 adds
+// are exact, so the result does not depend on the order in which CTAs flush.
+// What is dropped is at most ql/2 = 2^-41 of the bound per contribution.
+struct AdjGrid {
+  float qh, inv_qh, ql, inv_ql;
+};
+__device__ __forceinline__ AdjGrid adj_grid(double amax, int k) {
+  int ex = 0;
+  if (amax > 0.0 && amax < 1e300)
+    frexp(2.0 * amax * static_cast<double>(k) * sqrt(static_cast<double>(k)), &ex);
+  int eh = ex - 23;
+  eh = eh < -100 ? -100 : (eh > 100 ? 100 : eh);  // the lo grid stays above fp32 subnormals
+  AdjGrid g;
+  g.qh = ldexpf(1.f, eh);
+  g.inv_qh = ldexpf(1.f, -eh);
+  g.ql = ldexpf(1.f, eh - 17);
+  g.inv_ql = ldexpf(1.f, 17 - eh);
+  return g;
 }
 
 struct Geo {
@@ -113,8 +127,7 @@ __global__ void icnnm_coef(IterState* st, const double* theta, double* red, floa
                            IterStats* stats, int k, int kp, double kd, double res_scale,
                            double tol_p, double tol_c, double floor_rel, int exact, Partials P);
 __global__ void icnnm_fold(Partials P, int kp, double* red);
-__global__ void icnnm_adj_q2f(int64_t n, const IterState* st, int k, unsigned long long* adjq,
-                              float* adj);
+__global__ void icnnm_adj_q2f(int64_t n, const IterState* st, float2* adjq, float* adj);
 constexpr int UPD_U = 4;  // elements in flight per thread (icnnm_update)
 __global__ void icnnm_update(int64_t m, const IterState* st, double lambda, double kd,
                              float* adj, double* L, double* V, const float* pm,

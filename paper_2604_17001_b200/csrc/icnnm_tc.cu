@@ -69,6 +69,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef ICNNM_WAIT_HINT
+  // A/B: suspend-time hint (ns) -- a waiting warp sleeps longer per probe and
+  // takes fewer issue slots from the working warps
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(static_cast<uint32_t>(ICNNM_WAIT_HINT))
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -78,6 +91,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
@@ -1101,9 +1115,8 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       x = x >= n ? x - n : x;
       return (static_cast<unsigned>(x) < static_cast<unsigned>(n)) ? x : wrapi(x, n);
     };
-    // deterministic adjoint flush: 2^e of the fixed-point output (adjq_exp)
-    const double qscale =
-        (!FWD && a.adjq != nullptr) ? ldexp(1.0, adjq_exp(a.st->adj_amax, g.k)) : 1.0;
+    // deterministic adjoint flush: the {hi, lo} grids of this launch
+    const AdjGrid qg = adj_grid((!FWD && a.adjq != nullptr) ? a.st->adj_amax : 0.0, g.k);
     const uint32_t lead_accempty = PAIR ? mapa_u32(smem_u32(ACC_empty), 0) : 0u;
     for (int sl = sfirst; sl < nslot; sl += sstep, ++biter) {
       const int b = brick_of(sl);
@@ -1300,11 +1313,14 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           const size_t oi = (static_cast<size_t>(hs) * g.W + ws) * g.T + ts;
           if (a.adjq != nullptr) {
             // deterministic: the brick's partial sum (fixed order within the
-            // CTA) is added as a 64-bit fixed-point integer -- integer adds
-            // commute exactly, so the flush order across CTAs does not matter;
-            // icnnm_adj_q2f converts back (scale from the same st->adj_amax)
-            atomicAdd(a.adjq + oi, static_cast<unsigned long long>(
-                                       __double2ll_rn(static_cast<double>(sv) * qscale)));
+            // CTA) goes out as a {hi, lo} pair on fixed fp32 grids -- every
+            // add is exact, so the flush order across CTAs does not matter
+            // (adj_grid, icnnm_kernels.cuh); icnnm_adj_q2f folds the pairs
+            const float hi = rintf(sv * qg.inv_qh) * qg.qh;
+            const float lo = rintf((sv - hi) * qg.inv_ql) * qg.ql;
+            asm volatile("red.global.add.v2.f32 [%0], {%1, %2};\n" ::"l"(a.adjq + oi), "f"(hi),
+                         "f"(lo)
+                         : "memory");
           } else {
             atomicAdd(a.adj + oi, sv);
           }

@@ -77,7 +77,7 @@ struct alignas(64) TcArgs {
   int bres_stride;          // resident B: bytes per (tile, chunk) block
   int bres_bytes;           // resident B: SMEM bytes of the role's tiles x chunks
   // deterministic reductions (null: fp32 / fp64 atomics as before)
-  unsigned long long* adjq; // adjoint (mode 1): 64-bit fixed-point output, same layout as adj
+  float2* adjq;             // adjoint (mode 1): {hi, lo} fixed-grid output pairs, adj's layout
   double* npart;            // forward: per-CTA column partials [grid][kp] (mode 2: [grid])
   int nhb;                  // forward: halo buffers (2..NHB_MAX; the prep warps run nhb-2 ahead)
   int bstride;              // F16x3 single CTAs: B ring stage stride in bytes (0: B_STAGE_F16)
