@@ -660,7 +660,11 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   static const int sb_env = env_knob("ICNNM_TC_SB", -1);
   // F16x3 single CTAs: 8 stages (+1.8% / +1.3% over 4 / 6 on config 2,
   // profiles/ab_r1/tune/, profiles/ab_r1/sb8/)
-  const int sb_cap = sb_env > 0 ? sb_env : (pairs ? 8 : (t.f16 ? 8 : 4));
+  // (round 2: the F16x3 forward keeps 6 -- the shared memory of two more B
+  // stages holds two more 16 KB W-group stages, and the epilogue's W_old loads,
+  // not the B ring, are what its MMA warp ends up waiting for: config 2 forward
+  // 0.606 -> 0.583 ms, config 3 28.2 -> 28.1 ms; the adjoint loses with fewer)
+  const int sb_cap = sb_env > 0 ? sb_env : (pairs ? 8 : (t.f16 ? (fwd ? 6 : 8) : 4));
   static const int ws_cap = env_knob("ICNNM_TC_WS", icnnm_dev::tc::WS);
   // Adjoint epilogue: a second 4-warp half (alternate 32-column blocks, its
   // own 4 output bricks) when those bricks fit next to a B ring of >= 4
