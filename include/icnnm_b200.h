@@ -166,7 +166,9 @@ int icnnm_solver_kernel_times(icnnm_solver_t h, double* out_ms4);
 /* tcgen05 pipeline counters of the last run() with set_profile(h, 2):
  * 2 x 10 cycle sums (forward, adjoint): builder wait/work, MMA wait on A /
  * B / accumulator, epilogue wait/work, loader wait, MMA-thread total,
- * builder per-brick preparation (halo, operand scale). */
+ * builder per-brick preparation (halo, operand scale).  The counters are
+ * compiled into the experiments build only (make EXPERIMENTS=1); the product
+ * library reports zeros. */
 int icnnm_solver_tc_counters(icnnm_solver_t h, unsigned long long* out20);
 void icnnm_solver_destroy(icnnm_solver_t h);
 

@@ -332,7 +332,10 @@ TcPlan tc_plan(const Problem& p, bool f16 = false) {
   }
   best.nkc = kp / icnnm_dev::tc::KC;
   const int stage_cols = f16 ? icnnm_dev::tc::KC : 2 * icnnm_dev::tc::KC;
-  best.sa = std::min(icnnm_dev::tc::SA, (512 - 2 * best.wbase) / stage_cols);
+  // A stages: as many as TMEM leaves next to the two accumulators, up to a cap
+  // (ICNNM_TC_SA in the experiments build)
+  static const int sa_cap = env_knob("ICNNM_TC_SA", 6);
+  best.sa = std::min(std::min(icnnm_dev::tc::SA, sa_cap), (512 - 2 * best.wbase) / stage_cols);
   return best;
 }
 
@@ -677,6 +680,8 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   a.bres = 0;
   a.bres_stride = 0;
   a.bres_bytes = 0;
+  a.bmix = 0;
+  a.nresblk = 0;
   bool found = false;
   // Resident B (F16x3 single CTAs): when the basis tiles of one CTA role fit
   // in shared memory next to a W ring of >= 4 stages, they are loaded once
@@ -697,7 +702,45 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   static const int nhb_env = env_knob("ICNNM_TC_NHB", icnnm_dev::tc::NHB_MAX);
   for (int nhb = fwd ? std::min(nhb_env, icnnm_dev::tc::NHB_MAX) : 2; nhb >= 2 && !found; --nhb) {
   a.nhb = nhb;
-  if (t.f16 && !pairs && !a.mcb && have_b && bres_on) {
+  // Mixed residency (adjoint with tile groups): whole bricks per CTA -- the A
+  // operand (W c -> f16 hi/lo, the largest instruction item of the adjoint) is
+  // built once per brick and the col2im output box flushed once, instead of
+  // once per N-tile role -- with as many (tile, chunk) blocks of B resident
+  // as fit next to a tight ring of >= 3 stages for the rest.  Chosen when the
+  // whole basis does not fit (it does at ns = 1 only for small k) but at
+  // least a quarter of it does.  Measured at config 4: the halved builder and
+  // flush work is paid back by the MMA warp waiting on the half-streamed B
+  // (35% of its time; adjoint 0.362 vs 0.342 ms), so the mode is opt-in:
+  // ICNNM_TC_BMIX=1 (experiments build).
+  static const int bmix_env = env_knob("ICNNM_TC_BMIX", 0);  // measured slower (profiles/r2/README.md): opt-in
+  static const int bmix_sb = env_knob("ICNNM_TC_BMIX_SB", 4);
+  static const int bmix_ws = env_knob("ICNNM_TC_BMIX_WS", 4);
+  static const int bmix_eh = env_knob("ICNNM_TC_BMIX_EH", 2);
+  if (t.f16 && !pairs && !a.mcb && have_b && bres_on && !fwd && a.grp == 2 && bmix_env > 0) {
+    const int stride = t.wbase * icnnm_dev::tc::KC * 4;
+    const int nblk = t.ntn * t.nkc;
+    const int sbv = std::max(3, std::min(bmix_sb, icnnm_dev::tc::SB - 1));
+    const int wsv = std::max(4, std::min(bmix_ws, icnnm_dev::tc::WS) & ~1);
+    for (int eh = std::min(2, std::max(1, bmix_eh)); eh >= 1 && !found; --eh) {
+      const size_t base = icnnm_dev::tc::smem_bytes(gtc, fwd, sbv, wsv, t.f16, false, eh, 0, nhb, stride);
+      if (base >= 227 * 1024) continue;
+      const int fit = static_cast<int>((227 * 1024 - base) / stride);
+      // every block resident is the plain resident mode's business (below)
+      if (fit >= nblk || fit * 4 < nblk) continue;
+      a.nsplit = 1;
+      a.bres = 1;
+      a.bmix = 1;
+      a.nresblk = fit & ~1;  // chunk pairs are resident or streamed together
+      a.bres_stride = stride;
+      a.bres_bytes = a.nresblk * stride;
+      a.sb = sbv;
+      a.ws = wsv;
+      a.ehalf = eh;
+      a.bstride = stride;
+      found = true;
+    }
+  }
+  if (!found && t.f16 && !pairs && !a.mcb && have_b && bres_on) {
     const int stride = t.wbase * icnnm_dev::tc::KC * 4;
     for (int ns = 1; ns <= 4 && !found; ++ns) {
       if (ns > t.ntn) break;
@@ -726,7 +769,7 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   // shared memory holds up to twice as many chunks of lookahead
   static const int btight_env = env_knob("ICNNM_TC_BTIGHT", 0);
   const bool tight = t.f16 && !pairs && btight_env != 0;
-  a.bstride = tight ? t.wbase * icnnm_dev::tc::KC * 4 : 0;
+  if (!a.bmix) a.bstride = tight ? t.wbase * icnnm_dev::tc::KC * 4 : 0;
   const int sbc = tight ? std::max(sb_cap, icnnm_dev::tc::B_STAGE_F16 / std::max(1, a.bstride) * sb_cap)
                         : sb_cap;
   for (int eh = fwd ? 1 : (eh_env > 0 ? eh_env : 2); eh >= 1 && !found; --eh) {
@@ -747,7 +790,7 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   cfg.smem = icnnm_dev::tc::smem_bytes(gtc, fwd, a.sb, a.ws, t.f16, pairs, a.ehalf, a.bres_bytes,
-                                       a.nhb, a.bres ? 0 : a.bstride);
+                                       a.nhb, (a.bres && !a.bmix) ? 0 : a.bstride, a.bmix != 0);
   if (cfg.smem > 227 * 1024) invalid("icnnm_b200: tcgen05 engine shared memory exceeds 227 KB");
   cfg.fn = fwd ? icnnm_dev::tc::fwd_kernel_ptr(t.f16, a.cs > 1)
                : icnnm_dev::tc::adj_kernel_ptr(t.f16, a.cs > 1);
@@ -1362,10 +1405,13 @@ void launch_coef(Solver& S, const icnnm_solver_config& cfg, double kd, double re
   // sharded solves fold before the all-reduce (icnnm_fold); else the coef
   // kernel folds
   const icnnm_dev::Partials P = S.sharded ? icnnm_dev::Partials{} : partials(S);
+  // work-skipping timing experiments (experiments build): garbage iterates stop
+  // changing, which would end the solve on l_change = 0
+  static const bool never_stop = env_knob("ICNNM_NEVER_STOP", 0) != 0;
   icnnm_dev::icnnm_coef<<<1, 1024, 0, S.stream>>>(S.st.p, S.theta.p, S.red.p, S.cvec.p,
                                                   S.stats.p, S.p.k, engine_kp(S), kd, res_scale,
-                                                  cfg.tol_primal, cfg.tol_change, floor_rel,
-                                                  S.exact_res ? 1 : 0, P);
+                                                  cfg.tol_primal, never_stop ? -1.0 : cfg.tol_change,
+                                                  floor_rel, S.exact_res ? 1 : 0, P);
   CKL();
 }
 

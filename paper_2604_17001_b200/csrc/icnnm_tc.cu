@@ -45,10 +45,17 @@ namespace tc {
 
 // Work-skipping timing switches (TcArgs::skip) exist only in the experiments
 // build (make EXPERIMENTS=1); the shipped kernels compile them out.
+// So do the in-kernel pipeline counters (TcArgs::dbg) and the per-thread
+// barrier arrivals (TcArgs::warr = 0): in the shipped kernels every role's
+// chunk loop is short enough that these checks showed up in its time.
 #ifdef ICNNM_EXPERIMENTS
 #define TC_SKIP(a) ((a).skip)
+#define TC_DBG(a) ((a).dbg)
+#define TC_WARR(a) ((a).warr != 0)
 #else
 #define TC_SKIP(a) 0
+#define TC_DBG(a) (static_cast<unsigned long long*>(nullptr))
+#define TC_WARR(a) true
 #endif
 
 // ---------------------------------------------------------------------------
@@ -300,6 +307,48 @@ __device__ __forceinline__ void tc_chunk_f16(uint32_t d, uint32_t a, uint32_t al
       "r"(bar_acc), "r"(flags)
       : "memory");
 }
+// Lean form of tc_chunk_f16 for the product path (single CTAs): the B
+// descriptors arrive as their low words (the high word -- SBO 256 B, version 1,
+// SWIZZLE_NONE -- is a constant), the lo tile's descriptor is the hi tile's plus
+// a word offset, and the B-stage commit is optional (flags bit 2; resident
+// blocks release nothing).  flags: 1 = release the A stage, 2 = accumulator
+// complete, 4 = release the B stage.
+__device__ __forceinline__ void tc_chunk_f16_lean(uint32_t d, uint32_t a, uint32_t blo,
+                                                  uint32_t lo_off, uint32_t idesc, uint32_t accum,
+                                                  uint32_t bar_b, uint32_t bar_a, uint32_t bar_acc,
+                                                  uint32_t flags) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t, qa, qc, qb;\n"
+      ".reg .b32 f, l2, a2;\n"
+      ".reg .b64 dh, dl;\n"
+      "setp.ne.b32 p, %5, 0;\n"
+      "setp.eq.b32 t, %5, %5;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "and.b32 f, %9, 1;\n"
+      "setp.ne.b32 qa, f, 0;\n"
+      "and.b32 f, %9, 2;\n"
+      "setp.ne.b32 qc, f, 0;\n"
+      "and.b32 f, %9, 4;\n"
+      "setp.ne.b32 qb, f, 0;\n"
+      "and.pred qa, qa, e;\n"
+      "and.pred qc, qc, e;\n"
+      "and.pred qb, qb, e;\n"
+      "add.u32 l2, %2, %3;\n"
+      "add.u32 a2, %1, %10;\n"
+      "mov.b64 dh, {%2, %11};\n"
+      "mov.b64 dl, {l2, %11};\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], dh, %4, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], dh, %4, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], dl, %4, t;\n"
+      "@qb tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
+      "@qa tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n"
+      "@qc tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n"
+      "}\n" ::"r"(d),
+      "r"(a), "r"(blo), "r"(lo_off), "r"(idesc), "r"(accum), "r"(bar_b), "r"(bar_a), "r"(bar_acc),
+      "r"(flags), "r"(static_cast<uint32_t>(KC / 2)), "r"(0x4010u)
+      : "memory");
+}
 // tc_chunk_f16 for B-multicast clusters: the B-stage release is committed to
 // the barrier at the same offset in both CTAs of the 2-CTA cluster (the stage
 // is refilled, for both, only after both CTAs' MMAs have read it).
@@ -526,8 +575,11 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   uint8_t* p = smem;
   const int sbn = a.sb, wsn = a.ws, san = a.sa;
   const uint32_t a_col0 = 2u * static_cast<uint32_t>(a.accw);
+  // resident B blocks (a.bres) first, then the stage ring (absent when every
+  // block of the CTA's role is resident)
   float* Bst = reinterpret_cast<float*>(p);
-  p += a.bres ? a.bres_bytes : sbn * BSTG;
+  uint8_t* Bring = p + (a.bres ? a.bres_bytes : 0);
+  p = Bring + ((a.bres && !a.bmix) ? 0 : sbn * BSTG);
   float* Wst = reinterpret_cast<float*>(p);   // adjoint: W-chunk ring; forward: W-group ring
   p += wsn * (FWD ? WO_STAGE_BYTES : W_STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p);
@@ -587,7 +639,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
 
   // consumer / producer hand-over arrive of a whole warp: lane 0 after a warp
   // sync (a.warr), or every lane
-  const bool warr = a.warr != 0;
+  const bool warr = TC_WARR(a);
   auto warp_arrive = [&](uint64_t* b) {
     if (warr) {
       __syncwarp();
@@ -623,7 +675,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     // arrivals per barrier phase: one per warp (a.warr: the warp's lane 0 after
     // __syncwarp; 128 single-lane arrives on one mbarrier serialise in the
     // shared-memory atomic unit) or one per thread
-    const int per = a.warr ? 1 : 32;
+    const int per = TC_WARR(a) ? 1 : 32;
     const int nbuild = ((a.bsplit && !F16) ? NB : NB / 2) * per;  // builder arrivals / chunk
     // PAIR: the leader's A_full / ACC_empty count one arrival per warp of both
     // CTAs; its B_full the local expect_tx plus the peer's relayed arrival
@@ -678,7 +730,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       }
       off = (sh * g.HW + sw) * g.HT + st;
     }
-    tapoff[s] = off;
+    tapoff[s] = 4 * off;  // byte offsets: one subtraction per gathered / scattered element
   }
   // everything above reads only the launch parameters: with PDL it overlaps
   // the predecessor kernel; from here on the predecessor's writes are read
@@ -762,6 +814,12 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   auto bres_off = [&](int nt, int kc) {
     return static_cast<uint32_t>(((nt - ntb) * nkr + (kc - kcb)) * a.bres_stride);
   };
+  // mixed residency (a.bmix): only the role's first a.nresblk (tile, chunk)
+  // blocks are resident, the others stream through the ring
+  auto is_res = [&](int nt, int kc) {
+    return a.bres && (!a.bmix || (nt - ntb) * nkr + (kc - kcb) < a.nresblk);
+  };
+  uint64_t* const BRES_full = B_full + (SB - 1);   // resident fill (one phase per launch)
   int skew = a.skew < nkr / 2 ? a.skew : nkr / 2;
   skew = skew < san ? skew : san;
   skew = skew < 0 ? 0 : skew;
@@ -791,7 +849,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     const int hidx = ((vh + g.kh - 1) * g.HW + (vw + g.kw - 1)) * g.HT + (vt + g.kt - 1);
     const uint32_t lane_base = static_cast<uint32_t>(32 * quad) << 16;
     uint32_t cnt = 0;
-    Dbg dbg(lane == 0 ? a.dbg : nullptr);
+    Dbg dbg(lane == 0 ? TC_DBG(a) : nullptr);
     // F16x3 operand scale: forward per brick (the halo is prescaled in place);
     // adjoint: folded into cs
     // (the held chunk c and the next owned chunk c+2 must use different A and
@@ -820,10 +878,13 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     // its TMEM-store round trip; the loop visits only the owned chunks
     const int nchunk = ngrp * nkr;
     const int cstep = (F16 || !a.bsplit) ? 2 : 1;
+
     long long prep = 0;
     for (int sl = sfirst; sl < nslot; sl += sstep, ++iter) {
       const int hbuf = iter % nhb;
       float* hcur = halo + hbuf * nobp;
+      // this thread's halo element, as a byte pointer (tap offsets are in bytes)
+      const char* const hb = reinterpret_cast<const char*>(hcur + hidx);
       const long long tp0 = dbg.p ? clk() : 0;
       // forward: this brick's halo (prescaled / pre-split for F16x3) is
       // prepared by the prep warps while the previous brick is built
@@ -866,11 +927,11 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             }
             if (F16 && FWD) {
               // pre-split halo words {hi, lo}: hi pair = low halves, lo pair = high halves
-              const uint32_t* hw = reinterpret_cast<const uint32_t*>(hcur);
               uint32_t hi[8], lo[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const uint32_t w0 = hw[hidx - tq[2 * i]], w1 = hw[hidx - tq[2 * i + 1]];
+                const uint32_t w0 = *reinterpret_cast<const uint32_t*>(hb - tq[2 * i]);
+                const uint32_t w1 = *reinterpret_cast<const uint32_t*>(hb - tq[2 * i + 1]);
                 hi[i] = __byte_perm(w0, w1, 0x5410);
                 lo[i] = __byte_perm(w0, w1, 0x7632);
               }
@@ -884,7 +945,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
                 float x[2];
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                  x[u] = FWD ? hcur[hidx - tq[2 * i + u]]
+                  x[u] = FWD ? *reinterpret_cast<const float*>(hb - tq[2 * i + u])
                              : Wst[wsi * (W_STAGE_BYTES / 4) + (2 * i + u) * 128 + row] * cq[2 * i + u];
                 }
                 hi[i] = pack_f16x2(x[0], x[1]);
@@ -899,7 +960,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 const int q = kc * KC + 8 * half + i;
-                const float x = FWD ? hcur[hidx - tapoff[q]]
+                const float x = FWD ? *reinterpret_cast<const float*>(hb - tapoff[q])
                                     : Wst[wsi * (W_STAGE_BYTES / 4) + (8 * half + i) * 128 + row] * cs[q];
                 const uint32_t h = f2tf32(x);
                 hi[i] = h;
@@ -913,7 +974,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
                 uint32_t hi[8], lo[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                  const float x = FWD ? hcur[hidx - tq[8 * hh + i]]
+                  const float x = FWD ? *reinterpret_cast<const float*>(hb - tq[8 * hh + i])
                                       : Wst[wsi * (W_STAGE_BYTES / 4) + (8 * hh + i) * 128 + row] * cq[8 * hh + i];
                   const uint32_t h = f2tf32(x);
                   hi[i] = h;
@@ -1096,7 +1157,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     uint32_t gbase = 0;  // forward: W-group ring slot of the current tile's first group
     float gacc = 0.f;  // mode 2: this thread's share of ||(1-c)W - A(L)K||^2
     uint32_t tcount = 0;
-    Dbg dbg(lane == 0 ? a.dbg : nullptr);
+    Dbg dbg(lane == 0 ? TC_DBG(a) : nullptr);
     float us_adj = 1.f;  // F16x3 adjoint: 2^-(eA + eB)
     if (F16 && !FWD)
       us_adj = a.bunscale / f16_scale(a.mode >= 1 ? static_cast<float>(a.st->adj_amax) : a.amax);
@@ -1233,14 +1294,14 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             if ((g.vmap ? g.kw : g.kh) >= 4 && ncol == 32 && s0 + 32 <= g.k) {
               // full block of real taps: the 4 tap offsets of a batch in one
               // broadcast 128-bit load, no per-column predicates
-              float* const obase = myob + hidx;
+              char* const obase = reinterpret_cast<char*>(myob + hidx);
 #pragma unroll
               for (int i = 0; i < 32; i += 4) {
                 const int4 t4 = *reinterpret_cast<const int4*>(tapoff + s0 + i);
-                float* const o0 = obase - t4.x;
-                float* const o1 = obase - t4.y;
-                float* const o2 = obase - t4.z;
-                float* const o3 = obase - t4.w;
+                float* const o0 = reinterpret_cast<float*>(obase - t4.x);
+                float* const o1 = reinterpret_cast<float*>(obase - t4.y);
+                float* const o2 = reinterpret_cast<float*>(obase - t4.z);
+                float* const o3 = reinterpret_cast<float*>(obase - t4.w);
                 const float x0 = *o0, x1 = *o1, x2 = *o2, x3 = *o3;
                 if (F16) {
                   *o0 = fmaf(__uint_as_float(u[i]), us, x0);
@@ -1266,7 +1327,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
                 for (int q = 0; q < 4; ++q) {
                   const int sidx = s0 + i + q;
                   const bool ok = (i + q < ncol) && sidx < g.k;
-                  o[q] = myob + (ok ? hidx - tapoff[sidx] : nobp + lane);  // per-lane scratch
+                  o[q] = myob + (ok ? hidx - (tapoff[sidx] >> 2) : nobp + lane);  // per-lane scratch
                   v[q] = ok ? __uint_as_float(u[i + q]) : 0.f;
                 }
                 float x[4];
@@ -1281,7 +1342,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
               for (int i = 0; i < 32; ++i) {
                 const int sidx = s0 + i;
                 if (i < ncol && sidx < g.k) {
-                  float* o = myob + (hidx - tapoff[sidx]);
+                  float* o = myob + (hidx - (tapoff[sidx] >> 2));
                   *o += accv(i);
                 }
                 __syncwarp();
@@ -1302,7 +1363,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           dbg.acc[1] += t2c - t1c;
         }
       }
-      if (!FWD) {
+      if (!FWD && !(TC_SKIP(a) & 128)) {
         named_sync(2, nepi_act * 32);
         // flush: element e = (aa*HW + bb)*HT + c of the output box, advanced by
         // the step in mixed radix (no per-element divisions)
@@ -1435,11 +1496,11 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       uint32_t cnt = 0, tcount = 0;
       int sb = 0;
       uint32_t bph = 0;
-      const uint32_t bs0 = smem_u32(Bst);
+      const uint32_t bs0 = smem_u32(Bst), br0 = smem_u32(Bring);
       const uint32_t bar_af = smem_u32(A_full), bar_ae = smem_u32(A_empty);
       const uint32_t bar_bf = smem_u32(B_full), bar_be = smem_u32(B_empty);
       const uint32_t bar_accf = smem_u32(ACC_full);
-      long long wa = 0, wb = 0, wacc = 0, tstart = a.dbg ? clk() : 0;
+      long long wa = 0, wb = 0, wacc = 0, tstart = TC_DBG(a) ? clk() : 0;
       uint32_t idesc_t[2], dcol_t[2];
       int wn_t[2];
       // MMAs of chunk kc (A stage sa, parity aph) into tile t of the current group
@@ -1448,26 +1509,27 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       auto issue = [&](int t, int kc, int sa, uint32_t aph, bool first_use, bool last_use) {
         if (kc == kcb) {
           const uint32_t tci = tcount + static_cast<uint32_t>(t);
-          long long q0 = a.dbg ? clk() : 0;
+          long long q0 = TC_DBG(a) ? clk() : 0;
           if (!(TC_SKIP(a) & 32)) {
             if (PAIR)
               pwait(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
             else
               mbar_wait(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
           }
-          if (a.dbg) wacc += clk() - q0;
+          if (TC_DBG(a)) wacc += clk() - q0;
         }
-        long long q1 = a.dbg ? clk() : 0;
+        long long q1 = TC_DBG(a) ? clk() : 0;
         if (first_use && !(TC_SKIP(a) & 8)) {
           if (PAIR)
             pwait(A_full + sa, aph);
           else
             mbar_wait(A_full + sa, aph);
         }
-        long long q2 = a.dbg ? clk() : 0;
-        if (a.bres) {
+        long long q2 = TC_DBG(a) ? clk() : 0;
+        const bool res = is_res(cur_nt0 + t, kc);
+        if (res) {
           if (!bres_ready) {
-            mbar_wait(B_full, 0);  // resident B: one fill per launch (phase 0)
+            mbar_wait(BRES_full, 0);  // resident B: one fill per launch (phase 0)
             bres_ready = true;
           }
         } else if (!(TC_SKIP(a) & 16)) {
@@ -1476,31 +1538,33 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           else
             mbar_wait(B_full + sb, bph);
         }
-        if (a.dbg) {
+        if (TC_DBG(a)) {
           long long q3 = clk();
           wa += q2 - q1;
           wb += q3 - q2;
         }
         tc_fence_after();
         const uint32_t acol = tbase + a_col0 + sa * ASC;
-        const uint32_t bhi = a.bres ? bs0 + bres_off(cur_nt0 + t, kc) : bs0 + sb * BSTG;
+        const uint32_t bhi = res ? bs0 + bres_off(cur_nt0 + t, kc) : br0 + sb * BSTG;
+        // resident blocks release no stage: their commit goes to a barrier nobody waits on
+        const uint32_t bar_b = bar_be + 8u * static_cast<uint32_t>(res ? SB - 1 : sb);
         const uint32_t dcol = dcol_t[t], idesc = idesc_t[t];
         const int wn = wn_t[t];
         const bool acc_done = kc == kce - 1 && !(TC_SKIP(a) & 32);
         if (PAIR) {
           // this CTA's half of B: hi rows [0, wn/2) then lo rows (wn/2 x 32 B each)
           tc_chunk_f16_pair(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + (wn / 2) * 32), idesc,
-                            kc == kcb ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
+                            kc == kcb ? 0u : 1u, bar_b, bar_ae + 8u * sa,
                             bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
                             (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
         } else if (MCB && !(TC_SKIP(a) & 24)) {
           tc_chunk_f16_mcb(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + wn * 32), idesc,
-                           kc == kcb ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
+                           kc == kcb ? 0u : 1u, bar_b, bar_ae + 8u * sa,
                            bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
                            (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
         } else if (F16 && !(TC_SKIP(a) & 24)) {
           tc_chunk_f16(dcol, acol, acol + ALO, bdesc(bhi), bdesc(bhi + wn * 32), idesc,
-                       kc == kcb ? 0u : 1u, bar_be + 8u * sb, bar_ae + 8u * sa,
+                       kc == kcb ? 0u : 1u, bar_b, bar_ae + 8u * sa,
                        bar_accf + 8u * ((tcount + static_cast<uint32_t>(t)) & 1),
                        (last_use ? 1u : 0u) | (acc_done ? 2u : 0u));
         } else {
@@ -1523,16 +1587,17 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             }
           }
           if (last_use && !(TC_SKIP(a) & 8)) tc_commit_elect(A_empty + sa);
-          if (!(TC_SKIP(a) & 16) && !a.bres) tc_commit_elect(B_empty + sb);
+          if (!(TC_SKIP(a) & 16) && !res) tc_commit_elect(B_empty + sb);
           if (acc_done) tc_commit_elect(ACC_full + ((tcount + static_cast<uint32_t>(t)) & 1));
         }
-        if (++sb == sbn) {
+        if (!res && ++sb == sbn) {
           sb = 0;
           bph ^= 1u;
         }
       };
       (void)bar_af;
       (void)bar_bf;
+
       // A-stage (index, parity) of chunk ci, advanced incrementally within a phase
       struct StageIt {
         int s;
@@ -1547,6 +1612,95 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           x.ph ^= 1u;
         }
       };
+      // Product fast path (F16x3 single CTAs, no counters): the per-chunk issue
+      // sequence was the serial bottleneck of both kernels -- ~70 instructions
+      // and ~370 non-waiting cycles per 192-cycle chunk at k = 245
+      // (profiles/r2/README.md) -- so this loop keeps every launch parameter in
+      // registers, advances descriptors / stages incrementally and commits
+      // nothing for resident B blocks.
+      bool lean = false;
+      if constexpr (F16 && !PAIR) lean = !MCB && TC_DBG(a) == nullptr && (TC_SKIP(a) & ~(1 | 2 | 128 | 256)) == 0;
+      if (lean) {
+        const uint32_t a0 = tbase + a_col0;
+        const int bres = a.bres, bmix = a.bmix, nresblk = a.nresblk;
+        const uint32_t res_lo0 = ((bs0 >> 4) & 0x3FFFu) | 0x80000u;   // LBO 128 B
+        const uint32_t ring_lo0 = ((br0 >> 4) & 0x3FFFu) | 0x80000u;
+        const uint32_t res_step = static_cast<uint32_t>(a.bres_stride) >> 4;
+        const uint32_t ring_step = static_cast<uint32_t>(BSTG) >> 4;
+        const uint32_t accw = static_cast<uint32_t>(a.accw);
+        // one K-chunk of tile t of the current group from A stage (sa, aph)
+        auto chunk = [&](int t, int c, int sa, uint32_t aph, bool first_use, bool last_use) {
+          const uint32_t tci = tcount + static_cast<uint32_t>(t);
+          if (c == 0) mbar_wait(ACC_empty + (tci & 1), ((tci >> 1) & 1) ^ 1);
+          if (first_use) mbar_wait(A_full + sa, aph);
+          const int blk = (cur_nt0 + t - ntb) * nkr + c;
+          uint32_t blo, fl = (last_use ? 1u : 0u) | (c == nkr - 1 ? 2u : 0u);
+          if (bres && (!bmix || blk < nresblk)) {
+            if (!bres_ready) {
+              mbar_wait(BRES_full, 0);
+              bres_ready = true;
+            }
+            blo = res_lo0 + static_cast<uint32_t>(blk) * res_step;
+          } else {
+            mbar_wait(B_full + sb, bph);
+            blo = ring_lo0 + static_cast<uint32_t>(sb) * ring_step;
+            fl |= 4u;
+          }
+          tc_fence_after();
+          tc_chunk_f16_lean(tbase + (tci & 1) * accw, a0 + sa * ASC, blo,
+                            static_cast<uint32_t>(wn_t[t]) * 2u, idesc_t[t], c == 0 ? 0u : 1u,
+                            bar_be + 8u * sb, bar_ae + 8u * sa, bar_accf + 8u * (tci & 1), fl);
+          if ((fl & 4u) && ++sb == sbn) {
+            sb = 0;
+            bph ^= 1u;
+          }
+        };
+        int sa = 0;        // A stage of the next chunk (chunks are consumed in build order)
+        uint32_t aph = 0;
+        for (int sl = sfirst; sl < nslot; sl += sstep) {
+          for (int gi = 0; gi < ngrp; ++gi) {
+            const int nt0 = ntb + gi * grp;
+            const int gsz = (nte - nt0) < grp ? (nte - nt0) : grp;
+            cur_nt0 = nt0;
+            for (int t = 0; t < gsz; ++t) {
+              wn_t[t] = tile_width(a, nt0 + t);
+              idesc_t[t] = idesc_f16(wn_t[t]);
+            }
+            auto adv = [&](int& s_, uint32_t& p_) {
+              if (++s_ == san) {
+                s_ = 0;
+                p_ ^= 1u;
+              }
+            };
+            if (gsz == 1) {
+              for (int c = 0; c < nkr; ++c) {
+                chunk(0, c, sa, aph, true, true);
+                adv(sa, aph);
+              }
+            } else {  // the tg_seq order, phase by phase (A stage iterators x, y)
+              int xs = sa;
+              uint32_t xp = aph;
+              for (int c = 0; c < skew; ++c, adv(xs, xp)) chunk(0, c, xs, xp, true, false);
+              xs = sa;
+              xp = aph;
+              for (int c = 0; c < skew; ++c, adv(xs, xp)) chunk(1, c, xs, xp, false, true);
+              for (int c = skew; c < nkr - skew; ++c, adv(xs, xp)) {
+                chunk(0, c, xs, xp, true, false);
+                chunk(1, c, xs, xp, false, true);
+              }
+              const int ys = xs;
+              const uint32_t yp = xp;
+              for (int c = nkr - skew; c < nkr; ++c, adv(xs, xp)) chunk(0, c, xs, xp, true, false);
+              xs = ys;
+              xp = yp;
+              for (int c = nkr - skew; c < nkr; ++c, adv(xs, xp)) chunk(1, c, xs, xp, false, true);
+              sa = xs;
+              aph = xp;
+            }
+            tcount += static_cast<uint32_t>(gsz);
+          }
+        }
+      } else
       for (int sl = sfirst; sl < nslot; sl += sstep) {
         for (int gi = 0; gi < ngrp; ++gi) {
           const int nt0 = ntb + gi * grp;
@@ -1578,60 +1732,64 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           tcount += static_cast<uint32_t>(gsz);
         }
       }
-      if (a.dbg && lane == 0) {
-        atomicAdd(a.dbg + DBG_MMA_WAIT_A, static_cast<unsigned long long>(wa));
-        atomicAdd(a.dbg + DBG_MMA_WAIT_B, static_cast<unsigned long long>(wb));
-        atomicAdd(a.dbg + DBG_MMA_WAIT_ACC, static_cast<unsigned long long>(wacc));
-        atomicAdd(a.dbg + DBG_TOTAL, static_cast<unsigned long long>(clk() - tstart));
+      if (TC_DBG(a) && lane == 0) {
+        atomicAdd(TC_DBG(a) + DBG_MMA_WAIT_A, static_cast<unsigned long long>(wa));
+        atomicAdd(TC_DBG(a) + DBG_MMA_WAIT_B, static_cast<unsigned long long>(wb));
+        atomicAdd(TC_DBG(a) + DBG_MMA_WAIT_ACC, static_cast<unsigned long long>(wacc));
+        atomicAdd(TC_DBG(a) + DBG_TOTAL, static_cast<unsigned long long>(clk() - tstart));
       }
     }
     __syncwarp();
   } else if (warp == WLOAD) {
     // ===================== B loader =====================
-    if (lane == 0 && a.bres) {
-      // resident B: this CTA's tiles x chunks, loaded once (one barrier phase)
-      // and read by every brick's MMAs; only when the CTA has a brick (its
-      // MMA warp then waits for the fill before the CTA can exit)
-      if (sfirst < nslot) {
-        uint32_t total = 0;
-        for (int nt = ntb; nt < nte; ++nt)
-          total += static_cast<uint32_t>(nkr * tile_width(a, nt) * KC * (F16 ? 4 : 8));
-        mbar_arrive_expect_tx(B_full, total);
-        for (int nt = ntb; nt < nte; ++nt) {
-          const uint32_t bytes = static_cast<uint32_t>(tile_width(a, nt)) * KC * (F16 ? 4 : 8);
-          for (int kc = kcb; kc < kce; ++kc)
+    if (lane == 0 && a.bres && sfirst < nslot) {
+      // resident B: this CTA's (tile, chunk) blocks -- all of them, or the first
+      // a.nresblk (mixed residency) -- loaded once (one barrier phase) and read
+      // by every brick's MMAs; only when the CTA has a brick (its MMA warp then
+      // waits for the fill before the CTA can exit)
+      uint32_t total = 0;
+      for (int nt = ntb; nt < nte; ++nt)
+        for (int kc = kcb; kc < kce; ++kc)
+          if (is_res(nt, kc)) total += static_cast<uint32_t>(tile_width(a, nt) * KC * (F16 ? 4 : 8));
+      mbar_arrive_expect_tx(BRES_full, total);
+      for (int nt = ntb; nt < nte; ++nt) {
+        const uint32_t bytes = static_cast<uint32_t>(tile_width(a, nt)) * KC * (F16 ? 4 : 8);
+        for (int kc = kcb; kc < kce; ++kc)
+          if (is_res(nt, kc))
             bulk_g2s(reinterpret_cast<uint8_t*>(Bst) + bres_off(nt, kc),
                      a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4), bytes,
-                     B_full);
-        }
+                     BRES_full);
       }
-    } else if (lane == 0 && !(TC_SKIP(a) & 16)) {
+    }
+    if (lane == 0 && (!a.bres || a.bmix) && !(TC_SKIP(a) & 16)) {
       uint32_t bcnt = 0;
       long long wl = 0;
       for (int sl = sfirst; sl < nslot; sl += sstep) {
         for (int gi = 0; gi < ngrp; ++gi) {
           const int nt0 = ntb + gi * grp;
           const int gsz = (nte - nt0) < grp ? (nte - nt0) : grp;
-          for (int i = 0; i < gsz * nkr; ++i, ++bcnt) {
+          for (int i = 0; i < gsz * nkr; ++i) {
             int t, kc;
             tg_seq(i, gsz, nkr, skew, t, kc);
             kc += kcb;
             const int nt = nt0 + t;
+            if (is_res(nt, kc)) continue;  // resident block: no stage
             const int wn = tile_width(a, nt);
             const uint32_t bytes = static_cast<uint32_t>(wn) * KC * (F16 ? 4 : 8);
             const int sb = bcnt % sbn;
-            long long q0 = a.dbg ? clk() : 0;
+            long long q0 = TC_DBG(a) ? clk() : 0;
             if (CL2)
               pwait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
             else
               mbar_wait(B_empty + sb, ((bcnt / sbn) & 1) ^ 1);
-            if (a.dbg) wl += clk() - q0;
+            ++bcnt;
+            if (TC_DBG(a)) wl += clk() - q0;
             if (TC_SKIP(a) & 4) {
               mbar_arrive(B_full + sb);  // timing experiment: no B traffic
               continue;
             }
             const float* src = a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4);
-            uint8_t* dst = reinterpret_cast<uint8_t*>(Bst) + sb * BSTG;
+            uint8_t* dst = Bring + sb * BSTG;
             if (PAIR && a.tma_pair) {
               // this CTA's half of the N rows (hi, then lo) as two 2-SM tensor
               // copies that complete_tx on the leader's B_full, which expects
@@ -1672,7 +1830,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       if (CL2)
         for (int q = 0; q < sbn; ++q, ++bcnt)
           pwait(B_empty + bcnt % sbn, ((bcnt / sbn) & 1) ^ 1);
-      if (a.dbg) atomicAdd(a.dbg + DBG_LOAD_WAIT, static_cast<unsigned long long>(wl));
+      if (TC_DBG(a)) atomicAdd(TC_DBG(a) + DBG_LOAD_WAIT, static_cast<unsigned long long>(wl));
     }
     __syncwarp();
   } else if (FWD && warp == WLOAD + 1) {
@@ -1716,6 +1874,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           for (int kc = kcb; kc < kce; ++kc, ++wcnt) {
             const int wsi = wcnt % wsn;
             mbar_wait(W_empty + wsi, ((wcnt / wsn) & 1) ^ 1);
+            if (TC_SKIP(a) & 256) {  // timing experiment: no W traffic
+              mbar_arrive(W_full + wsi);
+              continue;
+            }
             mbar_arrive_expect_tx(W_full + wsi, W_STAGE_BYTES);
             const float* src = a.Win + (static_cast<size_t>(b) * g.kp + kc * KC) * 128;
             bulk_g2s(reinterpret_cast<uint8_t*>(Wst) + wsi * W_STAGE_BYTES, src, W_STAGE_BYTES,

@@ -12,7 +12,7 @@ namespace icnnm_dev {
 namespace tc {
 
 constexpr int KC = 16;                         // K per chunk (tf32: 2 MMA K-steps of 8; f16: 1 of 16)
-constexpr int SA = 6;                          // TMEM A stages (max; runtime a.sa); tf32: 2*KC
+constexpr int SA = 16;                         // TMEM A stages (max; runtime a.sa); tf32: 2*KC
                                                // columns each, f16: KC columns (2 halves / column)
 constexpr int NSC = 8;                         // F16x3 forward: per-brick scale ring
 constexpr int SB = 16;                         // SMEM B stages (max; runtime a.sb)
@@ -23,7 +23,7 @@ constexpr int NTMAX = 208;                     // max accumulator width (N per t
 constexpr int B_STAGE_BYTES = 256 * KC * 4 * 2;    // hi + lo, up to 256 rows = 32 KB (tf32;
                                                    // also the packed-block stride in global)
 constexpr int B_STAGE_F16 = 256 * KC * 2 * 2;      // f16 hi + lo: 16 KB SMEM stage
-constexpr int BAR_BYTES = 768;  // mbarriers + scale ring + halo maxima + halo barriers
+constexpr int BAR_BYTES = 1024;  // mbarriers + scale ring + halo maxima + halo barriers
 static_assert((2 * SA + 2 * SB + 4 + 2 * WS + NSC) * 8 + NSC * 4 + 16 * 4 + 2 * 4 * 8 <= BAR_BYTES,
               "barrier block overflows BAR_BYTES");
 constexpr int NPREP = 4;  // forward: halo-preparation warps
@@ -75,7 +75,11 @@ struct alignas(64) TcArgs {
                             // ranges, adjoint: K-chunk ranges (single CTAs only)
   int bres;                 // 1: the role's B tiles are resident in SMEM (one load per launch)
   int bres_stride;          // resident B: bytes per (tile, chunk) block
-  int bres_bytes;           // resident B: SMEM bytes of the role's tiles x chunks
+  int bres_bytes;           // resident B: SMEM bytes of the role's resident blocks
+  int bmix;                 // 1: mixed residency -- only the role's first nresblk (tile, chunk)
+                            // blocks are resident, the rest stream through the sb-stage ring
+                            // (whole bricks per CTA: A built once per brick, B half-streamed)
+  int nresblk;              // mixed residency: resident blocks, in (tile, chunk) order
   // deterministic reductions (null: fp32 / fp64 atomics as before)
   float2* adjq;             // adjoint (mode 1): {hi, lo} fixed-grid output pairs, adj's layout
   double* npart;            // forward: per-CTA column partials [grid][kp] (mode 2: [grid])
@@ -99,11 +103,13 @@ void* adj_kernel_ptr(bool f16, bool pair = false);
 inline int threads(bool fwd) { return fwd ? 608 + 32 * NPREP : 608; }
 
 inline size_t smem_bytes(const Geo& g, bool fwd, int sb, int ws, bool f16, bool pair = false,
-                         int ehalf = 1, int bres_bytes = 0, int nhb = 2, int bstride = 0) {
+                         int ehalf = 1, int bres_bytes = 0, int nhb = 2, int bstride = 0,
+                         bool bmix = false) {
   const size_t nob = static_cast<size_t>(g.HH) * g.HW * g.HT;
   const size_t nobp = ((nob + 3) / 4) * 4;
   const size_t stage = bstride > 0 ? static_cast<size_t>(bstride) : b_stage_bytes(f16, pair);
-  size_t b = (bres_bytes > 0 ? static_cast<size_t>(bres_bytes) : static_cast<size_t>(sb) * stage) +
+  size_t b = static_cast<size_t>(bres_bytes) +
+             ((bres_bytes > 0 && !bmix) ? 0 : static_cast<size_t>(sb) * stage) +
              static_cast<size_t>(ws) * (fwd ? WO_STAGE_BYTES : W_STAGE_BYTES) + BAR_BYTES + 16;
   b += ((g.ktp * 4 + 15) / 16) * 16;
   b += ((g.kp * 4 + 15) / 16) * 16;

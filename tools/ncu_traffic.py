@@ -38,12 +38,14 @@ def main():
         i = hdr.index(key)
         v = float(r[i].replace(",", ""))
         u = units[i]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1,
                  "usecond": 1e-6, "msecond": 1e-3, "second": 1}.get(u, 1)
         return v * scale
     res = {}
-    for kind, tag in (("forward", "icnnm_tc_kernel<(bool)1"), ("adjoint", "icnnm_tc_kernel<(bool)0")):
-        ks = [r for r in data if tag in r[name_i].replace("true", "(bool)1").replace("false", "(bool)0")]
+    def norm(n):  # "<true, ...>", "<(bool)1, ...>" and "<1, ...>" spellings of the same kernel
+        return n.replace("(bool)", "").replace("true", "1").replace("false", "0")
+    for kind, tag in (("forward", "icnnm_tc_kernel<1"), ("adjoint", "icnnm_tc_kernel<0")):
+        ks = [r for r in data if tag in norm(r[name_i])]
         if not ks:
             continue
         t = [col(r, "gpu__time_duration.sum") for r in ks]
