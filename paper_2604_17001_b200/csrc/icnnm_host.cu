@@ -1321,8 +1321,10 @@ void launch_adj(Solver& S, Slab& s) {
                      S.tc_counters ? S.dbg.p + icnnm_dev::tc::DBG_SLOTS : nullptr, 0.f,
                      use_pdl(S), S.det ? s.adjq.p : nullptr);
     ++S.launches;
-    if (S.det) {
+    if (S.det && S.sharded) {
       // {hi, lo} pairs -> adj (fp32), accumulator cleared for the next launch
+      // (sharded: the halo rows of adj are exchanged before the update; the
+      // unsharded update folds the pairs itself, launch_update)
       const int64_t n = static_cast<int64_t>(s.gtc.Hsrc) * s.gtc.W * s.gtc.T;
       cudaLaunchConfig_t lc{};
       cudaLaunchAttribute at{};
@@ -1433,7 +1435,9 @@ void launch_update(Solver& S, Slab& s, const icnnm_solver_config& cfg, double kd
                         static_cast<const float*>(s.mask.p), s.Lt.p + s.halo_elems,
                         S.red.p + engine_kp(S),
                         S.exact_res ? s.Lr.p + s.halo_elems : static_cast<float*>(nullptr),
-                        upart));
+                        upart,
+                        (S.det && !S.sharded && is_tc(S.engine)) ? s.adjq.p
+                                                                 : static_cast<float2*>(nullptr)));
 }
 
 void allreduce_red(Solver& S) {

@@ -631,7 +631,7 @@ icnnm_update(int64_t m, const IterState* __restrict__ st, double lambda, double 
              float* __restrict__ adj, double* __restrict__ L, double* __restrict__ V,
              const float* __restrict__ pm, const float* __restrict__ mask,
              float* __restrict__ Lt, double* __restrict__ slot, float* __restrict__ Lr,
-             double* __restrict__ upart) {
+             double* __restrict__ upart, float2* __restrict__ adjq) {
   pdl_wait();
   pdl_trigger();
   if (!st->active) return;
@@ -648,7 +648,14 @@ icnnm_update(int64_t m, const IterState* __restrict__ st, double lambda, double 
     for (int u = 0; u < UPD_U; ++u) {
       const int64_t i = i0 + u * stride;
       if (i < m) {
-        a_[u] = adj[i];
+        if (adjq != nullptr) {
+          // deterministic adjoint, unsharded: fold the {hi, lo} grid pair here
+          // (the rounding of icnnm_adj_q2f) and clear it for the next launch
+          const float2 q = adjq[i];
+          a_[u] = static_cast<float>(static_cast<double>(q.x) + static_cast<double>(q.y));
+        } else {
+          a_[u] = adj[i];
+        }
         lo_[u] = L[i];
         mk_[u] = mask[i];
         p_[u] = pm[i];
@@ -669,7 +676,10 @@ icnnm_update(int64_t m, const IterState* __restrict__ st, double lambda, double 
       L[i] = ln;
       Lt[i] = static_cast<float>(ln + r * d);
       if (Lr != nullptr) Lr[i] = static_cast<float>(ln);
-      adj[i] = 0.f;
+      if (adjq != nullptr)
+        adjq[i] = make_float2(0.f, 0.f);
+      else
+        adj[i] = 0.f;
       V[i] = r * (kd * lo - a - kd * ln);
       const double f = mk * (ln - p);
       acc[0] += d * d;

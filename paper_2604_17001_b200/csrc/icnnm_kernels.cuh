@@ -132,7 +132,7 @@ constexpr int UPD_U = 4;  // elements in flight per thread (icnnm_update)
 __global__ void icnnm_update(int64_t m, const IterState* st, double lambda, double kd,
                              float* adj, double* L, double* V, const float* pm,
                              const float* mask, float* Lt, double* slot, float* Lr,
-                             double* upart);
+                             double* upart, float2* adjq);
 __global__ void icnnm_add_rows(int64_t n, float* dst, float* src);
 __global__ void icnnm_setup(int64_t m, const double* M, const double* msk, int mean_fill,
                             double mean, float* pm, float* maskf, double* L, double* V,
