@@ -137,13 +137,18 @@ def load_peaks():
 
 
 def lib_sha16() -> str:
-    """Identity of the product library build (pairs ncu traffic with a build)."""
-    path = os.path.join(ROOT, "paper_2604_17001_b200", "libicnnm_b200.so")
+    """Identity of the product library's kernel sources (pairs an ncu traffic
+    capture with a build: the hash of the tcgen05 / elementwise kernel sources,
+    which a rebuild on another box reproduces, unlike a hash of the .so)."""
+    h = hashlib.sha256()
+    base = os.path.join(ROOT, "paper_2604_17001_b200", "csrc")
     try:
-        with open(path, "rb") as f:
-            return hashlib.sha256(f.read()).hexdigest()[:16]
+        for name in ("icnnm_tc.cu", "icnnm_tc.cuh", "icnnm_kernels.cu", "icnnm_kernels.cuh"):
+            with open(os.path.join(base, name), "rb") as f:
+                h.update(f.read())
     except OSError:
         return "missing"
+    return h.hexdigest()[:16]
 
 
 def load_ncu_traffic(config: int, engine: str):

@@ -785,6 +785,7 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
         }
   }
   }  // nhb
+  icnnm_dev::tc::tc_fill_taps(a, fwd);
   a.nbricks = n_bricks(gtc);
   int dev = 0, nsm = 148;
   CK(cudaGetDevice(&dev));

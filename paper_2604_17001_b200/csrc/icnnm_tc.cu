@@ -52,10 +52,12 @@ namespace tc {
 #define TC_SKIP(a) ((a).skip)
 #define TC_DBG(a) ((a).dbg)
 #define TC_WARR(a) ((a).warr != 0)
+#define TC_BPAIR(a) ((a).bpair != 0)
 #else
 #define TC_SKIP(a) 0
 #define TC_DBG(a) (static_cast<unsigned long long*>(nullptr))
 #define TC_WARR(a) true
+#define TC_BPAIR(a) false
 #endif
 
 // ---------------------------------------------------------------------------
@@ -600,7 +602,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
   p += BAR_BYTES;  // 2*SA + 2*SB + 4 + 2*WS + NSC mbarriers, NSC scales, 16 maxima
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p);
   p += 16;
-  int* tapoff = reinterpret_cast<int*>(p);
+  // (ktp words kept in the carve-up: smem_bytes() is shared with the host)
   p += ((g.ktp * 4 + 15) / 16) * 16;
   float* cs = reinterpret_cast<float*>(p);
   p += ((g.kp * 4 + 15) / 16) * 16;
@@ -702,36 +704,9 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int s = tid; s < g.ktp; s += blockDim.x) {
-    int off = 0;
-    if (s < g.k) {
-      int st, sw, sh;
-      if (FWD) {
-        st = s % g.kt;
-        const int q = s / g.kt;
-        sw = q % g.kw;
-        sh = q / g.kw;
-      } else {
-        // adjoint N order (host adj_tap): vmap 0 -- sh fastest: within a warp
-        // the 32 rows share vh, so taps with different sh never hit the same
-        // output cell and the col2im scatter can batch them hazard-free;
-        // vmap 1 -- the rows share vw, sw fastest
-        if (g.vmap) {
-          sw = s % g.kw;
-          const int q = s / g.kw;
-          st = q % g.kt;
-          sh = q / g.kt;
-        } else {
-          sh = s % g.kh;
-          const int q = s / g.kh;
-          st = q % g.kt;
-          sw = q / g.kt;
-        }
-      }
-      off = (sh * g.HW + sw) * g.HT + st;
-    }
-    tapoff[s] = 4 * off;  // byte offsets: one subtraction per gathered / scattered element
-  }
+  // (tap offsets: a.tapn, negative byte offsets filled by the host -- read
+  // through the constant bank with warp-uniform indices, so gathers and
+  // scatters address shared memory as [thread base + uniform offset])
   // everything above reads only the launch parameters: with PDL it overlaps
   // the predecessor kernel; from here on the predecessor's writes are read
   pdl_wait();
@@ -854,7 +829,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     // adjoint: folded into cs
     // (the held chunk c and the next owned chunk c+2 must use different A and
     // W stages: sa >= 3 always; the adjoint's W ring needs 4)
-    const bool pair = !PAIR && (F16 || !a.bsplit) && a.bpair && san >= 3 && (FWD || wsn >= 4);
+    const bool pair = TC_BPAIR(a) && !PAIR && (F16 || !a.bsplit) && san >= 3 && (FWD || wsn >= 4);
     const uint32_t lead_afull = PAIR ? mapa_u32(smem_u32(A_full), 0) : 0u;
     int pend_sa = -1, pend_wsi = 0;
     int iter = 0;
@@ -918,7 +893,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
 #pragma unroll
             for (int v4 = 0; v4 < KC / 4; ++v4) {
               if (FWD) {
-                const int4 t4 = reinterpret_cast<const int4*>(tapoff + kc * KC)[v4];
+                const int4 t4 = reinterpret_cast<const int4*>(a.tapn + kc * KC)[v4];
                 tq[4 * v4] = t4.x; tq[4 * v4 + 1] = t4.y; tq[4 * v4 + 2] = t4.z; tq[4 * v4 + 3] = t4.w;
               } else {
                 const float4 c4 = reinterpret_cast<const float4*>(cs + kc * KC)[v4];
@@ -930,8 +905,8 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
               uint32_t hi[8], lo[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const uint32_t w0 = *reinterpret_cast<const uint32_t*>(hb - tq[2 * i]);
-                const uint32_t w1 = *reinterpret_cast<const uint32_t*>(hb - tq[2 * i + 1]);
+                const uint32_t w0 = *reinterpret_cast<const uint32_t*>(hb + tq[2 * i]);
+                const uint32_t w1 = *reinterpret_cast<const uint32_t*>(hb + tq[2 * i + 1]);
                 hi[i] = __byte_perm(w0, w1, 0x5410);
                 lo[i] = __byte_perm(w0, w1, 0x7632);
               }
@@ -945,7 +920,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
                 float x[2];
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
-                  x[u] = FWD ? *reinterpret_cast<const float*>(hb - tq[2 * i + u])
+                  x[u] = FWD ? *reinterpret_cast<const float*>(hb + tq[2 * i + u])
                              : Wst[wsi * (W_STAGE_BYTES / 4) + (2 * i + u) * 128 + row] * cq[2 * i + u];
                 }
                 hi[i] = pack_f16x2(x[0], x[1]);
@@ -960,7 +935,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 const int q = kc * KC + 8 * half + i;
-                const float x = FWD ? *reinterpret_cast<const float*>(hb - tapoff[q])
+                const float x = FWD ? *reinterpret_cast<const float*>(hb + a.tapn[q])
                                     : Wst[wsi * (W_STAGE_BYTES / 4) + (8 * half + i) * 128 + row] * cs[q];
                 const uint32_t h = f2tf32(x);
                 hi[i] = h;
@@ -974,7 +949,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
                 uint32_t hi[8], lo[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                  const float x = FWD ? *reinterpret_cast<const float*>(hb - tq[8 * hh + i])
+                  const float x = FWD ? *reinterpret_cast<const float*>(hb + tq[8 * hh + i])
                                       : Wst[wsi * (W_STAGE_BYTES / 4) + (8 * hh + i) * 128 + row] * cq[8 * hh + i];
                   const uint32_t h = f2tf32(x);
                   hi[i] = h;
@@ -1008,7 +983,20 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             if (!FWD) warp_arrive(W_empty + wsi);
           } else {
             tc_fence_before();
-            warp_arrive2(A_full + sa, FWD ? nullptr : W_empty + wsi);
+            if constexpr (FWD) {
+              warp_arrive(A_full + sa);
+            } else {  // one warp sync, both arrivals from lane 0
+              if (warr) {
+                __syncwarp();
+                if (lane == 0) {
+                  mbar_arrive(A_full + sa);
+                  mbar_arrive(W_empty + wsi);
+                }
+              } else {
+                mbar_arrive(A_full + sa);
+                mbar_arrive(W_empty + wsi);
+              }
+            }
           }
           if (dbg.p) {
             long long t2c = clk();
@@ -1297,11 +1285,11 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
               char* const obase = reinterpret_cast<char*>(myob + hidx);
 #pragma unroll
               for (int i = 0; i < 32; i += 4) {
-                const int4 t4 = *reinterpret_cast<const int4*>(tapoff + s0 + i);
-                float* const o0 = reinterpret_cast<float*>(obase - t4.x);
-                float* const o1 = reinterpret_cast<float*>(obase - t4.y);
-                float* const o2 = reinterpret_cast<float*>(obase - t4.z);
-                float* const o3 = reinterpret_cast<float*>(obase - t4.w);
+                const int4 t4 = *reinterpret_cast<const int4*>(a.tapn + s0 + i);
+                float* const o0 = reinterpret_cast<float*>(obase + t4.x);
+                float* const o1 = reinterpret_cast<float*>(obase + t4.y);
+                float* const o2 = reinterpret_cast<float*>(obase + t4.z);
+                float* const o3 = reinterpret_cast<float*>(obase + t4.w);
                 const float x0 = *o0, x1 = *o1, x2 = *o2, x3 = *o3;
                 if (F16) {
                   *o0 = fmaf(__uint_as_float(u[i]), us, x0);
@@ -1327,7 +1315,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
                 for (int q = 0; q < 4; ++q) {
                   const int sidx = s0 + i + q;
                   const bool ok = (i + q < ncol) && sidx < g.k;
-                  o[q] = myob + (ok ? hidx - (tapoff[sidx] >> 2) : nobp + lane);  // per-lane scratch
+                  o[q] = myob + (ok ? hidx + (a.tapn[sidx] >> 2) : nobp + lane);  // per-lane scratch
                   v[q] = ok ? __uint_as_float(u[i + q]) : 0.f;
                 }
                 float x[4];
@@ -1342,7 +1330,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
               for (int i = 0; i < 32; ++i) {
                 const int sidx = s0 + i;
                 if (i < ncol && sidx < g.k) {
-                  float* o = myob + (hidx - (tapoff[sidx] >> 2));
+                  float* o = myob + (hidx + (a.tapn[sidx] >> 2));
                   *o += accv(i);
                 }
                 __syncwarp();
@@ -1921,5 +1909,42 @@ void* adj_kernel_ptr(bool f16, bool pair) {
              : reinterpret_cast<void*>(&icnnm_tc_kernel<false, false, false>);
 }
 
+}  // namespace tc
+}  // namespace icnnm_dev
+
+namespace icnnm_dev {
+namespace tc {
+// Host: the tap table of one kernel (TcArgs::tapn) from its geometry.
+void tc_fill_taps(TcArgs& a, bool fwd) {
+  const Geo& g = a.g;
+  for (int s = 0; s < TAPMAX; ++s) {
+    int off = 0;
+    if (s < g.k) {
+      int st, sw, sh;
+      if (fwd) {
+        st = s % g.kt;
+        const int q = s / g.kt;
+        sw = q % g.kw;
+        sh = q / g.kw;
+      } else if (g.vmap) {
+        // adjoint N order (host adj_tap): vmap 1 -- the warp's rows share vw, sw fastest
+        sw = s % g.kw;
+        const int q = s / g.kw;
+        st = q % g.kt;
+        sh = q / g.kt;
+      } else {
+        // vmap 0 -- sh fastest: within a warp the 32 rows share vh, so taps
+        // with different sh never hit the same output cell and the col2im
+        // scatter can batch them hazard-free
+        sh = s % g.kh;
+        const int q = s / g.kh;
+        st = q % g.kt;
+        sw = q / g.kt;
+      }
+      off = (sh * g.HW + sw) * g.HT + st;
+    }
+    a.tapn[s] = -4 * off;
+  }
+}
 }  // namespace tc
 }  // namespace icnnm_dev

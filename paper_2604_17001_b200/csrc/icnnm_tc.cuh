@@ -33,6 +33,8 @@ inline int b_stage_bytes(bool f16, bool pair = false) {
   return f16 ? (pair ? B_STAGE_F16 / 2 : B_STAGE_F16) : B_STAGE_BYTES;
 }
 
+constexpr int TAPMAX = 4096;  // taps (the C ABI's kernel-size limit), padded to 32
+
 struct alignas(64) TcArgs {
   // CTA pairs (F16x3): 2-D views (rows of 32 B) of the packed B tiles for
   // cp.async.bulk.tensor .cta_group::2 -- each CTA's half-tile copy signals
@@ -86,7 +88,13 @@ struct alignas(64) TcArgs {
   int nhb;                  // forward: halo buffers (2..NHB_MAX; the prep warps run nhb-2 ahead)
   int bstride;              // F16x3 single CTAs: B ring stage stride in bytes (0: B_STAGE_F16)
   int warr;                 // 1: one mbarrier arrival per warp (lane 0 after __syncwarp); 0: per thread
+  // Tap table: minus the byte offset of tap s inside the halo / output box, in
+  // this kernel's tap order (forward: t fastest; adjoint: the N order of its B
+  // tiles).  In the parameters so that the warp-uniform index reads go through
+  // the constant bank into uniform registers (tc_fill_taps).
+  alignas(16) int tapn[TAPMAX];
 };
+void tc_fill_taps(TcArgs& a, bool fwd);
 
 // dbg slots (cycles summed over CTAs)
 enum { DBG_BUILD_WAIT = 0, DBG_BUILD_WORK, DBG_MMA_WAIT_A, DBG_MMA_WAIT_B, DBG_MMA_WAIT_ACC,

@@ -57,8 +57,12 @@ def main():
         res[kind + "_write"] = wr
         res[kind + "_ncu_ms"] = statistics.median(col(r, "gpu__time_duration.sum") for r in big) * 1e3
         res[kind + "_launches"] = len(big)
-    with open(a.lib, "rb") as f:
-        res["lib_sha16"] = hashlib.sha256(f.read()).hexdigest()[:16]
+    # the kernel sources' hash, as bench.py's lib_sha16() (the capture must be of this tree)
+    h = hashlib.sha256()
+    for name in ("icnnm_tc.cu", "icnnm_tc.cuh", "icnnm_kernels.cu", "icnnm_kernels.cuh"):
+        with open(os.path.join(ROOT, "paper_2604_17001_b200", "csrc", name), "rb") as f:
+            h.update(f.read())
+    res["lib_sha16"] = h.hexdigest()[:16]
     res["report"] = os.path.basename(a.report)
     try:
         with open(a.out) as f:
