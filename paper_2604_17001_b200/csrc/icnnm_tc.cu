@@ -395,6 +395,20 @@ __device__ __forceinline__ void unpack_f16x2(uint32_t h, float& x0, float& x1) {
       : "=f"(x0), "=f"(x1)
       : "r"(h));
 }
+// Packed fp32 pairs (sm_100 FMUL2 / FADD2): one instruction per two products /
+// differences of the adjoint's operand build.
+__device__ __forceinline__ void mul_f32x2(float& a0, float& a1, float b0, float b1) {
+  asm("{\n.reg .b64 a, b;\nmov.b64 a, {%0, %1};\nmov.b64 b, {%2, %3};\nmul.rn.f32x2 a, a, b;\n"
+      "mov.b64 {%0, %1}, a;\n}\n"
+      : "+f"(a0), "+f"(a1)
+      : "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void sub_f32x2(float& a0, float& a1, float b0, float b1) {
+  asm("{\n.reg .b64 a, b;\nmov.b64 a, {%0, %1};\nmov.b64 b, {%2, %3};\nsub.rn.f32x2 a, a, b;\n"
+      "mov.b64 {%0, %1}, a;\n}\n"
+      : "+f"(a0), "+f"(a1)
+      : "f"(b0), "f"(b1));
+}
 // Power-of-2 scale putting values of magnitude <= amax below 2^14 (f16 max 65504).
 __device__ __forceinline__ float f16_scale(float amax) {
   if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
@@ -921,12 +935,14 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
                   x[u] = FWD ? *reinterpret_cast<const float*>(hb + tq[2 * i + u])
-                             : Wst[wsi * (W_STAGE_BYTES / 4) + (2 * i + u) * 128 + row] * cq[2 * i + u];
+                             : Wst[wsi * (W_STAGE_BYTES / 4) + (2 * i + u) * 128 + row];
                 }
+                if (!FWD) mul_f32x2(x[0], x[1], cq[2 * i], cq[2 * i + 1]);
                 hi[i] = pack_f16x2(x[0], x[1]);
                 float h0, h1;
                 unpack_f16x2(hi[i], h0, h1);
-                lo[i] = pack_f16x2(x[0] - h0, x[1] - h1);
+                sub_f32x2(x[0], x[1], h0, h1);
+                lo[i] = pack_f16x2(x[0], x[1]);
               }
               tmem_st8(tbase + lane_base + col, hi);
               tmem_st8(tbase + lane_base + col + ALO, lo);
