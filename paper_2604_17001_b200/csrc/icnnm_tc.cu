@@ -826,6 +826,35 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     return bb < nbr ? bb : nbr - 1;
   };
   auto real_slot = [&](int sl) { return sl * ncta + crank < nbr; };
+  // Brick coordinates (t fastest) of this CTA's slots, advanced by sstep in
+  // mixed radix for single CTAs (three integer divisions per brick and thread
+  // otherwise: 3-4% of either kernel's instructions at k = 245); clusters
+  // (clamped dummy tail brick) divide.
+  struct BrickIt {
+    int bt, bw, bh;
+  };
+  const int bs_t = sstep % g.nbt, bs_w = (sstep / g.nbt) % g.nbw, bs_h = sstep / (g.nbt * g.nbw);
+  auto brick_at = [&](int b) {
+    BrickIt x;
+    x.bt = b % g.nbt;
+    const int q = b / g.nbt;
+    x.bw = q % g.nbw;
+    x.bh = q / g.nbw;
+    return x;
+  };
+  auto brick_next = [&](BrickIt& x, int sl_next) {
+    if (ncta > 1) {
+      x = brick_at(brick_of(sl_next));
+      return;
+    }
+    x.bt += bs_t;
+    int cy = x.bt >= g.nbt ? 1 : 0;
+    x.bt -= cy * g.nbt;
+    x.bw += bs_w + cy;
+    cy = x.bw >= g.nbw ? 1 : 0;
+    x.bw -= cy * g.nbw;
+    x.bh += bs_h + cy;
+  };
 
   if (warp < NB && !(TC_SKIP(a) & 8)) {
     // ===================== builders =====================
@@ -869,6 +898,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     const int cstep = (F16 || !a.bsplit) ? 2 : 1;
 
     long long prep = 0;
+    int f = cstep == 2 ? half : 0;  // my next chunk, relative to the current brick
+    adv_stage(f);
+    int kc = kcb + f;
+    if (kc >= kce) kc -= nkr;
     for (int sl = sfirst; sl < nslot; sl += sstep, ++iter) {
       const int hbuf = iter % nhb;
       float* hcur = halo + hbuf * nobp;
@@ -879,11 +912,10 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       // prepared by the prep warps while the previous brick is built
       if (FWD) mbar_wait(HALO_full + hbuf, static_cast<uint32_t>(iter / nhb) & 1u);
       if (dbg.p) prep += clk() - tp0;
-      int f = cstep == 2 ? ((static_cast<int>(cnt) ^ half) & 1) : 0;  // my first chunk
-      adv_stage(f);
-      int kc = kcb + f;
-      if (kc >= kce) kc -= nkr;
       {
+        // (this group's chunks are every cstep-th of the global chunk sequence:
+        // its stage iterator, kc and brick-local index f simply advance by
+        // cstep, across bricks too)
         for (; f < nchunk; f += cstep) {
           // A / W stage (index, parity) of this chunk, advanced incrementally
           // (cnt % san and cnt / san were a 32-bit division per chunk)
@@ -1019,12 +1051,13 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             dbg.acc[0] += t1c - t0c;
             dbg.acc[1] += t2c - t1c;
           }
-          adv_stage((nchunk - f) < cstep ? (nchunk - f) : cstep);
+          adv_stage(cstep);
           kc += cstep;
-          while (kc >= kce) kc -= nkr;
+          if (kc >= kce) kc -= nkr;
         }
       }
       cnt += static_cast<uint32_t>(nchunk);
+      f -= nchunk;
       if (pair && pend_sa >= 0) {  // flush the brick's last owned chunk
         if (!(TC_SKIP(a) & 1)) tmem_wait_st();
         tc_fence_before();
@@ -1065,15 +1098,16 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       x = x >= n ? x - n : x;
       return (static_cast<unsigned>(x) < static_cast<unsigned>(n)) ? x : wrapi(x, n);
     };
+    BrickIt pk = brick_at(brick_of(sfirst < nslot ? sfirst : 0));
     auto issue = [&](int i, int sl) {
       const int buf = i % nhb;
       float* hdst = halo + buf * nobp;
       // (timing experiments without builders: nobody releases the buffers)
       if (!(TC_SKIP(a) & 8)) mbar_wait(HALO_empty + buf, (static_cast<uint32_t>(i / nhb) & 1u) ^ 1u);
-      const int b = brick_of(sl);
-      const int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
-      const int hb0 = bh_i * g.bh - (g.kh - 1) + g.hoff, wb0 = bw_i * g.bw - (g.kw - 1),
-                tb0 = bt_i * g.bt - (g.kt - 1);
+      // (issue() is called for this CTA's slots in order: pk is slot sl's brick)
+      const int hb0 = pk.bh * g.bh - (g.kh - 1) + g.hoff, wb0 = pk.bw * g.bw - (g.kw - 1),
+                tb0 = pk.bt * g.bt - (g.kt - 1);
+      brick_next(pk, sl + sstep);
       int c = c0, bb = bb0, aa = aa0;
       for (int e = pt; e < ngrp_h; e += PSTEP) {
         int hs = hb0 + aa;
@@ -1159,6 +1193,8 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     float* myob = ob + (FWD ? quad : ew) * obs;  // adjoint: one output brick per warp
     const int NHALF = ehalf;
     uint32_t gbase = 0;  // forward: W-group ring slot of the current tile's first group
+    int ep_ws = half;    // forward: this half's next W-group ring slot and its parity
+    uint32_t ep_wph = 0;
     float gacc = 0.f;  // mode 2: this thread's share of ||(1-c)W - A(L)K||^2
     uint32_t tcount = 0;
     Dbg dbg(lane == 0 ? TC_DBG(a) : nullptr);
@@ -1183,11 +1219,11 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     // deterministic adjoint flush: the {hi, lo} grids of this launch
     const AdjGrid qg = adj_grid((!FWD && a.adjq != nullptr) ? a.st->adj_amax : 0.0, g.k);
     const uint32_t lead_accempty = PAIR ? mapa_u32(smem_u32(ACC_empty), 0) : 0u;
-    for (int sl = sfirst; sl < nslot; sl += sstep, ++biter) {
+    BrickIt bk = brick_at(brick_of(sfirst < nslot ? sfirst : 0));
+    for (int sl = sfirst; sl < nslot; sl += sstep, ++biter, brick_next(bk, sl)) {
       const int b = brick_of(sl);
       const bool breal = real_slot(sl);  // false: the pair's dummy tail brick, nothing written
-      int bt_i = b % g.nbt, tmp = b / g.nbt, bw_i = tmp % g.nbw, bh_i = tmp / g.nbw;
-      const int h0 = bh_i * g.bh, w0 = bw_i * g.bw, t0 = bt_i * g.bt;
+      const int h0 = bk.bh * g.bh, w0 = bk.bw * g.bw, t0 = bk.bt * g.bt;
       const bool valid = breal && (h0 + vh < g.H) && (w0 + vw < g.W) && (t0 + vt < g.T);
       const bool bfull = (h0 + g.bh <= g.H) && (w0 + g.bw <= g.W) && (t0 + g.bt <= g.T);
       float us = us_adj;
@@ -1209,9 +1245,14 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           // column norms and written back with one bulk store
           const int ng = (wn + 31) / 32, ngp = ng + (ng & 1);  // even: one half per stage
           for (int gq = half; gq < ngp; gq += 2) {
-            const uint32_t gsl = gbase + gq;
-            const int wsl = static_cast<int>(gsl % wsn);
-            mbar_wait(W_full + wsl, (gsl / wsn) & 1);
+            // this half's ring slot: two groups further every visit (even ring)
+            const int wsl = ep_ws;
+            mbar_wait(W_full + wsl, ep_wph);
+            ep_ws += 2;
+            if (ep_ws >= wsn) {
+              ep_ws -= wsn;
+              ep_wph ^= 1u;
+            }
             if (gq < ng && !(TC_SKIP(a) & 2)) {
               const int c0 = 32 * gq;
               const int ncol = (wn - c0) < 32 ? (wn - c0) : 32;
