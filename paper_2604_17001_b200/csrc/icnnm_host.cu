@@ -639,9 +639,24 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   // TMEM but loads only half of every B tile (N split across the pair), so the
   // B stream -- 13.3 KB per 312-cycle chunk and SM, the largest L2 and SMEM
   // consumer (and a quarter of the board power, profiles/ab_r1) -- halves.
-  // ICNNM_TC_CS=2 enables (A/B experiments; first measurement: slower, see DESIGN).
+  // With a streamed B they are on par with single CTAs (DESIGN 11), so the
+  // default uses them only where they change what fits in shared memory: the
+  // adjoint of a basis that single CTAs can keep resident only as two N-tile
+  // roles (each building the brick's A operand, flushing its own output box and
+  // streaming W again) but a pair keeps resident as halves with whole bricks per
+  // CTA (config 4: adjoint 0.295 -> 0.249 ms; the forward, whose tiles do not
+  // share built chunks, loses 11% and stays on single CTAs).
+  // ICNNM_TC_CS=1|2 (experiments build) forces single CTAs / pairs for both kernels.
   static const int cs_env = env_knob("ICNNM_TC_CS", -1);
-  a.cs = cs_env >= 0 ? cs_env : 1;  // pairs: opt-in until they beat single CTAs
+  a.cs = cs_env >= 0 ? cs_env : 1;
+  if (cs_env < 0 && !fwd && t.f16 && have_b && env_knob("ICNNM_TC_BRES", -1) != 0) {
+    const int full = t.ntn * t.nkc * t.wbase * icnnm_dev::tc::KC * 4;
+    const bool single_fits =
+        icnnm_dev::tc::smem_bytes(gtc, fwd, 1, 4, true, false, 1, full, 2) <= 227 * 1024;
+    const bool pair_fits =
+        icnnm_dev::tc::smem_bytes(gtc, fwd, 1, 4, true, true, 1, full / 2, 2) <= 227 * 1024;
+    if (!single_fits && pair_fits && t.ntn >= 2 && t.sa >= 4) a.cs = 2;
+  }
   if (!t.f16 || n_bricks(gtc) < 2) a.cs = 1;
   const bool pairs = a.cs > 1;
   // pairs: the peer's half of every B stage signals the leader's barrier
@@ -739,6 +754,26 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
       a.bstride = stride;
       found = true;
     }
+  }
+  // CTA pairs with resident B: each CTA keeps its half of every tile's N rows
+  // (hi half, lo half), so a basis that needs two N-tile roles as single CTAs
+  // (config 4: 256 KB) is resident with whole bricks per CTA -- A built once
+  // per brick, one output-box flush, one W stream -- and no B ring at all.
+  if (!found && t.f16 && pairs && have_b && bres_on) {
+    const int stride = t.wbase * icnnm_dev::tc::KC * 4 / 2;
+    const int need = t.ntn * t.nkc * stride;
+    for (int eh = fwd ? 1 : 2; eh >= 1 && !found; --eh)
+      for (int wsv = std::min(ws_cap, icnnm_dev::tc::WS) & ~1; wsv >= 4 && !found; wsv -= 2)
+        if (icnnm_dev::tc::smem_bytes(gtc, fwd, 1, wsv, t.f16, true, eh, need, nhb) <= 227 * 1024) {
+          a.nsplit = 1;
+          a.bres = 1;
+          a.bres_stride = stride;
+          a.bres_bytes = need;
+          a.sb = 1;
+          a.ws = wsv;
+          a.ehalf = eh;
+          found = true;
+        }
   }
   if (!found && t.f16 && !pairs && !a.mcb && have_b && bres_on) {
     const int stride = t.wbase * icnnm_dev::tc::KC * 4;
@@ -856,22 +891,24 @@ void launch_tc_kernel(const Geo& gtc, const TcPlan& t, bool fwd, int mode, const
   void* args[] = {&a};
   const dim3 block(icnnm_dev::tc::threads(fwd));
   cudaLaunchConfig_t lc{};
-  cudaLaunchAttribute at{};
+  cudaLaunchAttribute at[2]{};
   lc.gridDim = dim3(cfg.grid);
   lc.blockDim = block;
   lc.dynamicSmemBytes = cfg.smem;
   lc.stream = stream;
-  lc.attrs = &at;
+  lc.attrs = at;
+  lc.numAttrs = 0;
   if (cfg.cluster) {
-    at.id = cudaLaunchAttributeClusterDimension;
-    at.val.clusterDim.x = 2;
-    at.val.clusterDim.y = 1;
-    at.val.clusterDim.z = 1;
-    lc.numAttrs = 1;
-  } else {
-    at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at.val.programmaticStreamSerializationAllowed = 1;
-    lc.numAttrs = pdl ? 1 : 0;
+    at[lc.numAttrs].id = cudaLaunchAttributeClusterDimension;
+    at[lc.numAttrs].val.clusterDim.x = 2;
+    at[lc.numAttrs].val.clusterDim.y = 1;
+    at[lc.numAttrs].val.clusterDim.z = 1;
+    ++lc.numAttrs;
+  }
+  if (pdl) {
+    at[lc.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[lc.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++lc.numAttrs;
   }
   CK(cudaLaunchKernelExC(&lc, cfg.fn, args));
 }

@@ -700,7 +700,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       mbar_init(A_empty + i, 1);
     }
     for (int i = 0; i < SB; ++i) {
-      mbar_init(B_full + i, (PAIR && !a.tma_pair && (blockIdx.x & 1u) == 0) ? 2 : 1);
+      mbar_init(B_full + i, (PAIR && !a.tma_pair && !a.bres && (blockIdx.x & 1u) == 0) ? 2 : 1);
       mbar_init(B_empty + i, MCB ? 2 : 1);  // MCB: released by both CTAs' MMAs
     }
     for (int i = 0; i < 2; ++i) {
@@ -1545,7 +1545,11 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     if (PAIR && crank != 0) {
       // peer CTA of a pair: the leader issues the pair's MMAs; without tma_pair
       // this warp relays "my half of B stage sb landed" to the leader's B_full
-      if (lane == 0 && !(TC_SKIP(a) & 16) && !a.tma_pair) {
+      if (lane == 0 && a.bres && sfirst < nslot) {
+        // resident B: one relay per launch -- "my half of every tile landed"
+        mbar_wait(BRES_full, 0);
+        mbar_arrive_cluster(mapa_u32(smem_u32(B_full + (SB - 2)), 0));
+      } else if (lane == 0 && !(TC_SKIP(a) & 16) && !a.tma_pair) {
         const uint32_t lead_bfull = mapa_u32(smem_u32(B_full), 0);
         int sb = 0;
         uint32_t bph = 0;
@@ -1597,6 +1601,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         if (res) {
           if (!bres_ready) {
             mbar_wait(BRES_full, 0);  // resident B: one fill per launch (phase 0)
+            if (PAIR) pwait(B_full + (SB - 2), 0);  // ... and the peer's half (its relay)
             bres_ready = true;
           }
         } else if (!(TC_SKIP(a) & 16)) {
@@ -1814,18 +1819,28 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       // a.nresblk (mixed residency) -- loaded once (one barrier phase) and read
       // by every brick's MMAs; only when the CTA has a brick (its MMA warp then
       // waits for the fill before the CTA can exit)
+      // (CTA pairs hold their half of every tile's N rows: hi half, then lo half)
       uint32_t total = 0;
       for (int nt = ntb; nt < nte; ++nt)
         for (int kc = kcb; kc < kce; ++kc)
-          if (is_res(nt, kc)) total += static_cast<uint32_t>(tile_width(a, nt) * KC * (F16 ? 4 : 8));
+          if (is_res(nt, kc))
+            total += static_cast<uint32_t>(tile_width(a, nt) * KC * (F16 ? 4 : 8)) / (PAIR ? 2u : 1u);
       mbar_arrive_expect_tx(BRES_full, total);
       for (int nt = ntb; nt < nte; ++nt) {
         const uint32_t bytes = static_cast<uint32_t>(tile_width(a, nt)) * KC * (F16 ? 4 : 8);
-        for (int kc = kcb; kc < kce; ++kc)
-          if (is_res(nt, kc))
-            bulk_g2s(reinterpret_cast<uint8_t*>(Bst) + bres_off(nt, kc),
-                     a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4), bytes,
-                     BRES_full);
+        for (int kc = kcb; kc < kce; ++kc) {
+          if (!is_res(nt, kc)) continue;
+          uint8_t* dst = reinterpret_cast<uint8_t*>(Bst) + bres_off(nt, kc);
+          const float* src = a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * (B_STAGE_BYTES / 4);
+          if (PAIR) {
+            const uint32_t hb = bytes / 4;  // half of the rows of the hi (or lo) tile
+            const uint8_t* s8 = reinterpret_cast<const uint8_t*>(src);
+            bulk_g2s(dst, s8 + crank * hb, hb, BRES_full);
+            bulk_g2s(dst + hb, s8 + bytes / 2 + crank * hb, hb, BRES_full);
+          } else {
+            bulk_g2s(dst, src, bytes, BRES_full);
+          }
+        }
       }
     }
     if (lane == 0 && (!a.bres || a.bmix) && !(TC_SKIP(a) & 16)) {
