@@ -351,6 +351,44 @@ __device__ __forceinline__ void tc_chunk_f16_lean(uint32_t d, uint32_t a, uint32
       "r"(flags), "r"(static_cast<uint32_t>(KC / 2)), "r"(0x4010u)
       : "memory");
 }
+// The same for the leader of a CTA pair (cta_group::2, M = 256: 128 rows from
+// each CTA's TMEM A stage, B halves from both CTAs' shared memory); commits are
+// multicast to the barrier at the same offset in both CTAs.  Resident B only
+// (no B-stage release).  flags: 1 = release the A stage, 2 = accumulator done.
+__device__ __forceinline__ void tc_chunk_f16_lean_pair(uint32_t d, uint32_t a, uint32_t blo,
+                                                       uint32_t lo_off, uint32_t idesc,
+                                                       uint32_t accum, uint32_t bar_a,
+                                                       uint32_t bar_acc, uint32_t flags) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t, qa, qc;\n"
+      ".reg .b32 f, l2, a2;\n"
+      ".reg .b64 dh, dl;\n"
+      ".reg .b16 m;\n"
+      "mov.b16 m, 3;\n"
+      "setp.ne.b32 p, %5, 0;\n"
+      "setp.eq.b32 t, %5, %5;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "and.b32 f, %8, 1;\n"
+      "setp.ne.b32 qa, f, 0;\n"
+      "and.b32 f, %8, 2;\n"
+      "setp.ne.b32 qc, f, 0;\n"
+      "and.pred qa, qa, e;\n"
+      "and.pred qc, qc, e;\n"
+      "add.u32 l2, %2, %3;\n"
+      "add.u32 a2, %1, %9;\n"
+      "mov.b64 dh, {%2, %10};\n"
+      "mov.b64 dl, {l2, %10};\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], dh, %4, p;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], dh, %4, t;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], dl, %4, t;\n"
+      "@qa tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%6], m;\n"
+      "@qc tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%7], m;\n"
+      "}\n" ::"r"(d),
+      "r"(a), "r"(blo), "r"(lo_off), "r"(idesc), "r"(accum), "r"(bar_a), "r"(bar_acc), "r"(flags),
+      "r"(static_cast<uint32_t>(KC / 2)), "r"(0x4010u)
+      : "memory");
+}
 // tc_chunk_f16 for B-multicast clusters: the B-stage release is committed to
 // the barrier at the same offset in both CTAs of the 2-CTA cluster (the stage
 // is refilled, for both, only after both CTAs' MMAs have read it).
@@ -1691,7 +1729,9 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       // registers, advances descriptors / stages incrementally and commits
       // nothing for resident B blocks.
       bool lean = false;
-      if constexpr (F16 && !PAIR) lean = !MCB && TC_DBG(a) == nullptr && (TC_SKIP(a) & ~(1 | 2 | 128 | 256)) == 0;
+      if constexpr (F16)
+        lean = !MCB && TC_DBG(a) == nullptr && (TC_SKIP(a) & ~(1 | 2 | 128 | 256)) == 0 &&
+               (!PAIR || (a.bres && !a.bmix));  // pairs: resident B only
       if (lean) {
         const uint32_t a0 = tbase + a_col0;
         const int bres = a.bres, bmix = a.bmix, nresblk = a.nresblk;
@@ -1710,6 +1750,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
           if (bres && (!bmix || blk < nresblk)) {
             if (!bres_ready) {
               mbar_wait(BRES_full, 0);
+              if (PAIR) mbar_wait(B_full + (SB - 2), 0);  // the peer's half (its relay)
               bres_ready = true;
             }
             blo = res_lo0 + static_cast<uint32_t>(blk) * res_step;
@@ -1719,9 +1760,14 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             fl |= 4u;
           }
           tc_fence_after();
-          tc_chunk_f16_lean(tbase + (tci & 1) * accw, a0 + sa * ASC, blo,
-                            static_cast<uint32_t>(wn_t[t]) * 2u, idesc_t[t], c == 0 ? 0u : 1u,
-                            bar_be + 8u * sb, bar_ae + 8u * sa, bar_accf + 8u * (tci & 1), fl);
+          if constexpr (PAIR)  // this CTA's half: hi rows, then lo rows (wn / 2 x 32 B each)
+            tc_chunk_f16_lean_pair(tbase + (tci & 1) * accw, a0 + sa * ASC, blo,
+                                   static_cast<uint32_t>(wn_t[t]), idesc_t[t], c == 0 ? 0u : 1u,
+                                   bar_ae + 8u * sa, bar_accf + 8u * (tci & 1), fl);
+          else
+            tc_chunk_f16_lean(tbase + (tci & 1) * accw, a0 + sa * ASC, blo,
+                              static_cast<uint32_t>(wn_t[t]) * 2u, idesc_t[t], c == 0 ? 0u : 1u,
+                              bar_be + 8u * sb, bar_ae + 8u * sa, bar_accf + 8u * (tci & 1), fl);
           if ((fl & 4u) && ++sb == sbn) {
             sb = 0;
             bph ^= 1u;
@@ -1736,7 +1782,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
             cur_nt0 = nt0;
             for (int t = 0; t < gsz; ++t) {
               wn_t[t] = tile_width(a, nt0 + t);
-              idesc_t[t] = idesc_f16(wn_t[t]);
+              idesc_t[t] = PAIR ? idesc_f16_m256(wn_t[t]) : idesc_f16(wn_t[t]);
             }
             auto adv = [&](int& s_, uint32_t& p_) {
               if (++s_ == san) {
