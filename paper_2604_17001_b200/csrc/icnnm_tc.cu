@@ -1471,8 +1471,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         };
         // deterministic flush, two frames per atomic: an even first frame and an
         // even T keep each frame pair contiguous, 16-byte aligned and on one
-        // side of the periodic wrap (red.global.add.v4.f32: half the atomics,
-        // the flush's red issue was the adjoint's largest stall item)
+        // side of the periodic wrap (red.global.add.v4.f32: half the atomics)
         const bool pair_ok = a.adjq != nullptr && (((tbase_ | g.T) & 1) == 0);
         auto emit2 = [&](float s0, float s1, int hs, int ws, int cc) {
           if (s0 == 0.f && s1 == 0.f) return;
