@@ -596,7 +596,7 @@ struct TcConfig {
   void* fn = nullptr;
 };
 
-TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
+TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b, bool no_auto_pairs = false) {
   TcConfig cfg;
   icnnm_dev::tc::TcArgs& a = cfg.a;
   a.bunscale = t.bunscale;
@@ -649,13 +649,17 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
   // ICNNM_TC_CS=1|2 (experiments build) forces single CTAs / pairs for both kernels.
   static const int cs_env = env_knob("ICNNM_TC_CS", -1);
   a.cs = cs_env >= 0 ? cs_env : 1;
-  if (cs_env < 0 && !fwd && t.f16 && have_b && env_knob("ICNNM_TC_BRES", -1) != 0) {
+  bool auto_pairs = false;
+  if (cs_env < 0 && !no_auto_pairs && !fwd && t.f16 && have_b && env_knob("ICNNM_TC_BRES", -1) != 0) {
     const int full = t.ntn * t.nkc * t.wbase * icnnm_dev::tc::KC * 4;
     const bool single_fits =
         icnnm_dev::tc::smem_bytes(gtc, fwd, 1, 4, true, false, 1, full, 2) <= 227 * 1024;
     const bool pair_fits =
         icnnm_dev::tc::smem_bytes(gtc, fwd, 1, 4, true, true, 1, full / 2, 2) <= 227 * 1024;
-    if (!single_fits && pair_fits && t.ntn >= 2 && t.sa >= 4) a.cs = 2;
+    if (!single_fits && pair_fits && t.ntn >= 2 && t.sa >= 4) {
+      a.cs = 2;
+      auto_pairs = true;
+    }
   }
   if (!t.f16 || n_bricks(gtc) < 2) a.cs = 1;
   const bool pairs = a.cs > 1;
@@ -855,6 +859,10 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b) {
       it = max_pairs.emplace(key, std::max(1, n)).first;
     }
     const int64_t nslot = (a.nbricks + 1) / 2;
+    // a device on which fewer than 80% of the SMs can run as co-resident pairs
+    // (disabled SMs splitting TPCs) keeps the automatic choice on single CTAs
+    if (auto_pairs && a.cs > 1 && 2 * it->second * 5 < nsm * 4 && nslot > it->second)
+      return tc_config(gtc, t, fwd, have_b, true);
     cfg.grid = 2u * static_cast<unsigned>(std::min<int64_t>(nslot, it->second));
   } else {
     // split mode: a multiple of nsplit CTAs, role = blockIdx % nsplit

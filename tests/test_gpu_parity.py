@@ -72,8 +72,10 @@ def test_forward_matches_basis_convolver(gpu, dims, ks, engine):
 @pytest.mark.parametrize("dims,ks", [((32, 32, 8), (5, 5, 3)), ((5, 6, 7), (2, 3, 4)),
                                      ((4, 4), (2, 2)), ((10,), (4,)), ((8, 8, 16), (8, 8, 3)),
                                      ((20, 20, 16), (9, 9, 5)),
-                                     # k = 245: whole bricks per CTA with mixed B residency
-                                     ((16, 24, 16), (7, 7, 5))])
+                                     # k = 245: the adjoint runs on CTA pairs with resident B
+                                     # halves (even and odd brick counts: dummy tail brick)
+                                     ((16, 24, 16), (7, 7, 5)), ((12, 12, 8), (7, 7, 5)),
+                                     ((20, 12, 24), (7, 7, 5))])
 @pytest.mark.parametrize("engine", ENGINES)
 def test_adjoint_bit_exact_on_integers(gpu, dims, ks, engine):
     """conv_adjoint (conv_op.cpp:57-77) on integer W: exact in fp32."""
