@@ -650,7 +650,11 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b, bool 
   static const int cs_env = env_knob("ICNNM_TC_CS", -1);
   a.cs = cs_env >= 0 ? cs_env : 1;
   bool auto_pairs = false;
-  if (cs_env < 0 && !no_auto_pairs && !fwd && t.f16 && have_b && env_knob("ICNNM_TC_BRES", -1) != 0) {
+#ifndef ICNNM_FWD_PAIRS
+#define ICNNM_FWD_PAIRS 0  // build-time A/B: the forward on resident pairs too
+#endif
+  if (cs_env < 0 && !no_auto_pairs && (!fwd || ICNNM_FWD_PAIRS) && t.f16 && have_b &&
+      env_knob("ICNNM_TC_BRES", -1) != 0) {
     const int full = t.ntn * t.nkc * t.wbase * icnnm_dev::tc::KC * 4;
     const bool single_fits =
         icnnm_dev::tc::smem_bytes(gtc, fwd, 1, 4, true, false, 1, full, 2) <= 227 * 1024;
