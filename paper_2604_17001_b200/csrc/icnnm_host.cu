@@ -648,7 +648,10 @@ TcConfig tc_config(const Geo& gtc, const TcPlan& t, bool fwd, bool have_b, bool 
   // share built chunks, loses 11% and stays on single CTAs).
   // ICNNM_TC_CS=1|2 (experiments build) forces single CTAs / pairs for both kernels.
   static const int cs_env = env_knob("ICNNM_TC_CS", -1);
-  a.cs = cs_env >= 0 ? cs_env : 1;
+#ifndef ICNNM_DEFAULT_CS
+#define ICNNM_DEFAULT_CS 1  // build-time A/B: 2 = CTA pairs wherever they are possible
+#endif
+  a.cs = cs_env >= 0 ? cs_env : ICNNM_DEFAULT_CS;
   bool auto_pairs = false;
 #ifndef ICNNM_FWD_PAIRS
 #define ICNNM_FWD_PAIRS 0  // build-time A/B: the forward on resident pairs too

@@ -1888,7 +1888,49 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         }
       }
     }
-    if (lane == 0 && (!a.bres || a.bmix) && !(TC_SKIP(a) & 16)) {
+    if (lane == 0 && (!a.bres || a.bmix) && !CL2 && TC_SKIP(a) == 0 && TC_DBG(a) == nullptr) {
+      // Single CTAs, product path: the ring is fed by ONE thread, so its
+      // instruction count per stage bounds the B stream (the general loop
+      // below -- two 32-bit divisions for the ring slot and parity plus the
+      // tile-group sequence decode per stage -- kept this thread busy 80% of
+      // the time with the MMA warp waiting on B half of its time at k = 405:
+      // profiles/r2/README.md).  Ring slot, parity and the tile-group order
+      // advance incrementally here.
+      int sb = 0;
+      uint32_t bwph = 1;  // parity of B_empty to wait on
+      const size_t blkf = B_STAGE_BYTES / 4;  // floats per packed (tile, chunk) block
+      auto put = [&](int nt, int kc, uint32_t bytes) {
+        if (is_res(nt, kc)) return;  // resident block: no stage
+        mbar_wait(B_empty + sb, bwph);
+        mbar_arrive_expect_tx(B_full + sb, bytes);
+        bulk_g2s(Bring + sb * BSTG, a.Bpk + (static_cast<size_t>(nt) * nkc + kc) * blkf, bytes,
+                 B_full + sb);
+        if (++sb == sbn) {
+          sb = 0;
+          bwph ^= 1u;
+        }
+      };
+      for (int sl = sfirst; sl < nslot; sl += sstep) {
+        for (int gi = 0; gi < ngrp; ++gi) {
+          const int nt0 = ntb + gi * grp;
+          const int gsz = (nte - nt0) < grp ? (nte - nt0) : grp;
+          const uint32_t by0 = static_cast<uint32_t>(tile_width(a, nt0)) * KC * (F16 ? 4 : 8);
+          if (gsz == 1) {
+            for (int kc = kcb; kc < kce; ++kc) put(nt0, kc, by0);
+          } else {  // the tg_seq order, phase by phase (as the MMA warp consumes it)
+            const uint32_t by1 = static_cast<uint32_t>(tile_width(a, nt0 + 1)) * KC * (F16 ? 4 : 8);
+            for (int kc = kcb; kc < kcb + skew; ++kc) put(nt0, kc, by0);
+            for (int kc = kcb; kc < kcb + skew; ++kc) put(nt0 + 1, kc, by1);
+            for (int kc = kcb + skew; kc < kce - skew; ++kc) {
+              put(nt0, kc, by0);
+              put(nt0 + 1, kc, by1);
+            }
+            for (int kc = kce - skew; kc < kce; ++kc) put(nt0, kc, by0);
+            for (int kc = kce - skew; kc < kce; ++kc) put(nt0 + 1, kc, by1);
+          }
+        }
+      }
+    } else if (lane == 0 && (!a.bres || a.bmix) && !(TC_SKIP(a) & 16)) {
       uint32_t bcnt = 0;
       long long wl = 0;
       for (int sl = sfirst; sl < nslot; sl += sstep) {
@@ -1966,15 +2008,20 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       // the [brick][j][row] layout) into the ring ahead of the epilogue; mode 0
       // has no W_old (the slot is only handed over).  Tiles are padded to an
       // even number of groups so that each stage serves one epilogue half.
-      uint32_t gs = 0;
+      int wsl_it = 0;        // ring slot and parity, advanced incrementally (one thread
+      uint32_t wwph = 1;     // feeds the ring: no per-group divisions)
       for (int sl = sfirst; sl < nslot; sl += sstep) {
         const int b = brick_of(sl);
         for (int nt = ntb; nt < nte; ++nt) {
           const int wn = tile_width(a, nt);
           const int ng = (wn + 31) / 32, ngp = ng + (ng & 1);
-          for (int gq = 0; gq < ngp; ++gq, ++gs) {
-            const int wsl = static_cast<int>(gs % wsn);
-            mbar_wait(W_empty + wsl, ((gs / wsn) & 1) ^ 1);
+          for (int gq = 0; gq < ngp; ++gq) {
+            const int wsl = wsl_it;
+            mbar_wait(W_empty + wsl, wwph);
+            if (++wsl_it == wsn) {
+              wsl_it = 0;
+              wwph ^= 1u;
+            }
             if (gq < ng && a.mode >= 1 && !(TC_SKIP(a) & 2)) {
               const int ncol = (wn - 32 * gq) < 32 ? (wn - 32 * gq) : 32;
               const uint32_t bytes = static_cast<uint32_t>(ncol) * 512u;
@@ -1994,13 +2041,18 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
     if (lane == 0) {
       // adjoint: stream W chunks (16 columns x 128 rows, 8 KB contiguous in the
       // [brick][j][row] layout) ahead of the builders
-      uint32_t wcnt = 0;
+      int wsi_it = 0;        // ring slot and parity, advanced incrementally
+      uint32_t wwph = 1;
       for (int sl = sfirst; sl < nslot; sl += sstep) {
         const int b = brick_of(sl);
         for (int gi = 0; gi < ngrp; ++gi) {
-          for (int kc = kcb; kc < kce; ++kc, ++wcnt) {
-            const int wsi = wcnt % wsn;
-            mbar_wait(W_empty + wsi, ((wcnt / wsn) & 1) ^ 1);
+          for (int kc = kcb; kc < kce; ++kc) {
+            const int wsi = wsi_it;
+            mbar_wait(W_empty + wsi, wwph);
+            if (++wsi_it == wsn) {
+              wsi_it = 0;
+              wwph ^= 1u;
+            }
             if (TC_SKIP(a) & 256) {  // timing experiment: no W traffic
               mbar_arrive(W_full + wsi);
               continue;
