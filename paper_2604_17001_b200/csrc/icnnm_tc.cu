@@ -1729,7 +1729,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
       // nothing for resident B blocks.
       bool lean = false;
       if constexpr (F16)
-        lean = !MCB && TC_DBG(a) == nullptr && (TC_SKIP(a) & ~(1 | 2 | 128 | 256)) == 0 &&
+        lean = !MCB && (TC_SKIP(a) & ~(1 | 2 | 128 | 256)) == 0 &&  // (counters: MMA waits read 0)
                (!PAIR || (a.bres && !a.bmix));  // pairs: resident B only
       if (lean) {
         const uint32_t a0 = tbase + a_col0;
@@ -1888,7 +1888,7 @@ icnnm_tc_kernel(const __grid_constant__ TcArgs a) {
         }
       }
     }
-    if (lane == 0 && (!a.bres || a.bmix) && !CL2 && TC_SKIP(a) == 0 && TC_DBG(a) == nullptr) {
+    if (lane == 0 && (!a.bres || a.bmix) && !CL2 && TC_SKIP(a) == 0) {
       // Single CTAs, product path: the ring is fed by ONE thread, so its
       // instruction count per stage bounds the B stream (the general loop
       // below -- two 32-bit divisions for the ring slot and parity plus the
