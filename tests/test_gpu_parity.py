@@ -442,6 +442,23 @@ def test_sharded_virtual_slabs_match_unsharded(gpu, engine):
         np.testing.assert_allclose(rep.objective, r1.objective, rtol=1e-5)
 
 
+def test_sharded_virtual_slabs_k245_pairs(gpu):
+    """The same with the 7x7x5 kernel (k = 245): the adjoint runs on CTA pairs
+    with resident B halves, here on slab geometry (halo rows, no H wrap inside a
+    slab) and through the sharded solve's separate pair-fold kernel."""
+    from paper_2604_17001_b200 import synth
+    X = synth.synth_video(48, 24, 16, 8, 2, 31)
+    mask = synth.synth_mask(48, 24, 16, synth.MASK_IID, 0.4, 32)
+    B = gpu.learn_ensemble_basis([synth.synth_video(48, 24, 16, 8, 2, 33)], (7, 7, 5))
+    cfg = gpu.SolverConfig(max_iters=30, engine="f16x3", **FIXED)
+    L1, r1 = gpu.icnnm_solve(X * mask, mask, B, cfg)
+    for G in (1, 2, 3):
+        row0, rows, rep = gpu.sharded_solve(X * mask, mask, B, cfg, local_slabs=G)
+        assert row0 == 0 and rows.shape == X.shape
+        assert _rel(rows, L1) < 1e-5, G
+        np.testing.assert_allclose(rep.objective, r1.objective, rtol=1e-5)
+
+
 # --------------------------------------------------------------------------
 # BASELINE recipes at oracle-feasible sizes (same generator, mask kind and
 # kernel box as configs 3-5; SURVEY §8c parity plan for the large configs)
